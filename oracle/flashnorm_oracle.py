@@ -1,0 +1,239 @@
+"""FlashNorm oracle: plain, slow, obviously-correct fp64 CPU definitions.
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this
+module.  The product path (``paper_2407_09577_b200``) never imports it and
+shares no code with it.
+
+Every function follows a passage of /root/reference/PAPER.md (arXiv 2407.09577,
+"FlashNorm: fast normalization for LLMs"), cited as PAPER.md:<line> (section).
+Where the paper is silent the reading taken is the one listed in DESIGN.md
+("Readings of the paper"), cited here as [reading cN].
+
+Conventions
+-----------
+* fp64 throughout (numpy float64); the only library primitive used as a step
+  is the matrix product ``@`` ("vector-matrix multiplication").
+* Paper convention for weights: ``W`` is n x k with ``y = x W``,
+  i.e. rows index the *input* features.  The CUDA boundary stores the
+  transpose ``Wt`` (N x K); callers pass ``Wt.T``.
+* Activations are a batch of row vectors ``a[M, n]``; RMS is per row
+  (PAPER.md:14 defines it per vector).
+
+Pins: tests/test_oracle_pins.py pins every function here to values/identities
+fixed by the paper and by mathematics (tests/golden/*.json).  DyT's elementwise
+formula is not stated by the paper: ``dyt`` is pinned only to reading c10
+("parity pinned to the stated reading").
+"""
+from __future__ import annotations
+
+import numpy as np
+
+MODES = ("rmsnorm", "layernorm", "dyt")
+
+
+def _f64(x):
+    return None if x is None else np.asarray(x, dtype=np.float64)
+
+
+# ---------------------------------------------------------------------------
+# RMS and its variants
+# ---------------------------------------------------------------------------
+
+def rms(a):
+    """RMS(a) = sqrt((1/n) sum_i a_i^2) per row.  PAPER.md:14 (§1)."""
+    a = _f64(a)
+    n = a.shape[-1]
+    return np.sqrt(np.sum(a * a, axis=-1) / n)
+
+
+def rmse(a, eps):
+    """RMSe(a) = sqrt(eps + (1/n) sum_i a_i^2).  PAPER.md:177 (App. A) [reading c1]."""
+    a = _f64(a)
+    n = a.shape[-1]
+    return np.sqrt(eps + np.sum(a * a, axis=-1) / n)
+
+
+def rss(a):
+    """RSS(a) = sqrt(sum_i a_i^2).  PAPER.md:185-187 (App. B)."""
+    a = _f64(a)
+    return np.sqrt(np.sum(a * a, axis=-1))
+
+
+def rsse(a, eps):
+    """RSSe(a) = sqrt(n eps + sum_i a_i^2).  PAPER.md:196-200 (App. B)."""
+    a = _f64(a)
+    n = a.shape[-1]
+    return np.sqrt(n * eps + np.sum(a * a, axis=-1))
+
+
+def mean_square(a):
+    """MS(a) = (1/n) sum a_i^2 = RMS(a)^2.  PAPER.md:70-73 (§2.2)."""
+    a = _f64(a)
+    return np.sum(a * a, axis=-1) / a.shape[-1]
+
+
+# ---------------------------------------------------------------------------
+# Normalizations (unfused, Fig 1(a))
+# ---------------------------------------------------------------------------
+
+def rmsnorm(a, g=None, b=None, eps=0.0):
+    """y_i = a_i / RMSe(a) * g_i (+ b_i).
+
+    PAPER.md:14 (§1) for y_i = a_i/RMS * g_i; PAPER.md:177 (App. A) for eps;
+    the optional bias b "right after scaling by weights g_i" PAPER.md:25 (§1.1).
+    """
+    a = _f64(a)
+    y = a / rmse(a, eps)[..., None]
+    if g is not None:
+        y = y * _f64(g)
+    if b is not None:
+        y = y + _f64(b)
+    return y
+
+
+def mean_center(y):
+    """a_j = y_j - mu, mu = (1/n) sum_j y_j.  PAPER.md:40, 45 (§1.2)."""
+    y = _f64(y)
+    return y - np.mean(y, axis=-1, keepdims=True)
+
+
+def layernorm(a, g=None, b=None, eps=0.0):
+    """LayerNorm = mean centering followed by RMSNorm.  PAPER.md:33 (§1.2) [reading c8]."""
+    return rmsnorm(mean_center(a), g, b, eps)
+
+
+def dyt(a, g=None, b=None, alpha=0.5):
+    """DyT: y = g * tanh(alpha * a) + b.
+
+    The paper names DyT and its bias b after g but
+    never states the elementwise formula: [reading c10].
+    """
+    a = _f64(a)
+    y = np.tanh(alpha * a)
+    if g is not None:
+        y = y * _f64(g)
+    if b is not None:
+        y = y + _f64(b)
+    return y
+
+
+def normalize(a, mode, g=None, b=None, eps=0.0, alpha=0.5):
+    if mode == "rmsnorm":
+        return rmsnorm(a, g, b, eps)
+    if mode == "layernorm":
+        return layernorm(a, g, b, eps)
+    if mode == "dyt":
+        return dyt(a, g, b, alpha)
+    raise ValueError(f"mode must be one of {MODES}, got {mode!r}")
+
+
+# ---------------------------------------------------------------------------
+# Linear layer and the unfused norm -> linear path (Fig 1(a))
+# ---------------------------------------------------------------------------
+
+def linear(y, W, c=None):
+    """z = y W (+ c).  W is n x k (paper convention)."""
+    z = _f64(y) @ _f64(W)
+    if c is not None:
+        z = z + _f64(c)
+    return z
+
+
+def norm_linear(a, W, g=None, b=None, c=None, eps=0.0, mode="rmsnorm", alpha=0.5):
+    """Unfused reference: z = Norm(a; g, b) W + c.  Fig 1(a).
+
+    This is what the CUDA path must equal (FlashNorm is "exact");
+    it never folds anything.
+    """
+    return linear(normalize(a, mode, g, b, eps, alpha), W, c)
+
+
+def upstream_layernorm_linear(x, V, b_prev, W, g=None, b=None, c=None, eps=0.0):
+    """Config 4 unfused: a = x V + b_prev, then LayerNorm(a; g, b) W + c.
+
+    PAPER.md:33 (Fig B(a)): linear layer V followed by mean centering and RMSNorm.
+    """
+    a = linear(x, V, b_prev)
+    return norm_linear(a, W, g, b, c, eps, "layernorm")
+
+
+# ---------------------------------------------------------------------------
+# The FlashNorm transforms, written out in fp64 (used to check the paper's
+# identities and as the exact target of the folded CUDA tensors)
+# ---------------------------------------------------------------------------
+
+def eliminate_norm_bias(W, b=None, c=None):
+    """c* = c + b W, with the ORIGINAL W (bias moved before the g merge).
+
+    PAPER.md:25 (§1.1, Fig A(b)) [reading c5].
+    """
+    W = _f64(W)
+    k = W.shape[1]
+    cstar = np.zeros(k) if c is None else _f64(c).copy()
+    if b is not None:
+        cstar = cstar + _f64(b) @ W
+    return cstar
+
+
+def merge_norm_weights(W, g=None):
+    """W*_{i,j} = g_i W_{i,j}.  PAPER.md:16 (§1, Fig 1(b))."""
+    W = _f64(W)
+    if g is None:
+        return W.copy()
+    return _f64(g)[:, None] * W
+
+
+def fold_weights(W, g=None, b=None, c=None):
+    """(W*, c*) in the paper's order: Fig A first, then Fig 1(b)."""
+    return merge_norm_weights(W, g), eliminate_norm_bias(W, b, c)
+
+
+def deferred_linear(a, Wstar, cstar=None, eps=0.0):
+    """Deferred normalization z = (a W*) * 1/RMSe(a) (+ c*, added AFTER scaling).
+
+    PAPER.md:17 (§1, Fig 1(c)): "normalization ... must be done before adding
+    the bias" [reading c4]; eps per App. A.
+    """
+    a = _f64(a)
+    z = (a @ _f64(Wstar)) / rmse(a, eps)[..., None]
+    if cstar is not None:
+        z = z + _f64(cstar)
+    return z
+
+
+def row_sums(V):
+    """s_i = sum_j v_{i,j} (sum of row i of V).  PAPER.md:44 (§1.2)."""
+    return np.sum(_f64(V), axis=1)
+
+
+def mean_via_s(x, V):
+    """mu = (1/n) sum_i x_i s_i.  PAPER.md:42 (§1.2); n = number of outputs of V [reading c6]."""
+    V = _f64(V)
+    n = V.shape[1]
+    return (_f64(x) @ row_sums(V)) / n
+
+
+def fold_mean_center(V, b_prev=None):
+    """V*_{i,j} = v_{i,j} - s_i / n.  PAPER.md:49 (§1.2, Fig B(b)).
+
+    V's own bias (the paper is silent): b_prev* = b_prev - mean(b_prev) [reading c7].
+    """
+    V = _f64(V)
+    n = V.shape[1]
+    Vstar = V - row_sums(V)[:, None] / n
+    bstar = None if b_prev is None else _f64(b_prev) - np.mean(_f64(b_prev))
+    return Vstar, bstar
+
+
+# ---------------------------------------------------------------------------
+# Parity metric [reading c12]
+# ---------------------------------------------------------------------------
+
+def rowwise_rel_err(z, zref):
+    """max_m ||z_m - zref_m||_inf / ||zref_m||_inf  (SPEC.md:432 style, per row)."""
+    z = np.asarray(z, dtype=np.float64)
+    zref = np.asarray(zref, dtype=np.float64)
+    num = np.max(np.abs(z - zref), axis=-1)
+    den = np.maximum(np.max(np.abs(zref), axis=-1), 1e-30)
+    return float(np.max(num / den)) if num.size else 0.0

@@ -1,0 +1,280 @@
+"""Pins for the fp64 oracle (oracle/flashnorm_oracle.py) — CPU only.
+
+The oracle is pinned to things other than itself:
+  * hand-derived worked examples with citations (tests/golden/worked_examples.json),
+  * closed forms and the paper's identities,
+  * an independent library routine (torch.nn.functional.rms_norm / layer_norm in
+    float64, math.tanh) on random inputs,
+  * brute force with exact rational arithmetic (fractions) on tiny inputs,
+  * fault injection: plausible mistakes (eps outside sqrt, 1/(n-1), bias before
+    scale, c* from W*, dropped b_prev centering) must FAIL at least one pin.
+"""
+import math
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+from oracle import flashnorm_oracle as O
+
+
+def ev(expr):
+    return float(eval(str(expr), {"__builtins__": {}}, {k: getattr(math, k) for k in ("sqrt", "tanh")}))
+
+
+def evv(lst):
+    return np.array([ev(e) for e in lst], dtype=np.float64)
+
+
+# ---------------------------------------------------------------- worked examples
+
+def test_rms_family_worked(golden):
+    for ex in golden["rms"]:
+        assert O.rms(np.array(ex["a"], float)) == pytest.approx(ev(ex["expect"]), rel=1e-15, abs=0), ex["cite"]
+    for ex in golden["rmse"]:
+        assert O.rmse(np.array(ex["a"], float), ex["eps"]) == pytest.approx(ev(ex["expect"]), rel=1e-15), ex["cite"]
+    for ex in golden["rss"]:
+        assert O.rss(np.array(ex["a"], float)) == pytest.approx(ev(ex["expect"]), rel=1e-15), ex["cite"]
+    for ex in golden["rsse"]:
+        assert O.rsse(np.array(ex["a"], float), ex["eps"]) == pytest.approx(ev(ex["expect"]), rel=1e-15), ex["cite"]
+
+
+def test_mean_center_worked(golden):
+    for ex in golden["mean_center"]:
+        np.testing.assert_allclose(O.mean_center(np.array(ex["y"], float)), evv(ex["expect"]), atol=1e-15)
+
+
+def test_norms_worked(golden):
+    for ex in golden["norms"]:
+        y = O.normalize(np.array(ex["a"], float), ex["mode"], ex["g"], ex["b"], ex["eps"],
+                        ex["alpha"] if ex["alpha"] is not None else 0.5)
+        np.testing.assert_allclose(y, evv(ex["expect"]), rtol=1e-14, atol=1e-15, err_msg=ex["cite"])
+
+
+def test_norm_linear_worked(golden):
+    for ex in golden["norm_linear"]:
+        z = O.norm_linear(np.array(ex["a"], float), np.array(ex["W"], float), ex["g"], ex["b"], ex["c"],
+                          ex["eps"], ex["mode"])
+        np.testing.assert_allclose(z, np.array([evv(r) for r in ex["expect"]]), rtol=1e-14, err_msg=ex["cite"])
+
+
+def test_folds_worked(golden):
+    for ex in golden["fold_weights"]:
+        Ws, cs = O.fold_weights(np.array(ex["W"], float), ex["g"], ex["b"], ex["c"])
+        np.testing.assert_array_equal(Ws, np.array(ex["W_star"], float), err_msg=ex["cite"])
+        if ex["c_star"] is not None:
+            np.testing.assert_array_equal(cs, np.array(ex["c_star"], float), err_msg=ex["cite"])
+    for ex in golden["fold_mean_center"]:
+        V = np.array(ex["V"], float)
+        np.testing.assert_array_equal(O.row_sums(V), np.array(ex["s"], float))
+        Vs, bs = O.fold_mean_center(V, ex["b_prev"])
+        np.testing.assert_array_equal(Vs, np.array(ex["V_star"], float), err_msg=ex["cite"])
+        if ex["b_prev_star"] is not None:
+            np.testing.assert_array_equal(bs, np.array(ex["b_prev_star"], float))
+
+
+def test_mean_retrofit_worked(golden):
+    for ex in golden["mean_retrofit"]:
+        x, V = np.array(ex["x"], float), np.array(ex["V"], float)
+        np.testing.assert_array_equal(O.linear(x, V), np.array(ex["y"], float))
+        assert O.mean_via_s(x, V) == ev(ex["mu"])
+        Vs, _ = O.fold_mean_center(V)
+        np.testing.assert_allclose(O.linear(x, Vs), np.array(ex["centered"], float), atol=1e-15)
+
+
+# ---------------------------------------------------------------- independent library routines
+
+@pytest.mark.parametrize("eps", [0.0, 1e-5, 0.3])
+def test_rmsnorm_matches_torch_f64(eps):
+    import torch
+    rng = np.random.default_rng(1)
+    a = rng.standard_normal((7, 48)) * rng.uniform(0.01, 10, (7, 1))
+    g = rng.uniform(0.5, 1.5, 48)
+    ref = torch.nn.functional.rms_norm(torch.from_numpy(a), (48,), torch.from_numpy(g), eps=eps).numpy()
+    np.testing.assert_allclose(O.rmsnorm(a, g, None, eps), ref, rtol=1e-13, atol=1e-14)
+
+
+@pytest.mark.parametrize("eps", [0.0, 1e-5, 0.3])
+def test_layernorm_matches_torch_f64(eps):
+    import torch
+    rng = np.random.default_rng(2)
+    a = rng.standard_normal((5, 40)) * 3 + 7.0
+    g = rng.uniform(0.5, 1.5, 40)
+    b = rng.uniform(-0.1, 0.1, 40)
+    ref = torch.nn.functional.layer_norm(torch.from_numpy(a), (40,), torch.from_numpy(g), torch.from_numpy(b),
+                                         eps=eps).numpy()
+    np.testing.assert_allclose(O.layernorm(a, g, b, eps), ref, rtol=1e-12, atol=1e-13)
+
+
+def test_dyt_matches_math_tanh():
+    rng = np.random.default_rng(3)
+    a = rng.standard_normal((3, 16)) * 4
+    g = rng.uniform(0.5, 1.5, 16)
+    b = rng.uniform(-0.1, 0.1, 16)
+    ref = np.array([[g[k] * math.tanh(0.7 * a[m, k]) + b[k] for k in range(16)] for m in range(3)])
+    np.testing.assert_allclose(O.dyt(a, g, b, 0.7), ref, rtol=1e-15, atol=1e-15)
+
+
+def test_identity_weights_reduce_to_rmsnorm():
+    """Special case W = I, g = 1, no biases: z = a / RMSe(a) (textbook RMSNorm)."""
+    import torch
+    rng = np.random.default_rng(4)
+    a = rng.standard_normal((6, 32))
+    z = O.norm_linear(a, np.eye(32), None, None, None, 1e-5, "rmsnorm")
+    ref = torch.nn.functional.rms_norm(torch.from_numpy(a), (32,), eps=1e-5).numpy()
+    np.testing.assert_allclose(z, ref, rtol=1e-13)
+
+
+# ---------------------------------------------------------------- exact brute force (fractions)
+
+def _brute_norm_linear_exact(a, W, g, b, c, mode, eps_num):
+    """Exact rational evaluation of Fig 1(a) except for one sqrt (done last in float)."""
+    M, n = len(a), len(a[0])
+    k = len(W[0])
+    out = []
+    for m in range(M):
+        x = [Fraction(v) for v in a[m]]
+        if mode == "layernorm":
+            mu = sum(x, Fraction(0)) / n
+            x = [v - mu for v in x]
+        ms = sum((v * v for v in x), Fraction(0)) / n + Fraction(eps_num)
+        r = 1.0 / math.sqrt(ms)  # only irrational step
+        # z_j = r * sum_i x_i g_i W_ij + sum_i b_i W_ij + c_j  (expanded exactly)
+        row = []
+        for j in range(k):
+            lin = sum((x[i] * Fraction(g[i]) * Fraction(W[i][j]) for i in range(n)), Fraction(0))
+            bias = sum((Fraction(b[i]) * Fraction(W[i][j]) for i in range(n)), Fraction(0)) + Fraction(c[j])
+            row.append(float(lin) * r + float(bias))
+        out.append(row)
+    return np.array(out)
+
+
+@pytest.mark.parametrize("mode", ["rmsnorm", "layernorm"])
+def test_brute_force_tiny(mode):
+    rng = np.random.default_rng(5)
+    M, n, k = 3, 5, 4
+    a = rng.integers(-9, 10, (M, n)) / 4.0
+    W = rng.integers(-9, 10, (n, k)) / 8.0
+    g = rng.integers(1, 9, n) / 4.0
+    b = rng.integers(-4, 5, n) / 16.0
+    c = rng.integers(-4, 5, k) / 16.0
+    eps = 0.0625
+    ref = _brute_norm_linear_exact(a.tolist(), W.tolist(), g, b, c, mode, eps)
+    z = O.norm_linear(a, W, g, b, c, eps, mode)
+    np.testing.assert_allclose(z, ref, rtol=1e-13, atol=1e-13)
+
+
+# ---------------------------------------------------------------- the paper's identities (fp64, random)
+
+def _rand_layer(seed, M=8, n=64, k=48):
+    rng = np.random.default_rng(seed)
+    a = rng.standard_normal((M, n))
+    W = rng.standard_normal((n, k)) / np.sqrt(n)
+    g = rng.uniform(0.5, 1.5, n)
+    b = rng.uniform(-0.1, 0.1, n)
+    c = rng.uniform(-0.1, 0.1, k)
+    return a, W, g, b, c
+
+
+@pytest.mark.parametrize("eps", [0.0, 1e-5])
+def test_identity_merged_and_deferred(eps):
+    """(a r g) W + ... = (a r) W* = (a W*) r, bias after scale."""
+    a, W, g, b, c = _rand_layer(6)
+    ref = O.norm_linear(a, W, g, b, c, eps, "rmsnorm")
+    Ws, cs = O.fold_weights(W, g, b, c)
+    merged = O.linear(O.rmsnorm(a, None, None, eps), Ws, cs)
+    deferred = O.deferred_linear(a, Ws, cs, eps)
+    assert O.rowwise_rel_err(merged, ref) < 1e-13
+    assert O.rowwise_rel_err(deferred, ref) < 1e-13
+
+
+def test_identity_bias_elimination():
+    """(y + b) W + c = y W + (c + b W)."""
+    a, W, g, b, c = _rand_layer(7)
+    y = O.rmsnorm(a, g, None, 1e-5)
+    lhs = O.linear(y + b, W, c)
+    rhs = O.linear(y, W, O.eliminate_norm_bias(W, b, c))
+    assert O.rowwise_rel_err(rhs, lhs) < 1e-13
+
+
+def test_identity_mean_via_row_sums_and_vstar():
+    """mu = x s / n = mean(x V) and x V* = mean_center(x V)."""
+    rng = np.random.default_rng(8)
+    x = rng.standard_normal((9, 24))
+    V = rng.standard_normal((24, 40)) + rng.uniform(-0.5, 0.5, (24, 1))
+    bp = rng.uniform(-0.5, 1.5, 40)
+    np.testing.assert_allclose(O.mean_via_s(x, V), np.mean(x @ V, axis=1), rtol=1e-13)
+    Vs, bs = O.fold_mean_center(V, bp)
+    assert np.max(np.abs(Vs.sum(axis=1))) <= 1e-12 * 40
+    np.testing.assert_allclose(O.linear(x, Vs, bs), O.mean_center(O.linear(x, V, bp)), atol=1e-12)
+
+
+def test_identity_layernorm_retrofit():
+    """LayerNorm after V  ==  RMSNorm after V* (PAPER.md:49 'retrofit ... without retraining')."""
+    rng = np.random.default_rng(9)
+    x = rng.standard_normal((6, 32))
+    V = rng.standard_normal((32, 48)) / 6 + rng.uniform(-0.3, 0.3, (32, 1))
+    bp = rng.uniform(-0.5, 1.5, 48)
+    W = rng.standard_normal((48, 16)) / 7
+    g, b, c = rng.uniform(0.5, 1.5, 48), rng.uniform(-0.1, 0.1, 48), rng.uniform(-0.1, 0.1, 16)
+    ref = O.upstream_layernorm_linear(x, V, bp, W, g, b, c, 1e-5)
+    Vs, bs = O.fold_mean_center(V, bp)
+    Ws, cs = O.fold_weights(W, g, b, c)
+    got = O.deferred_linear(O.linear(x, Vs, bs), Ws, cs, 1e-5)
+    assert O.rowwise_rel_err(got, ref) < 1e-12
+
+
+def test_identity_dyt_fold():
+    """DyT bias/weights fold the same way: z = tanh(alpha a) W* + c*."""
+    a, W, g, b, c = _rand_layer(10)
+    ref = O.norm_linear(a, W, g, b, c, 0.0, "dyt", 0.5)
+    Ws, cs = O.fold_weights(W, g, b, c)
+    assert O.rowwise_rel_err(O.linear(np.tanh(0.5 * a), Ws, cs), ref) < 1e-13
+
+
+def test_appendix_identities():
+    """RMS = sqrt(1/n) RSS; RMSe = sqrt(1/n) RSSe; g* = sqrt(n) g gives the same y."""
+    rng = np.random.default_rng(11)
+    a = rng.standard_normal((5, 64))
+    g = rng.uniform(0.5, 1.5, 64)
+    np.testing.assert_allclose(O.rms(a), np.sqrt(1 / 64) * O.rss(a), rtol=1e-15)
+    np.testing.assert_allclose(O.rmse(a, 1e-5), np.sqrt(1 / 64) * O.rsse(a, 1e-5), rtol=1e-15)
+    np.testing.assert_allclose(O.rmsnorm(a, g, None, 0.0), a / O.rss(a)[:, None] * (np.sqrt(64) * g), rtol=1e-14)
+    np.testing.assert_allclose(O.mean_square(a), O.rms(a) ** 2, rtol=1e-14)
+
+
+def test_rms_scale_invariance():
+    """RMS(s a) = s RMS(a), exact only without eps."""
+    rng = np.random.default_rng(12)
+    a = rng.standard_normal((4, 64))
+    for s in (1e-3, 0.5, 7.0):
+        np.testing.assert_allclose(O.rms(s * a), s * O.rms(a), rtol=1e-14)
+        np.testing.assert_allclose(O.rmsnorm(s * a, None, None, 0.0), O.rmsnorm(a, None, None, 0.0), rtol=1e-13)
+    # with eps the invariance breaks for low-energy vectors (App. A / PAPER.md:128)
+    assert not np.allclose(O.rmsnorm(1e-3 * a, None, None, 1e-5), O.rmsnorm(a, None, None, 1e-5), rtol=1e-3)
+
+
+# ---------------------------------------------------------------- fault injection: pins are not vacuous
+
+def test_faults_are_detected(golden):
+    ex = golden["rmse"][2]
+    a = np.array(ex["a"], float)
+    eps_outside = O.rms(a) + ex["eps"]                    # 1/(rms + eps) reading
+    assert abs(eps_outside - ev(ex["expect"])) > 1e-6
+    a34 = np.array([3.0, 4.0])
+    unbiased = np.sqrt(np.sum(a34 ** 2) / (2 - 1))          # 1/(n-1)
+    assert abs(unbiased - ev(golden["rms"][1]["expect"])) > 1e-3
+    fw = golden["fold_weights"][2]
+    W = np.array(fw["W"], float)
+    Ws = O.merge_norm_weights(W, fw["g"])
+    cs_wrong = np.array(fw["c"]) + np.array(fw["b"]) @ Ws   # c* built from W* (reading c5 violated)
+    assert not np.allclose(cs_wrong, fw["c_star"])
+    nl = golden["norm_linear"][0]
+    a2, W2 = np.array(nl["a"], float), np.array(nl["W"], float)
+    Ws2, cs2 = O.fold_weights(W2, nl["g"], nl["b"], nl["c"])
+    bias_before_scale = (a2 @ Ws2 + cs2) / O.rms(a2)[:, None]  # reading c4 violated
+    assert not np.allclose(bias_before_scale, [[ev(e) for e in nl["expect"][0]]], rtol=1e-3)
+    fm = golden["fold_mean_center"][0]
+    _, bs = O.fold_mean_center(np.array(fm["V"], float), None)
+    assert bs is None  # dropping b_prev centering leaves b_prev un-centered: [1,3] != [-1,1]
+    assert not np.allclose(fm["b_prev"], fm["b_prev_star"])
