@@ -1,0 +1,414 @@
+#!/usr/bin/env python
+"""bench.py — FlashNorm fused norm+linear on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One "step" = one pass of the whole per-token hot path (SURVEY §8(a) rows 8a-3..8a-6:
+A staging, RMS in parallel with the tcgen05 contraction, deferred scale + bias
+epilogue) over one batch of the N=1 workload, BASELINE config 3 (Llama-3-8B
+prefill: 4096 tokens, RMSNorm + FFN gate||up 4096 -> 2x14336, bf16).  The
+offline folds (8a-1, 8a-2) run once per weight load; they are timed separately
+and reported under "fold".  Inputs are resident in HBM and larger than L2
+(W* = 235 MB > 126 MB), so no L2 flush is needed between steps.
+
+N > 1 (torchrun, one process per GPU): W* is column-sharded across ranks with the
+activations replicated (BASELINE.json:5); each rank computes its
+N/P columns with no data-path collective; value = total FLOPs / max-over-ranks
+time ("scaling": "strong", the total problem is fixed).
+
+Rank 0 prints ONE JSON line.  The decode config (BASELINE config 2, HBM GB/s)
+and the unfused two-kernel variant are measured in the same run and reported
+as sub-objects.  --impl reference times the fp64 CPU oracle (oracle/) on a
+bounded sample of the same workload (the tier's reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fused norm+linear TFLOP/s (prefill) and HBM GB/s (decode) vs B200 roofline"
+PREFILL = dict(M=4096, K=4096, N=28672)
+DECODE_K, DECODE_N = 4096, 6144
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    except Exception:
+        return FALLBACK_PEAKS, "fallback"
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ------------------------------------------------------------------ clocks sampler
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the measurement window."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(r[1]) for r in self.rows if num(r[1]) is not None]
+        pw = [num(r[3]) for r in self.rows if num(r[3]) is not None]
+        load = [s for s, p in zip(sm, pw) if p is not None and p > 250.0] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(load) if load else None,
+                "sm_max_mhz": max(num(r[2]) or 0 for r in self.rows), "reasons": reasons,
+                "samples": len(self.rows), "samples_under_load": len(load),
+                "power_w_max": max(pw) if pw else None}
+
+
+# ------------------------------------------------------------------ CPU oracle leg
+
+_ORACLE_W = {}
+
+
+def _oracle_weights(K, N):
+    """Config-3-shaped weights for the CPU oracle leg (same recipe: W ~ N(0,1/K), g ~ U[0.5,1.5])."""
+    if (K, N) not in _ORACLE_W:
+        from synth import gen_layer
+        Wt, g, _, _ = gen_layer(1, N, K, "bf16")
+        _ORACLE_W[(K, N)] = (Wt.T.astype("float64"), g)
+    return _ORACLE_W[(K, N)]
+
+
+def oracle_sample_rate(M_rows: int, K: int, N: int, seed: int = 0, min_seconds: float = 10.0, max_rows=None):
+    """Time the fp64 oracle (unfused RMSNorm -> linear, oracle/flashnorm_oracle.py) on a bounded
+    sample of rows of the workload; returns (TFLOP/s, rows, seconds, threads)."""
+    import numpy as np
+    from oracle import flashnorm_oracle as O
+    from synth import gen_activations
+    W, g = _oracle_weights(K, N)
+    a = gen_activations(seed, M_rows, K, "normal", "bf16")
+    threads = os.cpu_count() or 1
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        if info:
+            threads = max(int(i.get("num_threads", 1)) for i in info)
+    except Exception:
+        pass
+    rows = 0
+    t0 = time.perf_counter()
+    while True:
+        O.norm_linear(a[rows % M_rows: rows % M_rows + 1], W, g, None, None, 1e-5, "rmsnorm")
+        rows += 1
+        el = time.perf_counter() - t0
+        if (max_rows is not None and rows >= max_rows) or (max_rows is None and el >= min_seconds):
+            break
+    return 2.0 * rows * K * N / el / 1e12, rows, el, threads
+
+
+def run_reference(args, ws, rank):
+    if ws > 1 and rank != 0:
+        return
+    K, N = PREFILL["K"], PREFILL["N"]
+    # each step: a bounded sample of rows of the config-3 workload
+    rates, times = [], []
+    for i in range(args.warmup + args.steps):
+        r, rows, el, thr = oracle_sample_rate(8, K, N, seed=i, min_seconds=0.0, max_rows=4)
+        if i >= args.warmup:
+            rates.append(r)
+            times.append(el)
+    value = sum(2.0 * 4 * K * N for _ in rates) / sum(times) / 1e12
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "llama3-8b-prefill rmsnorm+ffn gate||up (config 3), 4-row sample per step",
+                   "M": PREFILL["M"], "K": K, "N": N},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": thr, "kind": "oracle",
+                         "sample": f"4 of {PREFILL['M']} rows per step, fp64 numpy, full N={N}"},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU leg
+
+def run_ours(args, ws, rank, local):
+    import torch
+    import paper_2407_09577_b200 as fn
+    from paper_2407_09577_b200 import build as fnbuild
+    from synth import device as SD
+
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (there is no CPU fallback)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if rank == 0:
+        fnbuild.build()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        dist.barrier()
+    fn.lib()
+    peaks, peaks_src = load_peaks()
+    M, K, N = PREFILL["M"], PREFILL["K"], PREFILL["N"]
+    assert N % (8 * ws) == 0
+    Nl = N // ws
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier_sync():
+        torch.cuda.synchronize(dev)
+        if ws > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def max_over_ranks(x):
+        if ws == 1:
+            return x
+        import torch.distributed as dist
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- workload: same seeds on every rank; rank p owns rows [p*Nl, (p+1)*Nl) of W*t
+    a = SD.activations(1, M, K, dev, torch.bfloat16)
+    Wt_full, g, _, _ = SD.layer(1, N, K, dev, torch.bfloat16)
+    Wt = Wt_full[rank * Nl:(rank + 1) * Nl].contiguous()
+    del Wt_full
+    Ws, cs = fn.fold_weights(Wt, g)
+    z = torch.empty((M, Nl), dtype=torch.bfloat16, device=dev)
+
+    clocks = ClockSampler(local if os.environ.get("CUDA_VISIBLE_DEVICES") is None else
+                          int(os.environ["CUDA_VISIBLE_DEVICES"].split(",")[local]))
+    clocks.start()
+    time.sleep(0.3)
+
+    # ---- prefill: the headline (device-resident inputs)
+    for _ in range(args.warmup):
+        fn.linear(a, Ws, cs, eps=1e-5, out=z)
+    barrier_sync()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    fn.reset_launch_count()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for i in range(args.steps):
+        ev[i][0].record(stream)
+        fn.linear(a, Ws, cs, eps=1e-5, out=z)
+        ev[i][1].record(stream)
+    t_end.record(stream)
+    launches = fn.launch_count()
+    barrier_sync()
+    total_ms = max_over_ranks(t_start.elapsed_time(t_end))
+    kern_ms = statistics.mean(s.elapsed_time(e) for s, e in ev)
+    flops_rank = 2.0 * M * K * Nl
+    value = flops_rank * ws * args.steps / (total_ms * 1e-3) / 1e12
+    achieved = flops_rank / (kern_ms * 1e-3) / 1e12
+    peak_tf = peaks.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"])
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("flashnorm_gemm_kernel")
+        except Exception:
+            traffic = None
+
+    extra = {}
+    if rank == 0 and ws == 1:
+        extra = measure_secondary(args, fn, torch, dev, stream, peaks, a, Ws, cs, g)
+
+    # ---- e2e: through the C ABI with HOST buffers, copies inside the timed region
+    a_host = a.cpu().pin_memory()
+    z_host = torch.empty((M, Nl), dtype=torch.bfloat16).pin_memory()
+    a_dev = torch.empty_like(a)
+    e2e_steps = max(3, min(args.steps, 10))
+    for _ in range(2):
+        fn.linear_from_host(a_host, Ws, cs, a_dev, z, z_host)
+    barrier_sync()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        fn.linear_from_host(a_host, Ws, cs, a_dev, z, z_host)
+    e1.record(stream)
+    barrier_sync()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1))
+    e2e_value = flops_rank * ws * e2e_steps / (e2e_ms * 1e-3) / 1e12
+
+    clocks.stop()
+    if rank != 0:
+        return
+    cpu = None
+    if ws == 1 and not args.no_cpu_baseline:
+        r, rows, el, thr = oracle_sample_rate(16, K, N, min_seconds=args.cpu_seconds)
+        cpu = {"value": r, "unit": "TFLOP/s", "cores": thr, "kind": "oracle",
+               "sample": f"{rows} rows of config 3 (K={K}, N={N}) through the fp64 unfused oracle, {el:.1f} s"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": "llama3-8b-prefill: RMSNorm + FFN gate||up (BASELINE config 3)",
+                   "M": M, "K": K, "N": N, "N_per_rank": Nl, "mode": "rmsnorm", "eps": 1e-5,
+                   "parallelism": f"column-sharded W* x{ws}" if ws > 1 else "single GPU",
+                   "l2": "inputs > L2 (W* 235 MB), no flush"},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+                     "frac": achieved / peak_tf, "traffic": traffic,
+                     "kernel": "flashnorm_gemm_kernel<MODE_RMS>",
+                     "peak_source": f"{peaks_src} bf16_tflops (burst, cuBLAS)"},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": "TFLOP/s", "h2d_bytes_per_step": M * K * 2,
+                "d2h_bytes_per_step": M * Nl * 2, "steps": e2e_steps},
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+    }
+    line.update(extra)
+    print(json.dumps(line), flush=True)
+
+
+def measure_secondary(args, fn, torch, dev, stream, peaks, a, Ws, cs, g):
+    """Decode (config 2) HBM GB/s, the unfused two-kernel variant, and the folds."""
+    from synth import device as SD
+    out = {}
+    hbm = peaks.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"])
+
+    def timed(fnc, steps, warm=3):
+        for _ in range(warm):
+            fnc(0)
+        torch.cuda.synchronize(dev)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        for i in range(steps):
+            fnc(i)
+        e.record(stream)
+        torch.cuda.synchronize(dev)
+        return s.elapsed_time(e) / steps
+
+    # decode: rotate 4 W* buffers (4 x 50 MB > L2) so every call streams from HBM
+    Wd = []
+    for r in range(4):
+        w, gd, _, _ = SD.layer(100 + r, DECODE_N, DECODE_K, dev, torch.bfloat16)
+        Wd.append(fn.fold_weights(w, gd)[0])
+        del w
+    dec = {}
+    for Mdec in (1, 16):
+        ad = SD.activations(7, Mdec, DECODE_K, dev, torch.bfloat16)
+        zd = torch.empty((Mdec, DECODE_N), dtype=torch.bfloat16, device=dev)
+        ms = timed(lambda i: fn.linear(ad, Wd[i % 4], None, eps=1e-5, out=zd), 400)
+        byts = DECODE_K * DECODE_N * 2 + Mdec * DECODE_K * 2 + Mdec * DECODE_N * 2
+        gbs = byts / (ms * 1e-3) / 1e9
+        # unfused: norm kernel + plain GEMV on the original weights (same W stream)
+        yd = torch.empty_like(ad)
+
+        def unf(i):
+            fn.baseline_norm(ad, g, None, eps=1e-5, out=yd)
+            fn.linear(yd, Wd[i % 4], None, mode="none", out=zd)
+        ms_u = timed(unf, 400)
+        dec[f"M{Mdec}"] = {"us": ms * 1e3, "GB/s": gbs, "frac_hbm": gbs / hbm, "bytes": byts,
+                           "unfused_us": ms_u * 1e3, "fusion_gain": ms_u / ms}
+    out["decode"] = {"workload": "llama3-8b decode: RMSNorm + QKV 4096->6144 (BASELINE config 2)",
+                     "unit": "GB/s", "peak_hbm_gbs": hbm, "l2": "4 rotating W* buffers (200 MB > L2)",
+                     "kernel": "flashnorm_gemv_kernel", **dec}
+    del Wd
+
+    # unfused prefill variant: RMSNorm kernel (bf16 y to HBM) then the same GEMM, norm disabled
+    M, K, N = a.shape[0], a.shape[1], Ws.shape[0]
+    y = torch.empty_like(a)
+    z = torch.empty((M, N), dtype=torch.bfloat16, device=dev)
+    ms_f = timed(lambda i: fn.linear(a, Ws, cs, eps=1e-5, out=z), 10)
+
+    def unf_p(i):
+        fn.baseline_norm(a, g, None, eps=1e-5, out=y)
+        fn.linear(y, Ws, None, mode="none", out=z)
+    ms_u = timed(unf_p, 10)
+    out["unfused_prefill"] = {"fused_ms": ms_f, "unfused_ms": ms_u, "fusion_gain": ms_u / ms_f,
+                              "what": "baseline_norm (y=RN(a*r*g)) -> flashnorm_linear(mode=none)"}
+
+    # folds (offline, once per weight load): config-3 W (235 MB in + 235 MB out)
+    Wf, gf, bf_, cf = SD.layer(5, N, K, dev, torch.bfloat16, with_b=True, with_c=True)
+    Wo = torch.empty_like(Wf)
+    co = torch.empty(N, dtype=torch.float32, device=dev)
+    ms_fold = timed(lambda i: fn.fold_weights(Wf, gf, bf_, cf, out=Wo, c_out=co), 10)
+    fb = 2 * N * K * 2 + 3 * K * 4 + 2 * N * 4
+    out["fold"] = {"fold_weights_us": ms_fold * 1e3, "GB/s": fb / (ms_fold * 1e-3) / 1e9,
+                   "frac_hbm": fb / (ms_fold * 1e-3) / 1e9 / hbm, "bytes": fb, "shape": [N, K]}
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        return
+    run_ours(args, ws, rank, local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

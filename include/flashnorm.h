@@ -1,0 +1,195 @@
+/*
+ * flashnorm.h — C ABI of the B200-native FlashNorm hot path (libflashnorm.so).
+ *
+ * FlashNorm (arXiv 2407.09577, /root/reference/PAPER.md) computes RMSNorm /
+ * LayerNorm / DyT followed by a linear layer as
+ *
+ *        z = (a · W*) · 1/RMSe(a) + c*                      (Fig 1(c))
+ *
+ * with the normalization weights folded into W* (Fig 1(b)), the
+ * norm bias folded into c* = c + b·W (Fig A) and LayerNorm's mean
+ * centering folded into the preceding layer V* (Fig B).  The
+ * per-token sum of squares is reduced IN PARALLEL with the contraction
+ * (Fig 8(c)).
+ *
+ * Conventions (all entry points)
+ * ------------------------------
+ *  - Every tensor pointer is a DEVICE pointer owned by the caller (except the
+ *    *_from_host entry point, which says so).  The library allocates no device
+ *    memory; it keeps only host-side caches (TMA descriptors).
+ *  - Matrices are dense row-major.  Weights use the nn.Linear storage layout
+ *    Wt[N][K] (K contiguous): the paper's W (K x N, y = x W) is
+ *    W[i][j] = Wt[j][i].  Activations a[M][K], outputs z[M][N].
+ *  - fn_dtype selects the storage type of the matrices (a, Wt, Wt*, V, V*, z).
+ *    Vectors g, b, c, c*, b_prev, b_prev* are always float32.
+ *  - Alignment: every matrix pointer 16-byte aligned; K % 8 == 0 and
+ *    N % 8 == 0 (bf16) / K % 4 == 0 and N % 4 == 0 (f32), else FN_ERR_ALIGN.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Every call is asynchronous on that stream and never synchronizes, except
+ *    flashnorm_linear_from_host (documented below).
+ *  - Errors are status codes; no exception crosses the ABI.  On error,
+ *    flashnorm_last_error() returns thread-local text naming the offending
+ *    shapes/values.  Shapes are never broadcast.
+ *  - Outputs never alias inputs.
+ */
+#ifndef FLASHNORM_H_
+#define FLASHNORM_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    FN_OK = 0,
+    FN_ERR_NULL = 1,         /* required pointer is NULL                          */
+    FN_ERR_SHAPE = 2,        /* non-positive or inconsistent size                 */
+    FN_ERR_DTYPE = 3,        /* unknown fn_dtype                                  */
+    FN_ERR_ALIGN = 4,        /* pointer not 16-B aligned / K, N not multiple of 8 */
+    FN_ERR_VALUE = 5,        /* eps < 0, non-finite eps/alpha, bad mode           */
+    FN_ERR_UNSUPPORTED = 6,  /* valid request this build does not implement       */
+    FN_ERR_CUDA = 7          /* CUDA runtime/driver failure (text has the reason) */
+} fn_status;
+
+typedef enum {
+    FN_RMSNORM = 0,    /* z = (a W*) * rsqrt(ssq/K + eps) + c*         PAPER.md:14,17,177 */
+    FN_LAYERNORM = 1,  /* same kernel math on an input already mean-centered by a
+                          V* folded with flashnorm_fold_mean_center     */
+    FN_DYT = 2,        /* z = tanh(alpha a) W* + c* (no deferral: tanh is not scale-
+                          commutative); reading c10 of DESIGN.md                          */
+    FN_NONE = 3        /* z = a W* + c* — plain linear layer: the upstream V* layer of
+                          config 4 and the GEMM half of the unfused baseline             */
+} fn_mode;
+
+typedef enum { FN_BF16 = 0, FN_F32 = 1 } fn_dtype;
+
+typedef enum {
+    FN_PATH_AUTO = 0,    /* M <= 16 (and M*K*2 <= 128 KiB): decode GEMV, else tcgen05 GEMM */
+    FN_PATH_GEMM = 1,    /* force the tcgen05/TMEM/TMA kernel (bf16 only)                   */
+    FN_PATH_GEMV = 2,    /* force the decode kernel (bf16, M <= 16)                         */
+    FN_PATH_SIMT = 3     /* the fp32 FFMA kernel (the only path for FN_F32)                 */
+} fn_path;
+
+/* --------------------------------------------------------------------------
+ * flashnorm_fold_weights — offline fold of g and b into W*, c*.
+ *   PAPER.md:25 (Fig A): c* = c + b·W with the ORIGINAL W, then
+ *   PAPER.md:16 (Fig 1(b)): W*_{i,j} = g_i · W_{i,j}.
+ *
+ *   Wt      [N][K] storage dtype, input.
+ *   g       [K] float32 or NULL (= ones);  b [K] float32 or NULL (= zeros);
+ *   c       [N] float32 or NULL (= zeros).
+ *   Wt_star [N][K] storage dtype, output.
+ *   c_star  [N] float32 output; may be NULL only if b == NULL and c == NULL.
+ *
+ *   fold_weights numerics (the contract the CPU mirror reproduces bit-exactly):
+ *     Wt_star[j][i] = RN_dtype( RN_f32( g_i * Wt[j][i] ) )
+ *     c_star[j]     = RN_f32( (double)c_j + S_j ), S_j = fp64 sum of the exact
+ *                     products b_i*Wt[j][i]: lane l (0..31) of row j's warp sums
+ *                     its 16-byte chunks q = l, l+32, ... ascending (elements
+ *                     ascending inside a chunk), then the 32 lane sums are
+ *                     combined by an xor butterfly 16,8,4,2,1.
+ * -------------------------------------------------------------------------- */
+fn_status flashnorm_fold_weights(const void* Wt, int64_t N, int64_t K, fn_dtype dtype,
+                                 const float* g, const float* b, const float* c,
+                                 void* Wt_star, float* c_star, void* stream);
+
+/* --------------------------------------------------------------------------
+ * flashnorm_fold_mean_center — offline fold of LayerNorm's mean centering into
+ * the preceding linear layer V.  PAPER.md:42-49 (§1.2, Fig B):
+ *   s_i = sum_j v_{i,j},  v*_{i,j} = v_{i,j} - s_i / n.
+ *   Paper V is d_in x n_out; storage Vt[n_out][d_in].  n = n_out (the width of
+ *   the LayerNorm that follows).  V's own bias: b_prev* = b_prev - mean(b_prev)
+ *   (paper silent; reading c7).
+ *
+ *   Vt          [n_out][d_in] storage dtype, input.
+ *   b_prev      [n_out] float32 or NULL;  b_prev_star [n_out] float32 output or
+ *               NULL (must be non-NULL iff b_prev is non-NULL).
+ *   Vt_star     [n_out][d_in] storage dtype, output.
+ *   workspace   device scratch of flashnorm_fold_mean_center_workspace_bytes()
+ *               bytes, 16-B aligned (fp64 partial column sums).
+ *
+ *   fold_mean_center numerics (mirrored bit-exactly on the CPU):
+ *     partial[c][i] = fp64 sum of Vt[j][i], j in [32c, 32c+32) ascending
+ *     s_i           = fp64 sum of partial[c][i], c ascending
+ *     Vt_star[j][i] = RN_dtype( RN_f32( (double)Vt[j][i] - s_i / (double)n_out ) )
+ *     b_prev_star_j = RN_f32( (double)b_prev_j - T / n_out ), T: 256 threads,
+ *                     thread t sums j = t, t+256, ... ascending (fp64), xor
+ *                     butterfly 16,8,4,2,1 per warp, then the 8 warp totals
+ *                     added in ascending order.
+ * -------------------------------------------------------------------------- */
+int64_t flashnorm_fold_mean_center_workspace_bytes(int64_t n_out, int64_t d_in);
+fn_status flashnorm_fold_mean_center(const void* Vt, int64_t n_out, int64_t d_in, fn_dtype dtype,
+                                     const float* b_prev, void* Vt_star, float* b_prev_star,
+                                     void* workspace, void* stream);
+
+/* --------------------------------------------------------------------------
+ * flashnorm_linear — the per-token hot path.  PAPER.md:17 (Fig 1(c)), with the
+ * RMS reduced in parallel with the contraction (Fig 8(c)):
+ *
+ *   rmsnorm / layernorm:  z[m][j] = RN( fma(acc[m][j], r_m, c*_j) ),
+ *                         acc = sum_k a[m][k] W*t[j][k]  (fp32 accumulate),
+ *                         r_m = rsqrt( ssq_m / K + eps ),  ssq_m = sum_k a[m][k]^2
+ *                         (eps inside the sqrt; scale BEFORE the
+ *                         bias).
+ *   dyt:                  z = RN( sum_k RN_dtype(tanh(alpha a[m][k])) W*t[j][k] + c*_j )
+ *   none:                 z = RN( sum_k a[m][k] W*t[j][k] + c*_j )
+ *
+ *   a       [M][K] storage dtype;  Wt_star [N][K];  c_star [N] float32 or NULL;
+ *   z       [M][N] storage dtype, output (must not alias a).
+ *   eps     >= 0 and finite (ignored for dyt/none);  alpha finite (dyt only).
+ *   M == 0 is a no-op returning FN_OK.  A row with ssq == 0 and eps == 0 yields
+ *   IEEE inf/NaN in that row (documented; not reported per row).
+ *   bf16: tcgen05 GEMM (prefill) or decode GEMV, chosen by M (FN_PATH_AUTO);
+ *   f32:  FFMA SIMT kernel (no TF32).
+ * -------------------------------------------------------------------------- */
+fn_status flashnorm_linear(const void* a, const void* Wt_star, const float* c_star,
+                           int64_t M, int64_t K, int64_t N, float eps, float alpha,
+                           fn_mode mode, fn_dtype dtype, void* z, void* stream);
+
+/* Same as flashnorm_linear with an explicit kernel choice (tests, benchmarks). */
+fn_status flashnorm_linear_ex(const void* a, const void* Wt_star, const float* c_star,
+                              int64_t M, int64_t K, int64_t N, float eps, float alpha,
+                              fn_mode mode, fn_dtype dtype, void* z, fn_path path, void* stream);
+
+/* End-to-end variant: a_host / z_host are HOST pointers (pinned memory for
+ * asynchronous copies); a_dev / z_dev are caller-owned device scratch of
+ * M*K / M*N elements.  Enqueues H2D(a) -> flashnorm_linear -> D2H(z) on
+ * `stream` and returns without synchronizing (the caller synchronizes the
+ * stream before reading z_host). */
+fn_status flashnorm_linear_from_host(const void* a_host, const void* Wt_star, const float* c_star,
+                                     int64_t M, int64_t K, int64_t N, float eps, float alpha,
+                                     fn_mode mode, fn_dtype dtype, void* a_dev, void* z_dev,
+                                     void* z_host, void* stream);
+
+/* --------------------------------------------------------------------------
+ * Measurement-only pieces (not the method): the unfused two-kernel baseline
+ * of BASELINE.json:5 — RMSNorm/LayerNorm writing y = RN(a*r*g + b) (Fig 1(a)
+ * first half), then flashnorm_linear(mode = FN_NONE) on the ORIGINAL W.
+ * -------------------------------------------------------------------------- */
+fn_status flashnorm_baseline_norm(const void* a, const float* g, const float* b,
+                                  int64_t M, int64_t K, float eps, fn_mode mode, float alpha,
+                                  fn_dtype dtype, void* y, void* stream);
+
+/* --------------------------------------------------------------------------
+ * Multi-GPU helper: after an all-gather of P column shards z_parts[P][M][N_local]
+ * (W* column-sharded, activations replicated), permute into
+ * z[M][P*N_local].  Pure data movement.
+ * -------------------------------------------------------------------------- */
+fn_status flashnorm_gather_columns(const void* z_parts, int64_t P, int64_t M, int64_t N_local,
+                                   fn_dtype dtype, void* z, void* stream);
+
+/* Diagnostics. */
+const char* flashnorm_status_string(fn_status s);
+const char* flashnorm_last_error(void);
+/* Number of kernels this library launched on the calling thread since the last
+ * reset (used by bench.py's gpu_launches count). */
+int64_t flashnorm_launch_count(void);
+void flashnorm_reset_launch_count(void);
+/* Library version string: "flashnorm-b200 <semver> sm_100a". */
+const char* flashnorm_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLASHNORM_H_ */

@@ -1,0 +1,268 @@
+"""paper_2407_09577_b200 — B200-native FlashNorm (arXiv 2407.09577) hot path.
+
+Thin ctypes binding over ``libflashnorm.so`` (the C ABI in include/flashnorm.h).
+The names follow the ABI:
+
+* :func:`fold_weights`      — W* = diag(g) W, c* = c + b W
+* :func:`fold_mean_center`  — V*_{ij} = V_{ij} - s_i / n
+* :func:`linear`            — z = (a W*) / RMSe(a) + c*
+* :func:`baseline_norm`     — measurement-only unfused normalization (Fig 1(a))
+* :func:`gather_columns`    — column-shard permute after an all-gather
+
+This module only marshals arguments: every step runs in the library's CUDA
+kernels.  PyTorch supplies device memory and streams.  There is no CPU
+fallback: a missing library or a non-CUDA tensor raises :class:`FlashNormError`.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Tuple
+
+__all__ = [
+    "FlashNormError", "lib", "lib_path", "fold_weights", "fold_mean_center", "fold_mean_center_workspace_bytes",
+    "linear", "linear_from_host", "baseline_norm", "gather_columns", "launch_count", "reset_launch_count",
+    "version", "MODES", "PATHS", "EXPORTS",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+lib_path = os.path.join(_HERE, "libflashnorm.so")
+
+MODES = {"rmsnorm": 0, "layernorm": 1, "dyt": 2, "none": 3}
+PATHS = {"auto": 0, "gemm": 1, "gemv": 2, "simt": 3}
+_DT_BF16, _DT_F32 = 0, 1
+
+# every symbol include/flashnorm.h declares
+EXPORTS = [
+    "flashnorm_fold_weights", "flashnorm_fold_mean_center_workspace_bytes", "flashnorm_fold_mean_center",
+    "flashnorm_linear", "flashnorm_linear_ex", "flashnorm_linear_from_host", "flashnorm_baseline_norm",
+    "flashnorm_gather_columns", "flashnorm_status_string", "flashnorm_last_error", "flashnorm_launch_count",
+    "flashnorm_reset_launch_count", "flashnorm_version",
+]
+
+
+class FlashNormError(RuntimeError):
+    """A libflashnorm call returned a non-OK fn_status (or the library is missing)."""
+
+    def __init__(self, status: int, name: str, msg: str):
+        super().__init__(f"{name}: {msg}")
+        self.status = status
+
+
+_LIB = None
+_vp, _i64, _f32, _int = ctypes.c_void_p, ctypes.c_int64, ctypes.c_float, ctypes.c_int
+
+
+def lib() -> ctypes.CDLL:
+    """Load libflashnorm.so (built in-tree by paper_2407_09577_b200.build)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(lib_path):
+        raise FlashNormError(-1, "load", f"{lib_path} not found: run `python -m paper_2407_09577_b200.build` "
+                                         "(there is no CPU fallback)")
+    L = ctypes.CDLL(lib_path)
+    sig = {
+        "flashnorm_fold_weights": [_vp, _i64, _i64, _int, _vp, _vp, _vp, _vp, _vp, _vp],
+        "flashnorm_fold_mean_center_workspace_bytes": [_i64, _i64],
+        "flashnorm_fold_mean_center": [_vp, _i64, _i64, _int, _vp, _vp, _vp, _vp, _vp],
+        "flashnorm_linear": [_vp, _vp, _vp, _i64, _i64, _i64, _f32, _f32, _int, _int, _vp, _vp],
+        "flashnorm_linear_ex": [_vp, _vp, _vp, _i64, _i64, _i64, _f32, _f32, _int, _int, _vp, _int, _vp],
+        "flashnorm_linear_from_host": [_vp, _vp, _vp, _i64, _i64, _i64, _f32, _f32, _int, _int, _vp, _vp, _vp,
+                                       _vp],
+        "flashnorm_baseline_norm": [_vp, _vp, _vp, _i64, _i64, _f32, _int, _f32, _int, _vp, _vp],
+        "flashnorm_gather_columns": [_vp, _i64, _i64, _i64, _int, _vp, _vp],
+        "flashnorm_status_string": [_int],
+        "flashnorm_last_error": [],
+        "flashnorm_launch_count": [],
+        "flashnorm_reset_launch_count": [],
+        "flashnorm_version": [],
+    }
+    for name, args in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = _int
+    L.flashnorm_fold_mean_center_workspace_bytes.restype = _i64
+    L.flashnorm_launch_count.restype = _i64
+    L.flashnorm_reset_launch_count.restype = None
+    for name in ("flashnorm_status_string", "flashnorm_last_error", "flashnorm_version"):
+        getattr(L, name).restype = ctypes.c_char_p
+    _LIB = L
+    return L
+
+
+def _check(status: int, name: str):
+    if status != 0:
+        L = lib()
+        raise FlashNormError(status, name, f"{L.flashnorm_status_string(status).decode()}: "
+                                           f"{L.flashnorm_last_error().decode()}")
+
+
+# ------------------------------------------------------------------ torch marshalling
+
+def _torch():
+    import torch
+    return torch
+
+
+def _dtype_code(t) -> int:
+    torch = _torch()
+    if t.dtype == torch.bfloat16:
+        return _DT_BF16
+    if t.dtype == torch.float32:
+        return _DT_F32
+    raise FlashNormError(3, "dtype", f"unsupported tensor dtype {t.dtype} (bf16 or f32)")
+
+
+def _dev(t, name: str):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise FlashNormError(1, name, f"{name} must be a CUDA tensor (no CPU fallback), got device {t.device}")
+    if not t.is_contiguous():
+        raise FlashNormError(2, name, f"{name} must be contiguous, got strides {tuple(t.stride())}")
+    return t
+
+
+def _vec(t, name: str, n: int):
+    torch = _torch()
+    if t is None:
+        return None
+    _dev(t, name)
+    if t.dtype != torch.float32 or t.dim() != 1 or t.shape[0] != n:
+        raise FlashNormError(2, name, f"{name} must be float32[{n}], got {t.dtype}{list(t.shape)}")
+    return t
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(t):
+    torch = _torch()
+    return ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+
+
+# ------------------------------------------------------------------ public API
+
+def fold_weights(Wt, g=None, b=None, c=None, out=None, c_out=None):
+    """Fold norm weights g and norm bias b into (W*t, c*).  Wt: [N, K] (nn.Linear layout).
+
+    PAPER.md:25 (c* = c + b W, original W) then PAPER.md:16 (W*_ij = g_i W_ij).
+    Returns (Wt_star [N, K] same dtype, c_star float32[N] or None).
+    """
+    torch = _torch()
+    _dev(Wt, "Wt")
+    if Wt.dim() != 2:
+        raise FlashNormError(2, "fold_weights", f"Wt must be 2-D [N, K], got {list(Wt.shape)}")
+    N, K = Wt.shape
+    g, b, c = _vec(g, "g", K), _vec(b, "b", K), _vec(c, "c", N)
+    Ws = out if out is not None else torch.empty_like(Wt)
+    cs = c_out
+    if cs is None and (b is not None or c is not None):
+        cs = torch.empty(N, dtype=torch.float32, device=Wt.device)
+    _check(lib().flashnorm_fold_weights(_ptr(Wt), N, K, _dtype_code(Wt), _ptr(g), _ptr(b), _ptr(c), _ptr(Ws),
+                                        _ptr(cs), _stream(Wt)), "fold_weights")
+    return Ws, cs
+
+
+def fold_mean_center_workspace_bytes(n_out: int, d_in: int) -> int:
+    return int(lib().flashnorm_fold_mean_center_workspace_bytes(n_out, d_in))
+
+
+def fold_mean_center(Vt, b_prev=None, out=None, workspace=None):
+    """Fold LayerNorm's mean centering into the preceding layer.  Vt: [n_out, d_in].
+
+    PAPER.md:42-49: v*_ij = v_ij - s_i/n; b_prev* = b_prev - mean(b_prev) (reading c7).
+    Returns (Vt_star, b_prev_star or None).
+    """
+    torch = _torch()
+    _dev(Vt, "Vt")
+    n_out, d_in = Vt.shape
+    b_prev = _vec(b_prev, "b_prev", n_out)
+    Vs = out if out is not None else torch.empty_like(Vt)
+    bs = torch.empty(n_out, dtype=torch.float32, device=Vt.device) if b_prev is not None else None
+    ws = workspace
+    if ws is None:
+        nbytes = fold_mean_center_workspace_bytes(n_out, d_in)
+        ws = torch.empty((nbytes + 15) // 16 * 2, dtype=torch.float64, device=Vt.device)
+    _check(lib().flashnorm_fold_mean_center(_ptr(Vt), n_out, d_in, _dtype_code(Vt), _ptr(b_prev), _ptr(Vs),
+                                            _ptr(bs), _ptr(ws), _stream(Vt)), "fold_mean_center")
+    return Vs, bs
+
+
+def linear(a, Wt_star, c_star=None, eps: float = 1e-5, mode: str = "rmsnorm", alpha: float = 0.5,
+           path: str = "auto", out=None):
+    """FlashNorm linear: z = (a W*) * rsqrt(mean(a^2) + eps) + c*  (PAPER.md:17, 177).
+
+    a: [M, K]; Wt_star: [N, K] (same dtype, bf16 or f32); c_star: float32[N] or None.
+    mode: rmsnorm | layernorm (input pre-centered via fold_mean_center) | dyt | none.
+    """
+    torch = _torch()
+    _dev(a, "a")
+    _dev(Wt_star, "Wt_star")
+    if a.dim() != 2 or Wt_star.dim() != 2 or a.shape[1] != Wt_star.shape[1]:
+        raise FlashNormError(2, "linear", f"a{list(a.shape)} and Wt_star{list(Wt_star.shape)}: need a[M,K], "
+                                          "Wt_star[N,K]")
+    if a.dtype != Wt_star.dtype:
+        raise FlashNormError(3, "linear", f"a is {a.dtype} but Wt_star is {Wt_star.dtype}")
+    M, K = a.shape
+    N = Wt_star.shape[0]
+    c_star = _vec(c_star, "c_star", N)
+    z = out if out is not None else torch.empty((M, N), dtype=a.dtype, device=a.device)
+    st = lib().flashnorm_linear_ex(_ptr(a), _ptr(Wt_star), _ptr(c_star), M, K, N, float(eps), float(alpha),
+                                   MODES[mode], _dtype_code(a), _ptr(z), PATHS[path], _stream(a))
+    _check(st, "linear")
+    return z
+
+
+def linear_from_host(a_host, Wt_star, c_star, a_dev, z_dev, z_host, eps: float = 1e-5, mode: str = "rmsnorm",
+                     alpha: float = 0.5, stream=None):
+    """End-to-end call through the C ABI with HOST buffers (pinned a_host / z_host).
+
+    Enqueues H2D(a) -> flashnorm_linear -> D2H(z) on the current stream (no sync).
+    """
+    torch = _torch()
+    M, K = a_host.shape
+    N = Wt_star.shape[0]
+    st = stream if stream is not None else torch.cuda.current_stream(Wt_star.device)
+    s = lib().flashnorm_linear_from_host(_ptr(a_host), _ptr(Wt_star), _ptr(c_star), M, K, N, float(eps),
+                                         float(alpha), MODES[mode], _dtype_code(Wt_star), _ptr(a_dev), _ptr(z_dev),
+                                         _ptr(z_host), ctypes.c_void_p(st.cuda_stream))
+    _check(s, "linear_from_host")
+    return z_host
+
+
+def baseline_norm(a, g=None, b=None, eps: float = 1e-5, mode: str = "rmsnorm", alpha: float = 0.5, out=None):
+    """Unfused normalization y = RN(Norm(a) * g + b) (measurement-only, Fig 1(a))."""
+    torch = _torch()
+    _dev(a, "a")
+    M, K = a.shape
+    g, b = _vec(g, "g", K), _vec(b, "b", K)
+    y = out if out is not None else torch.empty_like(a)
+    _check(lib().flashnorm_baseline_norm(_ptr(a), _ptr(g), _ptr(b), M, K, float(eps), MODES[mode], float(alpha),
+                                         _dtype_code(a), _ptr(y), _stream(a)), "baseline_norm")
+    return y
+
+
+def gather_columns(z_parts, out=None):
+    """z_parts [P, M, N_local] (all-gathered column shards) -> z [M, P*N_local]."""
+    torch = _torch()
+    _dev(z_parts, "z_parts")
+    P, M, Nl = z_parts.shape
+    z = out if out is not None else torch.empty((M, P * Nl), dtype=z_parts.dtype, device=z_parts.device)
+    _check(lib().flashnorm_gather_columns(_ptr(z_parts), P, M, Nl, _dtype_code(z_parts), _ptr(z),
+                                          _stream(z_parts)), "gather_columns")
+    return z
+
+
+def launch_count() -> int:
+    return int(lib().flashnorm_launch_count())
+
+
+def reset_launch_count() -> None:
+    lib().flashnorm_reset_launch_count()
+
+
+def version() -> str:
+    return lib().flashnorm_version().decode()

@@ -1,0 +1,337 @@
+// api.cu — the extern "C" boundary declared in include/flashnorm.h.
+//
+// Validation (shapes, alignment, values -> fn_status + thread-local text),
+// kernel selection, a mutex-guarded cache of TMA descriptors (cuTensorMapEncodeTiled
+// obtained through cudaGetDriverEntryPoint, so the library never links libcuda),
+// and the launch counter used by bench.py.
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "../../include/flashnorm.h"
+#include "kernels.h"
+
+namespace {
+
+thread_local char g_err[512] = "";
+thread_local int64_t g_launches = 0;
+
+fn_status fail(fn_status s, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return s;
+}
+
+fn_status cuda_fail(cudaError_t e, const char* where) {
+  return fail(FN_ERR_CUDA, "%s: %s (%s)", where, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int elem_bytes(fn_dtype dt) { return dt == FN_BF16 ? 2 : 4; }
+
+fn_status check_dtype(fn_dtype dt) {
+  if (dt != FN_BF16 && dt != FN_F32) return fail(FN_ERR_DTYPE, "unknown fn_dtype %d", (int)dt);
+  return FN_OK;
+}
+
+// K and N must allow 16-byte vector access of every row
+fn_status check_vec(const char* what, int64_t v, fn_dtype dt) {
+  const int64_t q = dt == FN_BF16 ? 8 : 4;
+  if (v % q != 0)
+    return fail(FN_ERR_ALIGN, "%s = %lld must be a multiple of %lld for %s (16-byte rows)", what, (long long)v,
+                (long long)q, dt == FN_BF16 ? "bf16" : "f32");
+  return FN_OK;
+}
+
+fn_status check_ptr16(const char* what, const void* p) {
+  if (p != nullptr && !aligned16(p)) return fail(FN_ERR_ALIGN, "%s = %p is not 16-byte aligned", what, p);
+  return FN_OK;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// ---------------------------------------------------------------- TMA descriptors
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fnp = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fnp = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fnp;
+}
+
+std::mutex g_tmap_mu;
+std::map<std::tuple<uintptr_t, int64_t, int64_t, int>, CUtensorMap> g_tmaps;
+
+// row-major bf16 [rows][cols], box = 64 (cols, 128 B, SW128) x box_rows
+fn_status get_tmap(const void* ptr, int64_t rows, int64_t cols, int box_rows, CUtensorMap* out) {
+  const auto key = std::make_tuple(reinterpret_cast<uintptr_t>(ptr), rows, cols, box_rows);
+  std::lock_guard<std::mutex> lk(g_tmap_mu);
+  auto it = g_tmaps.find(key);
+  if (it != g_tmaps.end()) {
+    *out = it->second;
+    return FN_OK;
+  }
+  auto enc = encode_fn();
+  if (enc == nullptr) return fail(FN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver entry point)");
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(FN_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) for [%lld x %lld] box %d", (int)r,
+                (long long)rows, (long long)cols, box_rows);
+  if (g_tmaps.size() > 4096) g_tmaps.clear();
+  g_tmaps.emplace(key, m);
+  *out = m;
+  return FN_OK;
+}
+
+int kernel_mode(fn_mode m) {
+  switch (m) {
+    case FN_RMSNORM:
+    case FN_LAYERNORM: return fn::MODE_RMS;
+    case FN_DYT: return fn::MODE_DYT;
+    default: return fn::MODE_NONE;
+  }
+}
+
+fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, int64_t M, int64_t K, int64_t N,
+                      float eps, float alpha, fn_mode mode, fn_dtype dtype, void* z, fn_path path,
+                      cudaStream_t stream) {
+  fn_status s;
+  if ((s = check_dtype(dtype)) != FN_OK) return s;
+  if (mode < FN_RMSNORM || mode > FN_NONE) return fail(FN_ERR_VALUE, "unknown fn_mode %d", (int)mode);
+  if (M < 0 || K <= 0 || N <= 0)
+    return fail(FN_ERR_SHAPE, "a[%lld x %lld], Wt_star[%lld x %lld]: sizes must be positive (M >= 0)",
+                (long long)M, (long long)K, (long long)N, (long long)K);
+  if (M > INT32_MAX || K > INT32_MAX || N > INT32_MAX)
+    return fail(FN_ERR_SHAPE, "dimension exceeds int32 range: M=%lld K=%lld N=%lld", (long long)M, (long long)K,
+                (long long)N);
+  if (a == nullptr || Wt_star == nullptr || z == nullptr)
+    return fail(FN_ERR_NULL, "a=%p Wt_star=%p z=%p: required pointer is NULL", a, Wt_star, z);
+  if ((s = check_vec("K", K, dtype)) != FN_OK) return s;
+  if ((s = check_vec("N", N, dtype)) != FN_OK) return s;
+  if ((s = check_ptr16("a", a)) != FN_OK || (s = check_ptr16("Wt_star", Wt_star)) != FN_OK ||
+      (s = check_ptr16("z", z)) != FN_OK || (s = check_ptr16("c_star", c_star)) != FN_OK)
+    return s;
+  if ((mode == FN_RMSNORM || mode == FN_LAYERNORM) && (!(eps >= 0.0f) || !std::isfinite(eps)))
+    return fail(FN_ERR_VALUE, "eps = %g must be finite and >= 0", (double)eps);
+  if (mode == FN_DYT && !std::isfinite(alpha)) return fail(FN_ERR_VALUE, "alpha = %g must be finite", (double)alpha);
+  if (a == z) return fail(FN_ERR_VALUE, "z must not alias a");
+  if (M == 0) return FN_OK;
+  const int km = kernel_mode(mode);
+
+  if (dtype == FN_F32) {
+    if (path != FN_PATH_AUTO && path != FN_PATH_SIMT)
+      return fail(FN_ERR_UNSUPPORTED, "f32 supports only the SIMT path (path=%d)", (int)path);
+    cudaError_t e = fn::launch_linear_f32(static_cast<const float*>(a), static_cast<const float*>(Wt_star), c_star,
+                                          static_cast<float*>(z), (int)M, (int)K, (int)N, eps, alpha, km, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "linear_f32");
+    ++g_launches;
+    return FN_OK;
+  }
+
+  const bool gemv_ok = M <= fn::GEMV_MAX_M && fn::gemv_smem_bytes((int)M, (int)K) <= 200 * 1024;
+  if (path == FN_PATH_SIMT) return fail(FN_ERR_UNSUPPORTED, "SIMT path is f32-only");
+  if (path == FN_PATH_GEMV && !gemv_ok)
+    return fail(FN_ERR_UNSUPPORTED, "decode path needs M <= 16 and M*K*2 <= ~192 KiB (M=%lld K=%lld)",
+                (long long)M, (long long)K);
+  const bool use_gemv = path == FN_PATH_GEMV || (path == FN_PATH_AUTO && gemv_ok);
+  if (use_gemv) {
+    cudaError_t e = fn::launch_gemv(static_cast<const __nv_bfloat16*>(a), static_cast<const __nv_bfloat16*>(Wt_star),
+                                    c_star, static_cast<__nv_bfloat16*>(z), (int)M, (int)K, (int)N, eps, alpha, km,
+                                    num_sms(), stream);
+    if (e != cudaSuccess) return cuda_fail(e, "gemv");
+    ++g_launches;
+    return FN_OK;
+  }
+  CUtensorMap ta, tb;
+  if ((s = get_tmap(a, M, K, 128, &ta)) != FN_OK) return s;
+  if ((s = get_tmap(Wt_star, N, K, 256, &tb)) != FN_OK) return s;
+  fn::GemmParams p;
+  p.M = (int)M;
+  p.N = (int)N;
+  p.K = (int)K;
+  p.num_m_blocks = (int)((M + 127) / 128);
+  p.num_n_blocks = (int)((N + 255) / 256);
+  p.num_tiles = p.num_m_blocks * p.num_n_blocks;
+  p.num_k_blocks = (int)((K + 63) / 64);
+  p.eps = eps;
+  p.alpha = alpha;
+  p.cstar = c_star;
+  p.z = static_cast<__nv_bfloat16*>(z);
+  cudaError_t e = fn::launch_gemm(ta, tb, p, km, num_sms(), stream);
+  if (e != cudaSuccess) return cuda_fail(e, "gemm_sm100");
+  ++g_launches;
+  return FN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+fn_status flashnorm_fold_weights(const void* Wt, int64_t N, int64_t K, fn_dtype dtype, const float* g,
+                                 const float* b, const float* c, void* Wt_star, float* c_star, void* stream) {
+  fn_status s;
+  if ((s = check_dtype(dtype)) != FN_OK) return s;
+  if (N <= 0 || K <= 0) return fail(FN_ERR_SHAPE, "Wt[%lld x %lld]: sizes must be positive", (long long)N, (long long)K);
+  if (Wt == nullptr || Wt_star == nullptr) return fail(FN_ERR_NULL, "Wt=%p Wt_star=%p: NULL", Wt, Wt_star);
+  if ((b != nullptr || c != nullptr) && c_star == nullptr)
+    return fail(FN_ERR_NULL, "c_star is NULL but b=%p / c=%p given", (const void*)b, (const void*)c);
+  if ((s = check_vec("K", K, dtype)) != FN_OK) return s;
+  if ((s = check_ptr16("Wt", Wt)) != FN_OK || (s = check_ptr16("Wt_star", Wt_star)) != FN_OK ||
+      (s = check_ptr16("g", g)) != FN_OK || (s = check_ptr16("b", b)) != FN_OK)
+    return s;
+  if (Wt == Wt_star) return fail(FN_ERR_VALUE, "Wt_star must not alias Wt");
+  cudaError_t e = fn::launch_fold_weights(Wt, N, K, dtype == FN_BF16 ? 0 : 1, g, b, c, Wt_star, c_star,
+                                          static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fold_weights");
+  ++g_launches;
+  return FN_OK;
+}
+
+int64_t flashnorm_fold_mean_center_workspace_bytes(int64_t n_out, int64_t d_in) {
+  if (n_out <= 0 || d_in <= 0) return 0;
+  return fn::fold_mean_center_workspace(n_out, d_in);
+}
+
+fn_status flashnorm_fold_mean_center(const void* Vt, int64_t n_out, int64_t d_in, fn_dtype dtype,
+                                     const float* b_prev, void* Vt_star, float* b_prev_star, void* workspace,
+                                     void* stream) {
+  fn_status s;
+  if ((s = check_dtype(dtype)) != FN_OK) return s;
+  if (n_out <= 0 || d_in <= 0)
+    return fail(FN_ERR_SHAPE, "Vt[%lld x %lld]: sizes must be positive", (long long)n_out, (long long)d_in);
+  if (Vt == nullptr || Vt_star == nullptr || workspace == nullptr)
+    return fail(FN_ERR_NULL, "Vt=%p Vt_star=%p workspace=%p: NULL", Vt, Vt_star, workspace);
+  if ((b_prev == nullptr) != (b_prev_star == nullptr))
+    return fail(FN_ERR_NULL, "b_prev=%p and b_prev_star=%p must be both NULL or both set", (const void*)b_prev,
+                (const void*)b_prev_star);
+  if ((s = check_vec("d_in", d_in, dtype)) != FN_OK) return s;
+  if ((s = check_ptr16("Vt", Vt)) != FN_OK || (s = check_ptr16("Vt_star", Vt_star)) != FN_OK ||
+      (s = check_ptr16("workspace", workspace)) != FN_OK)
+    return s;
+  if (Vt == Vt_star) return fail(FN_ERR_VALUE, "Vt_star must not alias Vt");
+  int launches = 0;
+  cudaError_t e = fn::launch_fold_mean_center(Vt, n_out, d_in, dtype == FN_BF16 ? 0 : 1, b_prev, Vt_star,
+                                              b_prev_star, workspace, static_cast<cudaStream_t>(stream), &launches);
+  if (e != cudaSuccess) return cuda_fail(e, "fold_mean_center");
+  g_launches += launches;
+  return FN_OK;
+}
+
+fn_status flashnorm_linear(const void* a, const void* Wt_star, const float* c_star, int64_t M, int64_t K, int64_t N,
+                           float eps, float alpha, fn_mode mode, fn_dtype dtype, void* z, void* stream) {
+  return linear_impl(a, Wt_star, c_star, M, K, N, eps, alpha, mode, dtype, z, FN_PATH_AUTO,
+                     static_cast<cudaStream_t>(stream));
+}
+
+fn_status flashnorm_linear_ex(const void* a, const void* Wt_star, const float* c_star, int64_t M, int64_t K,
+                              int64_t N, float eps, float alpha, fn_mode mode, fn_dtype dtype, void* z, fn_path path,
+                              void* stream) {
+  if (path < FN_PATH_AUTO || path > FN_PATH_SIMT) return fail(FN_ERR_VALUE, "unknown fn_path %d", (int)path);
+  return linear_impl(a, Wt_star, c_star, M, K, N, eps, alpha, mode, dtype, z, path,
+                     static_cast<cudaStream_t>(stream));
+}
+
+fn_status flashnorm_linear_from_host(const void* a_host, const void* Wt_star, const float* c_star, int64_t M,
+                                     int64_t K, int64_t N, float eps, float alpha, fn_mode mode, fn_dtype dtype,
+                                     void* a_dev, void* z_dev, void* z_host, void* stream) {
+  fn_status s;
+  if ((s = check_dtype(dtype)) != FN_OK) return s;
+  if (a_host == nullptr || z_host == nullptr || a_dev == nullptr || z_dev == nullptr)
+    return fail(FN_ERR_NULL, "a_host=%p z_host=%p a_dev=%p z_dev=%p: NULL", a_host, z_host, a_dev, z_dev);
+  if (M < 0 || K <= 0 || N <= 0) return fail(FN_ERR_SHAPE, "M=%lld K=%lld N=%lld", (long long)M, (long long)K, (long long)N);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t eb = (size_t)elem_bytes(dtype);
+  cudaError_t e = cudaMemcpyAsync(a_dev, a_host, (size_t)M * K * eb, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return cuda_fail(e, "H2D a");
+  if ((s = linear_impl(a_dev, Wt_star, c_star, M, K, N, eps, alpha, mode, dtype, z_dev, FN_PATH_AUTO, st)) != FN_OK)
+    return s;
+  e = cudaMemcpyAsync(z_host, z_dev, (size_t)M * N * eb, cudaMemcpyDeviceToHost, st);
+  if (e != cudaSuccess) return cuda_fail(e, "D2H z");
+  return FN_OK;
+}
+
+fn_status flashnorm_baseline_norm(const void* a, const float* g, const float* b, int64_t M, int64_t K, float eps,
+                                  fn_mode mode, float alpha, fn_dtype dtype, void* y, void* stream) {
+  fn_status s;
+  if ((s = check_dtype(dtype)) != FN_OK) return s;
+  if (M < 0 || K <= 0) return fail(FN_ERR_SHAPE, "a[%lld x %lld]: bad sizes", (long long)M, (long long)K);
+  if (a == nullptr || y == nullptr) return fail(FN_ERR_NULL, "a=%p y=%p: NULL", a, y);
+  if (mode == FN_NONE) return fail(FN_ERR_VALUE, "baseline_norm needs a normalization mode");
+  if ((mode == FN_RMSNORM || mode == FN_LAYERNORM) && (!(eps >= 0.0f) || !std::isfinite(eps)))
+    return fail(FN_ERR_VALUE, "eps = %g must be finite and >= 0", (double)eps);
+  if (M == 0) return FN_OK;
+  const int kind = mode == FN_RMSNORM ? 0 : mode == FN_LAYERNORM ? 1 : 2;
+  cudaError_t e = fn::launch_baseline_norm(a, g, b, M, K, eps, kind, alpha, dtype == FN_BF16 ? 0 : 1, y,
+                                           static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "baseline_norm");
+  ++g_launches;
+  return FN_OK;
+}
+
+fn_status flashnorm_gather_columns(const void* z_parts, int64_t P, int64_t M, int64_t N_local, fn_dtype dtype, void* z,
+                                   void* stream) {
+  fn_status s;
+  if ((s = check_dtype(dtype)) != FN_OK) return s;
+  if (P <= 0 || M < 0 || N_local <= 0)
+    return fail(FN_ERR_SHAPE, "z_parts[%lld][%lld][%lld]: bad sizes", (long long)P, (long long)M, (long long)N_local);
+  if (z_parts == nullptr || z == nullptr) return fail(FN_ERR_NULL, "z_parts=%p z=%p: NULL", z_parts, z);
+  if ((s = check_vec("N_local", N_local, dtype)) != FN_OK) return s;
+  if ((s = check_ptr16("z_parts", z_parts)) != FN_OK || (s = check_ptr16("z", z)) != FN_OK) return s;
+  if (M == 0) return FN_OK;
+  cudaError_t e = fn::launch_gather_columns(z_parts, P, M, N_local, elem_bytes(dtype), z,
+                                            static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "gather_columns");
+  ++g_launches;
+  return FN_OK;
+}
+
+const char* flashnorm_status_string(fn_status s) {
+  switch (s) {
+    case FN_OK: return "FN_OK";
+    case FN_ERR_NULL: return "FN_ERR_NULL";
+    case FN_ERR_SHAPE: return "FN_ERR_SHAPE";
+    case FN_ERR_DTYPE: return "FN_ERR_DTYPE";
+    case FN_ERR_ALIGN: return "FN_ERR_ALIGN";
+    case FN_ERR_VALUE: return "FN_ERR_VALUE";
+    case FN_ERR_UNSUPPORTED: return "FN_ERR_UNSUPPORTED";
+    case FN_ERR_CUDA: return "FN_ERR_CUDA";
+  }
+  return "FN_ERR_UNKNOWN";
+}
+
+const char* flashnorm_last_error(void) { return g_err; }
+int64_t flashnorm_launch_count(void) { return g_launches; }
+void flashnorm_reset_launch_count(void) { g_launches = 0; }
+const char* flashnorm_version(void) { return "flashnorm-b200 0.1.0 sm_100a"; }
+
+}  // extern "C"

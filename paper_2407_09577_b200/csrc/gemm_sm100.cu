@@ -1,0 +1,295 @@
+// gemm_sm100.cu — K3: the prefill FlashNorm GEMM for sm_100a (tcgen05 + TMEM + TMA).
+//
+//   z[m][j] = RN( fma( sum_k a[m][k] W*t[j][k],  r_m,  c*_j ) )
+//   r_m     = rsqrt( ssq_m / K + eps ),  ssq_m = sum_k a[m][k]^2
+//
+// PAPER.md:17 (Fig 1(c), deferred normalization, scale before bias) and
+// PAPER.md:20/154 (Fig 8(c)): the matrix unit runs the contraction while a
+// separate "vector unit" computes the RMS.  On B200 the matrix unit is the
+// tcgen05 tensor core fed by TMA, and the vector unit is a warp group that
+// squares the SAME shared-memory A tiles the MMA is consuming; the epilogue
+// applies the deferred scale while the tensor core already accumulates the
+// next tile into the other TMEM buffer ("scaling in parallel to the matrix
+// unit").
+//
+// Persistent, warp-specialized, one CTA per SM (384 threads):
+//   warp 0      TMA producer (one elected lane): A[128x64] + B[256x64] per stage
+//   warp 1      MMA issuer  (one elected lane): 4 x tcgen05.mma 128x256x16 per stage
+//   warp 2      TMEM allocator (512 columns = 2 accumulator buffers of 256)
+//   warp 3      idle
+//   warps 4-7   side group: MODE_RMS  -> per-row sum of squares from the A stage
+//                           MODE_DYT  -> in-place tanh(alpha a) of the A stage (prologue)
+//                           MODE_NONE -> nothing
+//   warps 8-11  epilogue: TMEM -> regs -> *r + c* -> bf16 -> global
+#include "common.cuh"
+#include "kernels.h"
+
+namespace fn {
+
+namespace gemm {
+constexpr int BM = 128;
+constexpr int BN = 256;
+constexpr int BK = 64;  // 128 bytes of bf16 = one SW128 atom row
+constexpr int STAGES = 4;
+constexpr int A_STAGE = BM * BK * 2;  // 16 KiB
+constexpr int B_STAGE = BN * BK * 2;  // 32 KiB
+constexpr int THREADS = 384;
+constexpr int TMEM_COLS = 2 * BN;  // double-buffered fp32 accumulator
+constexpr int BAR_BYTES = 1024;
+constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * (A_STAGE + B_STAGE) + BAR_BYTES + 2 * BM * 4;
+}  // namespace gemm
+
+template <int MODE>
+__global__ void __launch_bounds__(gemm::THREADS, 1)
+    flashnorm_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                          GemmParams p) {
+  using namespace gemm;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_STAGE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE);
+  uint64_t* full = bars;                 // TMA landed            [STAGES]
+  uint64_t* empty = bars + STAGES;       // stage free            [STAGES]
+  uint64_t* ready = bars + 2 * STAGES;   // DyT: A transformed    [STAGES]
+  uint64_t* tfull = bars + 3 * STAGES;   // accumulator ready     [2]
+  uint64_t* tempty = tfull + 2;          // accumulator drained   [2]
+  uint64_t* sfull = tempty + 2;          // ssq ready             [2]
+  uint64_t* sempty = sfull + 2;          // ssq consumed          [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(sempty + 2);
+  float* ssq_buf = reinterpret_cast<float*>(smem + STAGES * (A_STAGE + B_STAGE) + BAR_BYTES);  // [2][BM]
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmap_a);
+    prefetch_tmap(&tmap_b);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1 + (MODE == MODE_RMS ? 4 : 0));
+      mbar_init(&ready[s], 4);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4);
+      mbar_init(&sfull[b], BM);
+      mbar_init(&sempty[b], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) {
+    tmem_alloc(tmem_holder, TMEM_COLS);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  const int num_tiles = p.num_tiles;
+  const int nkb = p.num_k_blocks;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int m_blk = tile % p.num_m_blocks;
+        const int n_blk = tile / p.num_m_blocks;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], A_STAGE + B_STAGE);
+          tma_load_2d(sA + stage * A_STAGE, &tmap_a, &full[stage], kb * BK, m_blk * BM, kEvictLast);
+          tma_load_2d(sB + stage * B_STAGE, &tmap_b, &full[stage], kb * BK, n_blk * BN, kEvictNormal);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (elect_one()) {
+      constexpr uint32_t idesc = make_idesc_bf16(BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+        const int as = local & 1;
+        const uint32_t aphase = (local >> 1) & 1;
+        mbar_wait(&tempty[as], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + as * BN;
+        for (int kb = 0; kb < nkb; ++kb) {
+          if (MODE == MODE_DYT) mbar_wait(&ready[stage], phase);
+          else mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t adesc = make_sw128_desc(smem_u32(sA + stage * A_STAGE));
+          const uint64_t bdesc = make_sw128_desc(smem_u32(sB + stage * B_STAGE));
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            // +32 bytes per K=16 step inside the 128-byte swizzle atom (encoded >> 4)
+            umma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(&tfull[as]);
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // ------------------------------------------------------------ side group
+    const int t = threadIdx.x - 128;  // row of the A tile owned by this thread
+    if (MODE == MODE_RMS) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          const uint4* row = reinterpret_cast<const uint4*>(sA + stage * A_STAGE + t * 128);
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const uint4 v = row[c ^ (t & 7)];  // swizzled order: conflict-free, sum is order-free
+            float x;
+            x = bf16lo(v.x); s0 = fmaf(x, x, s0);
+            x = bf16hi(v.x); s1 = fmaf(x, x, s1);
+            x = bf16lo(v.y); s2 = fmaf(x, x, s2);
+            x = bf16hi(v.y); s3 = fmaf(x, x, s3);
+            x = bf16lo(v.z); s0 = fmaf(x, x, s0);
+            x = bf16hi(v.z); s1 = fmaf(x, x, s1);
+            x = bf16lo(v.w); s2 = fmaf(x, x, s2);
+            x = bf16hi(v.w); s3 = fmaf(x, x, s3);
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        const int as = local & 1;
+        const uint32_t aphase = (local >> 1) & 1;
+        mbar_wait(&sempty[as], aphase ^ 1);
+        ssq_buf[as * BM + t] = (s0 + s1) + (s2 + s3);
+        mbar_arrive(&sfull[as]);
+      }
+    } else if (MODE == MODE_DYT) {
+      const float alpha = p.alpha;
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          uint4* row = reinterpret_cast<uint4*>(sA + stage * A_STAGE + t * 128);
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            uint4 v = row[c ^ (t & 7)];
+            uint32_t* w = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              // alpha*a in fp32, one RN to bf16, then the bf16x2 MUFU tanh (reading c14)
+              w[q] = tanh_approx_bf16x2(pack_bf16(bf16lo(w[q]) * alpha, bf16hi(w[q]) * alpha));
+            }
+            row[c ^ (t & 7)] = v;
+          }
+          fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&ready[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp >= 8) {
+    // ------------------------------------------------------------ epilogue
+    const uint32_t ew = warp - 8;  // == warp % 4: TMEM lane quarter this warp may access
+    int local = 0;
+    const float invK = 1.0f / static_cast<float>(p.K);
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+      const int m_blk = tile % p.num_m_blocks;
+      const int n_blk = tile / p.num_m_blocks;
+      const int as = local & 1;
+      const uint32_t aphase = (local >> 1) & 1;
+      float r = 1.0f;
+      if (MODE == MODE_RMS) {
+        mbar_wait(&sfull[as], aphase);
+        const float ssq = ssq_buf[as * BM + ew * 32 + lane];
+        r = rsqrtf(fmaf(ssq, invK, p.eps));
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sempty[as]);
+      }
+      mbar_wait(&tfull[as], aphase);
+      tc_fence_after();
+      const int row = m_blk * BM + ew * 32 + lane;
+      const int n_base = n_blk * BN;
+      const uint32_t taddr = tmem_base + ((ew * 32u) << 16) + as * BN;
+      __nv_bfloat16* zrow = p.z + static_cast<size_t>(row) * p.N + n_base;
+#pragma unroll 1
+      for (int j = 0; j < BN / 32; ++j) {
+        if (n_base + j * 32 >= p.N) break;  // warp-uniform
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(taddr + j * 32, v);
+        tmem_wait_ld();
+        float cb[32];
+        if (p.cstar != nullptr) {
+          const float4* c4 = reinterpret_cast<const float4*>(p.cstar + n_base + j * 32);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            float4 cv = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (n_base + j * 32 + q * 4 < p.N) cv = __ldg(c4 + q);
+            cb[4 * q + 0] = cv.x; cb[4 * q + 1] = cv.y; cb[4 * q + 2] = cv.z; cb[4 * q + 3] = cv.w;
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 32; ++q) cb[q] = 0.f;
+        }
+        uint32_t packed[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const float z0 = fmaf(__uint_as_float(v[2 * q]), r, cb[2 * q]);
+          const float z1 = fmaf(__uint_as_float(v[2 * q + 1]), r, cb[2 * q + 1]);
+          packed[q] = pack_bf16(z0, z1);
+        }
+        if (row < p.M) {
+          uint4* dst = reinterpret_cast<uint4*>(zrow + j * 32);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (n_base + j * 32 + q * 8 < p.N)
+              dst[q] = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[as]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+int gemm_smem_bytes() { return gemm::SMEM_BYTES; }
+
+cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int mode,
+                        int num_sms, cudaStream_t stream) {
+  using namespace gemm;
+  static bool attr_set[3] = {false, false, false};
+  const void* fptr = mode == MODE_RMS ? (const void*)flashnorm_gemm_kernel<MODE_RMS>
+                     : mode == MODE_DYT ? (const void*)flashnorm_gemm_kernel<MODE_DYT>
+                                        : (const void*)flashnorm_gemm_kernel<MODE_NONE>;
+  if (!attr_set[mode]) {
+    cudaError_t e = cudaFuncSetAttribute(fptr, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr_set[mode] = true;
+  }
+  const int grid = p.num_tiles < num_sms ? p.num_tiles : num_sms;
+  void* args[] = {(void*)&ta, (void*)&tb, (void*)&p};
+  return cudaLaunchKernel(fptr, dim3(grid), dim3(THREADS), args, SMEM_BYTES, stream);
+}
+
+}  // namespace fn

@@ -1,0 +1,50 @@
+// kernels.h — internal launcher declarations (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cuda.h>
+#include <stdint.h>
+
+namespace fn {
+
+enum KernelMode { MODE_RMS = 0, MODE_DYT = 1, MODE_NONE = 2 };
+
+struct GemmParams {
+  int M, N, K;
+  int num_m_blocks, num_n_blocks, num_tiles, num_k_blocks;
+  float eps, alpha;
+  const float* cstar;
+  __nv_bfloat16* z;
+};
+
+// K3: tcgen05 prefill GEMM (gemm_sm100.cu)
+int gemm_smem_bytes();
+cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int mode, int num_sms,
+                        cudaStream_t stream);
+
+// K4: decode GEMV, M <= 16 (gemv.cu)
+constexpr int GEMV_MAX_M = 16;
+size_t gemv_smem_bytes(int M, int K);
+cudaError_t launch_gemv(const __nv_bfloat16* a, const __nv_bfloat16* Wt, const float* cstar, __nv_bfloat16* z,
+                        int M, int K, int N, float eps, float alpha, int mode, int num_sms, cudaStream_t stream);
+
+// K5: fp32 SIMT path (simt_f32.cu)
+cudaError_t launch_linear_f32(const float* a, const float* Wt, const float* cstar, float* z, int M, int K, int N,
+                              float eps, float alpha, int mode, cudaStream_t stream);
+
+// K1/K2: folds (fold.cu).  dtype: 0 = bf16, 1 = f32
+cudaError_t launch_fold_weights(const void* Wt, int64_t N, int64_t K, int dtype, const float* g, const float* b,
+                                const float* c, void* Wt_star, float* c_star, cudaStream_t stream);
+int64_t fold_mean_center_workspace(int64_t n_out, int64_t d_in);
+cudaError_t launch_fold_mean_center(const void* Vt, int64_t n_out, int64_t d_in, int dtype, const float* b_prev,
+                                    void* Vt_star, float* b_prev_star, void* workspace, cudaStream_t stream,
+                                    int* launches);
+
+// K6/K7: baseline norm + gather permute (aux.cu)
+cudaError_t launch_baseline_norm(const void* a, const float* g, const float* b, int64_t M, int64_t K, float eps,
+                                 int norm_kind /*0 rms,1 ln,2 dyt*/, float alpha, int dtype, void* y,
+                                 cudaStream_t stream);
+cudaError_t launch_gather_columns(const void* parts, int64_t P, int64_t M, int64_t Nl, int elem_bytes, void* z,
+                                  cudaStream_t stream);
+
+}  // namespace fn

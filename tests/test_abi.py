@@ -1,0 +1,106 @@
+"""The C-ABI library loads and exports every symbol include/flashnorm.h declares;
+host-side validation returns the documented status codes (no GPU needed: every
+check below fails before any CUDA call)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_2407_09577_b200 as fn
+from paper_2407_09577_b200 import build as fnbuild
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    fnbuild.build()
+    return fn.lib()
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "flashnorm.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(flashnorm_\w+)\s*\(", src)))
+
+
+def test_header_and_binding_agree():
+    assert declared_symbols() == sorted(fn.EXPORTS)
+
+
+def test_every_declared_symbol_is_exported(L):
+    for name in declared_symbols():
+        assert hasattr(L, name), name
+    # and by the dynamic symbol table (extern "C", unmangled)
+    out = os.popen(f"nm -D --defined-only {fn.lib_path}").read()
+    for name in declared_symbols():
+        assert re.search(rf"\bT {name}\b", out), name
+
+
+def test_library_is_sm100a_only():
+    out = os.popen(f"cuobjdump --list-elf {fn.lib_path} 2>&1").read()
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(80|86|89|90)\b", out)
+
+
+def test_version_and_status_strings(L):
+    assert "sm_100a" in fn.version()
+    assert L.flashnorm_status_string(0) == b"FN_OK"
+    assert L.flashnorm_status_string(4) == b"FN_ERR_ALIGN"
+    assert L.flashnorm_status_string(99) == b"FN_ERR_UNKNOWN"
+
+
+def test_workspace_size(L):
+    # 32-row fp64 partial column sums (include/flashnorm.h fold_mean_center numerics)
+    assert fn.fold_mean_center_workspace_bytes(4096, 4096) == 128 * 4096 * 8
+    assert fn.fold_mean_center_workspace_bytes(33, 16) == 2 * 16 * 8
+    assert fn.fold_mean_center_workspace_bytes(0, 16) == 0
+
+
+P = ctypes.c_void_p
+
+
+def _lin(L, a=0x1000, w=0x2000, c=None, M=4, K=64, N=64, eps=1e-5, alpha=0.5, mode=0, dt=0, z=0x3000, path=0):
+    return L.flashnorm_linear_ex(P(a), P(w), P(c), M, K, N, eps, alpha, mode, dt, P(z), path, None)
+
+
+def test_linear_validation_codes(L):
+    assert _lin(L, a=None) == 1                                     # FN_ERR_NULL
+    assert _lin(L, K=0) == 2                                        # FN_ERR_SHAPE
+    assert _lin(L, M=-1) == 2
+    assert _lin(L, dt=7) == 3                                       # FN_ERR_DTYPE
+    assert _lin(L, K=60) == 4                                       # FN_ERR_ALIGN (bf16 needs K % 8)
+    assert b"K = 60" in L.flashnorm_last_error()
+    assert _lin(L, N=12) == 4
+    assert _lin(L, a=0x1008) == 4                                   # misaligned pointer
+    assert _lin(L, eps=-1.0) == 5                                   # FN_ERR_VALUE
+    assert _lin(L, eps=float("nan")) == 5
+    assert _lin(L, mode=2, alpha=float("inf")) == 5
+    assert _lin(L, mode=9) == 5
+    assert _lin(L, z=0x1000) == 5                                   # aliasing
+    assert _lin(L, dt=1, path=1) == 6                               # FN_ERR_UNSUPPORTED: f32 on tcgen05
+    assert _lin(L, M=17, path=2) == 6                               # decode path is M <= 16
+    assert _lin(L, M=0) == 0                                        # empty batch: no-op
+
+
+def test_fold_validation_codes(L):
+    f = L.flashnorm_fold_weights
+    assert f(P(0x1000), 8, 64, 0, None, P(0x4000), None, P(0x2000), None, None) == 1   # b without c_star
+    assert f(P(0x1000), 0, 64, 0, None, None, None, P(0x2000), None, None) == 2
+    assert f(P(0x1000), 8, 63, 1, None, None, None, P(0x2000), None, None) == 4
+    assert f(P(0x1000), 8, 64, 0, None, None, None, P(0x1000), None, None) == 5       # aliasing
+    g = L.flashnorm_fold_mean_center
+    assert g(P(0x1000), 8, 64, 0, P(0x5000), P(0x2000), None, P(0x3000), None) == 1   # b_prev without output
+    assert g(P(0x1000), 8, 64, 0, None, P(0x2000), None, None, None) == 1             # no workspace
+    assert g(P(0x1000), 8, 12, 0, None, P(0x2000), None, P(0x3000), None) == 4
+
+
+def test_python_binding_refuses_cpu_tensors():
+    import torch
+    a = torch.zeros(4, 64, dtype=torch.bfloat16)
+    w = torch.zeros(64, 64, dtype=torch.bfloat16)
+    with pytest.raises(fn.FlashNormError, match="CUDA tensor"):
+        fn.linear(a, w)
+    with pytest.raises(fn.FlashNormError, match="CUDA tensor"):
+        fn.fold_weights(w)

@@ -1,0 +1,328 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle.
+
+* folds: BIT-EXACT against oracle/fold_mirror.py (same precision and order)
+* linear: row-wise inf-norm relative error (reading c12) against the fp64 oracle
+  on the same seeded inputs: <= 2e-2 for bf16, <= 1e-5 for f32 (BASELINE.json:5)
+* full BASELINE sizes in the launch configuration bench.py times: sampled rows
+  against the oracle + size-independent properties (determinism, row
+  permutation, column-shard concatenation)
+"""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import paper_2407_09577_b200 as fn  # noqa: E402
+from oracle import flashnorm_oracle as O  # noqa: E402
+from oracle import fold_mirror as FM  # noqa: E402
+from synth import bf16_bits, gen_activations, gen_layer, gen_upstream  # noqa: E402
+from synth import device as SD  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+TOL_BF16 = 2e-2
+TOL_F32 = 1e-5
+DEV = "cuda"
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    from paper_2407_09577_b200 import build
+    build.build()
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    fn.lib()
+
+
+def T(x, dtype="bf16"):
+    """host float32 values (already representable) -> device tensor (exact)."""
+    if x is None:
+        return None
+    t = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32))
+    if dtype == "bf16":
+        t = t.to(torch.bfloat16)
+    return t.to(DEV)
+
+
+def H(t):
+    return t.float().cpu().numpy()
+
+
+def bits(t):
+    return t.contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+# ============================================================ folds, bit-exact
+
+GBC = [(1, 1, 1), (1, 0, 0), (0, 1, 0), (0, 0, 1), (1, 1, 0), (0, 0, 0)]
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("N,K", [(8, 8), (64, 64), (13, 1000), (300, 4096), (1031, 2048)])
+@pytest.mark.parametrize("gbc", GBC)
+def test_fold_weights_bit_exact(dtype, N, K, gbc):
+    Wt, g, b, c = gen_layer(11, N, K, dtype, with_b=True, with_c=True)
+    g, b, c = (g if gbc[0] else None), (b if gbc[1] else None), (c if gbc[2] else None)
+    Ws, cs = fn.fold_weights(T(Wt, dtype), T(g, "f32"), T(b, "f32"), T(c, "f32"))
+    torch.cuda.synchronize()
+    store = bf16_bits(Wt) if dtype == "bf16" else Wt
+    Wm, cm = FM.fold_weights(store, g, b, c, dtype)
+    if dtype == "bf16":
+        np.testing.assert_array_equal(bits(Ws), Wm)
+    else:
+        np.testing.assert_array_equal(H(Ws).view(np.uint32), Wm.view(np.uint32))
+    if cm is not None:
+        np.testing.assert_array_equal(H(cs).view(np.uint32), cm.view(np.uint32))
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("n_out,d_in", [(8, 8), (40, 24), (100, 72), (33, 1000), (4096, 4096)])
+@pytest.mark.parametrize("with_b", [True, False])
+def test_fold_mean_center_bit_exact(dtype, n_out, d_in, with_b):
+    _, Vt, bp = gen_upstream(12, 2, d_in, n_out, dtype)
+    bp = bp if with_b else None
+    Vs, bs = fn.fold_mean_center(T(Vt, dtype), T(bp, "f32"))
+    torch.cuda.synchronize()
+    store = bf16_bits(Vt) if dtype == "bf16" else Vt
+    Vm, bm, _ = FM.fold_mean_center(store, bp, dtype)
+    if dtype == "bf16":
+        np.testing.assert_array_equal(bits(Vs), Vm)
+    else:
+        np.testing.assert_array_equal(H(Vs).view(np.uint32), Vm.view(np.uint32))
+    if with_b:
+        np.testing.assert_array_equal(H(bs).view(np.uint32), bm.view(np.uint32))
+
+
+# ============================================================ linear: f32 path (config 1)
+
+def _layer_and_ref(seed, M, K, N, dtype, mode, amode="normal", eps=1e-5, alpha=0.5, bias=True, tiny=False):
+    a = gen_activations(seed, M, K, "uniform" if tiny else amode, dtype)
+    if mode == "layernorm":  # input of the LayerNorm-mode kernel is pre-centered (reading c9)
+        a = a - a.mean(axis=1, keepdims=True)
+        if dtype == "bf16":
+            from synth import bf16_round
+            a = bf16_round(a.astype(np.float32))
+        a = a.astype(np.float32)
+    Wt, g, b, c = gen_layer(seed, N, K, dtype, with_b=bias and mode != "none", with_c=bias, tiny=tiny)
+    if mode == "none":
+        g = None
+    ref = O.norm_linear(a, Wt.T, g, b, c, eps, mode, alpha) if mode != "none" else O.linear(a, Wt.T, c)
+    return a, Wt, g, b, c, ref
+
+
+def _run(a, Wt, g, b, c, dtype, mode, eps=1e-5, alpha=0.5, path="auto"):
+    Ws, cs = fn.fold_weights(T(Wt, dtype), T(g, "f32"), T(b, "f32"), T(c, "f32"))
+    z = fn.linear(T(a, dtype), Ws, cs, eps=eps, mode=mode, alpha=alpha, path=path)
+    torch.cuda.synchronize()
+    return H(z)
+
+
+@pytest.mark.parametrize("mode", ["rmsnorm", "layernorm", "dyt", "none"])
+@pytest.mark.parametrize("eps", [1e-5, 0.0])
+@pytest.mark.parametrize("bias", [False, True])
+def test_f32_tiny_config(mode, eps, bias):
+    """BASELINE config 1: 8 tokens, n=64 -> 64 outputs, fp32, <= 1e-5."""
+    a, Wt, g, b, c, ref = _layer_and_ref(1, 8, 64, 64, "f32", mode, eps=eps, bias=bias, tiny=True)
+    z = _run(a, Wt, g, b, c, "f32", mode, eps=eps)
+    assert O.rowwise_rel_err(z, ref) <= TOL_F32
+
+
+@pytest.mark.parametrize("M,K,N", [(3, 4096, 72), (33, 520, 8)])
+@pytest.mark.parametrize("mode", ["rmsnorm", "dyt"])
+def test_f32_larger(M, K, N, mode):
+    a, Wt, g, b, c, ref = _layer_and_ref(2, M, K, N, "f32", mode)
+    assert O.rowwise_rel_err(_run(a, Wt, g, b, c, "f32", mode), ref) <= TOL_F32
+
+
+# ============================================================ linear: bf16 tcgen05 GEMM
+
+GEMM_SHAPES = [(128, 64, 256), (300, 1000, 520), (17, 4096, 256), (1000, 4096, 1024), (257, 8192, 264)]
+
+
+@pytest.mark.parametrize("M,K,N", GEMM_SHAPES)
+@pytest.mark.parametrize("mode", ["rmsnorm", "layernorm", "dyt", "none"])
+def test_gemm_parity(M, K, N, mode):
+    a, Wt, g, b, c, ref = _layer_and_ref(3, M, K, N, "bf16", mode)
+    z = _run(a, Wt, g, b, c, "bf16", mode, path="gemm")
+    err = O.rowwise_rel_err(z, ref)
+    assert err <= TOL_BF16, err
+
+
+@pytest.mark.parametrize("amode", ["outlier", "lowenergy"])
+@pytest.mark.parametrize("eps", [1e-5, 0.0])
+def test_gemm_input_modes(amode, eps):
+    """Llama-style outlier channels and low-energy rows (which pin eps inside the sqrt, App. A)."""
+    a, Wt, g, b, c, ref = _layer_and_ref(4, 384, 2048, 512, "bf16", "rmsnorm", amode=amode, eps=eps)
+    z = _run(a, Wt, g, b, c, "bf16", "rmsnorm", eps=eps, path="gemm")
+    assert O.rowwise_rel_err(z, ref) <= TOL_BF16
+
+
+def test_gemm_eps_placement_detectable():
+    """A kernel with eps outside the sqrt would fail: low-energy rows make the readings differ."""
+    a, Wt, g, b, c, ref = _layer_and_ref(5, 256, 1024, 256, "bf16", "rmsnorm", amode="lowenergy")
+    z = _run(a, Wt, g, b, c, "bf16", "rmsnorm", path="gemm")
+    r = O.rms(a)
+    wrong = O.linear(a / (r + 1e-5)[:, None] * g + b, Wt.T, c)
+    assert O.rowwise_rel_err(z, ref) <= TOL_BF16 < O.rowwise_rel_err(wrong, ref)
+
+
+# ============================================================ linear: bf16 decode GEMV
+
+@pytest.mark.parametrize("M", [1, 5, 16])
+@pytest.mark.parametrize("K,N", [(4096, 6144), (1000, 24), (8192, 136)])
+@pytest.mark.parametrize("mode", ["rmsnorm", "dyt", "none"])
+def test_gemv_parity(M, K, N, mode):
+    a, Wt, g, b, c, ref = _layer_and_ref(6, M, K, N, "bf16", mode)
+    path = "gemv" if M * K * 2 <= 150 * 1024 else "auto"
+    z = _run(a, Wt, g, b, c, "bf16", mode, path=path)
+    assert O.rowwise_rel_err(z, ref) <= TOL_BF16
+
+
+def test_decode_and_prefill_paths_agree():
+    a, Wt, g, b, c, ref = _layer_and_ref(7, 16, 4096, 1024, "bf16", "rmsnorm")
+    z1 = _run(a, Wt, g, b, c, "bf16", "rmsnorm", path="gemv")
+    z2 = _run(a, Wt, g, b, c, "bf16", "rmsnorm", path="gemm")
+    assert O.rowwise_rel_err(z1, ref) <= TOL_BF16 and O.rowwise_rel_err(z2, ref) <= TOL_BF16
+    assert O.rowwise_rel_err(z1, z2) <= 1e-2
+
+
+# ============================================================ edge cases
+
+def test_empty_batch_is_noop():
+    W = torch.zeros(64, 64, dtype=torch.bfloat16, device=DEV)
+    z = fn.linear(torch.zeros(0, 64, dtype=torch.bfloat16, device=DEV), W)
+    assert z.shape == (0, 64)
+
+
+def test_zero_row_with_eps_zero_is_isolated():
+    """A zero-energy row with eps=0 is IEEE inf/NaN in that row only (documented in flashnorm.h)."""
+    a, Wt, g, b, c, ref = _layer_and_ref(8, 130, 512, 256, "bf16", "rmsnorm", bias=False)
+    a[5] = 0.0
+    for path in ("gemm", "gemv"):
+        aa = a[:16].copy() if path == "gemv" else a
+        z = _run(aa, Wt, g, None, None, "bf16", "rmsnorm", eps=0.0, path=path)
+        assert not np.isfinite(z[5]).any()
+        keep = [i for i in range(aa.shape[0]) if i != 5]
+        assert O.rowwise_rel_err(z[keep], ref[: aa.shape[0]][keep]) <= TOL_BF16
+
+
+def test_minimum_shapes():
+    for M, K, N in [(1, 8, 8), (2, 8, 8), (129, 8, 8)]:
+        a, Wt, g, b, c, ref = _layer_and_ref(9, M, K, N, "bf16", "rmsnorm")
+        assert O.rowwise_rel_err(_run(a, Wt, g, b, c, "bf16", "rmsnorm"), ref) <= TOL_BF16
+
+
+def test_alignment_error_raised():
+    w = torch.zeros(64, 64, dtype=torch.bfloat16, device=DEV)
+    a = torch.zeros(4 * 64 + 1, dtype=torch.bfloat16, device=DEV)[1:].view(4, 64)
+    with pytest.raises(fn.FlashNormError, match="FN_ERR_ALIGN"):
+        fn.linear(a, w)
+
+
+# ============================================================ config 4: LayerNorm retrofit + DyT
+
+def test_config4_layernorm_retrofit_end_to_end():
+    """x -> V* (mean centering folded) -> FlashNorm linear (LN g,b folded)."""
+    M, d = 2048, 4096
+    x, Vt, bp = gen_upstream(21, M, d, d, "bf16")
+    Wt, g, b, c = gen_layer(21, d, d, "bf16", with_b=True, with_c=True)
+    Vs, bs = fn.fold_mean_center(T(Vt), T(bp, "f32"))
+    a_star = fn.linear(T(x), Vs, bs, mode="none")            # upstream layer, outputs centered
+    Ws, cs = fn.fold_weights(T(Wt), T(g, "f32"), T(b, "f32"), T(c, "f32"))
+    z = H(fn.linear(a_star, Ws, cs, eps=1e-5, mode="layernorm"))
+    rows = np.r_[0, 1, M - 1, np.random.default_rng(0).choice(M, 29, replace=False)]
+    ref = O.upstream_layernorm_linear(x[rows], Vt.T, bp, Wt.T, g, b, c, 1e-5)
+    assert O.rowwise_rel_err(z[rows], ref) <= TOL_BF16
+
+
+def test_config4_dyt_variant():
+    M, d = 2048, 4096
+    a = gen_activations(22, M, d, "normal", "bf16")
+    Wt, g, b, c = gen_layer(22, d, d, "bf16", with_b=True, with_c=True)
+    z = _run(a, Wt, g, b, c, "bf16", "dyt", alpha=0.5)
+    rows = np.r_[0, M - 1, np.random.default_rng(1).choice(M, 30, replace=False)]
+    ref = O.norm_linear(a[rows], Wt.T, g, b, c, 0.0, "dyt", 0.5)
+    assert O.rowwise_rel_err(z[rows], ref) <= TOL_BF16
+
+
+# ============================================================ full BASELINE sizes (bench launch config)
+
+def _oracle_rows(a_rows, Wt_dev, g, b, c, eps, mode, alpha=0.5, col_chunk=4096):
+    """Oracle on sampled rows, W streamed to the host in column chunks (memory only)."""
+    N = Wt_dev.shape[0]
+    out = np.empty((a_rows.shape[0], N))
+    for j0 in range(0, N, col_chunk):
+        j1 = min(N, j0 + col_chunk)
+        W = Wt_dev[j0:j1].float().cpu().numpy().T
+        out[:, j0:j1] = O.norm_linear(a_rows, W, g, b, None if c is None else c[j0:j1], eps, mode, alpha)
+    return out
+
+
+def _full_size(M, K, N, seed, mode="rmsnorm", with_bias=False):
+    a = SD.activations(seed, M, K, DEV, torch.bfloat16)
+    Wt, g, b, c = SD.layer(seed, N, K, DEV, torch.bfloat16, with_b=with_bias, with_c=with_bias)
+    Ws, cs = fn.fold_weights(Wt, g, b, c)
+    return a, Wt, g, b, c, Ws, cs
+
+
+@pytest.mark.parametrize("M", [1, 16])
+def test_config2_decode_full(M):
+    """Llama-3-8B decode: RMSNorm + QKV 4096 -> 6144, all outputs vs oracle."""
+    a, Wt, g, b, c, Ws, cs = _full_size(M, 4096, 6144, 31)
+    z = H(fn.linear(a, Ws, cs, eps=1e-5))
+    ref = _oracle_rows(H(a), Wt, H(g), None, None, 1e-5, "rmsnorm")
+    assert O.rowwise_rel_err(z, ref) <= TOL_BF16
+
+
+def test_config3_prefill_full_sampled():
+    """Llama-3-8B prefill: 4096 tokens, 4096 -> 28672 (gate||up), exactly as bench.py launches it."""
+    M, K, N = 4096, 4096, 28672
+    a, Wt, g, b, c, Ws, cs = _full_size(M, K, N, 32)
+    z = fn.linear(a, Ws, cs, eps=1e-5)
+    z2 = fn.linear(a, Ws, cs, eps=1e-5)
+    torch.cuda.synchronize()
+    assert torch.equal(z, z2), "not deterministic"
+    rows = np.r_[0, 1, 127, 128, M - 1, np.random.default_rng(2).choice(M, 11, replace=False)]
+    ref = _oracle_rows(H(a[torch.as_tensor(rows, device=DEV)]), Wt, H(g), None, None, 1e-5, "rmsnorm")
+    assert O.rowwise_rel_err(H(z)[rows], ref) <= TOL_BF16
+    # row-permutation equivariance (rows are independent): bit-exact
+    perm = torch.randperm(M, generator=torch.Generator().manual_seed(3)).to(DEV)
+    zp = fn.linear(a[perm].contiguous(), Ws, cs, eps=1e-5)
+    torch.cuda.synchronize()
+    assert torch.equal(zp, z[perm])
+
+
+@pytest.mark.slow
+def test_config5_column_shards_concatenate_bit_exact():
+    """Llama-3-70B FFN shapes, W* column-sharded P = 8 ways: the concatenated shards are
+    bit-identical to the unsharded result (per-tile math is independent of P)."""
+    M, K, N, P = 8192, 8192, 57344, 8
+    a, Wt, g, b, c, Ws, cs = _full_size(M, K, N, 33)
+    del Wt
+    z = fn.linear(a, Ws, cs, eps=1e-5)
+    Nl = N // P
+    for p in range(P):
+        zp = fn.linear(a, Ws[p * Nl:(p + 1) * Nl], None, eps=1e-5)
+        assert torch.equal(zp, z[:, p * Nl:(p + 1) * Nl]), p
+    rows = np.r_[0, M - 1, np.random.default_rng(4).choice(M, 6, replace=False)]
+    ref = _oracle_rows(H(a[torch.as_tensor(rows, device=DEV)]), Ws, None, None, None, 1e-5, "rmsnorm")
+    # reference built from the folded W* here (W itself freed): checks the GEMM at full size
+    assert O.rowwise_rel_err(H(z)[rows], ref) <= TOL_BF16
+
+
+def test_baseline_unfused_matches_oracle():
+    """The measurement-only unfused variant (RMSNorm kernel -> plain GEMM on the original W)."""
+    a, Wt, g, b, c, ref = _layer_and_ref(10, 512, 2048, 768, "bf16", "rmsnorm")
+    y = fn.baseline_norm(T(a), T(g, "f32"), T(b, "f32"), eps=1e-5)
+    z = H(fn.linear(y, T(Wt), T(c, "f32"), mode="none"))
+    assert O.rowwise_rel_err(z, ref) <= TOL_BF16
+
+
+def test_gather_columns_permute():
+    P, M, Nl = 4, 37, 64
+    parts = torch.randn(P, M, Nl, device=DEV).to(torch.bfloat16)
+    z = fn.gather_columns(parts)
+    torch.cuda.synchronize()
+    assert torch.equal(z, parts.permute(1, 0, 2).reshape(M, P * Nl))
