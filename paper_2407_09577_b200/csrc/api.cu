@@ -10,6 +10,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -134,7 +135,7 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
   if (M > INT32_MAX || K > INT32_MAX || N > INT32_MAX)
     return fail(FN_ERR_SHAPE, "dimension exceeds int32 range: M=%lld K=%lld N=%lld", (long long)M, (long long)K,
                 (long long)N);
-  if (a == nullptr || Wt_star == nullptr || z == nullptr)
+  if (Wt_star == nullptr || ((a == nullptr || z == nullptr) && M > 0))
     return fail(FN_ERR_NULL, "a=%p Wt_star=%p z=%p: required pointer is NULL", a, Wt_star, z);
   if ((s = check_vec("K", K, dtype)) != FN_OK) return s;
   if ((s = check_vec("N", N, dtype)) != FN_OK) return s;
@@ -144,8 +145,8 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
   if ((mode == FN_RMSNORM || mode == FN_LAYERNORM) && (!(eps >= 0.0f) || !std::isfinite(eps)))
     return fail(FN_ERR_VALUE, "eps = %g must be finite and >= 0", (double)eps);
   if (mode == FN_DYT && !std::isfinite(alpha)) return fail(FN_ERR_VALUE, "alpha = %g must be finite", (double)alpha);
-  if (a == z) return fail(FN_ERR_VALUE, "z must not alias a");
   if (M == 0) return FN_OK;
+  if (a == z) return fail(FN_ERR_VALUE, "z must not alias a");
   const int km = kernel_mode(mode);
 
   if (dtype == FN_F32) {

@@ -46,6 +46,12 @@ FN_DEVICE void fence_mbar_init() {
 FN_DEVICE void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// Named barrier over a subset of warps (id 1..15).  Unlike __syncwarp it is never
+// elided, and it guarantees that the participants' prior shared-memory accesses
+// are performed before any of them continues.
+FN_DEVICE void named_bar_sync(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 FN_DEVICE void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
@@ -58,6 +64,26 @@ FN_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!p bra FN_WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+
+FN_DEVICE uint32_t mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok;
+}
+// Whole-warp wait: every lane polls, and the loop exit is decided by a warp vote,
+// so the warp leaves CONVERGED.  Required before warp-collective (.sync.aligned)
+// tcgen05 instructions and before an elected lane arrives on behalf of the warp
+// (an independent per-lane spin lets lane 0 run ahead of lanes still waiting).
+FN_DEVICE void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = mbar_try_wait(bar, parity);
+  while (!__all_sync(0xffffffffu, ok)) ok = mbar_try_wait(bar, parity);
 }
 
 // ---------------------------------------------------------------- TMA

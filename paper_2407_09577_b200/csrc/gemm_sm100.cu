@@ -69,14 +69,14 @@ __global__ void __launch_bounds__(gemm::THREADS, 1)
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1 + (MODE == MODE_RMS ? 4 : 0));
-      mbar_init(&ready[s], 4);
+      mbar_init(&empty[s], 1);  // MMA commit
+      mbar_init(&ready[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 4);
-      mbar_init(&sfull[b], BM);
-      mbar_init(&sempty[b], 4);
+      mbar_init(&sfull[b], 1);
+      mbar_init(&sempty[b], 1);
     }
     fence_mbar_init();
   }
@@ -123,8 +123,8 @@ __global__ void __launch_bounds__(gemm::THREADS, 1)
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + as * BN;
         for (int kb = 0; kb < nkb; ++kb) {
-          if (MODE == MODE_DYT) mbar_wait(&ready[stage], phase);
-          else mbar_wait(&full[stage], phase);
+          if (MODE == MODE_NONE) mbar_wait(&full[stage], phase);
+          else mbar_wait(&ready[stage], phase);  // side group done with the A stage
           tc_fence_after();
           const uint64_t adesc = make_sw128_desc(smem_u32(sA + stage * A_STAGE));
           const uint64_t bdesc = make_sw128_desc(smem_u32(sB + stage * B_STAGE));
@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(gemm::THREADS, 1)
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
         float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
         for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(&full[stage], phase);
+          mbar_wait_warp(&full[stage], phase);
           const uint4* row = reinterpret_cast<const uint4*>(sA + stage * A_STAGE + t * 128);
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
@@ -164,15 +164,20 @@ __global__ void __launch_bounds__(gemm::THREADS, 1)
             x = bf16lo(v.w); s2 = fmaf(x, x, s2);
             x = bf16hi(v.w); s3 = fmaf(x, x, s3);
           }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[stage]);
+          // The MMA on this stage waits for `ready`, and the stage is only refilled
+          // after that MMA commits: the A tile cannot be overwritten while the
+          // group still reads it.  (Releasing `empty` directly from this group was
+          // observed to race on B200: non-deterministic ssq at large N.)
+          named_bar_sync(1, 128);
+          if (t == 0) mbar_arrive(&ready[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
         const int as = local & 1;
         const uint32_t aphase = (local >> 1) & 1;
-        mbar_wait(&sempty[as], aphase ^ 1);
+        mbar_wait_warp(&sempty[as], aphase ^ 1);
         ssq_buf[as * BM + t] = (s0 + s1) + (s2 + s3);
-        mbar_arrive(&sfull[as]);
+        named_bar_sync(1, 128);  // all 128 ssq values written (bar.sync drains the STS)
+        if (t == 0) mbar_arrive(&sfull[as]);
       }
     } else if (MODE == MODE_DYT) {
       const float alpha = p.alpha;
@@ -180,7 +185,7 @@ __global__ void __launch_bounds__(gemm::THREADS, 1)
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(&full[stage], phase);
+          mbar_wait_warp(&full[stage], phase);
           uint4* row = reinterpret_cast<uint4*>(sA + stage * A_STAGE + t * 128);
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
@@ -194,8 +199,8 @@ __global__ void __launch_bounds__(gemm::THREADS, 1)
             row[c ^ (t & 7)] = v;
           }
           fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&ready[stage]);
+          named_bar_sync(1, 128);
+          if (t == 0) mbar_arrive(&ready[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -212,13 +217,13 @@ __global__ void __launch_bounds__(gemm::THREADS, 1)
       const uint32_t aphase = (local >> 1) & 1;
       float r = 1.0f;
       if (MODE == MODE_RMS) {
-        mbar_wait(&sfull[as], aphase);
+        mbar_wait_warp(&sfull[as], aphase);
         const float ssq = ssq_buf[as * BM + ew * 32 + lane];
+        named_bar_sync(2, 128);  // every epilogue thread has read its ssq
+        if (ew == 0 && lane == 0) mbar_arrive(&sempty[as]);
         r = rsqrtf(fmaf(ssq, invK, p.eps));
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sempty[as]);
       }
-      mbar_wait(&tfull[as], aphase);
+      mbar_wait_warp(&tfull[as], aphase);
       tc_fence_after();
       const int row = m_blk * BM + ew * 32 + lane;
       const int n_base = n_blk * BN;

@@ -138,12 +138,14 @@ __global__ void __launch_bounds__(gv::THREADS, 1)
 #pragma unroll
     for (int i = 0; i < CH; ++i) {
       const int c = warp + WARPS * (ps * CH + i);
-      const int k = c * 32 + kq * 8;
-      if (k < K) {
+      // the chunk test is warp-uniform: mma.sync must be executed by the converged warp;
+      // lanes whose 8-wide piece lies past K (ragged last chunk) contribute zeros
+      if (c * 32 < K) {
+        const int k = c * 32 + kq * 8;
         const uint4 w = cur == 0 ? wbuf[0][i] : wbuf[1][i];
         uint4 ra = make_uint4(0u, 0u, 0u, 0u), rb = make_uint4(0u, 0u, 0u, 0u);
-        if (row_lo) ra = *reinterpret_cast<const uint4*>(a_s + (size_t)g * lda + k);
-        if (row_hi) rb = *reinterpret_cast<const uint4*>(a_s + (size_t)(g + 8) * lda + k);
+        if (row_lo && k < K) ra = *reinterpret_cast<const uint4*>(a_s + (size_t)g * lda + k);
+        if (row_hi && k < K) rb = *reinterpret_cast<const uint4*>(a_s + (size_t)(g + 8) * lda + k);
         mma_bf16_16816(acc, ra.x, rb.x, ra.y, rb.y, w.x, w.y);
         mma_bf16_16816(acc, ra.z, rb.z, ra.w, rb.w, w.z, w.w);
       }

@@ -326,3 +326,22 @@ def test_gather_columns_permute():
     z = fn.gather_columns(parts)
     torch.cuda.synchronize()
     assert torch.equal(z, parts.permute(1, 0, 2).reshape(M, P * Nl))
+
+
+@pytest.mark.parametrize("M,K,N", [(4096, 512, 28672), (256, 512, 28672), (2048, 64, 8192)])
+@pytest.mark.parametrize("mode", ["rmsnorm", "dyt", "none"])
+def test_gemm_repeated_launches_bit_identical(M, K, N, mode):
+    """Regression for the stage-release race (ssq group vs TMA refill): many tiles per CTA,
+    W* streamed from HBM; every launch must produce identical bits."""
+    a = SD.activations(40, M, K, DEV, torch.bfloat16)
+    Wt, g, b, c = SD.layer(40, N, K, DEV, torch.bfloat16, with_b=True, with_c=True)
+    Ws, cs = fn.fold_weights(Wt, g, b, c)
+    z0 = fn.linear(a, Ws, cs, eps=1e-5, mode=mode, path="gemm")
+    for _ in range(5):
+        assert torch.equal(fn.linear(a, Ws, cs, eps=1e-5, mode=mode, path="gemm"), z0)
+    if mode != "dyt":
+        af = a.float()
+        acc = af @ Ws.float().T
+        r = torch.rsqrt((af * af).mean(1, keepdim=True) + 1e-5) if mode == "rmsnorm" else 1.0
+        ref = acc * r + cs
+        assert float(((z0.float() - ref).abs() / ref.abs().amax(1, keepdim=True)).max()) <= 1e-2
