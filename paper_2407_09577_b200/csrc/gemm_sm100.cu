@@ -36,7 +36,7 @@ constexpr int B_STAGE = BN * BK * 2;  // 32 KiB
 constexpr int THREADS = 384;
 constexpr int TMEM_COLS = 2 * BN;  // double-buffered fp32 accumulator
 constexpr int BAR_BYTES = 1024;
-constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * (A_STAGE + B_STAGE) + BAR_BYTES + 2 * BM * 4;
+constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * (A_STAGE + B_STAGE) + BAR_BYTES + 4 * BM * 4;
 }  // namespace gemm
 
 template <int MODE>
@@ -58,6 +58,8 @@ __global__ void __launch_bounds__(gemm::THREADS, 1)
   uint64_t* sempty = sfull + 2;          // ssq consumed          [2]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(sempty + 2);
   float* ssq_buf = reinterpret_cast<float*>(smem + STAGES * (A_STAGE + B_STAGE) + BAR_BYTES);  // [2][BM]
+  float* ssq_fence = ssq_buf + 2 * BM;  // [BM] scratch: load-completion fence of the side group
+  float* epi_fence = ssq_fence + BM;    // [BM] scratch: load-completion fence of the epilogue
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -69,7 +71,7 @@ __global__ void __launch_bounds__(gemm::THREADS, 1)
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);  // MMA commit
+      mbar_init(&empty[s], MODE == MODE_RMS ? 2 : 1);  // MMA commit (+ ssq group)
       mbar_init(&ready[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -123,8 +125,8 @@ __global__ void __launch_bounds__(gemm::THREADS, 1)
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + as * BN;
         for (int kb = 0; kb < nkb; ++kb) {
-          if (MODE == MODE_NONE) mbar_wait(&full[stage], phase);
-          else mbar_wait(&ready[stage], phase);  // side group done with the A stage
+          if (MODE == MODE_DYT) mbar_wait(&ready[stage], phase);  // tanh prologue applied
+          else mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint64_t adesc = make_sw128_desc(smem_u32(sA + stage * A_STAGE));
           const uint64_t bdesc = make_sw128_desc(smem_u32(sB + stage * B_STAGE));
@@ -164,12 +166,18 @@ __global__ void __launch_bounds__(gemm::THREADS, 1)
             x = bf16lo(v.w); s2 = fmaf(x, x, s2);
             x = bf16hi(v.w); s3 = fmaf(x, x, s3);
           }
-          // The MMA on this stage waits for `ready`, and the stage is only refilled
-          // after that MMA commits: the A tile cannot be overwritten while the
-          // group still reads it.  (Releasing `empty` directly from this group was
-          // observed to race on B200: non-deterministic ssq at large N.)
+          // WAR hazard on the A stage: LDS results can still be in flight when a later
+          // barrier/arrive issues (neither waits on the LDS scoreboard; under full
+          // tensor-core SMEM load they were seen to return after the TMA refill,
+          // giving non-deterministic ssq on B200).  The store below cannot issue
+          // until every load of this stage has RETURNED (it consumes all four
+          // accumulators); bar.sync then drains the stores of all 128 threads, and
+          // only then does the group release the stage (2nd arrival on `empty`,
+          // next to the MMA commit).  The MMA itself never waits for this group:
+          // the RMS runs beside the contraction, not in front of it (Fig 8(c)).
+          ssq_fence[t] = (s0 + s1) + (s2 + s3);
           named_bar_sync(1, 128);
-          if (t == 0) mbar_arrive(&ready[stage]);
+          if (t == 0) mbar_arrive(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
         const int as = local & 1;
@@ -219,7 +227,8 @@ __global__ void __launch_bounds__(gemm::THREADS, 1)
       if (MODE == MODE_RMS) {
         mbar_wait_warp(&sfull[as], aphase);
         const float ssq = ssq_buf[as * BM + ew * 32 + lane];
-        named_bar_sync(2, 128);  // every epilogue thread has read its ssq
+        epi_fence[ew * 32 + lane] = ssq;  // issues only once the LDS above has returned
+        named_bar_sync(2, 128);           // ... and bar.sync drains it: ssq_buf[as] is free
         if (ew == 0 && lane == 0) mbar_arrive(&sempty[as]);
         r = rsqrtf(fmaf(ssq, invK, p.eps));
       }
