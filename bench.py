@@ -326,14 +326,30 @@ def measure_secondary(args, fn, torch, dev, stream, peaks, a, Ws, cs, g):
     out = {}
     hbm = peaks.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"])
 
-    def timed(fnc, steps, warm=3):
+    def timed(fnc, steps, warm=3, graph=False):
+        """ms per call.  graph=True: the `steps` calls are captured once into a CUDA graph
+        and replayed (launch-bound decode: what a serving loop does), timed with events."""
         for _ in range(warm):
             fnc(0)
         torch.cuda.synchronize(dev)
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if not graph:
+            s.record(stream)
+            for i in range(steps):
+                fnc(i)
+            e.record(stream)
+            torch.cuda.synchronize(dev)
+            return s.elapsed_time(e) / steps
+        g = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream(dev)
+        with torch.cuda.stream(cs):
+            with torch.cuda.graph(g, stream=cs):
+                for i in range(steps):
+                    fnc(i)
+        g.replay()
+        torch.cuda.synchronize(dev)
         s.record(stream)
-        for i in range(steps):
-            fnc(i)
+        g.replay()
         e.record(stream)
         torch.cuda.synchronize(dev)
         return s.elapsed_time(e) / steps
@@ -348,7 +364,8 @@ def measure_secondary(args, fn, torch, dev, stream, peaks, a, Ws, cs, g):
     for Mdec in (1, 16):
         ad = SD.activations(7, Mdec, DECODE_K, dev, torch.bfloat16)
         zd = torch.empty((Mdec, DECODE_N), dtype=torch.bfloat16, device=dev)
-        ms = timed(lambda i: fn.linear(ad, Wd[i % 4], None, eps=1e-5, out=zd), 400)
+        ms = timed(lambda i: fn.linear(ad, Wd[i % 4], None, eps=1e-5, out=zd), 200, graph=True)
+        ms_eager = timed(lambda i: fn.linear(ad, Wd[i % 4], None, eps=1e-5, out=zd), 200)
         byts = DECODE_K * DECODE_N * 2 + Mdec * DECODE_K * 2 + Mdec * DECODE_N * 2
         gbs = byts / (ms * 1e-3) / 1e9
         # unfused: norm kernel + plain GEMV on the original weights (same W stream)
@@ -357,11 +374,12 @@ def measure_secondary(args, fn, torch, dev, stream, peaks, a, Ws, cs, g):
         def unf(i):
             fn.baseline_norm(ad, g, None, eps=1e-5, out=yd)
             fn.linear(yd, Wd[i % 4], None, mode="none", out=zd)
-        ms_u = timed(unf, 400)
+        ms_u = timed(unf, 200, graph=True)
         dec[f"M{Mdec}"] = {"us": ms * 1e3, "GB/s": gbs, "frac_hbm": gbs / hbm, "bytes": byts,
-                           "unfused_us": ms_u * 1e3, "fusion_gain": ms_u / ms}
+                           "eager_us": ms_eager * 1e3, "unfused_us": ms_u * 1e3, "fusion_gain": ms_u / ms}
     out["decode"] = {"workload": "llama3-8b decode: RMSNorm + QKV 4096->6144 (BASELINE config 2)",
                      "unit": "GB/s", "peak_hbm_gbs": hbm, "l2": "4 rotating W* buffers (200 MB > L2)",
+                     "timing": "CUDA graph of 200 back-to-back calls (PDL-chained launches), events",
                      "kernel": "flashnorm_gemv_kernel", **dec}
     del Wd
 

@@ -86,6 +86,13 @@ FN_DEVICE void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
   while (!__all_sync(0xffffffffu, ok)) ok = mbar_try_wait(bar, parity);
 }
 
+// ---------------------------------------------------------------- PDL (programmatic dependent launch)
+// Wait until the preceding kernel in the stream (launched with programmatic
+// stream serialization) has completed / triggered; no-op for a plain launch.
+FN_DEVICE void pdl_wait_prior_grid() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Allow the next kernel in the stream to begin launching.
+FN_DEVICE void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---------------------------------------------------------------- TMA
 FN_DEVICE void prefetch_tmap(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");

@@ -42,6 +42,19 @@ FN_DEVICE uint4 ldg_stream(const void* p) {
   return r;
 }
 
+// predicated 16-byte streaming load; returns zeros when !pred (no branch)
+FN_DEVICE uint4 ldg_stream_pred(const void* p, bool pred) {
+  uint4 r;
+  asm volatile(
+      "{\n\t.reg .pred q;\n\t"
+      "setp.ne.b32 q, %5, 0;\n\t"
+      "mov.b32 %0, 0; mov.b32 %1, 0; mov.b32 %2, 0; mov.b32 %3, 0;\n\t"
+      "@q ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];\n\t}"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(p), "r"((uint32_t)pred));
+  return r;
+}
+
 FN_DEVICE void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
                               uint32_t b1) {
   asm volatile(
@@ -51,14 +64,14 @@ FN_DEVICE void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t 
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-size_t gemv_smem_bytes(int M, int K) {
+static size_t gemv_regs_smem_bytes(int M, int K) {
   const size_t a_bytes = ((size_t)M * (K + 32) * 2 + 15) / 16 * 16;
   return a_bytes + (size_t)gv::SEG * gv::WARPS * 128 * 4 + 16 * 4;
 }
 
 template <int MODE>
 __global__ void __launch_bounds__(gv::THREADS, 1)
-    flashnorm_gemv_kernel(const __nv_bfloat16* __restrict__ a, const __nv_bfloat16* __restrict__ Wt,
+    flashnorm_gemv_regs_kernel(const __nv_bfloat16* __restrict__ a, const __nv_bfloat16* __restrict__ Wt,
                           const float* __restrict__ cstar, __nv_bfloat16* __restrict__ z, int M, int K, int N,
                           float eps, float alpha) {
   using namespace gv;
@@ -82,25 +95,26 @@ __global__ void __launch_bounds__(gv::THREADS, 1)
   const int kchunks = (K + 31) >> 5;
   const int cpw = (kchunks - warp + WARPS - 1) / WARPS;  // chunks of this warp per tile (warp-uniform)
 
-  // flat per-warp stream over (tile, chunk) of the current segment
-  auto load_group = [&](int seg_t0, int item0, int items, uint4 (&w)[CH]) {
+  // Per-warp load stream of the current segment: groups of CH chunks, one group
+  // never spans two tiles, so group -> (tile, qb) is tracked incrementally
+  // (no integer division on the load path) and every load is a predicated
+  // 16-byte LDG (no branches between the loads in flight).
+  const int nqb = (cpw + CH - 1) / CH;  // chunk-groups per tile for this warp
+  auto load_group = [&](int tile, int qb, bool live, uint4 (&w)[CH]) {
+    const int n = (t0 + tile) * 8 + g;
+    const bool nvalid = live && n >= r0 && n < r1;
+    const __nv_bfloat16* rowp = Wt + (size_t)(nvalid ? n : r0) * K;
 #pragma unroll
     for (int i = 0; i < CH; ++i) {
-      w[i] = make_uint4(0u, 0u, 0u, 0u);
-      const int it = item0 + i;
-      if (it < items) {
-        const int tile = seg_t0 + it / cpw;
-        const int c = warp + WARPS * (it % cpw);
-        const int n = (t0 + tile) * 8 + g;
-        const int k = c * 32 + kq * 8;
-        if (n >= r0 && n < r1 && k < K) w[i] = ldg_stream(Wt + (size_t)n * K + k);
-      }
+      const int q = qb * CH + i;
+      const int k = (warp + WARPS * q) * 32 + kq * 8;
+      w[i] = ldg_stream_pred(rowp + (k < K ? k : 0), nvalid && q < cpw && k < K);
     }
   };
 
   uint4 wb0[CH], wb1[CH];
   const int seg0_tiles = ntiles < SEG ? ntiles : SEG;
-  load_group(0, 0, seg0_tiles * cpw, wb0);  // the W* stream starts before the RMS (Fig 8(c))
+  load_group(0, 0, seg0_tiles > 0 && nqb > 0, wb0);  // the W* stream starts before the RMS (Fig 8(c))
 
   // stage the M tokens into shared memory (DyT: tanh prologue applied here, once)
   const int kv = K >> 3;
@@ -140,58 +154,61 @@ __global__ void __launch_bounds__(gv::THREADS, 1)
 
   const bool row_lo = g < M;
   const bool row_hi = g + 8 < M;
-  bool first = true;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  auto compute_group = [&](int tile, int qb, const uint4 (&w)[CH]) {
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      const int q = qb * CH + i;
+      if (q < cpw) {  // warp-uniform: mma.sync needs the converged warp
+        const int k = (warp + WARPS * q) * 32 + kq * 8;
+        uint4 ra = make_uint4(0u, 0u, 0u, 0u), rb = make_uint4(0u, 0u, 0u, 0u);
+        if (row_lo && k < K) ra = *reinterpret_cast<const uint4*>(a_s + (size_t)g * lda + k);
+        if (row_hi && k < K) rb = *reinterpret_cast<const uint4*>(a_s + (size_t)(g + 8) * lda + k);
+        mma_bf16_16816(acc, ra.x, rb.x, ra.y, rb.y, w[i].x, w[i].y);
+        mma_bf16_16816(acc, ra.z, rb.z, ra.w, rb.w, w[i].z, w[i].w);
+      }
+    }
+    if (qb == nqb - 1) {  // last group of this warp for the tile: park the partial tile
+      *reinterpret_cast<float4*>(part + ((size_t)(tile % SEG) * WARPS + warp) * 128 + lane * 4) =
+          make_float4(acc[0], acc[1], acc[2], acc[3]);
+      acc[0] = acc[1] = acc[2] = acc[3] = 0.f;
+    }
+  };
+
   for (int seg_t0 = 0; seg_t0 < ntiles; seg_t0 += SEG) {
     const int seg_tiles = (ntiles - seg_t0) < SEG ? (ntiles - seg_t0) : SEG;
-    const int items = seg_tiles * cpw;
-    if (!first) load_group(seg_t0, 0, items, wb0);
-    first = false;
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-
-    auto compute_group = [&](int item0, const uint4 (&w)[CH]) {
-#pragma unroll
-      for (int i = 0; i < CH; ++i) {
-        const int it = item0 + i;
-        if (it < items) {  // warp-uniform
-          const int c = warp + WARPS * (it % cpw);
-          const int k = c * 32 + kq * 8;
-          uint4 ra = make_uint4(0u, 0u, 0u, 0u), rb = make_uint4(0u, 0u, 0u, 0u);
-          if (row_lo && k < K) ra = *reinterpret_cast<const uint4*>(a_s + (size_t)g * lda + k);
-          if (row_hi && k < K) rb = *reinterpret_cast<const uint4*>(a_s + (size_t)(g + 8) * lda + k);
-          mma_bf16_16816(acc, ra.x, rb.x, ra.y, rb.y, w[i].x, w[i].y);
-          mma_bf16_16816(acc, ra.z, rb.z, ra.w, rb.w, w[i].z, w[i].w);
-          if (it % cpw == cpw - 1) {  // last chunk of this warp for the tile: park the partial
-            const int tile = it / cpw;
-            *reinterpret_cast<float4*>(part + ((size_t)tile * WARPS + warp) * 128 + lane * 4) =
-                make_float4(acc[0], acc[1], acc[2], acc[3]);
-            acc[0] = acc[1] = acc[2] = acc[3] = 0.f;
-          }
-        }
-      }
-    };
-
-    for (int item0 = 0; item0 < items; item0 += 2 * CH) {
-      load_group(seg_t0, item0 + CH, items, wb1);
-      compute_group(item0, wb0);
-      load_group(seg_t0, item0 + 2 * CH, items, wb0);
-      compute_group(item0 + CH, wb1);
+    const int ngroups = seg_tiles * nqb;
+    if (seg_t0 > 0) load_group(seg_t0, 0, nqb > 0, wb0);
+    // (tile, qb) of the group held in each buffer / to be loaded next
+    int ct = seg_t0, cq = 0;                     // group in wb0
+    int lt = seg_t0, lq = 0;                     // last loaded group
+    auto next = [&](int& t, int& q) { if (++q == nqb) { q = 0; ++t; } };
+    for (int gi = 0; gi < ngroups; gi += 2) {
+      next(lt, lq);
+      load_group(lt, lq, gi + 1 < ngroups, wb1);
+      compute_group(ct, cq, wb0);
+      next(ct, cq);
+      next(lt, lq);
+      load_group(lt, lq, gi + 2 < ngroups, wb0);
+      if (gi + 1 < ngroups) compute_group(ct, cq, wb1);
+      next(ct, cq);
     }
-    if (cpw == 0) {  // warp without K chunks (K < 16*32): contributes zero partials
-      for (int tile = 0; tile < seg_tiles; ++tile)
-        *reinterpret_cast<float4*>(part + ((size_t)tile * WARPS + warp) * 128 + lane * 4) =
+    if (nqb == 0) {  // warp without K chunks (K < 16*32): contributes zero partials
+      for (int tile = seg_t0; tile < seg_t0 + seg_tiles; ++tile)
+        *reinterpret_cast<float4*>(part + ((size_t)(tile % SEG) * WARPS + warp) * 128 + lane * 4) =
             make_float4(0.f, 0.f, 0.f, 0.f);
     }
     __syncthreads();
     // fixed-order reduction over the 16 warps, deferred scale, bias, bf16 store
     for (int e = tid; e < seg_tiles * 128; e += THREADS) {
-      const int tile = e >> 7, slot = e & 127;
+      const int tile = seg_t0 + (e >> 7), slot = e & 127;
       float s = 0.f;
 #pragma unroll
-      for (int w = 0; w < WARPS; ++w) s += part[((size_t)tile * WARPS + w) * 128 + slot];
+      for (int w = 0; w < WARPS; ++w) s += part[((size_t)(tile % SEG) * WARPS + w) * 128 + slot];
       const int ln = slot >> 2, i = slot & 3;
       const int row = (ln >> 2) + (i >= 2 ? 8 : 0);
       const int col = (ln & 3) * 2 + (i & 1);
-      const int n = (t0 + seg_t0 + tile) * 8 + col;
+      const int n = (t0 + tile) * 8 + col;
       if (row < M && n >= r0 && n < r1) {
         const float r = MODE == MODE_RMS ? r_s[row] : 1.0f;
         const float cb = cstar != nullptr ? __ldg(cstar + n) : 0.0f;
@@ -202,12 +219,12 @@ __global__ void __launch_bounds__(gv::THREADS, 1)
   }
 }
 
-cudaError_t launch_gemv(const __nv_bfloat16* a, const __nv_bfloat16* Wt, const float* cstar, __nv_bfloat16* z,
+static cudaError_t launch_gemv_regs(const __nv_bfloat16* a, const __nv_bfloat16* Wt, const float* cstar, __nv_bfloat16* z,
                         int M, int K, int N, float eps, float alpha, int mode, int num_sms, cudaStream_t stream) {
-  const size_t smem = gemv_smem_bytes(M, K);
-  const void* fptr = mode == MODE_RMS ? (const void*)flashnorm_gemv_kernel<MODE_RMS>
-                     : mode == MODE_DYT ? (const void*)flashnorm_gemv_kernel<MODE_DYT>
-                                        : (const void*)flashnorm_gemv_kernel<MODE_NONE>;
+  const size_t smem = gemv_regs_smem_bytes(M, K);
+  const void* fptr = mode == MODE_RMS ? (const void*)flashnorm_gemv_regs_kernel<MODE_RMS>
+                     : mode == MODE_DYT ? (const void*)flashnorm_gemv_regs_kernel<MODE_DYT>
+                                        : (const void*)flashnorm_gemv_regs_kernel<MODE_NONE>;
   static size_t attr_set[3] = {0, 0, 0};
   if (smem > 48 * 1024 && attr_set[mode] < smem) {
     cudaError_t e = cudaFuncSetAttribute(fptr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -220,6 +237,320 @@ cudaError_t launch_gemv(const __nv_bfloat16* a, const __nv_bfloat16* Wt, const f
   void* args[] = {(void*)&a, (void*)&Wt, (void*)&cstar, (void*)&z, (void*)&M, (void*)&K, (void*)&N, (void*)&eps,
                   (void*)&alpha};
   return cudaLaunchKernel(fptr, dim3(grid), dim3(gv::THREADS), args, smem, stream);
+}
+
+// ============================================================================
+// Main decode kernel: W* streamed by the bulk-copy engine (cp.async.bulk) into
+// a shared-memory ring, tokens held in registers.
+//
+//  * warps 0..15 compute, warp 16 is the producer (one elected lane).
+//  * stage = one 8-row mma tile of W*t, full K (8 row copies into padded smem
+//    rows -> conflict-free B-fragment loads); ring of >= 2 stages (~128 KiB in
+//    flight per SM, independent of registers).
+//  * compute warp w owns the fixed K chunks [w*cpw, (w+1)*cpw): its A fragments
+//    (the M <= 16 tokens, DyT-transformed once) live in registers, so shared
+//    memory holds only the W* ring; its per-row partial ssq comes from the same
+//    registers (the RMS of Fig 8(c), computed while the first stages stream in).
+//  * per tile every warp parks its 16x8 partial in smem and releases the stage;
+//    the 16 partials are reduced in a fixed order once per segment of SEG tiles.
+// ============================================================================
+#ifdef FN_GEMV_TRACE  // tools/micro/gemv_trace.cu: per-CTA timeline (globaltimer, ns)
+__device__ unsigned long long g_gemv_trace[148 * 8];
+FN_DEVICE unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define FN_TRACE(slot) \
+  if (threadIdx.x == 0 && blockIdx.x < 148) g_gemv_trace[blockIdx.x * 8 + (slot)] = gtime()
+#else
+#define FN_TRACE(slot)
+#endif
+
+namespace gt {
+constexpr int CWARPS = 16;                 // all warps compute; warp 0 lane 0 also produces
+constexpr int THREADS = CWARPS * 32;
+constexpr int CPW_MAX = 8;                 // K <= 16 * 8 * 32 = 4096
+constexpr int SEG = 8;
+constexpr int MAX_STAGES = 8;
+constexpr int RING_BUDGET = 128 * 1024;
+}  // namespace gt
+
+FN_DEVICE void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(kEvictFirst)
+      : "memory");
+}
+
+static int gemv_tma_stages(int K) {
+  const int stage = 8 * (K * 2 + 64);
+  int s = gt::RING_BUDGET / stage;
+  if (s < 2) s = 2;
+  if (s > gt::MAX_STAGES) s = gt::MAX_STAGES;
+  return s;
+}
+
+static size_t gemv_tma_smem_bytes(int K) {
+  const int S = gemv_tma_stages(K);
+  return (size_t)S * 8 * (K * 2 + 64) + (size_t)gt::SEG * gt::CWARPS * 128 * 4 + gt::CWARPS * 16 * 4 + 16 * 4 +
+         gt::CWARPS * 32 * 4 + (2 * gt::MAX_STAGES + 2 * gt::SEG) * 8;
+}
+
+template <int MODE, bool M_HI>
+__global__ void __launch_bounds__(gt::THREADS, 1)
+    flashnorm_gemv_kernel(const __nv_bfloat16* __restrict__ a, const __nv_bfloat16* __restrict__ Wt,
+                          const float* __restrict__ cstar, __nv_bfloat16* __restrict__ z, int M, int K, int N,
+                          float eps, float alpha, int S) {
+  using namespace gt;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int ldb = K * 2 + 64;  // padded smem row stride (bytes)
+  uint8_t* ring = smem;
+  float* part = reinterpret_cast<float*>(smem + (size_t)S * 8 * ldb);  // [SEG][CWARPS][128]
+  float* ssq_part = part + SEG * CWARPS * 128;                          // [CWARPS][16]
+  float* r_s = ssq_part + CWARPS * 16;                                  // [16]
+  float* part_fence = r_s + 16;                                         // [CWARPS*32] scratch
+  uint64_t* full = reinterpret_cast<uint64_t*>(part_fence + CWARPS * 32);  // [S]
+  uint64_t* empty = full + MAX_STAGES;                                  // [S]
+  uint64_t* part_full = empty + MAX_STAGES;                             // [SEG]
+  uint64_t* part_empty = part_full + SEG;                               // [SEG]
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int r0 = (int)(((long long)blockIdx.x * N) / gridDim.x);
+  const int r1 = (int)(((long long)(blockIdx.x + 1) * N) / gridDim.x);
+  const int t0 = r0 >> 3;
+  const int ntiles = r1 > r0 ? ((r1 - 1) >> 3) - t0 + 1 : 0;
+
+  FN_TRACE(0);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CWARPS);
+    }
+    for (int s = 0; s < SEG; ++s) {
+      mbar_init(&part_full[s], CWARPS);
+      mbar_init(&part_empty[s], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  // producer = lane 0 of warp 0, interleaved with its own compute: it fills the
+  // ring up front and refills a stage as soon as all 16 warps have released it
+  auto issue_tile = [&](int t, int stg) {
+    const int n0 = (t0 + t) * 8;
+    const int lo = n0 > r0 ? n0 : r0;
+    const int hi = n0 + 8 < r1 ? n0 + 8 : r1;
+    mbar_arrive_expect_tx(&full[stg], (uint32_t)(hi - lo) * K * 2);
+    for (int n = lo; n < hi; ++n)
+      bulk_g2s(ring + ((size_t)stg * 8 + (n - n0)) * ldb, Wt + (size_t)n * K, K * 2, &full[stg]);
+  };
+  if (warp == 0 && lane == 0)
+    for (int t = 0; t < ntiles && t < S; ++t) issue_tile(t, t);
+  // W* is a constant operand: it streams before the programmatic dependency on
+  // the previous kernel resolves; the tokens `a` (possibly that kernel's output)
+  // are read, and z written, only after griddepcontrol.wait.
+  pdl_wait_prior_grid();
+  pdl_launch_dependents();
+  int next_issue = ntiles < S ? ntiles : S;  // next tile the producer lane will issue
+  // non-blocking refill (lane 0 of warp 0): issue every tile whose ring slot is free
+  auto try_refill = [&]() {
+    while (next_issue < ntiles) {
+      const int stg = next_issue % S;
+      const uint32_t par = (uint32_t)((next_issue - S) / S) & 1u;
+      if (!mbar_try_wait(&empty[stg], par)) break;
+      issue_tile(next_issue, stg);
+      ++next_issue;
+    }
+  };
+
+  // -------------------------------------------------------------- compute warps
+  const int g = lane >> 2;
+  const int kq = lane & 3;
+  const int kchunks = (K + 31) >> 5;
+  const int cpw = (kchunks + CWARPS - 1) / CWARPS;  // same for all warps; <= CPW_MAX
+  const int kbase = warp * cpw;
+
+  // A fragments (tokens) for this warp's K range, in registers
+  uint4 fa[CPW_MAX], fb[CPW_MAX];
+  float s_lo = 0.f, s_hi = 0.f;
+#pragma unroll
+  for (int j = 0; j < CPW_MAX; ++j) {
+    fa[j] = make_uint4(0u, 0u, 0u, 0u);
+    fb[j] = make_uint4(0u, 0u, 0u, 0u);
+    const int k = (kbase + j) * 32 + kq * 8;
+    if (j < cpw && k < K) {
+      if (g < M) fa[j] = *reinterpret_cast<const uint4*>(a + (size_t)g * K + k);
+      if (M_HI && g + 8 < M) fb[j] = *reinterpret_cast<const uint4*>(a + (size_t)(g + 8) * K + k);
+    }
+    if (MODE == MODE_RMS) {
+      const uint32_t* wa = reinterpret_cast<const uint32_t*>(&fa[j]);
+      const uint32_t* wb = reinterpret_cast<const uint32_t*>(&fb[j]);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float x;
+        x = bf16lo(wa[q]); s_lo = fmaf(x, x, s_lo);
+        x = bf16hi(wa[q]); s_lo = fmaf(x, x, s_lo);
+        if (M_HI) {
+          x = bf16lo(wb[q]); s_hi = fmaf(x, x, s_hi);
+          x = bf16hi(wb[q]); s_hi = fmaf(x, x, s_hi);
+        }
+      }
+    }
+    if (MODE == MODE_DYT) {
+      uint32_t* wa = reinterpret_cast<uint32_t*>(&fa[j]);
+      uint32_t* wb = reinterpret_cast<uint32_t*>(&fb[j]);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        wa[q] = tanh_approx_bf16x2(pack_bf16(bf16lo(wa[q]) * alpha, bf16hi(wa[q]) * alpha));
+        if (M_HI) wb[q] = tanh_approx_bf16x2(pack_bf16(bf16lo(wb[q]) * alpha, bf16hi(wb[q]) * alpha));
+      }
+    }
+  }
+  if (MODE == MODE_RMS) {  // reduce over the 4 kq lanes: partial ssq of rows g, g+8 over this warp's K range
+    s_lo += __shfl_xor_sync(0xffffffffu, s_lo, 1);
+    s_lo += __shfl_xor_sync(0xffffffffu, s_lo, 2);
+    s_hi += __shfl_xor_sync(0xffffffffu, s_hi, 1);
+    s_hi += __shfl_xor_sync(0xffffffffu, s_hi, 2);
+    if (kq == 0) {
+      ssq_part[warp * 16 + g] = s_lo;
+      ssq_part[warp * 16 + g + 8] = s_hi;
+    }
+  }
+
+  // r_m (the deferred scale) is formed lazily by each reducing warp from the 16
+  // per-warp partial ssq: part_full of its first tile orders those writes.
+  bool have_r = false;
+  float r_row = 1.0f;  // lanes 0..15: r for row = lane
+
+  // Tile t's 16 partials are reduced by warp (t % 16) as soon as they are all
+  // parked (part_full), overlapping the reduction with the W* stream; the slot
+  // is recycled through part_empty.  No CTA-wide barrier in the loop.
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int t = 0; t < ntiles; ++t) {
+    if (warp == 0) {  // the producer lane keeps refilling while it waits for data
+      uint32_t ok = 0;
+      do {
+        if (lane == 0) try_refill();
+        ok = mbar_try_wait(&full[stage], phase);
+      } while (!__all_sync(0xffffffffu, ok));
+    } else {
+      mbar_wait_warp(&full[stage], phase);
+    }
+    if (t == 0) FN_TRACE(1);
+    if (t == ntiles - 1) FN_TRACE(2);
+    const uint8_t* rowp = ring + ((size_t)stage * 8 + g) * ldb;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int j = 0; j < CPW_MAX; ++j) {
+      const int k = (kbase + j) * 32 + kq * 8;
+      if (j < cpw) {  // warp-uniform
+        uint4 w = make_uint4(0u, 0u, 0u, 0u);
+        if (k < K) w = *reinterpret_cast<const uint4*>(rowp + (size_t)k * 2);
+        mma_bf16_16816(acc, fa[j].x, fb[j].x, fa[j].y, fb[j].y, w.x, w.y);
+        mma_bf16_16816(acc, fa[j].z, fb[j].z, fa[j].w, fb[j].w, w.z, w.w);
+      }
+    }
+    const int slot = t % SEG;
+    const uint32_t sphase = (uint32_t)(t / SEG) & 1u;
+    if (t >= SEG) mbar_wait_warp(&part_empty[slot], sphase ^ 1u);  // reducer of tile t-SEG done
+    // the partial store consumes the MMA results (hence the LDS above): the stage
+    // is released only after this warp's shared-memory reads have returned
+    *reinterpret_cast<float4*>(part + ((size_t)slot * CWARPS + warp) * 128 + lane * 4) =
+        make_float4(acc[0], acc[1], acc[2], acc[3]);
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(&empty[stage]);
+      mbar_arrive(&part_full[slot]);
+    }
+    if (warp == 0 && lane == 0) try_refill();
+    if (++stage == S) { stage = 0; phase ^= 1; }
+
+    if (warp == (t % CWARPS)) {
+      // reduce tile t: fixed-order sum over the 16 warps, deferred scale, bias, bf16 store
+      mbar_wait_warp(&part_full[slot], sphase);
+      if (MODE == MODE_RMS && !have_r) {
+        float ss = 0.f;
+#pragma unroll
+        for (int w = 0; w < CWARPS; ++w) ss += ssq_part[w * 16 + (lane & 15)];
+        r_row = rsqrtf(fmaf(ss, 1.0f / (float)K, eps));
+        have_r = true;
+      }
+      const float* P = part + (size_t)slot * CWARPS * 128;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int e = q * 32 + lane;
+        float sum = 0.f;
+#pragma unroll
+        for (int w = 0; w < CWARPS; ++w) sum += P[w * 128 + e];
+        const int ln = e >> 2, i = e & 3;
+        const int row = (ln >> 2) + (i >= 2 ? 8 : 0);
+        const int col = (ln & 3) * 2 + (i & 1);
+        const int n = (t0 + t) * 8 + col;
+        const float r = __shfl_sync(0xffffffffu, r_row, row);
+        if (row < M && n >= r0 && n < r1) {
+          const float cb = cstar != nullptr ? __ldg(cstar + n) : 0.0f;
+          z[(size_t)row * N + n] = __float2bfloat16_rn(fmaf(sum, MODE == MODE_RMS ? r : 1.0f, cb));
+        }
+        part_fence[warp * 32 + lane] = sum;  // issues after every LDS of this tile returned
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&part_empty[slot]);
+    }
+  }
+#ifdef FN_GEMV_TRACE
+  if (lane == 0 && warp == ((ntiles - 1) % CWARPS) && blockIdx.x < 148) {
+    g_gemv_trace[blockIdx.x * 8 + 3] = gtime();
+    unsigned smid;
+    asm("mov.u32 %0, %smid;" : "=r"(smid));
+    g_gemv_trace[blockIdx.x * 8 + 4] = smid;
+  }
+#endif
+}
+
+size_t gemv_smem_bytes(int M, int K) {
+  if (K <= gt::CWARPS * gt::CPW_MAX * 32) return gemv_tma_smem_bytes(K);
+  return gemv_regs_smem_bytes(M, K);
+}
+
+cudaError_t launch_gemv(const __nv_bfloat16* a, const __nv_bfloat16* Wt, const float* cstar, __nv_bfloat16* z,
+                        int M, int K, int N, float eps, float alpha, int mode, int num_sms, cudaStream_t stream) {
+  if (K > gt::CWARPS * gt::CPW_MAX * 32)
+    return launch_gemv_regs(a, Wt, cstar, z, M, K, N, eps, alpha, mode, num_sms, stream);
+  const int S = gemv_tma_stages(K);
+  const size_t smem = gemv_tma_smem_bytes(K);
+  const bool hi = M > 8;
+  const void* fptr;
+  if (mode == MODE_RMS) fptr = hi ? (const void*)flashnorm_gemv_kernel<MODE_RMS, true> : (const void*)flashnorm_gemv_kernel<MODE_RMS, false>;
+  else if (mode == MODE_DYT) fptr = hi ? (const void*)flashnorm_gemv_kernel<MODE_DYT, true> : (const void*)flashnorm_gemv_kernel<MODE_DYT, false>;
+  else fptr = hi ? (const void*)flashnorm_gemv_kernel<MODE_NONE, true> : (const void*)flashnorm_gemv_kernel<MODE_NONE, false>;
+  static size_t attr_set[6] = {0, 0, 0, 0, 0, 0};
+  const int slot = mode * 2 + (hi ? 1 : 0);
+  if (attr_set[slot] < smem) {
+    cudaError_t e = cudaFuncSetAttribute(fptr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_set[slot] = smem;
+  }
+  int grid = (N + 7) / 8;
+  if (grid > num_sms) grid = num_sms;
+  void* args[] = {(void*)&a, (void*)&Wt, (void*)&cstar, (void*)&z, (void*)&M, (void*)&K, (void*)&N, (void*)&eps,
+                  (void*)&alpha, (void*)&S};
+  // programmatic dependent launch: the W* stream of this call may start while the
+  // previous kernel of the stream drains (the kernel waits before touching a / z)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(gt::THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, fptr, args);
 }
 
 }  // namespace fn
