@@ -364,8 +364,8 @@ def measure_secondary(args, fn, torch, dev, stream, peaks, a, Ws, cs, g):
     for Mdec in (1, 16):
         ad = SD.activations(7, Mdec, DECODE_K, dev, torch.bfloat16)
         zd = torch.empty((Mdec, DECODE_N), dtype=torch.bfloat16, device=dev)
-        ms = timed(lambda i: fn.linear(ad, Wd[i % 4], None, eps=1e-5, out=zd), 200, graph=True)
-        ms_eager = timed(lambda i: fn.linear(ad, Wd[i % 4], None, eps=1e-5, out=zd), 200)
+        ms = timed(lambda i: fn.linear(ad, Wd[i % 4], None, eps=1e-5, out=zd), args.secondary_iters, graph=True)
+        ms_eager = timed(lambda i: fn.linear(ad, Wd[i % 4], None, eps=1e-5, out=zd), args.secondary_iters)
         byts = DECODE_K * DECODE_N * 2 + Mdec * DECODE_K * 2 + Mdec * DECODE_N * 2
         gbs = byts / (ms * 1e-3) / 1e9
         # unfused: norm kernel + plain GEMV on the original weights (same W stream)
@@ -374,7 +374,7 @@ def measure_secondary(args, fn, torch, dev, stream, peaks, a, Ws, cs, g):
         def unf(i):
             fn.baseline_norm(ad, g, None, eps=1e-5, out=yd)
             fn.linear(yd, Wd[i % 4], None, mode="none", out=zd)
-        ms_u = timed(unf, 200, graph=True)
+        ms_u = timed(unf, args.secondary_iters, graph=True)
         dec[f"M{Mdec}"] = {"us": ms * 1e3, "GB/s": gbs, "frac_hbm": gbs / hbm, "bytes": byts,
                            "eager_us": ms_eager * 1e3, "unfused_us": ms_u * 1e3, "fusion_gain": ms_u / ms}
     out["decode"] = {"workload": "llama3-8b decode: RMSNorm + QKV 4096->6144 (BASELINE config 2)",
@@ -415,6 +415,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--secondary-iters", type=int, default=200,
+                    help="calls per decode/unfused timing loop (small values for profiler runs)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
