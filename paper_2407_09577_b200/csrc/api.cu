@@ -173,14 +173,17 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
     ++g_launches;
     return FN_OK;
   }
+  // CTA-pair (cta_group::2, 256x256 tiles) kernel for rmsnorm/layernorm/none when M > 128;
+  // the 1-CTA kernel for DyT (in-SMEM tanh prologue) and for M <= 128.
+  const bool pair = (km != fn::MODE_DYT) && M > 128 && (path != FN_PATH_GEMM1);
   CUtensorMap ta, tb;
   if ((s = get_tmap(a, M, K, 128, &ta)) != FN_OK) return s;
-  if ((s = get_tmap(Wt_star, N, K, 256, &tb)) != FN_OK) return s;
+  if ((s = get_tmap(Wt_star, N, K, pair ? 128 : 256, &tb)) != FN_OK) return s;
   fn::GemmParams p;
   p.M = (int)M;
   p.N = (int)N;
   p.K = (int)K;
-  p.num_m_blocks = (int)((M + 127) / 128);
+  p.num_m_blocks = (int)(pair ? (M + 255) / 256 : (M + 127) / 128);
   p.num_n_blocks = (int)((N + 255) / 256);
   p.num_tiles = p.num_m_blocks * p.num_n_blocks;
   p.num_k_blocks = (int)((K + 63) / 64);
@@ -188,8 +191,9 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
   p.alpha = alpha;
   p.cstar = c_star;
   p.z = static_cast<__nv_bfloat16*>(z);
-  cudaError_t e = fn::launch_gemm(ta, tb, p, km, num_sms(), stream);
-  if (e != cudaSuccess) return cuda_fail(e, "gemm_sm100");
+  cudaError_t e = pair ? fn::launch_gemm2(ta, tb, p, km, num_sms(), stream)
+                       : fn::launch_gemm(ta, tb, p, km, num_sms(), stream);
+  if (e != cudaSuccess) return cuda_fail(e, pair ? "gemm2_sm100" : "gemm_sm100");
   ++g_launches;
   return FN_OK;
 }
@@ -257,7 +261,7 @@ fn_status flashnorm_linear(const void* a, const void* Wt_star, const float* c_st
 fn_status flashnorm_linear_ex(const void* a, const void* Wt_star, const float* c_star, int64_t M, int64_t K,
                               int64_t N, float eps, float alpha, fn_mode mode, fn_dtype dtype, void* z, fn_path path,
                               void* stream) {
-  if (path < FN_PATH_AUTO || path > FN_PATH_SIMT) return fail(FN_ERR_VALUE, "unknown fn_path %d", (int)path);
+  if (path < FN_PATH_AUTO || path > FN_PATH_GEMM1) return fail(FN_ERR_VALUE, "unknown fn_path %d", (int)path);
   return linear_impl(a, Wt_star, c_star, M, K, N, eps, alpha, mode, dtype, z, path,
                      static_cast<cudaStream_t>(stream));
 }

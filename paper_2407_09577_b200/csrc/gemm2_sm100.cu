@@ -1,0 +1,282 @@
+// gemm2_sm100.cu — K3 (CTA-pair variant): the prefill FlashNorm GEMM on 2-SM tcgen05.
+//
+//   z[m][j] = RN( fma( sum_k a[m][k] W*t[j][k],  rsqrt(ssq_m/K + eps),  c*_j ) )
+//
+// Same method as gemm_sm100.cu (deferred normalization; the RMS reduced by a warp
+// group beside the tensor core, Fig 8(c)), but each 256x256 output tile is computed
+// by a CTA PAIR with tcgen05.mma.cta_group::2: CTA r of the pair holds A rows
+// [m0+128r, +128) and W* rows [n0+128r, +128) of every K-block, the leader's MMA
+// reads both halves, and each CTA's TMEM receives its own 128 rows x 256 columns.
+// Versus the 1-CTA kernel this halves the B operand traffic per SM (SMEM and L2),
+// and 32 KiB stages allow a 6-deep ring.
+//
+// Roles per CTA (384 threads):  warp 0 TMA producer (both CTAs, signalling the
+// leader's `full`), warp 1 MMA issuer (leader only), warp 2 TMEM allocator
+// (cta_group::2), warps 4-7 ssq group, warps 8-11 epilogue.
+//
+// Stage release (RMS): the leader's MMA commit multicasts `mma_done[s]` to both CTAs;
+// each CTA's ssq group reads its A half only after that (the data was consumed by
+// the MMA, so it has certainly landed), fences its loads (store consuming them +
+// bar.sync), and releases `empty[s]` for its own producer.  NONE mode: the commit
+// multicasts straight to `empty[s]`.  DyT stays on the 1-CTA kernel.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace fn {
+
+namespace gemm2 {
+constexpr int BM = 128;          // rows per CTA (pair tile = 256)
+constexpr int BN = 256;          // pair tile columns (accumulator width per CTA)
+constexpr int BNH = BN / 2;      // W* rows loaded per CTA
+constexpr int BK = 64;
+constexpr int STAGES = 6;
+constexpr int A_STAGE = BM * BK * 2;   // 16 KiB
+constexpr int B_STAGE = BNH * BK * 2;  // 16 KiB
+constexpr int THREADS = 384;
+constexpr int TMEM_COLS = 2 * BN;
+constexpr int BAR_BYTES = 1024;
+constexpr int SMEM_BYTES = 1024 + STAGES * (A_STAGE + B_STAGE) + BAR_BYTES + 4 * BM * 4;
+}  // namespace gemm2
+
+template <int MODE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
+    flashnorm_gemm2_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                           GemmParams p) {
+  using namespace gemm2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_STAGE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE);
+  uint64_t* full = bars;                    // [STAGES] leader: both CTAs' TMA bytes landed
+  uint64_t* empty = bars + STAGES;          // [STAGES] local: stage may be refilled
+  uint64_t* mma_done = bars + 2 * STAGES;   // [STAGES] local: MMA finished reading the stage
+  uint64_t* tfull = bars + 3 * STAGES;      // [2] local: accumulator ready (multicast commit)
+  uint64_t* tempty = tfull + 2;             // [2] leader: both CTAs drained the accumulator
+  uint64_t* sfull = tempty + 2;             // [2] local ssq handshake
+  uint64_t* sempty = sfull + 2;             // [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(sempty + 2);
+  float* ssq_buf = reinterpret_cast<float*>(smem + STAGES * (A_STAGE + B_STAGE) + BAR_BYTES);  // [2][BM]
+  float* ssq_fence = ssq_buf + 2 * BM;
+  float* epi_fence = ssq_fence + BM;
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cluster = blockIdx.x >> 1;
+  const int nclusters = gridDim.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmap_a);
+    prefetch_tmap(&tmap_b);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+      mbar_init(&mma_done[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 2);
+      mbar_init(&sfull[b], 1);
+      mbar_init(&sempty[b], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) {
+    tmem_alloc_pair(tmem_holder, TMEM_COLS);
+    tmem_relinquish_pair();
+  }
+  tc_fence_before();
+  cluster_sync_all();  // barrier inits + TMEM allocation visible pair-wide
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  const int num_tiles = p.num_tiles;  // pair tiles: num_m_blocks (of 256) x num_n_blocks
+  const int nkb = p.num_k_blocks;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (both CTAs)
+    if (elect_one()) {
+      const uint32_t full0 = mapa_shared(&full[0], 0);  // leader's barrier array
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+        const int m_blk = tile % p.num_m_blocks;
+        const int n_blk = tile / p.num_m_blocks;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (A_STAGE + B_STAGE));
+          const uint32_t fb = full0 + stage * 8;
+          tma_load_2d_pair(sA + stage * A_STAGE, &tmap_a, fb, kb * BK, m_blk * 2 * BM + rank * BM, kEvictLast);
+          tma_load_2d_pair(sB + stage * B_STAGE, &tmap_b, fb, kb * BK, n_blk * BN + rank * BNH, kEvictNormal);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (leader CTA)
+    if (leader && elect_one()) {
+      constexpr uint32_t idesc = make_idesc_bf16(2 * BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int tile = cluster; tile < num_tiles; tile += nclusters, ++local) {
+        const int as = local & 1;
+        const uint32_t aphase = (local >> 1) & 1;
+        mbar_wait(&tempty[as], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + as * BN;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint64_t adesc = make_sw128_desc(smem_u32(sA + stage * A_STAGE));
+          const uint64_t bdesc = make_sw128_desc(smem_u32(sB + stage * B_STAGE));
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) umma_bf16_pair(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+          umma_commit_pair_mc(MODE == MODE_RMS ? &mma_done[stage] : &empty[stage], 0x3);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit_pair_mc(&tfull[as], 0x3);
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // ------------------------------------------------------------ ssq group (both CTAs)
+    if (MODE == MODE_RMS) {
+      const int t = threadIdx.x - 128;
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int tile = cluster; tile < num_tiles; tile += nclusters, ++local) {
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait_warp(&mma_done[stage], phase);
+          const uint4* row = reinterpret_cast<const uint4*>(sA + stage * A_STAGE + t * 128);
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const uint4 v = row[c ^ (t & 7)];
+            float x;
+            x = bf16lo(v.x); s0 = fmaf(x, x, s0);
+            x = bf16hi(v.x); s1 = fmaf(x, x, s1);
+            x = bf16lo(v.y); s2 = fmaf(x, x, s2);
+            x = bf16hi(v.y); s3 = fmaf(x, x, s3);
+            x = bf16lo(v.z); s0 = fmaf(x, x, s0);
+            x = bf16hi(v.z); s1 = fmaf(x, x, s1);
+            x = bf16lo(v.w); s2 = fmaf(x, x, s2);
+            x = bf16hi(v.w); s3 = fmaf(x, x, s3);
+          }
+          ssq_fence[t] = (s0 + s1) + (s2 + s3);  // issues only after every LDS above returned
+          named_bar_sync(1, 128);                 // drains the 128 stores
+          if (t == 0) mbar_arrive(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        const int as = local & 1;
+        const uint32_t aphase = (local >> 1) & 1;
+        mbar_wait_warp(&sempty[as], aphase ^ 1);
+        ssq_buf[as * BM + t] = (s0 + s1) + (s2 + s3);
+        named_bar_sync(1, 128);
+        if (t == 0) mbar_arrive(&sfull[as]);
+      }
+    }
+  } else if (warp >= 8) {
+    // ------------------------------------------------------------ epilogue (both CTAs)
+    const uint32_t ew = warp - 8;
+    const uint32_t tempty0 = mapa_shared(&tempty[0], 0);
+    int local = 0;
+    const float invK = 1.0f / static_cast<float>(p.K);
+    for (int tile = cluster; tile < num_tiles; tile += nclusters, ++local) {
+      const int m_blk = tile % p.num_m_blocks;
+      const int n_blk = tile / p.num_m_blocks;
+      const int as = local & 1;
+      const uint32_t aphase = (local >> 1) & 1;
+      float r = 1.0f;
+      if (MODE == MODE_RMS) {
+        mbar_wait_warp(&sfull[as], aphase);
+        const float ssq = ssq_buf[as * BM + ew * 32 + lane];
+        epi_fence[ew * 32 + lane] = ssq;
+        named_bar_sync(2, 128);
+        if (ew == 0 && lane == 0) mbar_arrive(&sempty[as]);
+        r = rsqrtf(fmaf(ssq, invK, p.eps));
+      }
+      mbar_wait_warp(&tfull[as], aphase);
+      tc_fence_after();
+      const int row = m_blk * 2 * BM + rank * BM + ew * 32 + lane;
+      const int n_base = n_blk * BN;
+      const uint32_t taddr = tmem_base + ((ew * 32u) << 16) + as * BN;
+      __nv_bfloat16* zrow = p.z + static_cast<size_t>(row) * p.N + n_base;
+#pragma unroll 1
+      for (int j = 0; j < BN / 32; ++j) {
+        if (n_base + j * 32 >= p.N) break;  // warp-uniform
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(taddr + j * 32, v);
+        tmem_wait_ld();
+        float cb[32];
+        if (p.cstar != nullptr) {
+          const float4* c4 = reinterpret_cast<const float4*>(p.cstar + n_base + j * 32);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            float4 cv = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (n_base + j * 32 + q * 4 < p.N) cv = __ldg(c4 + q);
+            cb[4 * q + 0] = cv.x; cb[4 * q + 1] = cv.y; cb[4 * q + 2] = cv.z; cb[4 * q + 3] = cv.w;
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 32; ++q) cb[q] = 0.f;
+        }
+        uint32_t packed[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+          packed[q] = pack_bf16(fmaf(__uint_as_float(v[2 * q]), r, cb[2 * q]),
+                                fmaf(__uint_as_float(v[2 * q + 1]), r, cb[2 * q + 1]));
+        if (row < p.M) {
+          uint4* dst = reinterpret_cast<uint4*>(zrow + j * 32);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (n_base + j * 32 + q * 8 < p.N)
+              dst[q] = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+        }
+      }
+      tc_fence_before();
+      named_bar_sync(2, 128);  // all 4 warps' TMEM loads of this buffer completed
+      if (ew == 0 && lane == 0) mbar_arrive_cluster(tempty0 + as * 8);  // one arrival per CTA, at the leader
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // the peer must be done with the leader's barriers / TMEM
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, TMEM_COLS);
+  }
+}
+
+int gemm2_smem_bytes() { return gemm2::SMEM_BYTES; }
+
+cudaError_t launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb_half, const GemmParams& p, int mode,
+                         int num_sms, cudaStream_t stream) {
+  using namespace gemm2;
+  static bool attr_set[3] = {false, false, false};
+  const void* fptr = mode == MODE_RMS ? (const void*)flashnorm_gemm2_kernel<MODE_RMS>
+                                      : (const void*)flashnorm_gemm2_kernel<MODE_NONE>;
+  if (!attr_set[mode]) {
+    cudaError_t e = cudaFuncSetAttribute(fptr, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr_set[mode] = true;
+  }
+  int pairs = num_sms / 2;
+  if (p.num_tiles < pairs) pairs = p.num_tiles;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.stream = stream;
+  cfg.attrs = nullptr;
+  cfg.numAttrs = 0;  // cluster shape comes from __cluster_dims__
+  void* args[] = {(void*)&ta, (void*)&tb_half, (void*)&p};
+  return cudaLaunchKernelExC(&cfg, fptr, args);
+}
+
+}  // namespace fn

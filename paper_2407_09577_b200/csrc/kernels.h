@@ -22,6 +22,11 @@ int gemm_smem_bytes();
 cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int mode, int num_sms,
                         cudaStream_t stream);
 
+// K3 pair variant: cta_group::2, 256x256 tiles (gemm2_sm100.cu); RMS / NONE modes
+int gemm2_smem_bytes();
+cudaError_t launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb_half, const GemmParams& p, int mode,
+                         int num_sms, cudaStream_t stream);
+
 // K4: decode GEMV, M <= 16 (gemv.cu)
 constexpr int GEMV_MAX_M = 16;
 size_t gemv_smem_bytes(int M, int K);
