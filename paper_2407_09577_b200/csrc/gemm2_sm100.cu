@@ -14,11 +14,14 @@
 // leader's `full`), warp 1 MMA issuer (leader only), warp 2 TMEM allocator
 // (cta_group::2), warps 4-7 ssq group, warps 8-11 epilogue.
 //
-// Stage release (RMS): the leader's MMA commit multicasts `mma_done[s]` to both CTAs;
-// each CTA's ssq group reads its A half only after that (the data was consumed by
-// the MMA, so it has certainly landed), fences its loads (store consuming them +
-// bar.sync), and releases `empty[s]` for its own producer.  NONE mode: the commit
-// multicasts straight to `empty[s]`.  DyT stays on the 1-CTA kernel.
+// Stage flow (RMS): both CTAs' TMA complete on the leader's `full[s]`; the leader's
+// MMA commit multicasts `mma_done[s]` to both CTAs; each CTA's ssq group squares
+// its A half then (the tensor core has consumed the stage, so it has certainly
+// landed in both CTAs — the peer CTA has no cheaper local "landed" signal: relaying
+// `full` with a cluster-scope remote arrive was measured 2x slower), fences its
+// loads (a store consuming them + bar.sync) and releases `empty[s]` for its own
+// producer.  The ssq work of stage s overlaps the MMAs of stages s+1.. (Fig 8(c)).
+// NONE mode: the commit releases `empty[s]` directly.  DyT stays on the 1-CTA kernel.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -50,7 +53,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE);
   uint64_t* full = bars;                    // [STAGES] leader: both CTAs' TMA bytes landed
   uint64_t* empty = bars + STAGES;          // [STAGES] local: stage may be refilled
-  uint64_t* mma_done = bars + 2 * STAGES;   // [STAGES] local: MMA finished reading the stage
+  uint64_t* mma_done = bars + 2 * STAGES;   // [STAGES] local: the MMA finished reading the stage (multicast commit)
   uint64_t* tfull = bars + 3 * STAGES;      // [2] local: accumulator ready (multicast commit)
   uint64_t* tempty = tfull + 2;             // [2] leader: both CTAs drained the accumulator
   uint64_t* sfull = tempty + 2;             // [2] local ssq handshake
@@ -74,7 +77,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], 1);     // RMS: ssq group;  NONE: MMA commit
       mbar_init(&mma_done[s], 1);
     }
     for (int b = 0; b < 2; ++b) {

@@ -143,9 +143,11 @@ GEMM_SHAPES = [(128, 64, 256), (300, 1000, 520), (17, 4096, 256), (1000, 4096, 1
 
 @pytest.mark.parametrize("M,K,N", GEMM_SHAPES)
 @pytest.mark.parametrize("mode", ["rmsnorm", "layernorm", "dyt", "none"])
-def test_gemm_parity(M, K, N, mode):
+@pytest.mark.parametrize("path", ["gemm", "gemm1"])
+def test_gemm_parity(M, K, N, mode, path):
+    """path gemm: CTA-pair cta_group::2 kernel (M > 128, not DyT); gemm1: the 1-CTA kernel."""
     a, Wt, g, b, c, ref = _layer_and_ref(3, M, K, N, "bf16", mode)
-    z = _run(a, Wt, g, b, c, "bf16", mode, path="gemm")
+    z = _run(a, Wt, g, b, c, "bf16", mode, path=path)
     err = O.rowwise_rel_err(z, ref)
     assert err <= TOL_BF16, err
 
@@ -330,15 +332,16 @@ def test_gather_columns_permute():
 
 @pytest.mark.parametrize("M,K,N", [(4096, 512, 28672), (256, 512, 28672), (2048, 64, 8192)])
 @pytest.mark.parametrize("mode", ["rmsnorm", "dyt", "none"])
-def test_gemm_repeated_launches_bit_identical(M, K, N, mode):
+@pytest.mark.parametrize("path", ["gemm", "gemm1"])
+def test_gemm_repeated_launches_bit_identical(M, K, N, mode, path):
     """Regression for the stage-release race (ssq group vs TMA refill): many tiles per CTA,
     W* streamed from HBM; every launch must produce identical bits."""
     a = SD.activations(40, M, K, DEV, torch.bfloat16)
     Wt, g, b, c = SD.layer(40, N, K, DEV, torch.bfloat16, with_b=True, with_c=True)
     Ws, cs = fn.fold_weights(Wt, g, b, c)
-    z0 = fn.linear(a, Ws, cs, eps=1e-5, mode=mode, path="gemm")
+    z0 = fn.linear(a, Ws, cs, eps=1e-5, mode=mode, path=path)
     for _ in range(5):
-        assert torch.equal(fn.linear(a, Ws, cs, eps=1e-5, mode=mode, path="gemm"), z0)
+        assert torch.equal(fn.linear(a, Ws, cs, eps=1e-5, mode=mode, path=path), z0)
     if mode != "dyt":
         af = a.float()
         acc = af @ Ws.float().T
