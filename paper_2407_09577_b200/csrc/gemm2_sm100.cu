@@ -22,6 +22,13 @@
 // loads (a store consuming them + bar.sync) and releases `empty[s]` for its own
 // producer.  The ssq work of stage s overlaps the MMAs of stages s+1.. (Fig 8(c)).
 // NONE mode: the commit releases `empty[s]` directly.  DyT stays on the 1-CTA kernel.
+//
+// ssq reuse: the tiles of one CTA pair revisit the same 256-row M blocks (the
+// schedule walks M fastest so concurrent pairs share W* tiles in L2), so each CTA
+// keeps the reduced ssq of its 128 rows in a small direct-mapped SMEM table keyed
+// by M block.  A revisited block costs no SMEM reads; its stages are released by
+// the MMA commit alone.  The MMA thread mirrors the table's tags to pick the
+// commit target, so both sides take identical decisions without communicating.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -38,7 +45,8 @@ constexpr int B_STAGE = BNH * BK * 2;  // 16 KiB
 constexpr int THREADS = 384;
 constexpr int TMEM_COLS = 2 * BN;
 constexpr int BAR_BYTES = 1024;
-constexpr int SMEM_BYTES = 1024 + STAGES * (A_STAGE + B_STAGE) + BAR_BYTES + 4 * BM * 4;
+constexpr int SSQ_SLOTS = 16;          // per-CTA cache of reduced row ssq, by M block
+constexpr int SMEM_BYTES = 1024 + STAGES * (A_STAGE + B_STAGE) + BAR_BYTES + (4 + SSQ_SLOTS) * BM * 4;
 }  // namespace gemm2
 
 template <int MODE>
@@ -62,6 +70,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
   float* ssq_buf = reinterpret_cast<float*>(smem + STAGES * (A_STAGE + B_STAGE) + BAR_BYTES);  // [2][BM]
   float* ssq_fence = ssq_buf + 2 * BM;
   float* epi_fence = ssq_fence + BM;
+  float* ssq_cache = epi_fence + BM;  // [SSQ_SLOTS][BM]
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -123,12 +132,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
     // ------------------------------------------------------------ MMA issuer (leader CTA)
     if (leader && elect_one()) {
       constexpr uint32_t idesc = make_idesc_bf16(2 * BM, BN);
+      int tag[SSQ_SLOTS];  // mirrors the ssq group's cache decisions (same sequence, same updates)
+#pragma unroll
+      for (int i = 0; i < SSQ_SLOTS; ++i) tag[i] = -1;
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
       for (int tile = cluster; tile < num_tiles; tile += nclusters, ++local) {
         const int as = local & 1;
         const uint32_t aphase = (local >> 1) & 1;
+        const int m_blk = tile % p.num_m_blocks;
+        const int slot = m_blk % SSQ_SLOTS;
+        bool cached = false;
+#pragma unroll
+        for (int i = 0; i < SSQ_SLOTS; ++i)
+          if (i == slot) { cached = tag[i] == m_blk; tag[i] = m_blk; }
+        uint64_t* release = (MODE == MODE_RMS && !cached) ? mma_done : empty;
         mbar_wait(&tempty[as], aphase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + as * BN;
@@ -139,7 +158,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
           const uint64_t bdesc = make_sw128_desc(smem_u32(sB + stage * B_STAGE));
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) umma_bf16_pair(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
-          umma_commit_pair_mc(MODE == MODE_RMS ? &mma_done[stage] : &empty[stage], 0x3);
+          umma_commit_pair_mc(&release[stage], 0x3);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
         umma_commit_pair_mc(&tfull[as], 0x3);
@@ -149,36 +168,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
     // ------------------------------------------------------------ ssq group (both CTAs)
     if (MODE == MODE_RMS) {
       const int t = threadIdx.x - 128;
+      int tag[SSQ_SLOTS];
+#pragma unroll
+      for (int i = 0; i < SSQ_SLOTS; ++i) tag[i] = -1;
+      uint32_t md_phase = 0;  // per-stage parity of mma_done (used only on uncached tiles)
       int stage = 0;
-      uint32_t phase = 0;
       int local = 0;
       for (int tile = cluster; tile < num_tiles; tile += nclusters, ++local) {
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-        for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait_warp(&mma_done[stage], phase);
-          const uint4* row = reinterpret_cast<const uint4*>(sA + stage * A_STAGE + t * 128);
+        const int m_blk = tile % p.num_m_blocks;
+        const int slot = m_blk % SSQ_SLOTS;
+        bool cached = false;
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const uint4 v = row[c ^ (t & 7)];
-            float x;
-            x = bf16lo(v.x); s0 = fmaf(x, x, s0);
-            x = bf16hi(v.x); s1 = fmaf(x, x, s1);
-            x = bf16lo(v.y); s2 = fmaf(x, x, s2);
-            x = bf16hi(v.y); s3 = fmaf(x, x, s3);
-            x = bf16lo(v.z); s0 = fmaf(x, x, s0);
-            x = bf16hi(v.z); s1 = fmaf(x, x, s1);
-            x = bf16lo(v.w); s2 = fmaf(x, x, s2);
-            x = bf16hi(v.w); s3 = fmaf(x, x, s3);
+        for (int i = 0; i < SSQ_SLOTS; ++i)
+          if (i == slot) { cached = tag[i] == m_blk; tag[i] = m_blk; }
+        float ssq;
+        if (cached) {
+          // this CTA already reduced these 128 rows for an earlier N tile: the ring
+          // stages of this tile are released by the MMA commit alone
+          stage = (stage + nkb) % STAGES;
+          ssq = ssq_cache[slot * BM + t];
+        } else {
+          float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+          for (int kb = 0; kb < nkb; ++kb) {
+            mbar_wait_warp(&mma_done[stage], (md_phase >> stage) & 1u);
+            md_phase ^= 1u << stage;
+            const uint4* row = reinterpret_cast<const uint4*>(sA + stage * A_STAGE + t * 128);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const uint4 v = row[c ^ (t & 7)];
+              float x;
+              x = bf16lo(v.x); s0 = fmaf(x, x, s0);
+              x = bf16hi(v.x); s1 = fmaf(x, x, s1);
+              x = bf16lo(v.y); s2 = fmaf(x, x, s2);
+              x = bf16hi(v.y); s3 = fmaf(x, x, s3);
+              x = bf16lo(v.z); s0 = fmaf(x, x, s0);
+              x = bf16hi(v.z); s1 = fmaf(x, x, s1);
+              x = bf16lo(v.w); s2 = fmaf(x, x, s2);
+              x = bf16hi(v.w); s3 = fmaf(x, x, s3);
+            }
+            ssq_fence[t] = (s0 + s1) + (s2 + s3);  // issues only after every LDS above returned
+            named_bar_sync(1, 128);                 // drains the 128 stores
+            if (t == 0) mbar_arrive(&empty[stage]);
+            if (++stage == STAGES) stage = 0;
           }
-          ssq_fence[t] = (s0 + s1) + (s2 + s3);  // issues only after every LDS above returned
-          named_bar_sync(1, 128);                 // drains the 128 stores
-          if (t == 0) mbar_arrive(&empty[stage]);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          ssq = (s0 + s1) + (s2 + s3);
+          ssq_cache[slot * BM + t] = ssq;
         }
         const int as = local & 1;
         const uint32_t aphase = (local >> 1) & 1;
         mbar_wait_warp(&sempty[as], aphase ^ 1);
-        ssq_buf[as * BM + t] = (s0 + s1) + (s2 + s3);
+        ssq_buf[as * BM + t] = ssq;
         named_bar_sync(1, 128);
         if (t == 0) mbar_arrive(&sfull[as]);
       }

@@ -330,10 +330,11 @@ def test_gather_columns_permute():
     assert torch.equal(z, parts.permute(1, 0, 2).reshape(M, P * Nl))
 
 
-@pytest.mark.parametrize("M,K,N", [(4096, 512, 28672), (256, 512, 28672), (2048, 64, 8192)])
+@pytest.mark.parametrize("M,K,N", [(4096, 512, 28672), (256, 512, 28672), (2048, 64, 8192), (9000, 256, 4096)])
 @pytest.mark.parametrize("mode", ["rmsnorm", "dyt", "none"])
 @pytest.mark.parametrize("path", ["gemm", "gemm1"])
 def test_gemm_repeated_launches_bit_identical(M, K, N, mode, path):
+    """(9000, 256, 4096): 36 pair M blocks > the 16-slot ssq cache -> slot replacement; ragged M."""
     """Regression for the stage-release race (ssq group vs TMA refill): many tiles per CTA,
     W* streamed from HBM; every launch must produce identical bits."""
     a = SD.activations(40, M, K, DEV, torch.bfloat16)
