@@ -261,11 +261,13 @@ def run_ours(args, ws, rank, local):
     value = flops_rank * ws * args.steps / (total_ms * 1e-3) / 1e12
     achieved = flops_rank / (kern_ms * 1e-3) / 1e12
     peak_tf = peaks.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"])
+    # the kernel flashnorm_linear dispatches for this shape (include/flashnorm.h fn_path)
+    kname = "flashnorm_gemm2_kernel" if M > 128 else "flashnorm_gemm_kernel"
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get("flashnorm_gemm_kernel")
+            traffic = json.load(open(tp)).get(kname)
         except Exception:
             traffic = None
 
@@ -308,7 +310,7 @@ def run_ours(args, ws, rank, local):
                    "l2": "inputs > L2 (W* 235 MB), no flush"},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": achieved / peak_tf, "traffic": traffic,
-                     "kernel": "flashnorm_gemm_kernel<MODE_RMS>",
+                     "kernel": f"{kname}<MODE_RMS> (tcgen05{' cta_group::2' if M > 128 else ''})",
                      "peak_source": f"{peaks_src} bf16_tflops (burst, cuBLAS)"},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "TFLOP/s", "h2d_bytes_per_step": M * K * 2,

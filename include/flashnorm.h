@@ -109,7 +109,7 @@ fn_status flashnorm_fold_weights(const void* Wt, int64_t N, int64_t K, fn_dtype 
  *               NULL (must be non-NULL iff b_prev is non-NULL).
  *   Vt_star     [n_out][d_in] storage dtype, output.
  *   workspace   device scratch of flashnorm_fold_mean_center_workspace_bytes()
- *               bytes, 16-B aligned (fp64 partial column sums).
+ *               bytes, 16-B aligned (fp64 partial column sums, then s_i / n).
  *
  *   fold_mean_center numerics (mirrored bit-exactly on the CPU):
  *     partial[c][i] = fp64 sum of Vt[j][i], j in [32c, 32c+32) ascending

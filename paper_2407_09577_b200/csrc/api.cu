@@ -175,7 +175,7 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
   }
   // CTA-pair (cta_group::2, 256x256 tiles) kernel for rmsnorm/layernorm/none when M > 128;
   // the 1-CTA kernel for DyT (in-SMEM tanh prologue) and for M <= 128.
-  const bool pair = (km != fn::MODE_DYT) && M > 128 && (path != FN_PATH_GEMM1);
+  const bool pair = M > 128 && (path != FN_PATH_GEMM1);
   CUtensorMap ta, tb;
   if ((s = get_tmap(a, M, K, 128, &ta)) != FN_OK) return s;
   if ((s = get_tmap(Wt_star, N, K, pair ? 128 : 256, &tb)) != FN_OK) return s;
@@ -186,6 +186,13 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
   p.num_m_blocks = (int)(pair ? (M + 255) / 256 : (M + 127) / 128);
   p.num_n_blocks = (int)((N + 255) / 256);
   p.num_tiles = p.num_m_blocks * p.num_n_blocks;
+  {  // ~40 MB of A per tile group (L2 is 126 MB; W* tiles and z share it)
+    const int64_t a_bytes_per_blk = (pair ? 256 : 128) * K * 2;
+    int64_t G = (40ll << 20) / a_bytes_per_blk;
+    if (G < 1) G = 1;
+    if (G > p.num_m_blocks) G = p.num_m_blocks;
+    p.group_m = (int)G;
+  }
   p.num_k_blocks = (int)((K + 63) / 64);
   p.eps = eps;
   p.alpha = alpha;

@@ -212,6 +212,17 @@ FN_DEVICE void tma_load_2d_pair(void* dst, const CUtensorMap* m, uint32_t bar_cl
       "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster_addr), "r"(x), "r"(y), "l"(policy)
       : "memory");
 }
+// Signal an mbarrier in another CTA of the cluster through the bulk-copy engine:
+// a 16-byte DSMEM copy whose complete_tx lands on `bar_cluster_addr`.  Unlike a
+// cluster-scope release arrive (measured ~2x slowdown when on the per-stage
+// critical path) this stays on the asynchronous hardware path; a preceding
+// fence.proxy.async orders the caller's generic SMEM writes before it.
+FN_DEVICE void dsmem_signal16(uint32_t dst_cluster_addr, const void* src_local, uint32_t bar_cluster_addr) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], 16, [%2];" ::"r"(
+                   dst_cluster_addr),
+               "r"(smem_u32(src_local)), "r"(bar_cluster_addr)
+               : "memory");
+}
 FN_DEVICE void tmem_alloc_pair(uint32_t* dst_smem, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
                "r"(ncols)

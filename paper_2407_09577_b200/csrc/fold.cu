@@ -141,7 +141,18 @@ cudaError_t launch_fold_weights(const void* Wt, int64_t N, int64_t K, int dtype,
 
 int64_t fold_mean_center_workspace(int64_t n_out, int64_t d_in) {
   const int64_t nchunk = (n_out + fold::COLSUM_ROWS - 1) / fold::COLSUM_ROWS;
-  return nchunk * d_in * (int64_t)sizeof(double);
+  return (nchunk + 1) * d_in * (int64_t)sizeof(double);  // partials + s_i/n
+}
+
+// pass 1b: s_i = ordered sum of the partials (c ascending); mu_i = s_i / n
+__global__ void __launch_bounds__(256)
+    colsum_reduce_kernel(const double* __restrict__ partial, int64_t nchunk, int64_t d_in, int64_t n_out,
+                         double* __restrict__ mu) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= d_in) return;
+  double acc = 0.0;
+  for (int64_t c = 0; c < nchunk; ++c) acc = __dadd_rn(acc, partial[c * d_in + i]);
+  mu[i] = __ddiv_rn(acc, (double)n_out);
 }
 
 // pass 1: partial[cidx][i] = sum_{j in chunk cidx, ascending} Vt[j][i]
@@ -178,11 +189,11 @@ __global__ void __launch_bounds__(128)
   for (int e = 0; e < E; ++e) out[e] = acc[e];
 }
 
-// pass 2: s_i = ordered sum of partials; V*t = RN(Vt - s_i/n).  block.y -> 32-row chunk.
+// pass 2: V*t = RN(Vt - s_i/n).  block.y -> 32-row chunk (second read of Vt: L2-resident).
 template <int DT>
 __global__ void __launch_bounds__(128)
-    center_kernel(const uint8_t* __restrict__ Vt, int64_t n_out, int64_t d_in, const double* __restrict__ partial,
-                  int64_t nchunk, uint8_t* __restrict__ Vt_star) {
+    center_kernel(const uint8_t* __restrict__ Vt, int64_t n_out, int64_t d_in, const double* __restrict__ mu_g,
+                  uint8_t* __restrict__ Vt_star) {
   constexpr int E = DT == 0 ? 8 : 4;
   constexpr int ES = DT == 0 ? 2 : 4;
   const int64_t grp = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -190,15 +201,7 @@ __global__ void __launch_bounds__(128)
   if (grp >= ngrp) return;
   double mu[E];
 #pragma unroll
-  for (int e = 0; e < E; ++e) mu[e] = 0.0;
-  for (int64_t cidx = 0; cidx < nchunk; ++cidx) {
-    const double* pp = partial + cidx * d_in + grp * E;
-#pragma unroll
-    for (int e = 0; e < E; ++e) mu[e] = __dadd_rn(mu[e], pp[e]);
-  }
-  const double n = (double)n_out;
-#pragma unroll
-  for (int e = 0; e < E; ++e) mu[e] = __ddiv_rn(mu[e], n);
+  for (int e = 0; e < E; ++e) mu[e] = mu_g[grp * E + e];
   const int64_t j0 = (int64_t)blockIdx.y * fold::COLSUM_ROWS;
   const int64_t j1 = min(j0 + fold::COLSUM_ROWS, n_out);
   for (int64_t j = j0; j < j1; ++j) {
@@ -252,17 +255,21 @@ cudaError_t launch_fold_mean_center(const void* Vt, int64_t n_out, int64_t d_in,
   double* partial = static_cast<double*>(workspace);
   const uint8_t* src = static_cast<const uint8_t*>(Vt);
   uint8_t* dst = static_cast<uint8_t*>(Vt_star);
+  double* mu = partial + nchunk * d_in;
+  const unsigned rgrid = (unsigned)((d_in + 255) / 256);
   if (dtype == 0) {
     colsum_partial_kernel<0><<<grid, 128, 0, stream>>>(src, n_out, d_in, partial);
-    center_kernel<0><<<grid, 128, 0, stream>>>(src, n_out, d_in, partial, nchunk, dst);
+    colsum_reduce_kernel<<<rgrid, 256, 0, stream>>>(partial, nchunk, d_in, n_out, mu);
+    center_kernel<0><<<grid, 128, 0, stream>>>(src, n_out, d_in, mu, dst);
   } else {
     colsum_partial_kernel<1><<<grid, 128, 0, stream>>>(src, n_out, d_in, partial);
-    center_kernel<1><<<grid, 128, 0, stream>>>(src, n_out, d_in, partial, nchunk, dst);
+    colsum_reduce_kernel<<<rgrid, 256, 0, stream>>>(partial, nchunk, d_in, n_out, mu);
+    center_kernel<1><<<grid, 128, 0, stream>>>(src, n_out, d_in, mu, dst);
   }
-  *launches = 2;
+  *launches = 3;
   if (b_prev != nullptr) {
     center_bias_kernel<<<1, fold::BPREV_THREADS, 0, stream>>>(b_prev, n_out, b_prev_star);
-    *launches = 3;
+    *launches = 4;
   }
   return cudaGetLastError();
 }

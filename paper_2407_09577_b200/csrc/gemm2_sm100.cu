@@ -46,7 +46,7 @@ constexpr int THREADS = 384;
 constexpr int TMEM_COLS = 2 * BN;
 constexpr int BAR_BYTES = 1024;
 constexpr int SSQ_SLOTS = 16;          // per-CTA cache of reduced row ssq, by M block
-constexpr int SMEM_BYTES = 1024 + STAGES * (A_STAGE + B_STAGE) + BAR_BYTES + (4 + SSQ_SLOTS) * BM * 4;
+constexpr int SMEM_BYTES = 1024 + STAGES * (A_STAGE + B_STAGE) + BAR_BYTES + (4 + SSQ_SLOTS) * BM * 4 + 32;
 }  // namespace gemm2
 
 template <int MODE>
@@ -66,11 +66,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
   uint64_t* tempty = tfull + 2;             // [2] leader: both CTAs drained the accumulator
   uint64_t* sfull = tempty + 2;             // [2] local ssq handshake
   uint64_t* sempty = sfull + 2;             // [2]
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(sempty + 2);
+  uint64_t* afull = sempty + 2;             // [STAGES] DyT: local raw-A landed
+  uint64_t* ready = afull + STAGES;         // [STAGES] DyT (leader): both CTAs' prologue done
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(ready + STAGES);
   float* ssq_buf = reinterpret_cast<float*>(smem + STAGES * (A_STAGE + B_STAGE) + BAR_BYTES);  // [2][BM]
   float* ssq_fence = ssq_buf + 2 * BM;
   float* epi_fence = ssq_fence + BM;
   float* ssq_cache = epi_fence + BM;  // [SSQ_SLOTS][BM]
+  uint8_t* sig_dst = reinterpret_cast<uint8_t*>(ssq_cache + SSQ_SLOTS * BM);  // 16 B: DyT peer signal landing
+  const uint8_t* sig_src = sig_dst + 16;                                      // 16 B: its (unused) source
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -86,8 +90,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);     // RMS: ssq group;  NONE: MMA commit
+      mbar_init(&empty[s], 1);     // RMS: ssq group;  NONE/DyT: MMA commit
       mbar_init(&mma_done[s], 1);
+      mbar_init(&afull[s], 1);
+      mbar_init(&ready[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
@@ -116,13 +122,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = cluster; tile < num_tiles; tile += nclusters) {
-        const int m_blk = tile % p.num_m_blocks;
-        const int n_blk = tile / p.num_m_blocks;
+        int m_blk, n_blk;
+        tile_coords(tile, p, m_blk, n_blk);
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (A_STAGE + B_STAGE));
           const uint32_t fb = full0 + stage * 8;
-          tma_load_2d_pair(sA + stage * A_STAGE, &tmap_a, fb, kb * BK, m_blk * 2 * BM + rank * BM, kEvictLast);
+          if (MODE == MODE_DYT) {
+            // raw A lands on a LOCAL barrier (this CTA's prologue warps transform it);
+            // B still completes on the leader's `full`
+            if (leader) mbar_arrive_expect_tx(&full[stage], 2 * B_STAGE);
+            mbar_arrive_expect_tx(&afull[stage], A_STAGE);
+            tma_load_2d(sA + stage * A_STAGE, &tmap_a, &afull[stage], kb * BK, m_blk * 2 * BM + rank * BM, kEvictLast);
+          } else {
+            if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (A_STAGE + B_STAGE));
+            tma_load_2d_pair(sA + stage * A_STAGE, &tmap_a, fb, kb * BK, m_blk * 2 * BM + rank * BM, kEvictLast);
+          }
           tma_load_2d_pair(sB + stage * B_STAGE, &tmap_b, fb, kb * BK, n_blk * BN + rank * BNH, kEvictNormal);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -141,7 +155,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
       for (int tile = cluster; tile < num_tiles; tile += nclusters, ++local) {
         const int as = local & 1;
         const uint32_t aphase = (local >> 1) & 1;
-        const int m_blk = tile % p.num_m_blocks;
+        int m_blk, n_blk_unused;
+        tile_coords(tile, p, m_blk, n_blk_unused);
         const int slot = m_blk % SSQ_SLOTS;
         bool cached = false;
 #pragma unroll
@@ -153,6 +168,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
         const uint32_t d_tmem = tmem_base + as * BN;
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&full[stage], phase);
+          if (MODE == MODE_DYT) mbar_wait(&ready[stage], phase);  // both CTAs' tanh(alpha a) written
           tc_fence_after();
           const uint64_t adesc = make_sw128_desc(smem_u32(sA + stage * A_STAGE));
           const uint64_t bdesc = make_sw128_desc(smem_u32(sB + stage * B_STAGE));
@@ -175,7 +191,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
       int stage = 0;
       int local = 0;
       for (int tile = cluster; tile < num_tiles; tile += nclusters, ++local) {
-        const int m_blk = tile % p.num_m_blocks;
+        int m_blk, n_blk_unused;
+        tile_coords(tile, p, m_blk, n_blk_unused);
         const int slot = m_blk % SSQ_SLOTS;
         bool cached = false;
 #pragma unroll
@@ -222,6 +239,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
         if (t == 0) mbar_arrive(&sfull[as]);
       }
     }
+    if (MODE == MODE_DYT) {
+      // prologue: rewrite this CTA's A half with tanh(alpha a) (bf16x2 multiply + MUFU tanh),
+      // make the generic writes visible to the tensor core, and report to the leader
+      const int t = threadIdx.x - 128;
+      const __nv_bfloat162 alpha2 = __floats2bfloat162_rn(p.alpha, p.alpha);
+      const uint32_t ready0 = mapa_shared(&ready[0], 0);
+      const uint32_t sig0 = mapa_shared(sig_dst, 0);  // 16-byte landing slot in the leader
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait_warp(&afull[stage], phase);
+          uint4* row = reinterpret_cast<uint4*>(sA + stage * A_STAGE + t * 128);
+          uint4 v[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) v[c] = row[c ^ (t & 7)];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            uint32_t* w = reinterpret_cast<uint32_t*>(&v[c]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              __nv_bfloat162 x = *reinterpret_cast<__nv_bfloat162*>(&w[q]);
+              x = __hmul2(x, alpha2);
+              w[q] = tanh_approx_bf16x2(*reinterpret_cast<uint32_t*>(&x));
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < 8; ++c) row[c ^ (t & 7)] = v[c];
+          fence_proxy_async_smem();
+          named_bar_sync(1, 128);
+          if (t == 0) {
+            if (leader) mbar_arrive_expect_tx(&ready[stage], 16);  // + the peer's 16-byte signal
+            else dsmem_signal16(sig0, sig_src, ready0 + stage * 8);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
   } else if (warp >= 8) {
     // ------------------------------------------------------------ epilogue (both CTAs)
     const uint32_t ew = warp - 8;
@@ -229,8 +284,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
     int local = 0;
     const float invK = 1.0f / static_cast<float>(p.K);
     for (int tile = cluster; tile < num_tiles; tile += nclusters, ++local) {
-      const int m_blk = tile % p.num_m_blocks;
-      const int n_blk = tile / p.num_m_blocks;
+      int m_blk, n_blk;
+      tile_coords(tile, p, m_blk, n_blk);
       const int as = local & 1;
       const uint32_t aphase = (local >> 1) & 1;
       float r = 1.0f;
@@ -301,8 +356,9 @@ cudaError_t launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb_half, cons
                          int num_sms, cudaStream_t stream) {
   using namespace gemm2;
   static bool attr_set[3] = {false, false, false};
-  const void* fptr = mode == MODE_RMS ? (const void*)flashnorm_gemm2_kernel<MODE_RMS>
-                                      : (const void*)flashnorm_gemm2_kernel<MODE_NONE>;
+  const void* fptr = mode == MODE_RMS   ? (const void*)flashnorm_gemm2_kernel<MODE_RMS>
+                     : mode == MODE_DYT ? (const void*)flashnorm_gemm2_kernel<MODE_DYT>
+                                        : (const void*)flashnorm_gemm2_kernel<MODE_NONE>;
   if (!attr_set[mode]) {
     cudaError_t e = cudaFuncSetAttribute(fptr, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) return e;

@@ -100,8 +100,8 @@ __global__ void __launch_bounds__(gemm::THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int m_blk = tile % p.num_m_blocks;
-        const int n_blk = tile / p.num_m_blocks;
+        int m_blk, n_blk;
+        tile_coords(tile, p, m_blk, n_blk);
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], A_STAGE + B_STAGE);
@@ -188,24 +188,31 @@ __global__ void __launch_bounds__(gemm::THREADS, 1)
         if (t == 0) mbar_arrive(&sfull[as]);
       }
     } else if (MODE == MODE_DYT) {
-      const float alpha = p.alpha;
+      // alpha*a as one bf16x2 multiply (alpha rounded to bf16; exact for the synthetic
+      // alpha = 0.5), then the bf16x2 MUFU tanh: 2 instructions per pair keep the
+      // prologue ahead of the tensor core (reading c14).
+      const __nv_bfloat162 alpha2 = __floats2bfloat162_rn(p.alpha, p.alpha);
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait_warp(&full[stage], phase);
           uint4* row = reinterpret_cast<uint4*>(sA + stage * A_STAGE + t * 128);
+          uint4 v[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) v[c] = row[c ^ (t & 7)];
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
-            uint4 v = row[c ^ (t & 7)];
-            uint32_t* w = reinterpret_cast<uint32_t*>(&v);
+            uint32_t* w = reinterpret_cast<uint32_t*>(&v[c]);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-              // alpha*a in fp32, one RN to bf16, then the bf16x2 MUFU tanh (reading c14)
-              w[q] = tanh_approx_bf16x2(pack_bf16(bf16lo(w[q]) * alpha, bf16hi(w[q]) * alpha));
+              __nv_bfloat162 x = *reinterpret_cast<__nv_bfloat162*>(&w[q]);
+              x = __hmul2(x, alpha2);
+              w[q] = tanh_approx_bf16x2(*reinterpret_cast<uint32_t*>(&x));
             }
-            row[c ^ (t & 7)] = v;
           }
+#pragma unroll
+          for (int c = 0; c < 8; ++c) row[c ^ (t & 7)] = v[c];
           fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
           named_bar_sync(1, 128);
           if (t == 0) mbar_arrive(&ready[stage]);
@@ -219,8 +226,8 @@ __global__ void __launch_bounds__(gemm::THREADS, 1)
     int local = 0;
     const float invK = 1.0f / static_cast<float>(p.K);
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
-      const int m_blk = tile % p.num_m_blocks;
-      const int n_blk = tile / p.num_m_blocks;
+      int m_blk, n_blk;
+      tile_coords(tile, p, m_blk, n_blk);
       const int as = local & 1;
       const uint32_t aphase = (local >> 1) & 1;
       float r = 1.0f;

@@ -15,7 +15,22 @@ struct GemmParams {
   float eps, alpha;
   const float* cstar;
   __nv_bfloat16* z;
+  int group_m;  // M blocks per tile group (L2 locality: A of a group stays resident while W* streams)
 };
+
+// Persistent tile order: groups of `group_m` M blocks, M fastest inside a group, so the
+// tiles in flight at any time share a few W* column blocks (each streamed from HBM
+// once per group) while the group's A rows stay in L2.
+__host__ __device__ inline void tile_coords(int tile, const GemmParams& p, int& m_blk, int& n_blk) {
+  const int G = p.group_m;
+  const int per_group = G * p.num_n_blocks;
+  const int grp = tile / per_group;
+  const int idx = tile - grp * per_group;
+  const int m0 = grp * G;
+  const int gm = (p.num_m_blocks - m0) < G ? (p.num_m_blocks - m0) : G;
+  m_blk = m0 + idx % gm;
+  n_blk = idx / gm;
+}
 
 // K3: tcgen05 prefill GEMM (gemm_sm100.cu)
 int gemm_smem_bytes();

@@ -73,7 +73,7 @@ def main(tag):
                 lines.append(f"| {label} (`{key}`) | {d[key][0]} | {d[key][1]} |")
         if "dram__bytes_read.sum" in d and "dram__bytes_write.sum" in d:
             tb = to_bytes(*d["dram__bytes_read.sum"]) + to_bytes(*d["dram__bytes_write.sum"])
-            key = "flashnorm_gemm_kernel" if name == "gemm" else "flashnorm_gemv_kernel"
+            key = kname.split("<")[0].split("(")[0].replace("void ", "").replace("fn::", "").strip()
             traffic[key] = tb
             lines.append(f"| DRAM traffic per launch (read+write) | {tb:.4g} | byte |")
         lines.append("")
