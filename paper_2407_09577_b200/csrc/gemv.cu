@@ -25,6 +25,8 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <atomic>
+
 namespace fn {
 
 namespace gv {
@@ -241,18 +243,24 @@ static cudaError_t launch_gemv_regs(const __nv_bfloat16* a, const __nv_bfloat16*
 
 // ============================================================================
 // Main decode kernel: W* streamed by the bulk-copy engine (cp.async.bulk) into
-// a shared-memory ring, tokens held in registers.
+// a shared-memory ring, tokens held in registers, tiles scheduled dynamically.
 //
-//  * warps 0..15 compute, warp 16 is the producer (one elected lane).
-//  * stage = one 8-row mma tile of W*t, full K (8 row copies into padded smem
-//    rows -> conflict-free B-fragment loads); ring of >= 2 stages (~128 KiB in
-//    flight per SM, independent of registers).
-//  * compute warp w owns the fixed K chunks [w*cpw, (w+1)*cpw): its A fragments
-//    (the M <= 16 tokens, DyT-transformed once) live in registers, so shared
-//    memory holds only the W* ring; its per-row partial ssq comes from the same
-//    registers (the RMS of Fig 8(c), computed while the first stages stream in).
+//  * warp 15 is the producer (one lane): it owns the ring and the tile schedule;
+//    warps 0..14 compute.  (16 warps keep 4 per SM sub-partition, i.e. 128
+//    registers per thread for the token fragments.)
+//  * work unit = one 8-row mma tile of W*t, full K (64 KiB at K = 4096), copied as
+//    8 row copies into padded smem rows (conflict-free B-fragment loads).  The
+//    first S tiles of every CTA are static (b, b+G, ...), the rest are taken from
+//    a global atomic counter, so SMs that start late or stream slower take fewer
+//    tiles (the kernel ends within ~1 tile of perfect balance).  The counter
+//    lives in one of FN_GEMV_SLOTS launch slots and is reset by the last CTA.
+//  * compute warp w owns a fixed K range; its A fragments (the M <= 16 tokens,
+//    DyT-transformed once) live in registers, and its per-row partial ssq comes
+//    from the same registers while the first tiles stream in — the RMS no longer
+//    sits in front of the matrix unit (Fig 8(c)).
 //  * per tile every warp parks its 16x8 partial in smem and releases the stage;
-//    the 16 partials are reduced in a fixed order once per segment of SEG tiles.
+//    warp (seq % 15) reduces the tile in a fixed order and applies * r + c*,
+//    overlapped with the stream.
 // ============================================================================
 #ifdef FN_GEMV_TRACE  // tools/micro/gemv_trace.cu: per-CTA timeline (globaltimer, ns)
 __device__ unsigned long long g_gemv_trace[148 * 8];
@@ -262,19 +270,24 @@ FN_DEVICE unsigned long long gtime() {
   return t;
 }
 #define FN_TRACE(slot) \
-  if (threadIdx.x == 0 && blockIdx.x < 148) g_gemv_trace[blockIdx.x * 8 + (slot)] = gtime()
+  if ((threadIdx.x & 31) == 0 && (slot != 1 || threadIdx.x == 0) && blockIdx.x < 148) \
+    g_gemv_trace[blockIdx.x * 8 + (slot)] = gtime()
 #else
 #define FN_TRACE(slot)
 #endif
 
 namespace gt {
-constexpr int CWARPS = 16;                 // all warps compute; warp 0 lane 0 also produces
-constexpr int THREADS = CWARPS * 32;
-constexpr int CPW_MAX = 8;                 // K <= 16 * 8 * 32 = 4096
-constexpr int SEG = 8;
-constexpr int MAX_STAGES = 8;
-constexpr int RING_BUDGET = 128 * 1024;
+constexpr int CWARPS = 15;                 // compute warps
+constexpr int PWARP = CWARPS;              // producer warp index
+constexpr int THREADS = (CWARPS + 1) * 32;
+constexpr int CPW_MAX = 9;                 // K <= 15 * 9 * 32 = 4320
+constexpr int K_MAX = 4096;                // K handled by this kernel (stage = 8 rows x K)
+constexpr int SEG = 8;                     // partial-tile slots
+constexpr int STAGES = 2;
+constexpr int SLOTS = 64;                  // launch slots of the dynamic tile counter
 }  // namespace gt
+
+__device__ unsigned int g_gemv_sched[gt::SLOTS][2];  // [slot] = {next dynamic tile, CTAs done}
 
 FN_DEVICE void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -284,48 +297,37 @@ FN_DEVICE void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* ba
       : "memory");
 }
 
-static int gemv_tma_stages(int K) {
-  const int stage = 8 * (K * 2 + 64);
-  int s = gt::RING_BUDGET / stage;
-  if (s < 2) s = 2;
-  if (s > gt::MAX_STAGES) s = gt::MAX_STAGES;
-  return s;
-}
-
 static size_t gemv_tma_smem_bytes(int K) {
-  const int S = gemv_tma_stages(K);
-  return (size_t)S * 8 * (K * 2 + 64) + (size_t)gt::SEG * gt::CWARPS * 128 * 4 + gt::CWARPS * 16 * 4 + 16 * 4 +
-         gt::CWARPS * 32 * 4 + (2 * gt::MAX_STAGES + 2 * gt::SEG) * 8;
+  return (size_t)gt::STAGES * 8 * (K * 2 + 64) + (size_t)gt::SEG * gt::CWARPS * 128 * 4 + 16 * 16 * 4 +
+         gt::CWARPS * 32 * 4 + 16 + (2 * gt::STAGES + 2 * gt::SEG) * 8;
 }
 
 template <int MODE, bool M_HI>
 __global__ void __launch_bounds__(gt::THREADS, 1)
     flashnorm_gemv_kernel(const __nv_bfloat16* __restrict__ a, const __nv_bfloat16* __restrict__ Wt,
                           const float* __restrict__ cstar, __nv_bfloat16* __restrict__ z, int M, int K, int N,
-                          float eps, float alpha, int S) {
+                          float eps, float alpha, int slot_id) {
   using namespace gt;
   extern __shared__ __align__(128) uint8_t smem[];
   const int ldb = K * 2 + 64;  // padded smem row stride (bytes)
   uint8_t* ring = smem;
-  float* part = reinterpret_cast<float*>(smem + (size_t)S * 8 * ldb);  // [SEG][CWARPS][128]
-  float* ssq_part = part + SEG * CWARPS * 128;                          // [CWARPS][16]
-  float* r_s = ssq_part + CWARPS * 16;                                  // [16]
-  float* part_fence = r_s + 16;                                         // [CWARPS*32] scratch
-  uint64_t* full = reinterpret_cast<uint64_t*>(part_fence + CWARPS * 32);  // [S]
-  uint64_t* empty = full + MAX_STAGES;                                  // [S]
-  uint64_t* part_full = empty + MAX_STAGES;                             // [SEG]
-  uint64_t* part_empty = part_full + SEG;                               // [SEG]
+  float* part = reinterpret_cast<float*>(smem + (size_t)STAGES * 8 * ldb);  // [SEG][CWARPS][128]
+  float* ssq_part = part + SEG * CWARPS * 128;                               // [16 warps][16 rows]
+  float* part_fence = ssq_part + 16 * 16;                                    // [CWARPS*32] scratch
+  int* stage_tile = reinterpret_cast<int*>(part_fence + CWARPS * 32);        // [STAGES] (+pad)
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage_tile + 4);              // [STAGES]
+  uint64_t* empty = full + STAGES;                                           // [STAGES]
+  uint64_t* part_full = empty + STAGES;                                      // [SEG]
+  uint64_t* part_empty = part_full + SEG;                                    // [SEG]
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int r0 = (int)(((long long)blockIdx.x * N) / gridDim.x);
-  const int r1 = (int)(((long long)(blockIdx.x + 1) * N) / gridDim.x);
-  const int t0 = r0 >> 3;
-  const int ntiles = r1 > r0 ? ((r1 - 1) >> 3) - t0 + 1 : 0;
+  const int ntiles = (N + 7) >> 3;
+  const int G = gridDim.x;
 
   FN_TRACE(0);
   if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) {
+    for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], CWARPS);
     }
@@ -337,190 +339,185 @@ __global__ void __launch_bounds__(gt::THREADS, 1)
   }
   __syncthreads();
 
-  // producer = lane 0 of warp 0, interleaved with its own compute: it fills the
-  // ring up front and refills a stage as soon as all 16 warps have released it
-  auto issue_tile = [&](int t, int stg) {
-    const int n0 = (t0 + t) * 8;
-    const int lo = n0 > r0 ? n0 : r0;
-    const int hi = n0 + 8 < r1 ? n0 + 8 : r1;
-    mbar_arrive_expect_tx(&full[stg], (uint32_t)(hi - lo) * K * 2);
-    for (int n = lo; n < hi; ++n)
-      bulk_g2s(ring + ((size_t)stg * 8 + (n - n0)) * ldb, Wt + (size_t)n * K, K * 2, &full[stg]);
-  };
-  if (warp == 0 && lane == 0)
-    for (int t = 0; t < ntiles && t < S; ++t) issue_tile(t, t);
-  // W* is a constant operand: it streams before the programmatic dependency on
-  // the previous kernel resolves; the tokens `a` (possibly that kernel's output)
-  // are read, and z written, only after griddepcontrol.wait.
-  pdl_wait_prior_grid();
-  pdl_launch_dependents();
-  int next_issue = ntiles < S ? ntiles : S;  // next tile the producer lane will issue
-  // non-blocking refill (lane 0 of warp 0): issue every tile whose ring slot is free
-  auto try_refill = [&]() {
-    while (next_issue < ntiles) {
-      const int stg = next_issue % S;
-      const uint32_t par = (uint32_t)((next_issue - S) / S) & 1u;
-      if (!mbar_try_wait(&empty[stg], par)) break;
-      issue_tile(next_issue, stg);
-      ++next_issue;
-    }
-  };
-
-  // -------------------------------------------------------------- compute warps
-  const int g = lane >> 2;
-  const int kq = lane & 3;
-  const int kchunks = (K + 31) >> 5;
-  const int cpw = (kchunks + CWARPS - 1) / CWARPS;  // same for all warps; <= CPW_MAX
-  const int kbase = warp * cpw;
-
-  // A fragments (tokens) for this warp's K range, in registers
-  uint4 fa[CPW_MAX], fb[CPW_MAX];
-  float s_lo = 0.f, s_hi = 0.f;
-#pragma unroll
-  for (int j = 0; j < CPW_MAX; ++j) {
-    fa[j] = make_uint4(0u, 0u, 0u, 0u);
-    fb[j] = make_uint4(0u, 0u, 0u, 0u);
-    const int k = (kbase + j) * 32 + kq * 8;
-    if (j < cpw && k < K) {
-      if (g < M) fa[j] = *reinterpret_cast<const uint4*>(a + (size_t)g * K + k);
-      if (M_HI && g + 8 < M) fb[j] = *reinterpret_cast<const uint4*>(a + (size_t)(g + 8) * K + k);
-    }
-    if (MODE == MODE_RMS) {
-      const uint32_t* wa = reinterpret_cast<const uint32_t*>(&fa[j]);
-      const uint32_t* wb = reinterpret_cast<const uint32_t*>(&fb[j]);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        float x;
-        x = bf16lo(wa[q]); s_lo = fmaf(x, x, s_lo);
-        x = bf16hi(wa[q]); s_lo = fmaf(x, x, s_lo);
-        if (M_HI) {
-          x = bf16lo(wb[q]); s_hi = fmaf(x, x, s_hi);
-          x = bf16hi(wb[q]); s_hi = fmaf(x, x, s_hi);
+  if (warp == PWARP) {
+    // -------------------------------------------------------------- producer
+    pdl_launch_dependents();  // let the next call's CTAs queue for this SM right away
+    if (elect_one()) {
+      unsigned int* sched = g_gemv_sched[slot_id];
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int k = 0;; ++k) {
+        int t;
+        if (k < STAGES) t = blockIdx.x + k * G;                                    // static prologue
+        else t = STAGES * G + (int)atomicAdd(&sched[0], 1u);                        // dynamic
+        if (k >= STAGES) mbar_wait(&empty[stage], phase ^ 1);
+        if (t >= ntiles) {  // no more work: an empty stage carrying tile -1 ends the consumers
+          stage_tile[stage] = -1;
+          mbar_arrive(&full[stage]);
+          break;
         }
+        stage_tile[stage] = t;
+        const int n0 = t * 8;
+        const int hi = n0 + 8 < N ? n0 + 8 : N;
+        mbar_arrive_expect_tx(&full[stage], (uint32_t)(hi - n0) * K * 2);
+        for (int n = n0; n < hi; ++n)
+          bulk_g2s(ring + ((size_t)stage * 8 + (n - n0)) * ldb, Wt + (size_t)n * K, K * 2, &full[stage]);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
-    if (MODE == MODE_DYT) {
-      uint32_t* wa = reinterpret_cast<uint32_t*>(&fa[j]);
-      uint32_t* wb = reinterpret_cast<uint32_t*>(&fb[j]);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        wa[q] = tanh_approx_bf16x2(pack_bf16(bf16lo(wa[q]) * alpha, bf16hi(wa[q]) * alpha));
-        if (M_HI) wb[q] = tanh_approx_bf16x2(pack_bf16(bf16lo(wb[q]) * alpha, bf16hi(wb[q]) * alpha));
-      }
-    }
-  }
-  if (MODE == MODE_RMS) {  // reduce over the 4 kq lanes: partial ssq of rows g, g+8 over this warp's K range
-    s_lo += __shfl_xor_sync(0xffffffffu, s_lo, 1);
-    s_lo += __shfl_xor_sync(0xffffffffu, s_lo, 2);
-    s_hi += __shfl_xor_sync(0xffffffffu, s_hi, 1);
-    s_hi += __shfl_xor_sync(0xffffffffu, s_hi, 2);
-    if (kq == 0) {
-      ssq_part[warp * 16 + g] = s_lo;
-      ssq_part[warp * 16 + g + 8] = s_hi;
-    }
-  }
+    // W* is a constant operand and streamed above before any dependency wait; the
+    // producer never touches a or z.
+  } else {
+    // -------------------------------------------------------------- compute warps
+    // a (possibly the previous kernel's output) is read, and z written, only after
+    // the programmatic dependency resolved
+    pdl_wait_prior_grid();
+    pdl_launch_dependents();
+    const int g = lane >> 2;
+    const int kq = lane & 3;
+    const int kchunks = (K + 31) >> 5;
+    const int kbase = (warp * kchunks) / CWARPS;
+    const int cpw = ((warp + 1) * kchunks) / CWARPS - kbase;  // <= CPW_MAX
 
-  // r_m (the deferred scale) is formed lazily by each reducing warp from the 16
-  // per-warp partial ssq: part_full of its first tile orders those writes.
-  bool have_r = false;
-  float r_row = 1.0f;  // lanes 0..15: r for row = lane
-
-  // Tile t's 16 partials are reduced by warp (t % 16) as soon as they are all
-  // parked (part_full), overlapping the reduction with the W* stream; the slot
-  // is recycled through part_empty.  No CTA-wide barrier in the loop.
-  int stage = 0;
-  uint32_t phase = 0;
-  for (int t = 0; t < ntiles; ++t) {
-    if (warp == 0) {  // the producer lane keeps refilling while it waits for data
-      uint32_t ok = 0;
-      do {
-        if (lane == 0) try_refill();
-        ok = mbar_try_wait(&full[stage], phase);
-      } while (!__all_sync(0xffffffffu, ok));
-    } else {
-      mbar_wait_warp(&full[stage], phase);
-    }
-    if (t == 0) FN_TRACE(1);
-    if (t == ntiles - 1) FN_TRACE(2);
-    const uint8_t* rowp = ring + ((size_t)stage * 8 + g) * ldb;
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    uint4 fa[CPW_MAX], fb[CPW_MAX];
+    float s_lo = 0.f, s_hi = 0.f;
 #pragma unroll
     for (int j = 0; j < CPW_MAX; ++j) {
+      fa[j] = make_uint4(0u, 0u, 0u, 0u);
+      fb[j] = make_uint4(0u, 0u, 0u, 0u);
       const int k = (kbase + j) * 32 + kq * 8;
-      if (j < cpw) {  // warp-uniform
-        uint4 w = make_uint4(0u, 0u, 0u, 0u);
-        if (k < K) w = *reinterpret_cast<const uint4*>(rowp + (size_t)k * 2);
-        mma_bf16_16816(acc, fa[j].x, fb[j].x, fa[j].y, fb[j].y, w.x, w.y);
-        mma_bf16_16816(acc, fa[j].z, fb[j].z, fa[j].w, fb[j].w, w.z, w.w);
+      if (j < cpw && k < K) {
+        if (g < M) fa[j] = *reinterpret_cast<const uint4*>(a + (size_t)g * K + k);
+        if (M_HI && g + 8 < M) fb[j] = *reinterpret_cast<const uint4*>(a + (size_t)(g + 8) * K + k);
       }
-    }
-    const int slot = t % SEG;
-    const uint32_t sphase = (uint32_t)(t / SEG) & 1u;
-    if (t >= SEG) mbar_wait_warp(&part_empty[slot], sphase ^ 1u);  // reducer of tile t-SEG done
-    // the partial store consumes the MMA results (hence the LDS above): the stage
-    // is released only after this warp's shared-memory reads have returned
-    *reinterpret_cast<float4*>(part + ((size_t)slot * CWARPS + warp) * 128 + lane * 4) =
-        make_float4(acc[0], acc[1], acc[2], acc[3]);
-    __syncwarp();
-    if (lane == 0) {
-      mbar_arrive(&empty[stage]);
-      mbar_arrive(&part_full[slot]);
-    }
-    if (warp == 0 && lane == 0) try_refill();
-    if (++stage == S) { stage = 0; phase ^= 1; }
-
-    if (warp == (t % CWARPS)) {
-      // reduce tile t: fixed-order sum over the 16 warps, deferred scale, bias, bf16 store
-      mbar_wait_warp(&part_full[slot], sphase);
-      if (MODE == MODE_RMS && !have_r) {
-        float ss = 0.f;
+      if (MODE == MODE_RMS) {
+        const uint32_t* wa = reinterpret_cast<const uint32_t*>(&fa[j]);
+        const uint32_t* wb = reinterpret_cast<const uint32_t*>(&fb[j]);
 #pragma unroll
-        for (int w = 0; w < CWARPS; ++w) ss += ssq_part[w * 16 + (lane & 15)];
-        r_row = rsqrtf(fmaf(ss, 1.0f / (float)K, eps));
-        have_r = true;
-      }
-      const float* P = part + (size_t)slot * CWARPS * 128;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int e = q * 32 + lane;
-        float sum = 0.f;
-#pragma unroll
-        for (int w = 0; w < CWARPS; ++w) sum += P[w * 128 + e];
-        const int ln = e >> 2, i = e & 3;
-        const int row = (ln >> 2) + (i >= 2 ? 8 : 0);
-        const int col = (ln & 3) * 2 + (i & 1);
-        const int n = (t0 + t) * 8 + col;
-        const float r = __shfl_sync(0xffffffffu, r_row, row);
-        if (row < M && n >= r0 && n < r1) {
-          const float cb = cstar != nullptr ? __ldg(cstar + n) : 0.0f;
-          z[(size_t)row * N + n] = __float2bfloat16_rn(fmaf(sum, MODE == MODE_RMS ? r : 1.0f, cb));
+        for (int q = 0; q < 4; ++q) {
+          float x;
+          x = bf16lo(wa[q]); s_lo = fmaf(x, x, s_lo);
+          x = bf16hi(wa[q]); s_lo = fmaf(x, x, s_lo);
+          if (M_HI) {
+            x = bf16lo(wb[q]); s_hi = fmaf(x, x, s_hi);
+            x = bf16hi(wb[q]); s_hi = fmaf(x, x, s_hi);
+          }
         }
-        part_fence[warp * 32 + lane] = sum;  // issues after every LDS of this tile returned
       }
+      if (MODE == MODE_DYT) {
+        uint32_t* wa = reinterpret_cast<uint32_t*>(&fa[j]);
+        uint32_t* wb = reinterpret_cast<uint32_t*>(&fb[j]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          wa[q] = tanh_approx_bf16x2(pack_bf16(bf16lo(wa[q]) * alpha, bf16hi(wa[q]) * alpha));
+          if (M_HI) wb[q] = tanh_approx_bf16x2(pack_bf16(bf16lo(wb[q]) * alpha, bf16hi(wb[q]) * alpha));
+        }
+      }
+    }
+    if (MODE == MODE_RMS) {  // partial ssq of rows g, g+8 over this warp's K range
+      s_lo += __shfl_xor_sync(0xffffffffu, s_lo, 1);
+      s_lo += __shfl_xor_sync(0xffffffffu, s_lo, 2);
+      s_hi += __shfl_xor_sync(0xffffffffu, s_hi, 1);
+      s_hi += __shfl_xor_sync(0xffffffffu, s_hi, 2);
+      if (kq == 0) {
+        ssq_part[warp * 16 + g] = s_lo;
+        ssq_part[warp * 16 + g + 8] = s_hi;
+      }
+    }
+
+    // r_m is formed lazily by each reducing warp from the 15 partial ssq; part_full
+    // of its first tile orders those writes.
+    bool have_r = false;
+    float r_row = 1.0f;  // lanes 0..15: r for row = lane
+    const bool row_lo = g < M;
+    const bool row_hi = g + 8 < M;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int seq = 0;; ++seq) {
+      mbar_wait_warp(&full[stage], phase);
+      const int t = stage_tile[stage];
+      if (seq == 0) FN_TRACE(1);
+      if (t < 0) break;  // producer signalled the end (warp-uniform)
+      const uint8_t* rowp = ring + ((size_t)stage * 8 + g) * ldb;
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int j = 0; j < CPW_MAX; ++j) {
+        const int k = (kbase + j) * 32 + kq * 8;
+        if (j < cpw) {  // warp-uniform
+          uint4 w = make_uint4(0u, 0u, 0u, 0u);
+          if (k < K) w = *reinterpret_cast<const uint4*>(rowp + (size_t)k * 2);
+          mma_bf16_16816(acc, fa[j].x, fb[j].x, fa[j].y, fb[j].y, w.x, w.y);
+          mma_bf16_16816(acc, fa[j].z, fb[j].z, fa[j].w, fb[j].w, w.z, w.w);
+        }
+      }
+      const int slot = seq % SEG;
+      const uint32_t sphase = (uint32_t)(seq / SEG) & 1u;
+      if (seq >= SEG) mbar_wait_warp(&part_empty[slot], sphase ^ 1u);  // reducer of seq-SEG done
+      // the partial store consumes the MMA results (hence the LDS above): the stage is
+      // released only after this warp's shared-memory reads have returned
+      *reinterpret_cast<float4*>(part + ((size_t)slot * CWARPS + warp) * 128 + lane * 4) =
+          make_float4(acc[0], acc[1], acc[2], acc[3]);
       __syncwarp();
-      if (lane == 0) mbar_arrive(&part_empty[slot]);
+      if (lane == 0) {
+        mbar_arrive(&empty[stage]);
+        mbar_arrive(&part_full[slot]);
+      }
+      if (++stage == STAGES) { stage = 0; phase ^= 1; }
+
+      if (warp == seq % CWARPS) {
+        // reduce tile t: fixed-order sum over the 15 warps, deferred scale, bias, bf16 store
+        mbar_wait_warp(&part_full[slot], sphase);
+        if (MODE == MODE_RMS && !have_r) {
+          float ss = 0.f;
+#pragma unroll
+          for (int w = 0; w < CWARPS; ++w) ss += ssq_part[w * 16 + (lane & 15)];
+          r_row = rsqrtf(fmaf(ss, 1.0f / (float)K, eps));
+          have_r = true;
+        }
+        const float* P = part + (size_t)slot * CWARPS * 128;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int e = q * 32 + lane;
+          float sum = 0.f;
+#pragma unroll
+          for (int w = 0; w < CWARPS; ++w) sum += P[w * 128 + e];
+          const int ln = e >> 2, i = e & 3;
+          const int row = (ln >> 2) + (i >= 2 ? 8 : 0);
+          const int col = (ln & 3) * 2 + (i & 1);
+          const int n = t * 8 + col;
+          const float r = __shfl_sync(0xffffffffu, r_row, row);
+          if (row < M && n < N) {
+            const float cb = cstar != nullptr ? __ldg(cstar + n) : 0.0f;
+            z[(size_t)row * N + n] = __float2bfloat16_rn(fmaf(sum, MODE == MODE_RMS ? r : 1.0f, cb));
+          }
+          part_fence[warp * 32 + lane] = sum;  // issues after every LDS of this tile returned
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&part_empty[slot]);
+      }
     }
   }
-#ifdef FN_GEMV_TRACE
-  if (lane == 0 && warp == ((ntiles - 1) % CWARPS) && blockIdx.x < 148) {
-    g_gemv_trace[blockIdx.x * 8 + 3] = gtime();
-    unsigned smid;
-    asm("mov.u32 %0, %smid;" : "=r"(smid));
-    g_gemv_trace[blockIdx.x * 8 + 4] = smid;
+  // the last CTA to finish resets this launch slot's schedule counters
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    FN_TRACE(3);
+    __threadfence();
+    if (atomicAdd(&g_gemv_sched[slot_id][1], 1u) == gridDim.x - 1) {
+      g_gemv_sched[slot_id][0] = 0u;
+      g_gemv_sched[slot_id][1] = 0u;
+      __threadfence();
+    }
   }
-#endif
 }
 
 size_t gemv_smem_bytes(int M, int K) {
-  if (K <= gt::CWARPS * gt::CPW_MAX * 32) return gemv_tma_smem_bytes(K);
+  if (K <= gt::K_MAX) return gemv_tma_smem_bytes(K);
   return gemv_regs_smem_bytes(M, K);
 }
 
 cudaError_t launch_gemv(const __nv_bfloat16* a, const __nv_bfloat16* Wt, const float* cstar, __nv_bfloat16* z,
                         int M, int K, int N, float eps, float alpha, int mode, int num_sms, cudaStream_t stream) {
-  if (K > gt::CWARPS * gt::CPW_MAX * 32)
-    return launch_gemv_regs(a, Wt, cstar, z, M, K, N, eps, alpha, mode, num_sms, stream);
-  const int S = gemv_tma_stages(K);
+  if (K > gt::K_MAX) return launch_gemv_regs(a, Wt, cstar, z, M, K, N, eps, alpha, mode, num_sms, stream);
   const size_t smem = gemv_tma_smem_bytes(K);
   const bool hi = M > 8;
   const void* fptr;
@@ -528,16 +525,20 @@ cudaError_t launch_gemv(const __nv_bfloat16* a, const __nv_bfloat16* Wt, const f
   else if (mode == MODE_DYT) fptr = hi ? (const void*)flashnorm_gemv_kernel<MODE_DYT, true> : (const void*)flashnorm_gemv_kernel<MODE_DYT, false>;
   else fptr = hi ? (const void*)flashnorm_gemv_kernel<MODE_NONE, true> : (const void*)flashnorm_gemv_kernel<MODE_NONE, false>;
   static size_t attr_set[6] = {0, 0, 0, 0, 0, 0};
-  const int slot = mode * 2 + (hi ? 1 : 0);
-  if (attr_set[slot] < smem) {
+  const int aslot = mode * 2 + (hi ? 1 : 0);
+  if (attr_set[aslot] < smem) {
     cudaError_t e = cudaFuncSetAttribute(fptr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr_set[slot] = smem;
+    attr_set[aslot] = smem;
   }
+  // one launch slot of the dynamic tile counter per call (64 slots, round robin): calls
+  // in flight at the same time (PDL overlap, other streams) use distinct counters
+  static std::atomic<unsigned> seq{0};
+  int slot_id = (int)(seq.fetch_add(1u) % gt::SLOTS);
   int grid = (N + 7) / 8;
   if (grid > num_sms) grid = num_sms;
   void* args[] = {(void*)&a, (void*)&Wt, (void*)&cstar, (void*)&z, (void*)&M, (void*)&K, (void*)&N, (void*)&eps,
-                  (void*)&alpha, (void*)&S};
+                  (void*)&alpha, (void*)&slot_id};
   // programmatic dependent launch: the W* stream of this call may start while the
   // previous kernel of the stream drains (the kernel waits before touching a / z)
   cudaLaunchConfig_t cfg = {};
