@@ -150,8 +150,17 @@ __global__ void __launch_bounds__(256)
                          double* __restrict__ mu) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= d_in) return;
+  // loads issued 16 at a time (independent), summed strictly in ascending c
   double acc = 0.0;
-  for (int64_t c = 0; c < nchunk; ++c) acc = __dadd_rn(acc, partial[c * d_in + i]);
+  int64_t c = 0;
+  for (; c + 16 <= nchunk; c += 16) {
+    double v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) v[u] = partial[(c + u) * d_in + i];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) acc = __dadd_rn(acc, v[u]);
+  }
+  for (; c < nchunk; ++c) acc = __dadd_rn(acc, partial[c * d_in + i]);
   mu[i] = __ddiv_rn(acc, (double)n_out);
 }
 

@@ -13,7 +13,7 @@ def timed(f, steps=10, warm=3):
     for _ in range(steps): f()
     e.record(); torch.cuda.synchronize()
     return s.elapsed_time(e) / steps * 1e3
-shapes = [(4096, 4096, 28672), (2048, 4096, 4096), (2048, 4096, 16384), (8192, 8192, 14336)]
+shapes = [(4096, 4096, 28672), (8192, 8192, 28672), (8192, 8192, 14336), (8192, 8192, 7168)] if len(sys.argv) < 2 else eval(sys.argv[1])
 for (M, K, N) in shapes:
     a = SD.activations(1, M, K, dev, torch.bfloat16)
     W, g, b, c = SD.layer(1, N, K, dev, torch.bfloat16, with_b=True, with_c=True)

@@ -30,7 +30,8 @@ __global__ void __launch_bounds__(NT) bulk_kernel(const uint8_t* __restrict__ p,
   auto issue = [&](int t) {
     int s = t % S; size_t off = (size_t)t * STAGE; uint32_t b = (uint32_t)((per - off) < STAGE ? (per - off) : STAGE);
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(su32(&full[s])), "r"(b));
-    for (int q = 0; q < SPLIT; ++q) { uint32_t bb = b / SPLIT;
+    const int nsplit = (b == STAGE) ? SPLIT : 1;
+    for (int q = 0; q < nsplit; ++q) { uint32_t bb = b / nsplit;
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" :: "r"(su32(sm + s * STAGE + q * bb)), "l"(base + off + q * bb), "r"(bb), "r"(su32(&full[s])) : "memory"); }
   };
   if (threadIdx.x == 0) for (int t = 0; t < nst && t < S; ++t) issue(t);
