@@ -113,7 +113,9 @@ fn_status flashnorm_fold_weights(const void* Wt, int64_t N, int64_t K, fn_dtype 
  *
  *   fold_mean_center numerics (mirrored bit-exactly on the CPU):
  *     partial[c][i] = fp64 sum of Vt[j][i], j in [32c, 32c+32) ascending
- *     s_i           = fp64 sum of partial[c][i], c ascending
+ *     s_i           = fp64: lane l (0..31) sums partial[c][i] for c = l, l+32, ...
+ *                     ascending, then the 32 lane sums are combined by an xor
+ *                     butterfly 16,8,4,2,1
  *     Vt_star[j][i] = RN_dtype( RN_f32( (double)Vt[j][i] - s_i / (double)n_out ) )
  *     b_prev_star_j = RN_f32( (double)b_prev_j - T / n_out ), T: 256 threads,
  *                     thread t sums j = t, t+256, ... ascending (fp64), xor

@@ -97,7 +97,8 @@ def fold_mean_center(Vt, b_prev, dtype="bf16"):
     (Vt_star storage, b_prev_star float32 or None, s float64[d_in]).
 
     partial[c, i] = fp64 sum over rows j in [32c, 32c+32) ascending of Vt[j, i]
-    s_i           = fp64 sum over c ascending of partial[c, i]
+    s_i           = lane l sums partial[c, i], c = l, l+32, ... ascending; the 32 lane
+                    sums are combined by the xor butterfly 16,8,4,2,1
     V*t[j, i]     = RN_dtype( RN_f32( Vt[j, i] - s_i / n_out ) )      (PAPER.md:49)
     b_prev*_j     = RN_f32( b_prev_j - mean ), mean = T / n_out where thread t of
                     256 sums j = t, t+256, ... ascending, each warp of 32 threads
@@ -113,9 +114,16 @@ def fold_mean_center(Vt, b_prev, dtype="bf16"):
         for j in range(ci * COLSUM_ROWS, min((ci + 1) * COLSUM_ROWS, n_out)):
             acc = acc + v[j]
         partial[ci] = acc
-    s = np.zeros(d_in)
-    for ci in range(nchunk):
-        s = s + partial[ci]
+    rounds = -(-nchunk // LANES)
+    padp = np.zeros((rounds * LANES, d_in))
+    padp[:nchunk] = partial
+    lane_acc = np.zeros((LANES, d_in))
+    for r in range(rounds):
+        lane_acc = lane_acc + padp[r * LANES:(r + 1) * LANES]
+    idx = np.arange(LANES)
+    for off in (16, 8, 4, 2, 1):
+        lane_acc = lane_acc + lane_acc[idx ^ off]
+    s = lane_acc[0]
     vstar = (v - (s / float(n_out))[None, :]).astype(np.float32)
     Vt_star = _store(vstar, dtype)
 
