@@ -283,7 +283,8 @@ constexpr int THREADS = (CWARPS + 1) * 32;
 constexpr int CPW_MAX = 9;                 // K <= 15 * 9 * 32 = 4320
 constexpr int K_MAX = 4096;                // K handled by this kernel (stage = 8 rows x K)
 constexpr int SEG = 8;                     // partial-tile slots
-constexpr int STAGES = 2;
+constexpr int RPU = 8;                     // W* rows per work unit / ring stage (mma n = 8: rows >= RPU are zero)
+constexpr int STAGES = 2;                  // 2 x 8 rows x K -> 128 KiB in flight per SM at K = 4096
 constexpr int SLOTS = 64;                  // launch slots of the dynamic tile counter
 }  // namespace gt
 
@@ -298,7 +299,7 @@ FN_DEVICE void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* ba
 }
 
 static size_t gemv_tma_smem_bytes(int K) {
-  return (size_t)gt::STAGES * 8 * (K * 2 + 64) + (size_t)gt::SEG * gt::CWARPS * 128 * 4 + 16 * 16 * 4 +
+  return (size_t)gt::STAGES * gt::RPU * (K * 2 + 64) + (size_t)gt::SEG * gt::CWARPS * 128 * 4 + 16 * 16 * 4 +
          gt::CWARPS * 32 * 4 + 16 + (2 * gt::STAGES + 2 * gt::SEG) * 8;
 }
 
@@ -311,7 +312,7 @@ __global__ void __launch_bounds__(gt::THREADS, 1)
   extern __shared__ __align__(128) uint8_t smem[];
   const int ldb = K * 2 + 64;  // padded smem row stride (bytes)
   uint8_t* ring = smem;
-  float* part = reinterpret_cast<float*>(smem + (size_t)STAGES * 8 * ldb);  // [SEG][CWARPS][128]
+  float* part = reinterpret_cast<float*>(smem + (size_t)STAGES * RPU * ldb);  // [SEG][CWARPS][128]
   float* ssq_part = part + SEG * CWARPS * 128;                               // [16 warps][16 rows]
   float* part_fence = ssq_part + 16 * 16;                                    // [CWARPS*32] scratch
   int* stage_tile = reinterpret_cast<int*>(part_fence + CWARPS * 32);        // [STAGES] (+pad)
@@ -322,7 +323,7 @@ __global__ void __launch_bounds__(gt::THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int ntiles = (N + 7) >> 3;
+  const int ntiles = (N + RPU - 1) / RPU;  // work units of RPU rows
   const int G = gridDim.x;
 
   FN_TRACE(0);
@@ -357,11 +358,11 @@ __global__ void __launch_bounds__(gt::THREADS, 1)
           break;
         }
         stage_tile[stage] = t;
-        const int n0 = t * 8;
-        const int hi = n0 + 8 < N ? n0 + 8 : N;
+        const int n0 = t * RPU;
+        const int hi = n0 + RPU < N ? n0 + RPU : N;
         mbar_arrive_expect_tx(&full[stage], (uint32_t)(hi - n0) * K * 2);
         for (int n = n0; n < hi; ++n)
-          bulk_g2s(ring + ((size_t)stage * 8 + (n - n0)) * ldb, Wt + (size_t)n * K, K * 2, &full[stage]);
+          bulk_g2s(ring + ((size_t)stage * RPU + (n - n0)) * ldb, Wt + (size_t)n * K, K * 2, &full[stage]);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
@@ -438,14 +439,14 @@ __global__ void __launch_bounds__(gt::THREADS, 1)
       const int t = stage_tile[stage];
       if (seq == 0) FN_TRACE(1);
       if (t < 0) break;  // producer signalled the end (warp-uniform)
-      const uint8_t* rowp = ring + ((size_t)stage * 8 + g) * ldb;
+      const uint8_t* rowp = ring + ((size_t)stage * RPU + (g < RPU ? g : 0)) * ldb;
       float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int j = 0; j < CPW_MAX; ++j) {
         const int k = (kbase + j) * 32 + kq * 8;
         if (j < cpw) {  // warp-uniform
           uint4 w = make_uint4(0u, 0u, 0u, 0u);
-          if (k < K) w = *reinterpret_cast<const uint4*>(rowp + (size_t)k * 2);
+          if (k < K && g < RPU) w = *reinterpret_cast<const uint4*>(rowp + (size_t)k * 2);
           mma_bf16_16816(acc, fa[j].x, fb[j].x, fa[j].y, fb[j].y, w.x, w.y);
           mma_bf16_16816(acc, fa[j].z, fb[j].z, fa[j].w, fb[j].w, w.z, w.w);
         }
@@ -484,9 +485,9 @@ __global__ void __launch_bounds__(gt::THREADS, 1)
           const int ln = e >> 2, i = e & 3;
           const int row = (ln >> 2) + (i >= 2 ? 8 : 0);
           const int col = (ln & 3) * 2 + (i & 1);
-          const int n = t * 8 + col;
+          const int n = t * RPU + col;
           const float r = __shfl_sync(0xffffffffu, r_row, row);
-          if (row < M && n < N) {
+          if (row < M && col < RPU && n < N) {
             const float cb = cstar != nullptr ? __ldg(cstar + n) : 0.0f;
             z[(size_t)row * N + n] = __float2bfloat16_rn(fmaf(sum, MODE == MODE_RMS ? r : 1.0f, cb));
           }
@@ -535,7 +536,7 @@ cudaError_t launch_gemv(const __nv_bfloat16* a, const __nv_bfloat16* Wt, const f
   // in flight at the same time (PDL overlap, other streams) use distinct counters
   static std::atomic<unsigned> seq{0};
   int slot_id = (int)(seq.fetch_add(1u) % gt::SLOTS);
-  int grid = (N + 7) / 8;
+  int grid = (N + gt::RPU - 1) / gt::RPU;
   if (grid > num_sms) grid = num_sms;
   void* args[] = {(void*)&a, (void*)&Wt, (void*)&cstar, (void*)&z, (void*)&M, (void*)&K, (void*)&N, (void*)&eps,
                   (void*)&alpha, (void*)&slot_id};
