@@ -198,6 +198,7 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
   p.alpha = alpha;
   p.cstar = c_star;
   p.z = static_cast<__nv_bfloat16*>(z);
+  p.a = static_cast<const __nv_bfloat16*>(a);
   cudaError_t e = pair ? fn::launch_gemm2(ta, tb, p, km, num_sms(), stream)
                        : fn::launch_gemm(ta, tb, p, km, num_sms(), stream);
   if (e != cudaSuccess) return cuda_fail(e, pair ? "gemm2_sm100" : "gemm_sm100");

@@ -15,6 +15,7 @@ struct GemmParams {
   float eps, alpha;
   const float* cstar;
   __nv_bfloat16* z;
+  const __nv_bfloat16* a;  // activations (the DyT prologue of the pair kernel reads them directly)
   int group_m;  // M blocks per tile group (L2 locality: A of a group stays resident while W* streams)
 };
 
