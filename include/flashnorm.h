@@ -156,6 +156,30 @@ fn_status flashnorm_linear_ex(const void* a, const void* Wt_star, const float* c
                               int64_t M, int64_t K, int64_t N, float eps, float alpha,
                               fn_mode mode, fn_dtype dtype, void* z, fn_path path, void* stream);
 
+/* flashnorm_linear_ws — flashnorm_linear_ex with caller-owned device scratch.
+ * For mode == FN_DYT on a bf16 GEMM path (M > 16 or an explicit GEMM path) a
+ * workspace of flashnorm_linear_workspace_bytes() = M*K*2 bytes lets the
+ * library compute RN_bf16(tanh(alpha a)) ONCE per element (kernel K8, an
+ * HBM-bound pre-pass) and then run the GEMM in mode FN_NONE
+ * on it, instead of recomputing tanh in the A-tile prologue of every N tile
+ * (MUFU tanh: ~16 values/clk/SM on sm_100a, the same rate at which the tensor
+ * core consumes A at BN = 256, DESIGN.md §6 K8).  z is bit-identical to the
+ * prologue path.  Two kernel launches instead of one.
+ *   workspace        16-B aligned device scratch, or NULL (then workspace_bytes
+ *                    must be 0 and the call is exactly flashnorm_linear_ex);
+ *                    must not alias a, Wt_star or z.  Contents on return are
+ *                    unspecified; ownership stays with the caller.
+ *   workspace_bytes  its size; FN_ERR_VALUE if a DyT GEMM needs more.
+ * Other modes / paths ignore the workspace.
+ * flashnorm_linear_workspace_bytes returns the size a call with the same
+ * arguments would use (0 = none needed). */
+int64_t flashnorm_linear_workspace_bytes(int64_t M, int64_t K, int64_t N, fn_mode mode, fn_dtype dtype,
+                                         fn_path path);
+fn_status flashnorm_linear_ws(const void* a, const void* Wt_star, const float* c_star,
+                              int64_t M, int64_t K, int64_t N, float eps, float alpha,
+                              fn_mode mode, fn_dtype dtype, void* z, fn_path path,
+                              void* workspace, int64_t workspace_bytes, void* stream);
+
 /* End-to-end variant: a_host / z_host are HOST pointers (pinned memory for
  * asynchronous copies); a_dev / z_dev are caller-owned device scratch of
  * M*K / M*N elements.  Enqueues H2D(a) -> flashnorm_linear -> D2H(z) on

@@ -22,7 +22,7 @@ from typing import Optional, Tuple
 __all__ = [
     "FlashNormError", "lib", "lib_path", "fold_weights", "fold_mean_center", "fold_mean_center_workspace_bytes",
     "linear", "linear_from_host", "baseline_norm", "gather_columns", "launch_count", "reset_launch_count",
-    "version", "MODES", "PATHS", "EXPORTS",
+    "version", "linear_workspace_bytes", "MODES", "PATHS", "EXPORTS",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -35,7 +35,8 @@ _DT_BF16, _DT_F32 = 0, 1
 # every symbol include/flashnorm.h declares
 EXPORTS = [
     "flashnorm_fold_weights", "flashnorm_fold_mean_center_workspace_bytes", "flashnorm_fold_mean_center",
-    "flashnorm_linear", "flashnorm_linear_ex", "flashnorm_linear_from_host", "flashnorm_baseline_norm",
+    "flashnorm_linear", "flashnorm_linear_ex", "flashnorm_linear_workspace_bytes", "flashnorm_linear_ws",
+    "flashnorm_linear_from_host", "flashnorm_baseline_norm",
     "flashnorm_gather_columns", "flashnorm_status_string", "flashnorm_last_error", "flashnorm_launch_count",
     "flashnorm_reset_launch_count", "flashnorm_version",
 ]
@@ -68,6 +69,8 @@ def lib() -> ctypes.CDLL:
         "flashnorm_fold_mean_center": [_vp, _i64, _i64, _int, _vp, _vp, _vp, _vp, _vp],
         "flashnorm_linear": [_vp, _vp, _vp, _i64, _i64, _i64, _f32, _f32, _int, _int, _vp, _vp],
         "flashnorm_linear_ex": [_vp, _vp, _vp, _i64, _i64, _i64, _f32, _f32, _int, _int, _vp, _int, _vp],
+        "flashnorm_linear_workspace_bytes": [_i64, _i64, _i64, _int, _int, _int],
+        "flashnorm_linear_ws": [_vp, _vp, _vp, _i64, _i64, _i64, _f32, _f32, _int, _int, _vp, _int, _vp, _i64, _vp],
         "flashnorm_linear_from_host": [_vp, _vp, _vp, _i64, _i64, _i64, _f32, _f32, _int, _int, _vp, _vp, _vp,
                                        _vp],
         "flashnorm_baseline_norm": [_vp, _vp, _vp, _i64, _i64, _f32, _int, _f32, _int, _vp, _vp],
@@ -83,6 +86,7 @@ def lib() -> ctypes.CDLL:
         f.argtypes = args
         f.restype = _int
     L.flashnorm_fold_mean_center_workspace_bytes.restype = _i64
+    L.flashnorm_linear_workspace_bytes.restype = _i64
     L.flashnorm_launch_count.restype = _i64
     L.flashnorm_reset_launch_count.restype = None
     for name in ("flashnorm_status_string", "flashnorm_last_error", "flashnorm_version"):
@@ -192,11 +196,14 @@ def fold_mean_center(Vt, b_prev=None, out=None, workspace=None):
 
 
 def linear(a, Wt_star, c_star=None, eps: float = 1e-5, mode: str = "rmsnorm", alpha: float = 0.5,
-           path: str = "auto", out=None):
+           path: str = "auto", out=None, workspace="auto"):
     """FlashNorm linear: z = (a W*) * rsqrt(mean(a^2) + eps) + c*  (PAPER.md:17, 177).
 
     a: [M, K]; Wt_star: [N, K] (same dtype, bf16 or f32); c_star: float32[N] or None.
     mode: rmsnorm | layernorm (input pre-centered via fold_mean_center) | dyt | none.
+    workspace: "auto" allocates the scratch flashnorm_linear_workspace_bytes asks for
+    (DyT on the GEMM path: tanh pre-pass, include/flashnorm.h); None forces the
+    in-kernel tanh prologue; or a caller-owned CUDA tensor.
     """
     torch = _torch()
     _dev(a, "a")
@@ -210,10 +217,27 @@ def linear(a, Wt_star, c_star=None, eps: float = 1e-5, mode: str = "rmsnorm", al
     N = Wt_star.shape[0]
     c_star = _vec(c_star, "c_star", N)
     z = out if out is not None else torch.empty((M, N), dtype=a.dtype, device=a.device)
-    st = lib().flashnorm_linear_ex(_ptr(a), _ptr(Wt_star), _ptr(c_star), M, K, N, float(eps), float(alpha),
-                                   MODES[mode], _dtype_code(a), _ptr(z), PATHS[path], _stream(a))
+    if isinstance(workspace, str):
+        if workspace != "auto":
+            raise FlashNormError(5, "linear", f"workspace must be 'auto', None or a CUDA tensor, got {workspace!r}")
+        nb = linear_workspace_bytes(M, K, N, mode, a.dtype, path)
+        workspace = torch.empty(nb, dtype=torch.uint8, device=a.device) if nb > 0 else None
+    ws_bytes = 0
+    if workspace is not None:
+        _dev(workspace, "workspace")
+        ws_bytes = workspace.numel() * workspace.element_size()
+    st = lib().flashnorm_linear_ws(_ptr(a), _ptr(Wt_star), _ptr(c_star), M, K, N, float(eps), float(alpha),
+                                   MODES[mode], _dtype_code(a), _ptr(z), PATHS[path], _ptr(workspace), ws_bytes,
+                                   _stream(a))
     _check(st, "linear")
     return z
+
+
+def linear_workspace_bytes(M: int, K: int, N: int, mode: str = "rmsnorm", dtype=None, path: str = "auto") -> int:
+    """Scratch bytes flashnorm_linear_ws would use for this call (0 = none)."""
+    torch = _torch()
+    dt = _DT_F32 if dtype == torch.float32 else _DT_BF16
+    return int(lib().flashnorm_linear_workspace_bytes(M, K, N, MODES[mode], dt, PATHS[path]))
 
 
 def linear_from_host(a_host, Wt_star, c_star, a_dev, z_dev, z_host, eps: float = 1e-5, mode: str = "rmsnorm",

@@ -125,7 +125,7 @@ int kernel_mode(fn_mode m) {
 
 fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, int64_t M, int64_t K, int64_t N,
                       float eps, float alpha, fn_mode mode, fn_dtype dtype, void* z, fn_path path,
-                      cudaStream_t stream) {
+                      void* workspace, int64_t workspace_bytes, cudaStream_t stream) {
   fn_status s;
   if ((s = check_dtype(dtype)) != FN_OK) return s;
   if (mode < FN_RMSNORM || mode > FN_NONE) return fail(FN_ERR_VALUE, "unknown fn_mode %d", (int)mode);
@@ -147,7 +147,12 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
   if (mode == FN_DYT && !std::isfinite(alpha)) return fail(FN_ERR_VALUE, "alpha = %g must be finite", (double)alpha);
   if (M == 0) return FN_OK;
   if (a == z) return fail(FN_ERR_VALUE, "z must not alias a");
-  const int km = kernel_mode(mode);
+  int km = kernel_mode(mode);
+  if (workspace != nullptr) {
+    if ((s = check_ptr16("workspace", workspace)) != FN_OK) return s;
+    if (workspace == z || workspace == a || workspace == Wt_star)
+      return fail(FN_ERR_VALUE, "workspace must not alias a, Wt_star or z");
+  }
 
   if (dtype == FN_F32) {
     if (path != FN_PATH_AUTO && path != FN_PATH_SIMT)
@@ -173,8 +178,22 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
     ++g_launches;
     return FN_OK;
   }
-  // CTA-pair (cta_group::2, 256x256 tiles) kernel for rmsnorm/layernorm/none when M > 128;
-  // the 1-CTA kernel for DyT (in-SMEM tanh prologue) and for M <= 128.
+  // DyT with a workspace: K8 computes tanh(alpha a) once per element (dyt.cu explains why the
+  // in-SMEM prologue is MUFU-bound), then the GEMM runs in mode NONE on it — bit-identical z.
+  int launches = 1;
+  if (km == fn::MODE_DYT && workspace != nullptr) {
+    if (workspace_bytes < M * K * 2)
+      return fail(FN_ERR_VALUE, "workspace_bytes = %lld < M*K*2 = %lld", (long long)workspace_bytes,
+                  (long long)(M * K * 2));
+    cudaError_t e = fn::launch_dyt_prepass(static_cast<const __nv_bfloat16*>(a), static_cast<__nv_bfloat16*>(workspace),
+                                           M * K, alpha, num_sms(), stream);
+    if (e != cudaSuccess) return cuda_fail(e, "dyt_prepass");
+    a = workspace;
+    km = fn::MODE_NONE;
+    launches = 2;
+  }
+  // CTA-pair (cta_group::2, 256x256 tiles) kernel when M > 128; the 1-CTA kernel for M <= 128
+  // and FN_PATH_GEMM1.
   const bool pair = M > 128 && (path != FN_PATH_GEMM1);
   CUtensorMap ta, tb;
   if ((s = get_tmap(a, M, K, 128, &ta)) != FN_OK) return s;
@@ -202,7 +221,7 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
   cudaError_t e = pair ? fn::launch_gemm2(ta, tb, p, km, num_sms(), stream)
                        : fn::launch_gemm(ta, tb, p, km, num_sms(), stream);
   if (e != cudaSuccess) return cuda_fail(e, pair ? "gemm2_sm100" : "gemm_sm100");
-  ++g_launches;
+  g_launches += launches;
   return FN_OK;
 }
 
@@ -262,7 +281,7 @@ fn_status flashnorm_fold_mean_center(const void* Vt, int64_t n_out, int64_t d_in
 
 fn_status flashnorm_linear(const void* a, const void* Wt_star, const float* c_star, int64_t M, int64_t K, int64_t N,
                            float eps, float alpha, fn_mode mode, fn_dtype dtype, void* z, void* stream) {
-  return linear_impl(a, Wt_star, c_star, M, K, N, eps, alpha, mode, dtype, z, FN_PATH_AUTO,
+  return linear_impl(a, Wt_star, c_star, M, K, N, eps, alpha, mode, dtype, z, FN_PATH_AUTO, nullptr, 0,
                      static_cast<cudaStream_t>(stream));
 }
 
@@ -270,7 +289,26 @@ fn_status flashnorm_linear_ex(const void* a, const void* Wt_star, const float* c
                               int64_t N, float eps, float alpha, fn_mode mode, fn_dtype dtype, void* z, fn_path path,
                               void* stream) {
   if (path < FN_PATH_AUTO || path > FN_PATH_GEMM1) return fail(FN_ERR_VALUE, "unknown fn_path %d", (int)path);
-  return linear_impl(a, Wt_star, c_star, M, K, N, eps, alpha, mode, dtype, z, path,
+  return linear_impl(a, Wt_star, c_star, M, K, N, eps, alpha, mode, dtype, z, path, nullptr, 0,
+                     static_cast<cudaStream_t>(stream));
+}
+
+int64_t flashnorm_linear_workspace_bytes(int64_t M, int64_t K, int64_t N, fn_mode mode, fn_dtype dtype,
+                                         fn_path path) {
+  if (mode != FN_DYT || dtype != FN_BF16 || M <= 0 || K <= 0 || N <= 0) return 0;
+  if (path == FN_PATH_GEMV || path == FN_PATH_SIMT) return 0;
+  const bool gemv_ok = M <= fn::GEMV_MAX_M && fn::gemv_smem_bytes((int)M, (int)K) <= 200 * 1024;
+  if (path == FN_PATH_AUTO && gemv_ok) return 0;  // decode: tanh is computed once per CTA anyway
+  return M * K * 2;
+}
+
+fn_status flashnorm_linear_ws(const void* a, const void* Wt_star, const float* c_star, int64_t M, int64_t K,
+                              int64_t N, float eps, float alpha, fn_mode mode, fn_dtype dtype, void* z, fn_path path,
+                              void* workspace, int64_t workspace_bytes, void* stream) {
+  if (path < FN_PATH_AUTO || path > FN_PATH_GEMM1) return fail(FN_ERR_VALUE, "unknown fn_path %d", (int)path);
+  if (workspace == nullptr && workspace_bytes != 0)
+    return fail(FN_ERR_NULL, "workspace is NULL but workspace_bytes = %lld", (long long)workspace_bytes);
+  return linear_impl(a, Wt_star, c_star, M, K, N, eps, alpha, mode, dtype, z, path, workspace, workspace_bytes,
                      static_cast<cudaStream_t>(stream));
 }
 
@@ -286,7 +324,8 @@ fn_status flashnorm_linear_from_host(const void* a_host, const void* Wt_star, co
   const size_t eb = (size_t)elem_bytes(dtype);
   cudaError_t e = cudaMemcpyAsync(a_dev, a_host, (size_t)M * K * eb, cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) return cuda_fail(e, "H2D a");
-  if ((s = linear_impl(a_dev, Wt_star, c_star, M, K, N, eps, alpha, mode, dtype, z_dev, FN_PATH_AUTO, st)) != FN_OK)
+  if ((s = linear_impl(a_dev, Wt_star, c_star, M, K, N, eps, alpha, mode, dtype, z_dev, FN_PATH_AUTO, nullptr, 0,
+                       st)) != FN_OK)
     return s;
   e = cudaMemcpyAsync(z_host, z_dev, (size_t)M * N * eb, cudaMemcpyDeviceToHost, st);
   if (e != cudaSuccess) return cuda_fail(e, "D2H z");

@@ -62,6 +62,9 @@ cudaError_t launch_fold_mean_center(const void* Vt, int64_t n_out, int64_t d_in,
                                     int* launches);
 
 // K6/K7: baseline norm + gather permute (aux.cu)
+// K8: y = RN_bf16(tanh(alpha a)) over n elements (n % 8 == 0), bit-identical to the GEMM prologue.
+cudaError_t launch_dyt_prepass(const __nv_bfloat16* a, __nv_bfloat16* y, int64_t n, float alpha, int num_sms,
+                               cudaStream_t stream);
 cudaError_t launch_baseline_norm(const void* a, const float* g, const float* b, int64_t M, int64_t K, float eps,
                                  int norm_kind /*0 rms,1 ln,2 dyt*/, float alpha, int dtype, void* y,
                                  cudaStream_t stream);

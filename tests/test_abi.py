@@ -84,6 +84,21 @@ def test_linear_validation_codes(L):
     assert _lin(L, M=0) == 0                                        # empty batch: no-op
 
 
+def test_linear_ws_validation_codes(L):
+    f = L.flashnorm_linear_ws
+    args = (P(0x1000), P(0x2000), None, 300, 64, 64, 1e-5, 0.5, 2, 0, P(0x3000), 0)
+    assert f(*args, None, 16, None) == 1                              # bytes without a pointer
+    assert f(*args, P(0x4008), 300 * 64 * 2, None) == 4               # misaligned workspace
+    assert f(*args, P(0x3000), 300 * 64 * 2, None) == 5               # aliases z
+    assert f(*args, P(0x4000), 300 * 64 * 2 - 16, None) == 5          # too small for the DyT pre-pass
+    assert f(*args[:11], 9, P(0x4000), 0, None) == 5                  # unknown path
+    wb = L.flashnorm_linear_workspace_bytes
+    assert wb(300, 64, 64, 2, 0, 0) == 300 * 64 * 2                   # DyT GEMM: M*K*2
+    assert wb(8, 64, 64, 2, 0, 0) == 0                                # DyT decode: none
+    assert wb(300, 64, 64, 0, 0, 0) == 0                              # rmsnorm: none
+    assert wb(300, 64, 64, 2, 1, 0) == 0                              # f32: none
+
+
 def test_fold_validation_codes(L):
     f = L.flashnorm_fold_weights
     assert f(P(0x1000), 8, 64, 0, None, P(0x4000), None, P(0x2000), None, None) == 1   # b without c_star

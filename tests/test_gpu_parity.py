@@ -112,9 +112,9 @@ def _layer_and_ref(seed, M, K, N, dtype, mode, amode="normal", eps=1e-5, alpha=0
     return a, Wt, g, b, c, ref
 
 
-def _run(a, Wt, g, b, c, dtype, mode, eps=1e-5, alpha=0.5, path="auto"):
+def _run(a, Wt, g, b, c, dtype, mode, eps=1e-5, alpha=0.5, path="auto", workspace="auto"):
     Ws, cs = fn.fold_weights(T(Wt, dtype), T(g, "f32"), T(b, "f32"), T(c, "f32"))
-    z = fn.linear(T(a, dtype), Ws, cs, eps=eps, mode=mode, alpha=alpha, path=path)
+    z = fn.linear(T(a, dtype), Ws, cs, eps=eps, mode=mode, alpha=alpha, path=path, workspace=workspace)
     torch.cuda.synchronize()
     return H(z)
 
@@ -150,6 +150,45 @@ def test_gemm_parity(M, K, N, mode, path):
     z = _run(a, Wt, g, b, c, "bf16", mode, path=path)
     err = O.rowwise_rel_err(z, ref)
     assert err <= TOL_BF16, err
+
+
+@pytest.mark.parametrize("M,K,N", GEMM_SHAPES)
+@pytest.mark.parametrize("path", ["gemm", "gemm1"])
+def test_dyt_prologue_and_prepass(M, K, N, path):
+    """DyT two ways: tanh in the A-tile prologue (workspace=None) and the K8 pre-pass into a
+    workspace followed by the NONE GEMM.  Both meet the oracle; z is bit-identical (same bf16
+    multiply + tanh.approx.bf16x2, include/flashnorm.h flashnorm_linear_ws)."""
+    a, Wt, g, b, c, ref = _layer_and_ref(3, M, K, N, "bf16", "dyt")
+    Ws, cs = fn.fold_weights(T(Wt), T(g, "f32"), T(b, "f32"), T(c, "f32"))
+    ad = T(a)
+    assert fn.linear_workspace_bytes(M, K, N, "dyt", torch.bfloat16, path) == M * K * 2
+    z_pro = fn.linear(ad, Ws, cs, mode="dyt", alpha=0.5, path=path, workspace=None)
+    ws = torch.full((M * K * 2 + 64,), 0x7F, dtype=torch.uint8, device=DEV)   # poisoned, oversized
+    n0 = fn.launch_count()
+    z_pre = fn.linear(ad, Ws, cs, mode="dyt", alpha=0.5, path=path, workspace=ws)
+    assert fn.launch_count() - n0 == 2
+    assert O.rowwise_rel_err(H(z_pro), ref) <= TOL_BF16
+    assert O.rowwise_rel_err(H(z_pre), ref) <= TOL_BF16
+    assert torch.equal(z_pro, z_pre)
+
+
+def test_linear_workspace_rules():
+    M, K, N = 256, 128, 256
+    a = SD.activations(9, M, K, DEV, torch.bfloat16)
+    Wt = SD.layer(9, N, K, DEV, torch.bfloat16)[0]
+    assert fn.linear_workspace_bytes(M, K, N, "rmsnorm", torch.bfloat16) == 0
+    assert fn.linear_workspace_bytes(8, K, N, "dyt", torch.bfloat16) == 0          # decode GEMV
+    assert fn.linear_workspace_bytes(8, K, N, "dyt", torch.bfloat16, "gemm1") == 8 * K * 2
+    assert fn.linear_workspace_bytes(M, K, N, "dyt", torch.float32) == 0
+    small = torch.empty(M * K * 2 - 16, dtype=torch.uint8, device=DEV)
+    with pytest.raises(fn.FlashNormError, match="workspace_bytes"):
+        fn.linear(a, Wt, mode="dyt", workspace=small)
+    z = torch.empty(M, N, dtype=torch.bfloat16, device=DEV)
+    with pytest.raises(fn.FlashNormError, match="alias"):
+        fn.linear(a, Wt, mode="dyt", out=z, workspace=z)
+    # non-DyT modes ignore a workspace
+    ws = torch.empty(M * K * 2, dtype=torch.uint8, device=DEV)
+    assert torch.equal(fn.linear(a, Wt, mode="rmsnorm", workspace=ws), fn.linear(a, Wt, mode="rmsnorm"))
 
 
 @pytest.mark.parametrize("amode", ["outlier", "lowenergy"])

@@ -21,8 +21,10 @@ for (M, K, N) in shapes:
     del W
     z = torch.empty(M, N, dtype=torch.bfloat16, device=dev)
     out = []
-    for mode in ("rmsnorm", "none", "dyt"):
+    ws = torch.empty(M * K * 2, dtype=torch.uint8, device=dev)
+    for mode, wsv, tag in (("rmsnorm", None, "rmsnorm"), ("none", None, "none"), ("dyt", None, "dyt-prologue"),
+                           ("dyt", ws, "dyt-prepass")):
         for path in ("gemm", "gemm1"):
-            us = timed(lambda: fn.linear(a, Ws, cs, mode=mode, path=path, out=z))
-            out.append(f"{mode}/{path}={2*M*K*N/us/1e6:.0f}")
+            us = timed(lambda: fn.linear(a, Ws, cs, mode=mode, path=path, out=z, workspace=wsv))
+            out.append(f"{tag}/{path}={2*M*K*N/us/1e6:.0f}")
     print(f"M={M} K={K} N={N} TFLOP/s: " + " ".join(out), flush=True)
