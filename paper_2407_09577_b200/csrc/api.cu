@@ -87,6 +87,24 @@ std::mutex g_tmap_mu;
 std::map<std::tuple<uintptr_t, int64_t, int64_t, int>, CUtensorMap> g_tmaps;
 
 // row-major bf16 [rows][cols], box = 64 (cols, 128 B, SW128) x box_rows
+// Plain (unswizzled) row-major map for the fold kernels: box = FOLD_BOX_BYTES x 32 rows.
+fn_status get_tmap_fold(const void* ptr, int64_t rows, int64_t cols, fn_dtype dtype, CUtensorMap* out) {
+  auto enc = encode_fn();
+  if (enc == nullptr) return fail(FN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver entry point)");
+  const int eb = dtype == FN_BF16 ? 2 : 4;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * eb};
+  cuuint32_t box[2] = {(cuuint32_t)(fn::FOLD_BOX_BYTES / eb), 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(out, dtype == FN_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                   const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(FN_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) for fold map [%lld x %lld]", (int)r,
+                (long long)rows, (long long)cols);
+  return FN_OK;
+}
+
 fn_status get_tmap(const void* ptr, int64_t rows, int64_t cols, int box_rows, CUtensorMap* out) {
   const auto key = std::make_tuple(reinterpret_cast<uintptr_t>(ptr), rows, cols, box_rows);
   std::lock_guard<std::mutex> lk(g_tmap_mu);
@@ -271,8 +289,12 @@ fn_status flashnorm_fold_mean_center(const void* Vt, int64_t n_out, int64_t d_in
       (s = check_ptr16("workspace", workspace)) != FN_OK)
     return s;
   if (Vt == Vt_star) return fail(FN_ERR_VALUE, "Vt_star must not alias Vt");
+  if (n_out > INT32_MAX || d_in > INT32_MAX)
+    return fail(FN_ERR_SHAPE, "Vt[%lld x %lld]: dimension exceeds int32 range", (long long)n_out, (long long)d_in);
+  CUtensorMap tm;
+  if ((s = get_tmap_fold(Vt, n_out, d_in, dtype, &tm)) != FN_OK) return s;
   int launches = 0;
-  cudaError_t e = fn::launch_fold_mean_center(Vt, n_out, d_in, dtype == FN_BF16 ? 0 : 1, b_prev, Vt_star,
+  cudaError_t e = fn::launch_fold_mean_center(tm, Vt, n_out, d_in, dtype == FN_BF16 ? 0 : 1, b_prev, Vt_star,
                                               b_prev_star, workspace, static_cast<cudaStream_t>(stream), &launches);
   if (e != cudaSuccess) return cuda_fail(e, "fold_mean_center");
   g_launches += launches;

@@ -111,6 +111,16 @@ constexpr uint64_t kEvictFirst = 0x12F0000000000000ull;
 constexpr uint64_t kEvictLast = 0x14F0000000000000ull;
 constexpr uint64_t kEvictNormal = 0x1000000000000000ull;
 
+// 1-D bulk copy global -> this CTA's shared memory on the bulk-copy engine, completing
+// `bytes` of transaction count on `bar` (src/dst 16-B aligned, bytes % 16 == 0).
+FN_DEVICE void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t hint = kEvictFirst) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(hint)
+      : "memory");
+}
+
 FN_DEVICE void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }

@@ -13,10 +13,14 @@
 //    pass 2  V*t[j][i] = RN(Vt[j][i] - s_i/n)
 //    The second read of Vt is L2-resident for the config-4 sizes (33.5 MB < 126 MB).
 //
-// All fp64 arithmetic uses __dmul_rn/__dadd_rn so no FMA contraction changes
-// the rounding the CPU mirror reproduces.
+// All fp64 arithmetic uses explicit _rn intrinsics so no compiler contraction changes the
+// rounding the CPU mirror reproduces; the one fused multiply-add (K1's b*w) is exact-
+// equivalent because the product is exact.  bf16/f32 -> fp64 widening is done with integer
+// ops in a 2^-896-scaled domain (widen_scaled_hi), not on the quarter-rate conversion unit.
 #include "common.cuh"
 #include "kernels.h"
+
+#include <algorithm>
 
 namespace fn {
 
@@ -26,6 +30,8 @@ constexpr int ROWS_PER_WARP = 2;  // K1: rows sharing one g/b chunk load
 constexpr int CHUNK_UNROLL = 4;   // K1: chunks per lane in flight
 constexpr int COLSUM_ROWS = 32;  // rows per fp64 partial in K2 (contract constant)
 constexpr int BPREV_THREADS = 256;
+constexpr int K2_THREADS = 256;               // K2 passes 1/2: one 4-byte column group per thread
+constexpr int K2_TILE_BYTES = K2_THREADS * 4;  // bytes of each row per CTA tile
 }  // namespace fold
 
 FN_DEVICE uint4 ld_nc_v4(const void* p) {
@@ -34,6 +40,92 @@ FN_DEVICE uint4 ld_nc_v4(const void* p) {
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                : "l"(p));
   return r;
+}
+
+// Exact float -> double WITHOUT the conversion unit.  F2F.F64.F32 issues on the quarter-rate
+// XU pipe (ncu: 66-69 % XU utilisation in K1/K2), so normal numbers are widened with integer
+// ops — exponent re-bias (+896) and a 3-bit mantissa shift — and a chunk holding a zero,
+// subnormal, inf or NaN takes the hardware conversion as a whole.  Same values, so the
+// contract arithmetic (and the CPU mirror) is unchanged.
+FN_DEVICE double widen_normal(uint32_t x) {  // x: f32 bit pattern with exponent field in 1..254
+  return __hiloint2double((int)((((x & 0x7FFFFFFFu) >> 3) + 0x38000000u) | (x & 0x80000000u)), (int)(x << 29));
+}
+
+// NW 32-bit words of DT data (bf16 pairs or f32) -> 2*NW or NW doubles, exact.
+template <int DT, int NW>
+FN_DEVICE void widen_words(const uint32_t* w, double* out) {
+  uint32_t special = 0u;
+#pragma unroll
+  for (int k = 0; k < NW; ++k) {
+    if (DT == 0) {
+      const uint32_t t = (w[k] & 0x7F807F80u) + 0x00800080u;  // exponent 0 or 255 -> bits 14..8 / 30..24 clear
+      special |= (uint32_t)((t & 0x7F00u) == 0u) | (uint32_t)((t & 0x7F000000u) == 0u);
+      out[2 * k] = widen_normal(w[k] << 16);
+      out[2 * k + 1] = widen_normal(w[k] & 0xFFFF0000u);
+    } else {
+      const uint32_t t = (w[k] & 0x7F800000u) + 0x00800000u;
+      special |= (uint32_t)((t & 0x7F000000u) == 0u);
+      out[k] = widen_normal(w[k]);
+    }
+  }
+  if (special) {
+#pragma unroll
+    for (int k = 0; k < NW; ++k) {
+      if (DT == 0) {
+        out[2 * k] = (double)__uint_as_float(w[k] << 16);
+        out[2 * k + 1] = (double)__uint_as_float(w[k] & 0xFFFF0000u);
+      } else {
+        out[k] = (double)__uint_as_float(w[k]);
+      }
+    }
+  }
+}
+
+// Scaled widening (K2): the bit pattern of a bf16/f32 value x, with its 8-bit exponent field
+// moved into the low 8 bits of the double's 11-bit field, is the double x * 2^-896 — exact for
+// normal, zero AND subnormal x (the exponent field is not re-biased, so a zero field stays a
+// zero field).  Two integer ops per value: arithmetic shift right 3 (sign copied into bits
+// 31..28), clear bits 30..28.  Inf/NaN (field 255) are NOT mapped (they become finite); the
+// callers detect them with inf_nan_mark and redo that thread's work with hardware conversions.
+// Sums of such scaled values round exactly like the unscaled sums: results >= 2^-1022 are
+// normal (same 53-bit rounding), smaller ones are multiples of the inputs' granularity
+// (>= 2^-1045) and therefore exact.  K2 multiplies by 2^896 (exact) before any division.
+constexpr double kScaleDown = 0x1p-896;
+constexpr double kScaleUp = 0x1p896;
+FN_DEVICE double widen_scaled_hi(uint32_t hi16_in_top) {  // bf16 in bits 31..16, low bits ignored
+  return __hiloint2double((int)(((int32_t)hi16_in_top >> 3) & (int32_t)0x8FFFE000), 0);
+}
+FN_DEVICE double widen_scaled_f32(uint32_t u) {
+  return __hiloint2double((int)(((int32_t)u >> 3) & (int32_t)0x8FFFFFFF), (int)(u << 29));
+}
+// running max of the exponent|mantissa fields (per 16-bit half for bf16): >= 0x7F80 / 0x7F800000
+// means an inf/NaN was seen
+template <int DT>
+FN_DEVICE uint32_t inf_nan_mark(uint32_t mark, uint32_t w) {
+  return DT == 0 ? __vmaxu2(mark, w & 0x7FFF7FFFu) : max(mark, w & 0x7FFFFFFFu);
+}
+template <int DT>
+FN_DEVICE bool inf_nan_seen(uint32_t mark) {
+  return DT == 0 ? ((mark & 0xFFFFu) >= 0x7F80u || (mark >> 16) >= 0x7F80u) : mark >= 0x7F800000u;
+}
+// one 4-byte word -> its E scaled doubles (fast path) / hardware path (exact for every input)
+template <int DT>
+FN_DEVICE void widen_word_scaled(uint32_t w, double* d) {
+  if (DT == 0) {
+    d[0] = widen_scaled_hi(w << 16);
+    d[DT == 0 ? 1 : 0] = widen_scaled_hi(w);
+  } else {
+    d[0] = widen_scaled_f32(w);
+  }
+}
+template <int DT>
+FN_DEVICE void widen_word_hw(uint32_t w, double* d) {
+  if (DT == 0) {
+    d[0] = __dmul_rn((double)__uint_as_float(w << 16), kScaleDown);
+    d[DT == 0 ? 1 : 0] = __dmul_rn((double)__uint_as_float(w & 0xFFFF0000u), kScaleDown);
+  } else {
+    d[0] = __dmul_rn((double)__uint_as_float(w), kScaleDown);
+  }
 }
 
 // element e (0..E-1) of a 16-byte chunk as float
@@ -93,22 +185,47 @@ __global__ void __launch_bounds__(fold::WARPS_PER_CTA * 32)
         bv[4 * t] = x.x; bv[4 * t + 1] = x.y; bv[4 * t + 2] = x.z; bv[4 * t + 3] = x.w;
       }
     }
+    double bd[E];  // b_i * 2^896 (exact): multiplies the 2^-896-scaled widening of w, see below
+    if (HAS_B) {
+#pragma unroll
+      for (int e = 0; e < E; e += 4) widen_words<1, 4>(reinterpret_cast<const uint32_t*>(bv + e), bd + e);
+#pragma unroll
+      for (int e = 0; e < E; ++e) bd[e] = __dmul_rn(bd[e], kScaleUp);
+    }
 #pragma unroll
     for (int r = 0; r < RPW; ++r) {
       if (j0 + r >= N) break;
       uint4 o;
       uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
+      float ws[E];
+      double wd[E];
+      if (HAS_B) {
+        // w * 2^-896 by integer ops (widen_scaled_hi); (b 2^896)(w 2^-896) is the same real
+        // product b*w, so the rounded fp64 product is identical.  inf/NaN: hardware widening.
+        const uint32_t* vw = reinterpret_cast<const uint32_t*>(&v[r]);
+        uint32_t mark = 0u;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) mark = inf_nan_mark<DT>(mark, vw[k]);
+        if (!inf_nan_seen<DT>(mark)) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) widen_word_scaled<DT>(vw[k], wd + k * (E / 4));
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) widen_word_hw<DT>(vw[k], wd + k * (E / 4));
+        }
+      }
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         const float w = chunk_elem<DT>(v[r], e);
-        if (HAS_B) acc[r] = __dadd_rn(acc[r], __dmul_rn((double)bv[e], (double)w));  // exact product, ordered sum
-        const float ws = HAS_G ? __fmul_rn(gv[e], w) : w;
-        if (DT == 0) {
-          if (e & 1) ow[e >> 1] |= (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(ws)) << 16;
-          else ow[e >> 1] = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(ws));
-        } else {
-          ow[e] = __float_as_uint(ws);
-        }
+        // b*w is exact in fp64 (24 x 8 or 24 x 24 significand bits, no underflow), so the
+        // fused multiply-add rounds exactly like add(acc, mul(b, w)) in the mirror
+        if (HAS_B) acc[r] = __fma_rn(bd[e], wd[e], acc[r]);
+        ws[e] = HAS_G ? __fmul_rn(gv[e], w) : w;
+      }
+#pragma unroll
+      for (int e = 0; e < E; e += 2) {
+        if (DT == 0) ow[e >> 1] = pack_bf16(ws[e], ws[e + 1]);  // packed RNE (F2FP, not XU)
+        else { ow[e] = __float_as_uint(ws[e]); ow[e + 1] = __float_as_uint(ws[e + 1]); }
       }
       *reinterpret_cast<uint4*>(Wt_star + ((j0 + r) * K + q * E) * ES) = o;
     }
@@ -185,140 +302,255 @@ FN_DEVICE void center_bias_block(const float* __restrict__ b_prev, int64_t n_out
     b_star[j] = __double2float_rn(__dsub_rn((double)b_prev[j], mean));
 }
 
-// pass 1b: one warp per column i: lane l sums partials c = l, l+32, ... ascending, the
-// 32 lane sums are combined by the xor butterfly 16,8,4,2,1; mu_i = s_i / n.  The
-// extra last CTA centers b_prev (independent work, same launch).
+// pass 1b: s_i in the contract order — lane-sum l (l = 0..31) is the ascending sum of the
+// partials c = l, l+32, ..., and the 32 lane sums are combined as the xor butterfly
+// 16,8,4,2,1 leaves them in lane 0, i.e. the tree  a[l] += a[l+off] for l < off,
+// off = 16,8,4,2,1 (fp addition commutes, so a[l] + a[l^off] is the same number on both
+// lanes of a butterfly pair).  Mapping for coalesced loads: a CTA owns 32 columns, lane j
+// -> column, warp w (of 8) -> lane-sums l = w, w+8, w+16, w+24; offs 16 and 8 stay in the
+// thread, offs 4,2,1 go through SMEM.  mu_i = s_i / n.  The extra last CTA centers b_prev
+// (independent work, same launch).
 __global__ void __launch_bounds__(fold::BPREV_THREADS)
     colsum_reduce_kernel(const double* __restrict__ partial, int64_t nchunk, int64_t d_in, int64_t n_out,
                          double* __restrict__ mu, const float* __restrict__ b_prev, float* __restrict__ b_star) {
   __shared__ double wsum[fold::BPREV_THREADS / 32];
   __shared__ double mean_s;
-  const int64_t ncol_blocks = (d_in + fold::BPREV_THREADS / 32 - 1) / (fold::BPREV_THREADS / 32);
+  __shared__ double lsum[8][33];
+  pdl_wait_prior_grid();  // launched with programmatic stream serialization after pass 1
+  pdl_launch_dependents();
+  const int64_t ncol_blocks = (d_in + 31) / 32;
   if ((int64_t)blockIdx.x == ncol_blocks) {
     if (b_prev != nullptr) center_bias_block(b_prev, n_out, b_star, wsum, &mean_s);
     return;
   }
-  const int lane = threadIdx.x & 31;
-  const int64_t i = (int64_t)blockIdx.x * (fold::BPREV_THREADS / 32) + (threadIdx.x >> 5);
-  if (i >= d_in) return;
-  double v[8];
-  double acc = 0.0;
-  for (int64_t c0 = lane; c0 < nchunk; c0 += 32 * 8) {
+  const int j = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t i = (int64_t)blockIdx.x * 32 + j;
+  double a[4] = {0.0, 0.0, 0.0, 0.0};  // lane-sums l = w + 8q
+  constexpr int RB = 4;                // rounds of 32 partials with loads in flight together
+  if (i < d_in) {
+    for (int64_t c0 = 0; c0 < nchunk; c0 += 32 * RB) {
+      double v[RB][4];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int64_t c = c0 + u * 32;
-      v[u] = c < nchunk ? partial[c * d_in + i] : 0.0;
-    }
+      for (int rb = 0; rb < RB; ++rb)
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (c0 + u * 32 < nchunk) acc = __dadd_rn(acc, v[u]);
-  }
+        for (int q = 0; q < 4; ++q) {
+          const int64_t c = c0 + 32 * rb + w + 8 * q;
+          v[rb][q] = c < nchunk ? __ldcg(partial + c * d_in + i) : 0.0;
+        }
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, off));
-  if (lane == 0) mu[i] = __ddiv_rn(acc, (double)n_out);
-}
-
-// pass 1: partial[cidx][i] = sum_{j in chunk cidx, ascending} Vt[j][i]
-// thread -> one 16-byte column group (E columns), block.y -> one 32-row chunk
-template <int DT>
-__global__ void __launch_bounds__(128)
-    colsum_partial_kernel(const uint8_t* __restrict__ Vt, int64_t n_out, int64_t d_in, double* __restrict__ partial) {
-  constexpr int E = DT == 0 ? 8 : 4;
-  constexpr int ES = DT == 0 ? 2 : 4;
-  const int64_t grp = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t ngrp = d_in / E;
-  if (grp >= ngrp) return;
-  const int64_t cidx = blockIdx.y;
-  const int64_t j0 = cidx * fold::COLSUM_ROWS;
-  const int64_t j1 = min(j0 + fold::COLSUM_ROWS, n_out);
-  double acc[E];
+      for (int rb = 0; rb < RB; ++rb)
 #pragma unroll
-  for (int e = 0; e < E; ++e) acc[e] = 0.0;
-  const uint8_t* p = Vt + (j0 * d_in + grp * E) * ES;
-  for (int64_t j = j0; j < j1; j += 8) {
-    uint4 v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (j + u < j1) v[u] = ld_nc_v4(p + (j - j0 + u) * d_in * ES);
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      if (j + u >= j1) break;
-#pragma unroll
-      for (int e = 0; e < E; ++e) acc[e] = __dadd_rn(acc[e], (double)chunk_elem<DT>(v[u], e));
+        for (int q = 0; q < 4; ++q)
+          if (c0 + 32 * rb + w + 8 * q < nchunk) a[q] = __dadd_rn(a[q], v[rb][q]);
     }
   }
-  double* out = partial + cidx * d_in + grp * E;
+  a[0] = __dadd_rn(a[0], a[2]);  // off 16: l = w, w+8 take l+16
+  a[1] = __dadd_rn(a[1], a[3]);
+  a[0] = __dadd_rn(a[0], a[1]);  // off 8: l = w takes l+8
+  lsum[w][j] = a[0];
+  __syncthreads();
+  if (w == 0 && i < d_in) {
+    double t[8];
 #pragma unroll
-  for (int e = 0; e < E; ++e) out[e] = acc[e];
+    for (int l = 0; l < 8; ++l) t[l] = lsum[l][j];
+#pragma unroll
+    for (int off = 4; off > 0; off >>= 1)
+#pragma unroll
+      for (int l = 0; l < off; ++l) t[l] = __dadd_rn(t[l], t[l + off]);
+    mu[i] = __ddiv_rn(__dmul_rn(t[0], kScaleUp), (double)n_out);  // partials are 2^-896-scaled
+  }
 }
 
-// pass 2: V*t = RN(Vt - s_i/n).  block.y -> 32-row chunk (second read of Vt: L2-resident).
-template <int DT>
-__global__ void __launch_bounds__(128)
-    center_kernel(const uint8_t* __restrict__ Vt, int64_t n_out, int64_t d_in, const double* __restrict__ mu_g,
-                  uint8_t* __restrict__ Vt_star) {
-  constexpr int E = DT == 0 ? 8 : 4;
+// Passes 1 and 2 stream [32 rows x 1 KiB] tiles of Vt through SMEM with TMA (two 2-D boxes
+// of 512 B x 32 rows per tile, no swizzle, completing on the stage's mbarrier): a persistent
+// grid of 3 CTAs per SM, each double-buffering 2 x 32 KiB, so the next tile is in flight
+// while the current one is summed (pass 1) or centered and stored (pass 2).  Thread t owns
+// the 4-byte column group t of a tile: box t / 128, byte (t % 128) * 4 of each box row.
+template <int DT, bool CENTER>
+__global__ void __launch_bounds__(fold::K2_THREADS)
+    k2_tiles_kernel(const __grid_constant__ CUtensorMap tm_v, int64_t n_out, int64_t d_in, int ntiles_x, int ntiles,
+                    double* __restrict__ partial, const double* __restrict__ mu_g, uint8_t* __restrict__ Vt_star) {
+  constexpr int E = DT == 0 ? 2 : 1;  // elements per 4-byte group
   constexpr int ES = DT == 0 ? 2 : 4;
-  const int64_t grp = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t ngrp = d_in / E;
-  if (grp >= ngrp) return;
-  double mu[E];
+  constexpr int BOX_COLS = FOLD_BOX_BYTES / ES;
+  constexpr int BOX_SMEM = FOLD_BOX_BYTES * fold::COLSUM_ROWS;
+  constexpr int STAGE_SMEM = fold::COLSUM_ROWS * fold::K2_TILE_BYTES;
+  extern __shared__ __align__(128) uint8_t k2_smem[];  // [2 stages][2 boxes][COLSUM_ROWS][FOLD_BOX_BYTES]
+  __shared__ __align__(8) uint64_t bar[2];
+  const int64_t row_bytes = d_in * ES;
+  const int t = threadIdx.x;
+  auto tile_geom = [&](int tile, int64_t& c0b, uint32_t& seg, int64_t& j0, int& nrows) {
+    c0b = (int64_t)(tile % ntiles_x) * fold::K2_TILE_BYTES;
+    seg = (uint32_t)min((int64_t)fold::K2_TILE_BYTES, row_bytes - c0b);
+    j0 = (int64_t)(tile / ntiles_x) * fold::COLSUM_ROWS;
+    nrows = (int)min((int64_t)fold::COLSUM_ROWS, n_out - j0);
+  };
+  auto issue = [&](int tile, int stage) {
+    int64_t c0b, j0;
+    uint32_t seg;
+    int nrows;
+    tile_geom(tile, c0b, seg, j0, nrows);
+    const int nbox = seg > (uint32_t)FOLD_BOX_BYTES ? 2 : 1;  // out-of-range rows/cols are zero-filled
+    uint8_t* dst = k2_smem + stage * STAGE_SMEM;
+    mbar_arrive_expect_tx(&bar[stage], (uint32_t)(nbox * BOX_SMEM));
+    // pass 1 keeps Vt in L2 for pass 2 (config 4: 33.5 MB < 126 MB); pass 2 is its last use
+    for (int b = 0; b < nbox; ++b)
+      tma_load_2d(dst + b * BOX_SMEM, &tm_v, &bar[stage], (int32_t)(c0b / ES + b * BOX_COLS), (int32_t)j0,
+                  CENTER ? kEvictFirst : kEvictLast);
+  };
+  if (t == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (t == 0) {  // Vt is never written by the fold kernels: prefetch before any PDL wait
+    if ((int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
+    if ((int)(blockIdx.x + gridDim.x) < ntiles) issue(blockIdx.x + gridDim.x, 1);
+  }
+  if (CENTER) pdl_wait_prior_grid();  // mu_g comes from the reduce kernel
+  else pdl_launch_dependents();
+  int k = 0;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
+    const int stage = k & 1;
+    int64_t c0b, j0;
+    uint32_t seg;
+    int nrows;
+    tile_geom(tile, c0b, seg, j0, nrows);
+    mbar_wait(&bar[stage], (uint32_t)(k >> 1) & 1u);
+    const uint8_t* src = k2_smem + stage * STAGE_SMEM + (t >> 7) * BOX_SMEM + (t & 127) * 4;
+    if ((uint32_t)t * 4 < seg) {
+      const int64_t col0 = c0b / ES + t * E;
+      const uint32_t* col = reinterpret_cast<const uint32_t*>(src);
+      constexpr int RW = FOLD_BOX_BYTES / 4;  // words per box row
+      uint32_t mark = 0u;
+      if (!CENTER) {
+        // partial sums in the 2^-896-scaled domain (exactly equivalent, see widen_scaled_hi)
+        double acc[E];
 #pragma unroll
-  for (int e = 0; e < E; ++e) mu[e] = mu_g[grp * E + e];
-  const int64_t j0 = (int64_t)blockIdx.y * fold::COLSUM_ROWS;
-  const int64_t j1 = min(j0 + fold::COLSUM_ROWS, n_out);
-  for (int64_t j = j0; j < j1; j += 8) {
-    uint4 v[8];
+        for (int e = 0; e < E; ++e) acc[e] = 0.0;
+#pragma unroll 8
+        for (int r = 0; r < nrows; ++r) {
+          const uint32_t v = col[r * RW];
+          mark = inf_nan_mark<DT>(mark, v);
+          double d[E];
+          widen_word_scaled<DT>(v, d);
 #pragma unroll
-    for (int u = 0; u < 8; ++u)  // 8 independent 16-byte loads in flight
-      if (j + u < j1) v[u] = ld_nc_v4(Vt + ((j + u) * d_in + grp * E) * ES);
+          for (int e = 0; e < E; ++e) acc[e] = __dadd_rn(acc[e], d[e]);
+        }
+        if (inf_nan_seen<DT>(mark)) {  // rare: redo with hardware conversions (inf/NaN propagate)
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      if (j + u >= j1) break;
-      uint4 o;
-      uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
+          for (int e = 0; e < E; ++e) acc[e] = 0.0;
+          for (int r = 0; r < nrows; ++r) {
+            double d[E];
+            widen_word_hw<DT>(col[r * RW], d);
 #pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const float r32 = __double2float_rn(__dsub_rn((double)chunk_elem<DT>(v[u], e), mu[e]));
-        if (DT == 0) {
-          const uint32_t hb = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(r32));
-          if (e & 1) ow[e >> 1] |= hb << 16;
-          else ow[e >> 1] = hb;
-        } else {
-          ow[e] = __float_as_uint(r32);
+            for (int e = 0; e < E; ++e) acc[e] = __dadd_rn(acc[e], d[e]);
+          }
+        }
+        double* out = partial + (j0 / fold::COLSUM_ROWS) * d_in + col0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) out[e] = acc[e];
+      } else {
+        double mu[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) mu[e] = mu_g[col0 + e];
+        uint8_t* dst = Vt_star + (j0 * d_in + col0) * ES;
+#pragma unroll 8
+        for (int r = 0; r < nrows; ++r) {
+          const uint32_t v = col[r * RW];
+          mark = inf_nan_mark<DT>(mark, v);
+          double d[E];
+          widen_word_scaled<DT>(v, d);
+          float r32[E];
+#pragma unroll
+          for (int e = 0; e < E; ++e) r32[e] = __double2float_rn(__dsub_rn(__dmul_rn(d[e], kScaleUp), mu[e]));
+          const uint32_t o = DT == 0 ? pack_bf16(r32[0], r32[E - 1]) : __float_as_uint(r32[0]);
+          *reinterpret_cast<uint32_t*>(dst + (int64_t)r * d_in * ES) = o;
+        }
+        if (inf_nan_seen<DT>(mark)) {  // rare: rewrite this column group with hardware conversions
+          for (int r = 0; r < nrows; ++r) {
+            double d[E];
+            widen_word_hw<DT>(col[r * RW], d);
+            float r32[E];
+#pragma unroll
+            for (int e = 0; e < E; ++e) r32[e] = __double2float_rn(__dsub_rn(__dmul_rn(d[e], kScaleUp), mu[e]));
+            const uint32_t o = DT == 0 ? pack_bf16(r32[0], r32[E - 1]) : __float_as_uint(r32[0]);
+            *reinterpret_cast<uint32_t*>(dst + (int64_t)r * d_in * ES) = o;
+          }
         }
       }
-      *reinterpret_cast<uint4*>(Vt_star + ((j + u) * d_in + grp * E) * ES) = o;
     }
+    // Every value read from this stage has been consumed by an issued DADD/DSUB above
+    // (in-order issue), so after the barrier no LDS of the stage is outstanding.
+    __syncthreads();
+    if (t == 0 && tile + 2 * (int)gridDim.x < ntiles) issue(tile + 2 * gridDim.x, stage);
   }
 }
 
-cudaError_t launch_fold_mean_center(const void* Vt, int64_t n_out, int64_t d_in, int dtype, const float* b_prev,
-                                    void* Vt_star, float* b_prev_star, void* workspace, cudaStream_t stream,
-                                    int* launches) {
-  const int E = dtype == 0 ? 8 : 4;
-  const int64_t ngrp = d_in / E;
+cudaError_t launch_fold_mean_center(const CUtensorMap& tm_v, const void* Vt, int64_t n_out, int64_t d_in, int dtype,
+                                    const float* b_prev, void* Vt_star, float* b_prev_star, void* workspace,
+                                    cudaStream_t stream, int* launches) {
+  const int64_t row_bytes = d_in * (dtype == 0 ? 2 : 4);
   const int64_t nchunk = (n_out + fold::COLSUM_ROWS - 1) / fold::COLSUM_ROWS;
-  const dim3 grid((unsigned)((ngrp + 127) / 128), (unsigned)nchunk);
+  const int ntiles_x = (int)((row_bytes + fold::K2_TILE_BYTES - 1) / fold::K2_TILE_BYTES);
+  const int64_t ntiles64 = (int64_t)ntiles_x * nchunk;
+  if (ntiles64 > INT32_MAX) return cudaErrorInvalidValue;
+  const int ntiles = (int)ntiles64;
   double* partial = static_cast<double*>(workspace);
-  const uint8_t* src = static_cast<const uint8_t*>(Vt);
   uint8_t* dst = static_cast<uint8_t*>(Vt_star);
   double* mu = partial + nchunk * d_in;
-  const int64_t cols_per_cta = fold::BPREV_THREADS / 32;  // one warp per column
-  const unsigned rgrid = (unsigned)((d_in + cols_per_cta - 1) / cols_per_cta + 1);  // + the b_prev CTA
+  const unsigned rgrid = (unsigned)((d_in + 31) / 32 + 1);  // + the b_prev CTA
+  constexpr size_t smem = 2 * fold::COLSUM_ROWS * fold::K2_TILE_BYTES;
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(k2_tiles_kernel<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k2_tiles_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k2_tiles_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k2_tiles_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }
+  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)sms * 3);
+  // pass 1 in plain stream order; the reduce and pass 2 with programmatic dependent launch
+  // (griddepcontrol.wait before they read the previous pass's output) to hide launch gaps.
+  cudaLaunchAttribute pdl[1];
+  pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t rcfg = {};
+  rcfg.gridDim = dim3(rgrid);
+  rcfg.blockDim = dim3(fold::BPREV_THREADS);
+  rcfg.stream = stream;
+  rcfg.attrs = pdl;
+  rcfg.numAttrs = 1;
+  cudaLaunchConfig_t ccfg = rcfg;
+  ccfg.gridDim = dim3(grid);
+  ccfg.blockDim = dim3(fold::K2_THREADS);
+  ccfg.dynamicSmemBytes = smem;
+  const int64_t no = n_out, di = d_in;
+  const int ntx = ntiles_x, nt = ntiles;
+  double* const no_partial = nullptr;
+  const double* const no_mu = nullptr;
+  uint8_t* const no_dst = nullptr;
+  cudaError_t e;
   if (dtype == 0) {
-    colsum_partial_kernel<0><<<grid, 128, 0, stream>>>(src, n_out, d_in, partial);
-    colsum_reduce_kernel<<<rgrid, fold::BPREV_THREADS, 0, stream>>>(partial, nchunk, d_in, n_out, mu, b_prev,
-                                                                     b_prev_star);
-    center_kernel<0><<<grid, 128, 0, stream>>>(src, n_out, d_in, mu, dst);
+    k2_tiles_kernel<0, false><<<grid, fold::K2_THREADS, smem, stream>>>(tm_v, no, di, ntx, nt, partial, no_mu, no_dst);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    e = cudaLaunchKernelEx(&rcfg, colsum_reduce_kernel, (const double*)partial, nchunk, di, no, mu, b_prev,
+                           b_prev_star);
+    if (e != cudaSuccess) return e;
+    e = cudaLaunchKernelEx(&ccfg, k2_tiles_kernel<0, true>, tm_v, no, di, ntx, nt, no_partial, (const double*)mu, dst);
   } else {
-    colsum_partial_kernel<1><<<grid, 128, 0, stream>>>(src, n_out, d_in, partial);
-    colsum_reduce_kernel<<<rgrid, fold::BPREV_THREADS, 0, stream>>>(partial, nchunk, d_in, n_out, mu, b_prev,
-                                                                     b_prev_star);
-    center_kernel<1><<<grid, 128, 0, stream>>>(src, n_out, d_in, mu, dst);
+    k2_tiles_kernel<1, false><<<grid, fold::K2_THREADS, smem, stream>>>(tm_v, no, di, ntx, nt, partial, no_mu, no_dst);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    e = cudaLaunchKernelEx(&rcfg, colsum_reduce_kernel, (const double*)partial, nchunk, di, no, mu, b_prev,
+                           b_prev_star);
+    if (e != cudaSuccess) return e;
+    e = cudaLaunchKernelEx(&ccfg, k2_tiles_kernel<1, true>, tm_v, no, di, ntx, nt, no_partial, (const double*)mu, dst);
   }
   *launches = 3;
-  return cudaGetLastError();
+  return e;
 }
 
 }  // namespace fn

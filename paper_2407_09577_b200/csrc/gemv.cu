@@ -290,14 +290,6 @@ constexpr int SLOTS = 64;                  // launch slots of the dynamic tile c
 
 __device__ unsigned int g_gemv_sched[gt::SLOTS][2];  // [slot] = {next dynamic tile, CTAs done}
 
-FN_DEVICE void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(kEvictFirst)
-      : "memory");
-}
-
 static size_t gemv_tma_smem_bytes(int K) {
   return (size_t)gt::STAGES * gt::RPU * (K * 2 + 64) + (size_t)gt::SEG * gt::CWARPS * 128 * 4 + 16 * 16 * 4 +
          gt::CWARPS * 32 * 4 + 16 + (2 * gt::STAGES + 2 * gt::SEG) * 8;

@@ -57,9 +57,11 @@ cudaError_t launch_linear_f32(const float* a, const float* Wt, const float* csta
 cudaError_t launch_fold_weights(const void* Wt, int64_t N, int64_t K, int dtype, const float* g, const float* b,
                                 const float* c, void* Wt_star, float* c_star, cudaStream_t stream);
 int64_t fold_mean_center_workspace(int64_t n_out, int64_t d_in);
-cudaError_t launch_fold_mean_center(const void* Vt, int64_t n_out, int64_t d_in, int dtype, const float* b_prev,
-                                    void* Vt_star, float* b_prev_star, void* workspace, cudaStream_t stream,
-                                    int* launches);
+// tm_v: plain (no swizzle) 2-D map of Vt [n_out][d_in], box FOLD_BOX_BYTES wide x 32 rows.
+constexpr int FOLD_BOX_BYTES = 512;
+cudaError_t launch_fold_mean_center(const CUtensorMap& tm_v, const void* Vt, int64_t n_out, int64_t d_in, int dtype,
+                                    const float* b_prev, void* Vt_star, float* b_prev_star, void* workspace,
+                                    cudaStream_t stream, int* launches);
 
 // K6/K7: baseline norm + gather permute (aux.cu)
 // K8: y = RN_bf16(tanh(alpha a)) over n elements (n % 8 == 0), bit-identical to the GEMM prologue.

@@ -95,6 +95,70 @@ def test_fold_mean_center_bit_exact(dtype, n_out, d_in, with_b):
         np.testing.assert_array_equal(H(bs).view(np.uint32), bm.view(np.uint32))
 
 
+def _special_matrix(rows, cols, dtype, seed=5):
+    """Values that stress the exact fp64 fold arithmetic: zero columns, bf16/f32 subnormals,
+    huge and tiny magnitudes in one column (rounding in the fp64 sums), +-inf and NaN."""
+    rng = np.random.default_rng(seed)
+    x = rng.normal(0, 0.02, (rows, cols)).astype(np.float32)
+    x[:, 0] = 0.0
+    x[:, 1] = -0.0
+    x[:, 2] = rng.choice([1e-39, -3e-40, 9.2e-41], rows).astype(np.float32)   # subnormal (bf16 too)
+    x[:, 3] = rng.choice([3e38, -2e38, 1e-30, 7.0], rows).astype(np.float32)  # wide exponent range
+    x[:, 4] = rng.normal(0, 1, rows).astype(np.float32) * np.float32(2.0 ** 100)
+    x[rows // 2, 5] = np.inf
+    x[rows // 3, 6] = -np.inf
+    x[rows // 4, 7] = np.nan
+    if dtype == "bf16":
+        from synth import bf16_round
+        x = bf16_round(x).astype(np.float32)
+    return x
+
+
+def _bits_equal_nan_aware(got_bits, want_bits, dtype):
+    if dtype == "bf16":
+        g32 = (got_bits.astype(np.uint32) << 16).view(np.float32)
+        w32 = (want_bits.astype(np.uint32) << 16).view(np.float32)
+    else:
+        g32, w32 = got_bits.view(np.float32), want_bits.view(np.float32)
+    nan = np.isnan(w32)
+    np.testing.assert_array_equal(np.isnan(g32), nan)
+    np.testing.assert_array_equal(got_bits[~nan], want_bits[~nan])
+
+
+@pytest.mark.filterwarnings("ignore::RuntimeWarning")
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("n_out", [64, 1000])
+def test_fold_mean_center_special_values(dtype, n_out):
+    """zeros, subnormals, wide exponent ranges, +-inf, NaN: still bit-exact vs the mirror
+    (the K2 kernels widen bf16/f32 to fp64 with integer ops and fall back on inf/NaN)."""
+    Vt = _special_matrix(n_out, 1032, dtype)
+    bp = np.linspace(-1, 1, n_out).astype(np.float32)
+    Vs, bs = fn.fold_mean_center(T(Vt, dtype), T(bp, "f32"))
+    torch.cuda.synchronize()
+    store = bf16_bits(Vt) if dtype == "bf16" else Vt
+    Vm, bm, _ = FM.fold_mean_center(store, bp, dtype)
+    got = bits(Vs) if dtype == "bf16" else H(Vs).view(np.uint32)
+    _bits_equal_nan_aware(got, Vm if dtype == "bf16" else Vm.view(np.uint32), dtype)
+    np.testing.assert_array_equal(H(bs).view(np.uint32), bm.view(np.uint32))
+
+
+@pytest.mark.filterwarnings("ignore::RuntimeWarning")
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_fold_weights_special_values(dtype):
+    Wt = _special_matrix(1000, 1032, dtype).T.copy()   # [N=1032, K=1000]: specials in rows
+    K = Wt.shape[1]
+    g = np.linspace(0.5, 1.5, K).astype(np.float32)
+    b = np.linspace(-0.1, 0.1, K).astype(np.float32)
+    c = np.zeros(Wt.shape[0], np.float32)
+    Ws, cs = fn.fold_weights(T(Wt, dtype), T(g, "f32"), T(b, "f32"), T(c, "f32"))
+    torch.cuda.synchronize()
+    store = bf16_bits(Wt) if dtype == "bf16" else Wt
+    Wm, cm = FM.fold_weights(store, g, b, c, dtype)
+    got = bits(Ws) if dtype == "bf16" else H(Ws).view(np.uint32)
+    _bits_equal_nan_aware(got, Wm if dtype == "bf16" else Wm.view(np.uint32), dtype)
+    _bits_equal_nan_aware(H(cs).view(np.uint32), cm.view(np.uint32), "f32")
+
+
 # ============================================================ linear: f32 path (config 1)
 
 def _layer_and_ref(seed, M, K, N, dtype, mode, amode="normal", eps=1e-5, alpha=0.5, bias=True, tiny=False):
