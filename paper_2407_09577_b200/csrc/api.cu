@@ -182,7 +182,7 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
     return FN_OK;
   }
 
-  const bool gemv_ok = M <= fn::GEMV_MAX_M && fn::gemv_smem_bytes((int)M, (int)K) <= 200 * 1024;
+  const bool gemv_ok = fn::gemv_supported((int)M, (int)K);
   if (path == FN_PATH_SIMT) return fail(FN_ERR_UNSUPPORTED, "SIMT path is f32-only");
   if (path == FN_PATH_GEMV && !gemv_ok)
     return fail(FN_ERR_UNSUPPORTED, "decode path needs M <= 16 and M*K*2 <= ~192 KiB (M=%lld K=%lld)",
@@ -319,7 +319,7 @@ int64_t flashnorm_linear_workspace_bytes(int64_t M, int64_t K, int64_t N, fn_mod
                                          fn_path path) {
   if (mode != FN_DYT || dtype != FN_BF16 || M <= 0 || K <= 0 || N <= 0) return 0;
   if (path == FN_PATH_GEMV || path == FN_PATH_SIMT) return 0;
-  const bool gemv_ok = M <= fn::GEMV_MAX_M && fn::gemv_smem_bytes((int)M, (int)K) <= 200 * 1024;
+  const bool gemv_ok = fn::gemv_supported((int)M, (int)K);
   if (path == FN_PATH_AUTO && gemv_ok) return 0;  // decode: tanh is computed once per CTA anyway
   return M * K * 2;
 }

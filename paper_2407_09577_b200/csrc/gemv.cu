@@ -253,7 +253,9 @@ static cudaError_t launch_gemv_regs(const __nv_bfloat16* a, const __nv_bfloat16*
 //    first S tiles of every CTA are static (b, b+G, ...), the rest are taken from
 //    a global atomic counter, so SMs that start late or stream slower take fewer
 //    tiles (the kernel ends within ~1 tile of perfect balance).  The counter
-//    lives in one of FN_GEMV_SLOTS launch slots and is reset by the last CTA.
+//    lives in one of gt::SLOTS launch slots; the CTA whose fetch is the launch's
+//    last (the total number of fetches is known) stores 0 back — no end-of-kernel
+//    atomics or fences, and graph replays find it reset.
 //  * compute warp w owns a fixed K range; its A fragments (the M <= 16 tokens,
 //    DyT-transformed once) live in registers, and its per-row partial ssq comes
 //    from the same registers while the first tiles stream in — the RMS no longer
@@ -263,17 +265,21 @@ static cudaError_t launch_gemv_regs(const __nv_bfloat16* a, const __nv_bfloat16*
 //    overlapped with the stream.
 // ============================================================================
 #ifdef FN_GEMV_TRACE  // tools/micro/gemv_trace.cu: per-CTA timeline (globaltimer, ns)
-__device__ unsigned long long g_gemv_trace[148 * 8];
+__device__ unsigned long long g_gemv_trace[2][148 * 8];  // [launch slot parity]
 FN_DEVICE unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+__device__ unsigned long long g_gemv_ttrace[2][16][6];  // block 0: per seq event times
+#define FN_TTRACE(seq, ev) \
+  if (blockIdx.x == 0 && (seq) < 16) g_gemv_ttrace[slot_id & 1][(seq)][(ev)] = gtime()
 #define FN_TRACE(slot) \
   if ((threadIdx.x & 31) == 0 && (slot != 1 || threadIdx.x == 0) && blockIdx.x < 148) \
-    g_gemv_trace[blockIdx.x * 8 + (slot)] = gtime()
+    g_gemv_trace[slot_id & 1][blockIdx.x * 8 + (slot)] = gtime()
 #else
 #define FN_TRACE(slot)
+#define FN_TTRACE(seq, ev)
 #endif
 
 namespace gt {
@@ -282,24 +288,37 @@ constexpr int PWARP = CWARPS;              // producer warp index
 constexpr int THREADS = (CWARPS + 1) * 32;
 constexpr int CPW_MAX = 9;                 // K <= 15 * 9 * 32 = 4320
 constexpr int K_MAX = 4096;                // K handled by this kernel (stage = 8 rows x K)
-constexpr int SEG = 8;                     // partial-tile slots
+constexpr int SEG = 4;                     // partial-tile slots
 constexpr int RPU = 8;                     // W* rows per work unit / ring stage (mma n = 8: rows >= RPU are zero)
-constexpr int STAGES = 2;                  // 2 x 8 rows x K -> 128 KiB in flight per SM at K = 4096
+constexpr int MAX_STAGES = 4;              // ring depth: as many 8-row stages as fit (3 at K = 4096)
 constexpr int SLOTS = 64;                  // launch slots of the dynamic tile counter
+// Dynamic SMEM budget of the one CTA per SM (227 KiB opt-in).  The ring is sized to fill
+// it: W* prefetched before griddepcontrol.wait keeps HBM busy across the dependency on
+// the previous kernel of the stream (PDL), which a 2-stage ring could not.
+constexpr size_t SMEM_BUDGET = 232448;
 }  // namespace gt
 
-__device__ unsigned int g_gemv_sched[gt::SLOTS][2];  // [slot] = {next dynamic tile, CTAs done}
+__device__ unsigned int g_gemv_sched[gt::SLOTS];  // [slot] = next dynamic tile (0 between launches)
 
+static size_t gemv_fixed_smem_bytes() {
+  return (size_t)gt::SEG * gt::CWARPS * 128 * 4 + 16 * 16 * 4 + gt::CWARPS * 32 * 4 + 16 +
+         (2 * gt::MAX_STAGES + 2 * gt::SEG) * 8;
+}
+static int gemv_stages(int K) {
+  const size_t per = (size_t)gt::RPU * (K * 2 + 64);
+  size_t n = (gt::SMEM_BUDGET - gemv_fixed_smem_bytes()) / per;
+  if (n > (size_t)gt::MAX_STAGES) n = gt::MAX_STAGES;
+  return n < 2 ? 2 : (int)n;
+}
 static size_t gemv_tma_smem_bytes(int K) {
-  return (size_t)gt::STAGES * gt::RPU * (K * 2 + 64) + (size_t)gt::SEG * gt::CWARPS * 128 * 4 + 16 * 16 * 4 +
-         gt::CWARPS * 32 * 4 + 16 + (2 * gt::STAGES + 2 * gt::SEG) * 8;
+  return (size_t)gemv_stages(K) * gt::RPU * (K * 2 + 64) + gemv_fixed_smem_bytes();
 }
 
 template <int MODE, bool M_HI>
 __global__ void __launch_bounds__(gt::THREADS, 1)
     flashnorm_gemv_kernel(const __nv_bfloat16* __restrict__ a, const __nv_bfloat16* __restrict__ Wt,
                           const float* __restrict__ cstar, __nv_bfloat16* __restrict__ z, int M, int K, int N,
-                          float eps, float alpha, int slot_id) {
+                          float eps, float alpha, int slot_id, int STAGES) {
   using namespace gt;
   extern __shared__ __align__(128) uint8_t smem[];
   const int ldb = K * 2 + 64;  // padded smem row stride (bytes)
@@ -307,10 +326,10 @@ __global__ void __launch_bounds__(gt::THREADS, 1)
   float* part = reinterpret_cast<float*>(smem + (size_t)STAGES * RPU * ldb);  // [SEG][CWARPS][128]
   float* ssq_part = part + SEG * CWARPS * 128;                               // [16 warps][16 rows]
   float* part_fence = ssq_part + 16 * 16;                                    // [CWARPS*32] scratch
-  int* stage_tile = reinterpret_cast<int*>(part_fence + CWARPS * 32);        // [STAGES] (+pad)
+  int* stage_tile = reinterpret_cast<int*>(part_fence + CWARPS * 32);        // [MAX_STAGES]
   uint64_t* full = reinterpret_cast<uint64_t*>(stage_tile + 4);              // [STAGES]
-  uint64_t* empty = full + STAGES;                                           // [STAGES]
-  uint64_t* part_full = empty + STAGES;                                      // [SEG]
+  uint64_t* empty = full + MAX_STAGES;                                       // [STAGES]
+  uint64_t* part_full = empty + MAX_STAGES;                                  // [SEG]
   uint64_t* part_empty = part_full + SEG;                                    // [SEG]
 
   const int warp = threadIdx.x >> 5;
@@ -336,20 +355,35 @@ __global__ void __launch_bounds__(gt::THREADS, 1)
     // -------------------------------------------------------------- producer
     pdl_launch_dependents();  // let the next call's CTAs queue for this SM right away
     if (elect_one()) {
-      unsigned int* sched = g_gemv_sched[slot_id];
+      unsigned int* sched = &g_gemv_sched[slot_id];
+      // fetches this launch makes: every dynamic tile once, plus one failing fetch by each
+      // CTA whose static tiles are all valid; the fetch returning total-1 is the last one
+      const int n_dyn_tiles = ntiles > STAGES * G ? ntiles - STAGES * G : 0;
+      int n_dyn_ctas = ntiles - (STAGES - 1) * G;
+      n_dyn_ctas = n_dyn_ctas < 0 ? 0 : (n_dyn_ctas > G ? G : n_dyn_ctas);
+      const unsigned total_fetches = (unsigned)(n_dyn_tiles + n_dyn_ctas);
       int stage = 0;
       uint32_t phase = 0;
       for (int k = 0;; ++k) {
         int t;
         if (k < STAGES) t = blockIdx.x + k * G;                                    // static prologue
-        else t = STAGES * G + (int)atomicAdd(&sched[0], 1u);                        // dynamic
+        else {                                                                      // dynamic
+          const unsigned f = atomicAdd(sched, 1u);
+          if (f == total_fetches - 1u) *sched = 0u;  // last fetch of this launch: reset the slot
+          t = STAGES * G + (int)f;
+        }
         if (k >= STAGES) mbar_wait(&empty[stage], phase ^ 1);
         if (t >= ntiles) {  // no more work: an empty stage carrying tile -1 ends the consumers
+#ifdef FN_GEMV_TRACE
+          g_gemv_trace[slot_id & 1][blockIdx.x * 8 + 6] = gtime();
+          g_gemv_trace[slot_id & 1][blockIdx.x * 8 + 7] = (unsigned long long)k;
+#endif
           stage_tile[stage] = -1;
           mbar_arrive(&full[stage]);
           break;
         }
         stage_tile[stage] = t;
+        FN_TTRACE(k, 0);
         const int n0 = t * RPU;
         const int hi = n0 + RPU < N ? n0 + RPU : N;
         mbar_arrive_expect_tx(&full[stage], (uint32_t)(hi - n0) * K * 2);
@@ -366,6 +400,7 @@ __global__ void __launch_bounds__(gt::THREADS, 1)
     // the programmatic dependency resolved
     pdl_wait_prior_grid();
     pdl_launch_dependents();
+    if (warp == 0) FN_TRACE(2);
     const int g = lane >> 2;
     const int kq = lane & 3;
     const int kchunks = (K + 31) >> 5;
@@ -430,6 +465,7 @@ __global__ void __launch_bounds__(gt::THREADS, 1)
       mbar_wait_warp(&full[stage], phase);
       const int t = stage_tile[stage];
       if (seq == 0) FN_TRACE(1);
+      if (warp == 0 && lane == 0) FN_TTRACE(seq, 1);
       if (t < 0) break;  // producer signalled the end (warp-uniform)
       const uint8_t* rowp = ring + ((size_t)stage * RPU + (g < RPU ? g : 0)) * ldb;
       float acc[4] = {0.f, 0.f, 0.f, 0.f};
@@ -454,6 +490,8 @@ __global__ void __launch_bounds__(gt::THREADS, 1)
       if (lane == 0) {
         mbar_arrive(&empty[stage]);
         mbar_arrive(&part_full[slot]);
+        if (warp == 0) FN_TTRACE(seq, 2);
+        if (warp == CWARPS - 1) FN_TTRACE(seq, 4);
       }
       if (++stage == STAGES) { stage = 0; phase ^= 1; }
 
@@ -487,25 +525,31 @@ __global__ void __launch_bounds__(gt::THREADS, 1)
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&part_empty[slot]);
+        if (lane == 0) FN_TTRACE(seq, 3);
       }
     }
   }
-  // the last CTA to finish resets this launch slot's schedule counters
+#ifdef FN_GEMV_TRACE
   __syncthreads();
   if (threadIdx.x == 0) {
     FN_TRACE(3);
-    __threadfence();
-    if (atomicAdd(&g_gemv_sched[slot_id][1], 1u) == gridDim.x - 1) {
-      g_gemv_sched[slot_id][0] = 0u;
-      g_gemv_sched[slot_id][1] = 0u;
-      __threadfence();
-    }
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_gemv_trace[slot_id & 1][blockIdx.x * 8 + 4] = smid;
+    FN_TRACE(5);
   }
+#endif
 }
 
 size_t gemv_smem_bytes(int M, int K) {
   if (K <= gt::K_MAX) return gemv_tma_smem_bytes(K);
   return gemv_regs_smem_bytes(M, K);
+}
+
+bool gemv_supported(int M, int K) {
+  if (M < 1 || M > GEMV_MAX_M) return false;
+  if (K <= gt::K_MAX) return true;                       // ring kernel: always fits (>= 2 stages)
+  return gemv_regs_smem_bytes(M, K) <= 200 * 1024;       // register-streaming kernel
 }
 
 cudaError_t launch_gemv(const __nv_bfloat16* a, const __nv_bfloat16* Wt, const float* cstar, __nv_bfloat16* z,
@@ -530,8 +574,9 @@ cudaError_t launch_gemv(const __nv_bfloat16* a, const __nv_bfloat16* Wt, const f
   int slot_id = (int)(seq.fetch_add(1u) % gt::SLOTS);
   int grid = (N + gt::RPU - 1) / gt::RPU;
   if (grid > num_sms) grid = num_sms;
+  int nst = gemv_stages(K);
   void* args[] = {(void*)&a, (void*)&Wt, (void*)&cstar, (void*)&z, (void*)&M, (void*)&K, (void*)&N, (void*)&eps,
-                  (void*)&alpha, (void*)&slot_id};
+                  (void*)&alpha, (void*)&slot_id, (void*)&nst};
   // programmatic dependent launch: the W* stream of this call may start while the
   // previous kernel of the stream drains (the kernel waits before touching a / z)
   cudaLaunchConfig_t cfg = {};

@@ -45,6 +45,7 @@ cudaError_t launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb_half, cons
 
 // K4: decode GEMV, M <= 16 (gemv.cu)
 constexpr int GEMV_MAX_M = 16;
+bool gemv_supported(int M, int K);  // decode kernel handles this (M, K)
 size_t gemv_smem_bytes(int M, int K);
 cudaError_t launch_gemv(const __nv_bfloat16* a, const __nv_bfloat16* Wt, const float* cstar, __nv_bfloat16* z,
                         int M, int K, int N, float eps, float alpha, int mode, int num_sms, cudaStream_t stream);
