@@ -65,12 +65,14 @@ typedef enum {
 typedef enum { FN_BF16 = 0, FN_F32 = 1 } fn_dtype;
 
 typedef enum {
-    FN_PATH_AUTO = 0,    /* M <= 16 (and M*K*2 <= 128 KiB): decode GEMV, else tcgen05 GEMM */
+    FN_PATH_AUTO = 0,    /* M <= 16: decode kernel, else tcgen05 GEMM                       */
     FN_PATH_GEMM = 1,    /* force the tcgen05/TMEM/TMA kernel (bf16 only)                   */
-    FN_PATH_GEMV = 2,    /* force the decode kernel (bf16, M <= 16)                         */
+    FN_PATH_GEMV = 2,    /* force the decode kernel (bf16, M <= 16): the tcgen05 split-K
+                            kernel when ceil(N/128) <= #SMs, else the mma.sync kernel       */
     FN_PATH_SIMT = 3,    /* the fp32 FFMA kernel (the only path for FN_F32)                 */
-    FN_PATH_GEMM1 = 4    /* force the 1-CTA tcgen05 kernel (FN_PATH_GEMM picks the CTA-pair
-                            cta_group::2 kernel for rmsnorm/layernorm/none when M > 128)    */
+    FN_PATH_GEMM1 = 4,   /* force the 1-CTA tcgen05 kernel (FN_PATH_GEMM picks the CTA-pair
+                            cta_group::2 kernel when M > 128)                               */
+    FN_PATH_GEMV_MMA = 5 /* force the mma.sync decode kernel (comparison / fallback)        */
 } fn_path;
 
 /* --------------------------------------------------------------------------

@@ -29,7 +29,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 lib_path = os.path.join(_HERE, "libflashnorm.so")
 
 MODES = {"rmsnorm": 0, "layernorm": 1, "dyt": 2, "none": 3}
-PATHS = {"auto": 0, "gemm": 1, "gemv": 2, "simt": 3, "gemm1": 4}
+PATHS = {"auto": 0, "gemm": 1, "gemv": 2, "simt": 3, "gemm1": 4, "gemv_mma": 5}
 _DT_BF16, _DT_F32 = 0, 1
 
 # every symbol include/flashnorm.h declares

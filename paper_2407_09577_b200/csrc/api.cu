@@ -182,12 +182,24 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
     return FN_OK;
   }
 
-  const bool gemv_ok = fn::gemv_supported((int)M, (int)K);
+  const bool tc_ok = fn::gemv_tc_supported((int)M, (int)N, num_sms());
+  const bool mma_ok = fn::gemv_supported((int)M, (int)K);
+  const bool gemv_ok = tc_ok || mma_ok;
   if (path == FN_PATH_SIMT) return fail(FN_ERR_UNSUPPORTED, "SIMT path is f32-only");
-  if (path == FN_PATH_GEMV && !gemv_ok)
+  if ((path == FN_PATH_GEMV && !gemv_ok) || (path == FN_PATH_GEMV_MMA && !mma_ok))
     return fail(FN_ERR_UNSUPPORTED, "decode path needs M <= 16 and M*K*2 <= ~192 KiB (M=%lld K=%lld)",
                 (long long)M, (long long)K);
-  const bool use_gemv = path == FN_PATH_GEMV || (path == FN_PATH_AUTO && gemv_ok);
+  const bool use_gemv = path == FN_PATH_GEMV || path == FN_PATH_GEMV_MMA || (path == FN_PATH_AUTO && gemv_ok);
+  if (use_gemv && path != FN_PATH_GEMV_MMA && tc_ok) {
+    CUtensorMap tw, ta;
+    if ((s = get_tmap(Wt_star, N, K, 128, &tw)) != FN_OK) return s;
+    if ((s = get_tmap(a, M, K, 16, &ta)) != FN_OK) return s;
+    cudaError_t e = fn::launch_gemv_tc(tw, ta, c_star, static_cast<__nv_bfloat16*>(z), (int)M, (int)K, (int)N, eps,
+                                       alpha, km, num_sms(), stream);
+    if (e != cudaSuccess) return cuda_fail(e, "gemv_tc");
+    ++g_launches;
+    return FN_OK;
+  }
   if (use_gemv) {
     cudaError_t e = fn::launch_gemv(static_cast<const __nv_bfloat16*>(a), static_cast<const __nv_bfloat16*>(Wt_star),
                                     c_star, static_cast<__nv_bfloat16*>(z), (int)M, (int)K, (int)N, eps, alpha, km,
@@ -310,7 +322,7 @@ fn_status flashnorm_linear(const void* a, const void* Wt_star, const float* c_st
 fn_status flashnorm_linear_ex(const void* a, const void* Wt_star, const float* c_star, int64_t M, int64_t K,
                               int64_t N, float eps, float alpha, fn_mode mode, fn_dtype dtype, void* z, fn_path path,
                               void* stream) {
-  if (path < FN_PATH_AUTO || path > FN_PATH_GEMM1) return fail(FN_ERR_VALUE, "unknown fn_path %d", (int)path);
+  if (path < FN_PATH_AUTO || path > FN_PATH_GEMV_MMA) return fail(FN_ERR_VALUE, "unknown fn_path %d", (int)path);
   return linear_impl(a, Wt_star, c_star, M, K, N, eps, alpha, mode, dtype, z, path, nullptr, 0,
                      static_cast<cudaStream_t>(stream));
 }
@@ -318,8 +330,8 @@ fn_status flashnorm_linear_ex(const void* a, const void* Wt_star, const float* c
 int64_t flashnorm_linear_workspace_bytes(int64_t M, int64_t K, int64_t N, fn_mode mode, fn_dtype dtype,
                                          fn_path path) {
   if (mode != FN_DYT || dtype != FN_BF16 || M <= 0 || K <= 0 || N <= 0) return 0;
-  if (path == FN_PATH_GEMV || path == FN_PATH_SIMT) return 0;
-  const bool gemv_ok = fn::gemv_supported((int)M, (int)K);
+  if (path == FN_PATH_GEMV || path == FN_PATH_GEMV_MMA || path == FN_PATH_SIMT) return 0;
+  const bool gemv_ok = fn::gemv_tc_supported((int)M, (int)N, num_sms()) || fn::gemv_supported((int)M, (int)K);
   if (path == FN_PATH_AUTO && gemv_ok) return 0;  // decode: tanh is computed once per CTA anyway
   return M * K * 2;
 }
@@ -327,7 +339,7 @@ int64_t flashnorm_linear_workspace_bytes(int64_t M, int64_t K, int64_t N, fn_mod
 fn_status flashnorm_linear_ws(const void* a, const void* Wt_star, const float* c_star, int64_t M, int64_t K,
                               int64_t N, float eps, float alpha, fn_mode mode, fn_dtype dtype, void* z, fn_path path,
                               void* workspace, int64_t workspace_bytes, void* stream) {
-  if (path < FN_PATH_AUTO || path > FN_PATH_GEMM1) return fail(FN_ERR_VALUE, "unknown fn_path %d", (int)path);
+  if (path < FN_PATH_AUTO || path > FN_PATH_GEMV_MMA) return fail(FN_ERR_VALUE, "unknown fn_path %d", (int)path);
   if (workspace == nullptr && workspace_bytes != 0)
     return fail(FN_ERR_NULL, "workspace is NULL but workspace_bytes = %lld", (long long)workspace_bytes);
   return linear_impl(a, Wt_star, c_star, M, K, N, eps, alpha, mode, dtype, z, path, workspace, workspace_bytes,

@@ -276,13 +276,28 @@ def test_gemm_eps_placement_detectable():
 # ============================================================ linear: bf16 decode GEMV
 
 @pytest.mark.parametrize("M", [1, 5, 16])
-@pytest.mark.parametrize("K,N", [(4096, 6144), (1000, 24), (8192, 136)])
+@pytest.mark.parametrize("K,N", [(4096, 6144), (1000, 24), (8192, 136), (64, 8), (4160, 20000), (2048, 4104)])
 @pytest.mark.parametrize("mode", ["rmsnorm", "dyt", "none"])
-def test_gemv_parity(M, K, N, mode):
+@pytest.mark.parametrize("path", ["gemv", "gemv_mma"])
+def test_gemv_parity(M, K, N, mode, path):
+    """gemv: tcgen05 split-K decode kernel (clusters of up to 8 CTAs; N=20000 has more 128-row
+    tiles than SMs and falls back to mma.sync); gemv_mma: the mma.sync decode kernel."""
+    if path == "gemv_mma" and M * K * 2 > 150 * 1024:
+        path = "auto"
     a, Wt, g, b, c, ref = _layer_and_ref(6, M, K, N, "bf16", mode)
-    path = "gemv" if M * K * 2 <= 150 * 1024 else "auto"
     z = _run(a, Wt, g, b, c, "bf16", mode, path=path)
     assert O.rowwise_rel_err(z, ref) <= TOL_BF16
+
+
+@pytest.mark.parametrize("M,K,N", [(1, 4096, 6144), (16, 4096, 6144), (3, 8192, 1024)])
+@pytest.mark.parametrize("mode", ["rmsnorm", "dyt"])
+def test_gemv_repeated_launches_bit_identical(M, K, N, mode):
+    """split-K partials are summed in fixed rank order: every launch gives the same bits"""
+    a = SD.activations(41, M, K, DEV, torch.bfloat16)
+    Wt = SD.layer(41, N, K, DEV, torch.bfloat16)[0]
+    z0 = fn.linear(a, Wt, mode=mode, path="gemv")
+    for _ in range(5):
+        assert torch.equal(fn.linear(a, Wt, mode=mode, path="gemv"), z0)
 
 
 def test_decode_and_prefill_paths_agree():
