@@ -192,7 +192,7 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
   const bool use_gemv = path == FN_PATH_GEMV || path == FN_PATH_GEMV_MMA || (path == FN_PATH_AUTO && gemv_ok);
   if (use_gemv && path != FN_PATH_GEMV_MMA && tc_ok) {
     CUtensorMap tw, ta;
-    if ((s = get_tmap(Wt_star, N, K, 128, &tw)) != FN_OK) return s;
+    if ((s = get_tmap(Wt_star, N, K, fn::gemv_tc_tile_rows(km, (int)K, (int)N, num_sms()), &tw)) != FN_OK) return s;
     if ((s = get_tmap(a, M, K, 16, &ta)) != FN_OK) return s;
     cudaError_t e = fn::launch_gemv_tc(tw, ta, c_star, static_cast<__nv_bfloat16*>(z), (int)M, (int)K, (int)N, eps,
                                        alpha, km, num_sms(), stream);

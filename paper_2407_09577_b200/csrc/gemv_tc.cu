@@ -33,30 +33,33 @@
 
 #include <algorithm>
 #include <atomic>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 namespace fn {
 
 namespace dtc {
-constexpr int ROWS = 128;               // W* rows per tile (MMA M)
+constexpr int ROWS = 128;               // W* rows per MMA (M)
 constexpr int TOK = 16;                 // token rows (MMA N; rows >= M are TMA zero-fill)
 constexpr int BK = 64;                  // k per stage (one SW128 atom row of bf16)
-constexpr int STAGES = 12;  // 216 KiB ring: W* prefetched before griddepcontrol.wait
-constexpr int W_STAGE = ROWS * BK * 2;  // 16 KiB
 constexpr int T_STAGE = TOK * BK * 2;   // 2 KiB
 constexpr int THREADS = 192;
-constexpr int TMEM_COLS = 32;           // minimum allocation; D uses columns [0, 16)
-constexpr int MAX_S = 8;                // K splits per tile
+constexpr int TMEM_COLS = 32;           // D of MMA j in columns [16j, 16j+16), j < R <= 2
+constexpr int MAX_S = 8;                // K splits per tile (portable cluster size)
 constexpr int MAX_CTAS = 160;           // tiles * S <= #SMs (148)
-constexpr int SLOTS = 4;                // partial buffers, round robin over launches
-constexpr size_t RECV = (size_t)ROWS * TOK * 4 + TOK * 4;  // one partial accumulator + ssq
-constexpr size_t SMEM_MAX = 232448;                         // opt-in dynamic SMEM per CTA
-constexpr size_t smem_bytes(int S, bool cluster) {
-  return 1024 + (size_t)STAGES * (W_STAGE + T_STAGE) + (cluster ? (size_t)(S - 1) * RECV : 0) + 1024;
-}
+constexpr int SLOTS = 4;                // global-mode partial buffers, round robin over launches
+constexpr size_t SMEM_MAX = 232448;     // opt-in dynamic SMEM per CTA
+// tile = R x 128 W* rows (R MMAs per k step sharing the token operand)
+template <int R> struct Cfg {
+  static constexpr int W_STAGE = R * ROWS * BK * 2;                  // 16 / 32 KiB
+  static constexpr int STAGES = R == 1 ? 12 : 6;                     // ~204-216 KiB ring
+  static constexpr size_t SMEM = 1024 + (size_t)STAGES * (W_STAGE + T_STAGE) + 1024;
+};
 }  // namespace dtc
 
-// split-K partials: [slot][CTA = tile * S + rank][row][token]; arrival counter per tile
-__device__ float4 g_dtc_part[dtc::SLOTS][dtc::MAX_CTAS][dtc::ROWS * dtc::TOK / 4];
+// global-mode split-K partials: [slot][CTA = tile * S + rank][j][row][token]; counter per tile
+__device__ float4 g_dtc_part[dtc::SLOTS][dtc::MAX_CTAS][2 * dtc::ROWS * dtc::TOK / 4];
 __device__ float4 g_dtc_ssq[dtc::SLOTS][dtc::MAX_CTAS][dtc::TOK / 4];
 __device__ unsigned g_dtc_cnt[dtc::SLOTS][dtc::MAX_CTAS];
 
@@ -68,6 +71,14 @@ FN_DEVICE void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t (&r)[16]) {
         "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr)
       : "memory");
+}
+FN_DEVICE float4 ld_cluster_v4(uint32_t cluster_addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(cluster_addr)
+               : "memory");
+  return v;
 }
 
 #ifdef FN_GEMV_TC_TRACE  // tools/micro/gemv_tc_trace.cu: per-CTA timeline (globaltimer, ns)
@@ -83,19 +94,19 @@ FN_DEVICE unsigned long long tc_gtime() {
 #define TC_TRACE(ev)
 #endif
 
-template <int MODE>
+template <int MODE, int R>
 __global__ void __launch_bounds__(dtc::THREADS, 1)
     flashnorm_gemv_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_a,
                              const float* __restrict__ cstar, __nv_bfloat16* __restrict__ z, int M, int K, int N,
                              float eps, float alpha, int S, int slot, int use_cluster) {
   using namespace dtc;
+  constexpr int W_STAGE = Cfg<R>::W_STAGE;
+  constexpr int STAGES = Cfg<R>::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* sW = smem;                                  // [STAGES][128 x 64] SW128
-  uint8_t* sT = sW + STAGES * W_STAGE;                 // [STAGES][16 x 64]  SW128
-  float* recv = reinterpret_cast<float*>(sT + STAGES * T_STAGE);  // cluster mode: [S-1][128][16] (leader)
-  float* recv_ssq = recv + (size_t)(use_cluster ? S - 1 : 0) * ROWS * TOK;  // [S-1][16]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(recv_ssq + (use_cluster ? S - 1 : 0) * TOK);
+  uint8_t* sW = smem;                                  // [STAGES][R*128 x 64] SW128
+  uint8_t* sT = sW + STAGES * W_STAGE;                 // [STAGES][16 x 64]    SW128
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sT + STAGES * T_STAGE);
   uint64_t* full = bars;               // [STAGES] W* + tokens landed
   uint64_t* empty = bars + STAGES;     // [STAGES] stage consumed
   uint64_t* ready = bars + 2 * STAGES; // [STAGES] DyT: tokens transformed
@@ -104,12 +115,14 @@ __global__ void __launch_bounds__(dtc::THREADS, 1)
   float* ssq_own = reinterpret_cast<float*>(tmem_holder + 4);  // [16]
   float* side_fence = ssq_own + TOK;                           // [32] load-completion fence
   int* last_flag = reinterpret_cast<int*>(side_fence + 32);
+  // cluster mode: after the last MMA the ring is free; each CTA stages its partial there
+  float* part = reinterpret_cast<float*>(smem);                // [R][128][16]
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
-  const int rank = (int)(blockIdx.x % (unsigned)S);
+  const int rank = (int)(blockIdx.x % (unsigned)S);  // == %cluster_ctarank in cluster mode
   const int tile = (int)(blockIdx.x / (unsigned)S);
-  const int n0 = tile * ROWS;
+  const int n0 = tile * R * ROWS;
   const int nkb = (K + BK - 1) / BK;
   const int kb0 = (int)(((long long)rank * nkb) / S);
   const int kb1 = (int)(((long long)(rank + 1) * nkb) / S);
@@ -177,10 +190,14 @@ __global__ void __launch_bounds__(dtc::THREADS, 1)
         if (MODE == MODE_DYT) mbar_wait(&ready[stage], phase);
         else mbar_wait(&full[stage], phase);
         tc_fence_after();
-        const uint64_t adesc = make_sw128_desc(smem_u32(sW + stage * W_STAGE));
         const uint64_t bdesc = make_sw128_desc(smem_u32(sT + stage * T_STAGE));
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k) umma_bf16(tmem_base, adesc + 2 * k, bdesc + 2 * k, idesc, (i | k) != 0);
+        for (int j = 0; j < R; ++j) {  // rows [128j, 128j+128) of the tile: 16 KiB into the box
+          const uint64_t adesc = make_sw128_desc(smem_u32(sW + stage * W_STAGE + j * ROWS * BK * 2));
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            umma_bf16(tmem_base + j * TOK, adesc + 2 * k, bdesc + 2 * k, idesc, (i | k) != 0);
+        }
         umma_commit(&empty[stage]);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
@@ -257,47 +274,64 @@ __global__ void __launch_bounds__(dtc::THREADS, 1)
     mbar_wait_warp(tfull, 0);
     if (warp == 2 && lane == 0) TC_TRACE(2);
     tc_fence_after();
-    uint32_t v[16];
-    tmem_ld_32x32b_x16(tmem_base + ((q4 * 32u) << 16), v);
-    tmem_wait_ld();
-    float acc[TOK];
+    float acc[R][TOK];
 #pragma unroll
-    for (int m = 0; m < TOK; ++m) acc[m] = __uint_as_float(v[m]);
+    for (int j = 0; j < R; ++j) {
+      uint32_t v[16];
+      tmem_ld_32x32b_x16(tmem_base + ((q4 * 32u) << 16) + j * TOK, v);
+      tmem_wait_ld();
+#pragma unroll
+      for (int m = 0; m < TOK; ++m) acc[j][m] = __uint_as_float(v[m]);
+    }
+    float ssq[TOK];
+#pragma unroll
+    for (int m = 0; m < TOK; ++m) ssq[m] = MODE == MODE_RMS ? ssq_own[m] : 0.f;
     bool write_z = true;
     if (S > 1 && use_cluster) {
-      // cluster mode: partials go straight into the leader's SMEM (DSMEM), one cluster barrier
-      if (rank != 0) {
-        const uint32_t dst = mapa_shared(recv + ((size_t)(rank - 1) * ROWS + row) * TOK, 0);
+      // cluster mode: every CTA parks its partial in its own (now free) ring SMEM; after one
+      // cluster barrier the leader reads ranks 1..S-1 over DSMEM in fixed rank order; a
+      // second barrier keeps the other CTAs' SMEM alive until the leader is done
 #pragma unroll
-        for (int m = 0; m < TOK; m += 4)
-          asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dst + m * 4), "f"(acc[m]),
-                       "f"(acc[m + 1]), "f"(acc[m + 2]), "f"(acc[m + 3])
-                       : "memory");
-        if (MODE == MODE_RMS && warp == 2 && lane < TOK / 4) {
-          const uint32_t sd = mapa_shared(recv_ssq + (rank - 1) * TOK + lane * 4, 0);
-          asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(sd), "f"(ssq_own[4 * lane]),
-                       "f"(ssq_own[4 * lane + 1]), "f"(ssq_own[4 * lane + 2]), "f"(ssq_own[4 * lane + 3])
-                       : "memory");
-        }
-      }
-      cluster_sync_all();  // warps 0 and 1 join at the end of the kernel
+      for (int j = 0; j < R; ++j)
+#pragma unroll
+        for (int m4 = 0; m4 < TOK / 4; ++m4)
+          reinterpret_cast<float4*>(part)[(j * ROWS + row) * (TOK / 4) + m4] =
+              make_float4(acc[j][4 * m4], acc[j][4 * m4 + 1], acc[j][4 * m4 + 2], acc[j][4 * m4 + 3]);
+      if (MODE == MODE_RMS && warp == 2 && lane < TOK)
+        part[R * ROWS * TOK + lane] = ssq_own[lane];
+      cluster_sync_all();  // (1) partials visible cluster-wide; warps 0 and 1 join below
       write_z = rank == 0;
       if (write_z) {
         for (int r = 1; r < S; ++r) {  // fixed rank order
-          const float4* src = reinterpret_cast<const float4*>(recv + ((size_t)(r - 1) * ROWS + row) * TOK);
 #pragma unroll
-          for (int m4 = 0; m4 < TOK / 4; ++m4) {
-            const float4 p = src[m4];
-            acc[4 * m4] += p.x; acc[4 * m4 + 1] += p.y; acc[4 * m4 + 2] += p.z; acc[4 * m4 + 3] += p.w;
+          for (int j = 0; j < R; ++j) {
+            const uint32_t src = mapa_shared(part + (j * ROWS + row) * TOK, (uint32_t)r);
+#pragma unroll
+            for (int m4 = 0; m4 < TOK / 4; ++m4) {
+              const float4 p = ld_cluster_v4(src + m4 * 16);
+              acc[j][4 * m4] += p.x; acc[j][4 * m4 + 1] += p.y; acc[j][4 * m4 + 2] += p.z; acc[j][4 * m4 + 3] += p.w;
+            }
+          }
+          if (MODE == MODE_RMS) {
+            const uint32_t ss = mapa_shared(part + R * ROWS * TOK, (uint32_t)r);
+#pragma unroll
+            for (int m4 = 0; m4 < TOK / 4; ++m4) {
+              const float4 p = ld_cluster_v4(ss + m4 * 16);
+              ssq[4 * m4] += p.x; ssq[4 * m4 + 1] += p.y; ssq[4 * m4 + 2] += p.z; ssq[4 * m4 + 3] += p.w;
+            }
           }
         }
       }
+      cluster_sync_all();  // (2) the leader has read every remote partial
     } else if (S > 1) {
-      // publish this CTA's partial, then count arrivals on the tile; the last one reduces
+      // global mode: publish this CTA's partial, count arrivals on the tile; the last reduces
       float4* mine = g_dtc_part[slot][blockIdx.x];
 #pragma unroll
-      for (int m4 = 0; m4 < TOK / 4; ++m4)
-        __stcg(mine + row * (TOK / 4) + m4, make_float4(acc[4 * m4], acc[4 * m4 + 1], acc[4 * m4 + 2], acc[4 * m4 + 3]));
+      for (int j = 0; j < R; ++j)
+#pragma unroll
+        for (int m4 = 0; m4 < TOK / 4; ++m4)
+          __stcg(mine + (j * ROWS + row) * (TOK / 4) + m4,
+                 make_float4(acc[j][4 * m4], acc[j][4 * m4 + 1], acc[j][4 * m4 + 2], acc[j][4 * m4 + 3]));
       if (MODE == MODE_RMS && warp == 2 && lane < TOK / 4)
         __stcg(&g_dtc_ssq[slot][blockIdx.x][lane], make_float4(ssq_own[4 * lane], ssq_own[4 * lane + 1],
                                                                ssq_own[4 * lane + 2], ssq_own[4 * lane + 3]));
@@ -313,64 +347,62 @@ __global__ void __launch_bounds__(dtc::THREADS, 1)
       write_z = *last_flag != 0;
       if (write_z) {
         __threadfence();
-        float tot[TOK];
+        float tot[R][TOK], st[TOK];
 #pragma unroll
-        for (int m = 0; m < TOK; ++m) tot[m] = 0.f;
+        for (int m = 0; m < TOK; ++m) {
+          st[m] = 0.f;
+#pragma unroll
+          for (int j = 0; j < R; ++j) tot[j][m] = 0.f;
+        }
         for (int r = 0; r < S; ++r) {  // fixed rank order, own partial from registers
-          if (r == rank) {
+          const float4* src = g_dtc_part[slot][tile * S + r];
 #pragma unroll
-            for (int m = 0; m < TOK; ++m) tot[m] += acc[m];
-          } else {
-            const float4* src = g_dtc_part[slot][tile * S + r] + row * (TOK / 4);
+          for (int j = 0; j < R; ++j)
 #pragma unroll
             for (int m4 = 0; m4 < TOK / 4; ++m4) {
-              const float4 p = __ldcg(src + m4);
-              tot[4 * m4] += p.x; tot[4 * m4 + 1] += p.y; tot[4 * m4 + 2] += p.z; tot[4 * m4 + 3] += p.w;
+              const float4 p = r == rank ? make_float4(acc[j][4 * m4], acc[j][4 * m4 + 1], acc[j][4 * m4 + 2],
+                                                       acc[j][4 * m4 + 3])
+                                         : __ldcg(src + (j * ROWS + row) * (TOK / 4) + m4);
+              tot[j][4 * m4] += p.x; tot[j][4 * m4 + 1] += p.y; tot[j][4 * m4 + 2] += p.z; tot[j][4 * m4 + 3] += p.w;
             }
-          }
-        }
-#pragma unroll
-        for (int m = 0; m < TOK; ++m) acc[m] = tot[m];
-      }
-    }
-    if (write_z) {
-      float ssq[TOK];
-#pragma unroll
-      for (int m = 0; m < TOK; ++m) ssq[m] = 0.f;
-      if (MODE == MODE_RMS) {
-        if (S == 1 || use_cluster) {
-#pragma unroll
-          for (int m = 0; m < TOK; ++m) ssq[m] = ssq_own[m];
-          for (int r = 1; r < S; ++r) {  // fixed rank order (cluster mode)
-#pragma unroll
-            for (int m = 0; m < TOK; ++m) ssq[m] += recv_ssq[(r - 1) * TOK + m];
-          }
-        } else {
-          for (int r = 0; r < S; ++r) {  // fixed rank order
+          if (MODE == MODE_RMS) {
 #pragma unroll
             for (int m4 = 0; m4 < TOK / 4; ++m4) {
               const float4 p = __ldcg(&g_dtc_ssq[slot][tile * S + r][m4]);
-              ssq[4 * m4] += p.x; ssq[4 * m4 + 1] += p.y; ssq[4 * m4 + 2] += p.z; ssq[4 * m4 + 3] += p.w;
+              st[4 * m4] += p.x; st[4 * m4 + 1] += p.y; st[4 * m4 + 2] += p.z; st[4 * m4 + 3] += p.w;
             }
           }
         }
-      }
-      const int n = n0 + row;
-      if (n < N) {
-        const float cb = cstar != nullptr ? __ldg(cstar + n) : 0.0f;
-        const float invK = 1.0f / (float)K;
-        pdl_wait_prior_grid();  // z may still be read by the previous kernel of the stream
 #pragma unroll
         for (int m = 0; m < TOK; ++m) {
-          if (m < M) {
-            const float r = MODE == MODE_RMS ? rsqrtf(fmaf(ssq[m], invK, eps)) : 1.0f;
-            z[(size_t)m * N + n] = __float2bfloat16_rn(fmaf(acc[m], r, cb));
-          }
+          ssq[m] = st[m];
+#pragma unroll
+          for (int j = 0; j < R; ++j) acc[j][m] = tot[j][m];
+        }
+      }
+    }
+    if (write_z) {
+      const float invK = 1.0f / (float)K;
+      float rr[TOK];
+#pragma unroll
+      for (int m = 0; m < TOK; ++m) rr[m] = MODE == MODE_RMS ? rsqrtf(fmaf(ssq[m], invK, eps)) : 1.0f;
+      pdl_wait_prior_grid();  // z may still be read by the previous kernel of the stream
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        const int n = n0 + j * ROWS + row;
+        if (n < N) {
+          const float cb = cstar != nullptr ? __ldg(cstar + n) : 0.0f;
+#pragma unroll
+          for (int m = 0; m < TOK; ++m)
+            if (m < M) z[(size_t)m * N + n] = __float2bfloat16_rn(fmaf(acc[j][m], rr[m], cb));
         }
       }
     }
   }
-  if (S > 1 && use_cluster && warp < 2) cluster_sync_all();
+  if (S > 1 && use_cluster && warp < 2) {
+    cluster_sync_all();
+    cluster_sync_all();
+  }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -390,20 +422,32 @@ __global__ void __launch_bounds__(dtc::THREADS, 1)
 // ------------------------------------------------------------------ host side
 
 namespace {
-template <int MODE>
+template <int MODE, int R>
 const void* dtc_kernel() {
-  return (const void*)flashnorm_gemv_tc_kernel<MODE>;
+  return (const void*)flashnorm_gemv_tc_kernel<MODE, R>;
 }
-const void* dtc_fptr(int mode) {
-  return mode == MODE_RMS ? dtc_kernel<MODE_RMS>() : mode == MODE_DYT ? dtc_kernel<MODE_DYT>() : dtc_kernel<MODE_NONE>();
+const void* dtc_fptr(int mode, int R) {
+  if (R == 1)
+    return mode == MODE_RMS ? dtc_kernel<MODE_RMS, 1>() : mode == MODE_DYT ? dtc_kernel<MODE_DYT, 1>()
+                                                                           : dtc_kernel<MODE_NONE, 1>();
+  return mode == MODE_RMS ? dtc_kernel<MODE_RMS, 2>() : mode == MODE_DYT ? dtc_kernel<MODE_DYT, 2>()
+                                                                         : dtc_kernel<MODE_NONE, 2>();
 }
-// can `clusters` clusters of S CTAs be resident at once?
-bool cluster_fits(int mode, int S, int clusters) {
-  if (dtc::smem_bytes(S, true) > dtc::SMEM_MAX) return false;
+size_t dtc_smem(int R) { return R == 1 ? dtc::Cfg<1>::SMEM : dtc::Cfg<2>::SMEM; }
+void dtc_set_attr(int mode, int R) {
+  static bool done[3][3] = {};
+  if (!done[mode][R]) {
+    cudaFuncSetAttribute(dtc_fptr(mode, R), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dtc::SMEM_MAX);
+    done[mode][R] = true;
+  }
+}
+// can `clusters` clusters of S CTAs (tile height R x 128) be resident at once?
+bool cluster_fits(int mode, int R, int S, int clusters) {
+  dtc_set_attr(mode, R);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(clusters * S);
   cfg.blockDim = dim3(dtc::THREADS);
-  cfg.dynamicSmemBytes = dtc::smem_bytes(S, true);
+  cfg.dynamicSmemBytes = dtc_smem(R);
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = S;
@@ -412,60 +456,71 @@ bool cluster_fits(int mode, int S, int clusters) {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   int n = 0;
-  return cudaOccupancyMaxActiveClusters(&n, dtc_fptr(mode), &cfg) == cudaSuccess && n >= clusters;
+  return cudaOccupancyMaxActiveClusters(&n, dtc_fptr(mode, R), &cfg) == cudaSuccess && n >= clusters;
+}
+struct DtcPlan {
+  int R, S, cluster;
+};
+// Tile height (R x 128 rows) and K split S, with the S CTAs of a tile in one co-resident
+// cluster (DSMEM reduction).  R = 1 whenever its tiles fit the SMs; R = 2 extends the kernel
+// to N <= 256 * #SMs.  (Config 2, N = 6144: R = 1 -> 48 tiles x clusters of 2 (3 do not fit:
+// 45 max) = 96 CTAs, 10.2 us; R = 2 -> 24 tiles x clusters of 5 = 120 CTAs measured slower,
+// 13.2 us: the 5-way DSMEM reduction and the shallower 32 KiB-stage ring cost more than the
+// extra SMs bring.)
+DtcPlan dtc_plan(int mode, int K, int N, int num_sms) {
+  using namespace dtc;
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, int, int>, DtcPlan> cache;
+  const auto key = std::make_tuple(mode, K, N, num_sms);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  const int nkb = (K + BK - 1) / BK;
+  const int cap = std::min(num_sms, MAX_CTAS);
+  DtcPlan best{1, 1, 0};
+  int best_ctas = -1;
+  for (int R = 1; R <= 2; ++R) {
+    const int tiles = (N + R * ROWS - 1) / (R * ROWS);
+    if (tiles > cap) continue;
+    if (R == 2 && best_ctas > 0) break;  // R = 2 only when R = 1 does not fit
+    const int smax = std::max(1, std::min(std::min(cap / tiles, MAX_S), nkb));
+    int fit = 1;
+    for (int c = smax; c > 1; --c)
+      if (cluster_fits(mode, R, c, tiles)) { fit = c; break; }
+    DtcPlan p{R, fit, fit > 1 ? 1 : 0};
+    if (fit == 1 && smax > 1) p = DtcPlan{R, smax, 0};  // no cluster fits: global-memory reduction
+    const int ctas = tiles * p.S;
+    if (ctas > best_ctas) { best = p; best_ctas = ctas; }
+  }
+  std::lock_guard<std::mutex> lk(mu);
+  cache.emplace(key, best);
+  return best;
 }
 }  // namespace
 
-int gemv_tc_split(int K, int N, int num_sms) {
-  using namespace dtc;
-  const int tiles = (N + ROWS - 1) / ROWS;
-  const int nkb = (K + BK - 1) / BK;
-  int S = std::min(num_sms, MAX_CTAS) / tiles;
-  S = std::min(S, MAX_S);
-  S = std::min(S, nkb);
-  return std::max(S, 1);
-}
+int gemv_tc_split(int K, int N, int num_sms) { return dtc_plan(MODE_RMS, K, N, num_sms).S; }
 
 bool gemv_tc_supported(int M, int N, int num_sms) {
-  return M >= 1 && M <= dtc::TOK && (N + dtc::ROWS - 1) / dtc::ROWS <= std::min(num_sms, dtc::MAX_CTAS);
+  return M >= 1 && M <= dtc::TOK && (N + 2 * dtc::ROWS - 1) / (2 * dtc::ROWS) <= std::min(num_sms, dtc::MAX_CTAS);
 }
 
 cudaError_t launch_gemv_tc(const CUtensorMap& tw, const CUtensorMap& ta, const float* cstar, __nv_bfloat16* z,
                            int M, int K, int N, float eps, float alpha, int mode, int num_sms, cudaStream_t stream) {
   using namespace dtc;
-  const void* fptr = dtc_fptr(mode);
-  static bool attr_set[3] = {false, false, false};
-  if (!attr_set[mode]) {
-    cudaError_t e = cudaFuncSetAttribute(fptr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_MAX);
-    if (e != cudaSuccess) return e;
-    attr_set[mode] = true;
-  }
-  const int tiles = (N + ROWS - 1) / ROWS;
-  int S = gemv_tc_split(K, N, num_sms);
-  // Prefer a cluster (DSMEM reduction, ~1 us tail) of the largest size whose clusters are all
-  // co-resident (GPC shapes cap clusters of 3 at 45 on this part); fall back to the global-
-  // memory reduction with the full split when no cluster size > 1 fits.
-  int use_cluster = 0;
-  {
-    static int ck[3][3] = {{-1, -1, -1}, {-1, -1, -1}, {-1, -1, -1}};
-    if (ck[mode][0] == tiles && ck[mode][1] == S) {
-      if (ck[mode][2] > 1) { S = ck[mode][2]; use_cluster = 1; }
-    } else {
-      int fit = 1;
-      for (int c = S; c > 1; --c)
-        if (cluster_fits(mode, c, tiles)) { fit = c; break; }
-      ck[mode][0] = tiles; ck[mode][1] = S; ck[mode][2] = fit;
-      if (fit > 1) { S = fit; use_cluster = 1; }
-    }
-  }
-  // partial-buffer slot: launches in flight together (PDL overlap, graph replays) use
-  // different slots; SLOTS consecutive launches cannot overlap (each waits for the previous)
+  const DtcPlan p = dtc_plan(mode, K, N, num_sms);
+  dtc_set_attr(mode, p.R);
+  const void* fptr = dtc_fptr(mode, p.R);
+  const int tiles = (N + p.R * ROWS - 1) / (p.R * ROWS);
+  int S = p.S, use_cluster = p.cluster;
+  // global-mode partial-buffer slot: launches in flight together use different slots
   static std::atomic<unsigned> seq{0};
   int slot = (int)(seq.fetch_add(1u) % SLOTS);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(tiles * S);
   cfg.blockDim = dim3(THREADS);
-  cfg.dynamicSmemBytes = smem_bytes(S, use_cluster != 0);
+  cfg.dynamicSmemBytes = dtc_smem(p.R);
   cfg.stream = stream;
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -480,5 +535,7 @@ cudaError_t launch_gemv_tc(const CUtensorMap& tw, const CUtensorMap& ta, const f
                   (void*)&eps, (void*)&alpha, (void*)&S, (void*)&slot, (void*)&use_cluster};
   return cudaLaunchKernelExC(&cfg, fptr, args);
 }
+
+int gemv_tc_tile_rows(int mode, int K, int N, int num_sms) { return dtc_plan(mode, K, N, num_sms).R * dtc::ROWS; }
 
 }  // namespace fn

@@ -48,7 +48,8 @@ constexpr int GEMV_MAX_M = 16;
 bool gemv_supported(int M, int K);  // decode kernel handles this (M, K)
 // K4 on tcgen05 (gemv_tc.cu): tw = W* map (box 64 x 128), ta = token map (box 64 x 16)
 bool gemv_tc_supported(int M, int N, int num_sms);
-int gemv_tc_split(int K, int N, int num_sms);  // K splits per 128-row tile
+int gemv_tc_split(int K, int N, int num_sms);      // K splits per tile
+int gemv_tc_tile_rows(int mode, int K, int N, int num_sms);  // W* rows per tile (128 or 256; the TMA box)
 cudaError_t launch_gemv_tc(const CUtensorMap& tw, const CUtensorMap& ta, const float* cstar, __nv_bfloat16* z,
                            int M, int K, int N, float eps, float alpha, int mode, int num_sms, cudaStream_t stream);
 size_t gemv_smem_bytes(int M, int K);

@@ -276,7 +276,7 @@ def test_gemm_eps_placement_detectable():
 # ============================================================ linear: bf16 decode GEMV
 
 @pytest.mark.parametrize("M", [1, 5, 16])
-@pytest.mark.parametrize("K,N", [(4096, 6144), (1000, 24), (8192, 136), (64, 8), (4160, 20000), (2048, 4104)])
+@pytest.mark.parametrize("K,N", [(4096, 6144), (1000, 24), (8192, 136), (64, 8), (4160, 20000), (2048, 4104), (512, 40000)])
 @pytest.mark.parametrize("mode", ["rmsnorm", "dyt", "none"])
 @pytest.mark.parametrize("path", ["gemv", "gemv_mma"])
 def test_gemv_parity(M, K, N, mode, path):

@@ -24,7 +24,9 @@ int main(int argc, char** argv) {
   for (auto& w : W) { cudaMalloc(&w, (size_t)K * N * 2); cudaMemset(w, 0, (size_t)K * N * 2); }
   __nv_bfloat16 *a, *z; cudaMalloc(&a, K * 2 * 16); cudaMalloc(&z, N * 2 * 16); cudaMemset(a, 0, K * 32);
   CUtensorMap tw[4], ta = tmap(a, M, K, 16);
-  for (int i = 0; i < 4; ++i) tw[i] = tmap(W[i], N, K, 128);
+  const int tr_rows = fn::gemv_tc_tile_rows(0, K, N, 148);
+  printf("tile rows %d\n", tr_rows);
+  for (int i = 0; i < 4; ++i) tw[i] = tmap(W[i], N, K, tr_rows);
   auto launch = [&](int i) {
     unsigned v = (unsigned)i; cudaMemcpyToSymbolAsync(fn::g_tc_launch, &v, 4, 0, cudaMemcpyHostToDevice, 0);
     fn::launch_gemv_tc(tw[i % 4], ta, nullptr, z, M, K, N, 1e-5f, 0.5f, 0, 148, 0);
