@@ -382,7 +382,8 @@ def measure_secondary(args, fn, torch, dev, stream, peaks, a, Ws, cs, g):
     out["decode"] = {"workload": "llama3-8b decode: RMSNorm + QKV 4096->6144 (BASELINE config 2)",
                      "unit": "GB/s", "peak_hbm_gbs": hbm, "l2": "4 rotating W* buffers (200 MB > L2)",
                      "timing": "CUDA graph of 200 back-to-back calls (PDL-chained launches), events",
-                     "kernel": "flashnorm_gemv_kernel", **dec}
+                     "kernel": "flashnorm_gemv_tc_kernel (tcgen05 swap-AB split-K, DSMEM cluster reduction)",
+                     **dec}
     del Wd
 
     # unfused prefill variant: RMSNorm kernel (bf16 y to HBM) then the same GEMM, norm disabled
@@ -398,6 +399,18 @@ def measure_secondary(args, fn, torch, dev, stream, peaks, a, Ws, cs, g):
     out["unfused_prefill"] = {"fused_ms": ms_f, "unfused_ms": ms_u, "fusion_gain": ms_u / ms_f,
                               "what": "baseline_norm (y=RN(a*r*g)) -> flashnorm_linear(mode=none)"}
 
+    # DyT variant of the same shape: tanh pre-pass (K8) into a workspace + the GEMM in mode none,
+    # and the in-kernel tanh prologue (MUFU-bound) for comparison
+    ws_dyt = torch.empty(M * K * 2, dtype=torch.uint8, device=dev)
+    ms_d = timed(lambda i: fn.linear(a, Ws, cs, mode="dyt", alpha=0.5, out=z, workspace=ws_dyt), 10)
+    ms_dp = timed(lambda i: fn.linear(a, Ws, cs, mode="dyt", alpha=0.5, out=z, workspace=None), 5)
+    fl = 2.0 * M * K * N
+    out["dyt_prefill"] = {"ms": ms_d, "TFLOP/s": fl / (ms_d * 1e-3) / 1e12,
+                          "frac_bf16_peak": fl / (ms_d * 1e-3) / 1e12 / peaks.get("bf16_tflops", 1657.2),
+                          "prologue_ms": ms_dp, "prologue_TFLOP/s": fl / (ms_dp * 1e-3) / 1e12,
+                          "what": "dyt_prepass (tanh once per element) -> GEMM mode none; prologue = tanh in SMEM"}
+    del ws_dyt
+
     # folds (offline, once per weight load): config-3 W (235 MB in + 235 MB out)
     Wf, gf, bf_, cf = SD.layer(5, N, K, dev, torch.bfloat16, with_b=True, with_c=True)
     Wo = torch.empty_like(Wf)
@@ -406,6 +419,16 @@ def measure_secondary(args, fn, torch, dev, stream, peaks, a, Ws, cs, g):
     fb = 2 * N * K * 2 + 3 * K * 4 + 2 * N * 4
     out["fold"] = {"fold_weights_us": ms_fold * 1e3, "GB/s": fb / (ms_fold * 1e-3) / 1e9,
                    "frac_hbm": fb / (ms_fold * 1e-3) / 1e9 / hbm, "bytes": fb, "shape": [N, K]}
+    del Wf, Wo
+    # LayerNorm retrofit fold (config 4 V: 4096 x 4096 bf16 + b_prev), 3 kernels, CUDA graph
+    _, Vt, bp = SD.upstream(4, 16, 4096, 4096, dev, torch.bfloat16)
+    Vs = torch.empty_like(Vt)
+    wsv = torch.empty(fn.fold_mean_center_workspace_bytes(4096, 4096) // 8 + 2, dtype=torch.float64, device=dev)
+    ms_mc = timed(lambda i: fn.fold_mean_center(Vt, bp, out=Vs, workspace=wsv), 20, graph=True)
+    vb = 2 * 4096 * 4096 * 2
+    out["fold"].update({"fold_mean_center_us": ms_mc * 1e3, "fold_mean_center_GB/s": vb / (ms_mc * 1e-3) / 1e9,
+                        "fold_mean_center_frac_hbm": vb / (ms_mc * 1e-3) / 1e9 / hbm,
+                        "fold_mean_center_shape": [4096, 4096]})
     return out
 
 

@@ -238,33 +238,31 @@ __global__ void __launch_bounds__(dtc::THREADS, 1)
         float s = s0 + s1;
         s += __shfl_xor_sync(0xffffffffu, s, 1);  // lanes 2r, 2r+1 -> token row r (fixed order)
         if ((lane & 1) == 0) ssq_own[lane >> 1] = s;
-      } else if (MODE == MODE_DYT) {
-        const __nv_bfloat162 alpha2 = __floats2bfloat162_rn(alpha, alpha);
-        int stage = 0;
-        uint32_t phase = 0;
-        for (int i = 0; i < my_kb; ++i) {
-          mbar_wait_warp(&full[stage], phase);
-          uint4* p = reinterpret_cast<uint4*>(sT + stage * T_STAGE) + lane * 4;  // 64 B per lane
-          uint4 v[4];
+      }
+    }
+    if (MODE == MODE_DYT) {
+      // tanh(alpha a) in place on each token stage before its MMA: warps 2-5, one 16-byte
+      // chunk per thread (2 KiB per stage), so the transform keeps ahead of the W* stream
+      const __nv_bfloat162 alpha2 = __floats2bfloat162_rn(alpha, alpha);
+      const int t = (int)threadIdx.x - 64;  // 0..127
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int i = 0; i < my_kb; ++i) {
+        mbar_wait_warp(&full[stage], phase);
+        uint4* p = reinterpret_cast<uint4*>(sT + stage * T_STAGE) + t;
+        uint4 v = *p;
+        uint32_t* w = reinterpret_cast<uint32_t*>(&v);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) v[q] = p[q];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            uint32_t* w = reinterpret_cast<uint32_t*>(&v[q]);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              __nv_bfloat162 x = *reinterpret_cast<__nv_bfloat162*>(&w[e]);
-              x = __hmul2(x, alpha2);
-              w[e] = tanh_approx_bf16x2(*reinterpret_cast<uint32_t*>(&x));
-            }
-          }
-#pragma unroll
-          for (int q = 0; q < 4; ++q) p[q] = v[q];
-          fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&ready[stage]);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        for (int e = 0; e < 4; ++e) {
+          __nv_bfloat162 x = *reinterpret_cast<__nv_bfloat162*>(&w[e]);
+          x = __hmul2(x, alpha2);
+          w[e] = tanh_approx_bf16x2(*reinterpret_cast<uint32_t*>(&x));
         }
+        *p = v;
+        fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
+        named_bar_sync(2, 128);
+        if (t == 0) mbar_arrive(&ready[stage]);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
     // ---------------------------------------------------------------- epilogue (warps 2-5)

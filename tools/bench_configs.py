@@ -82,9 +82,9 @@ for r in range(4):
 for M in (1, 16):
     ad = SD.activations(7, M, K, dev, torch.bfloat16)
     zd = torch.empty(M, N, dtype=torch.bfloat16, device=dev)
-    for mode in ("rmsnorm", "dyt"):
-        us = timed(lambda i: fn.linear(ad, Wd[i % 4], None, mode=mode, out=zd), 200, graph=True)
-        report(f"2 decode M={M} K=4096 N=6144", f"linear {mode} (graph, 4 rotating W*)", us,
+    for mode, path in (("rmsnorm", "auto"), ("dyt", "auto"), ("rmsnorm", "gemv_mma")):
+        us = timed(lambda i: fn.linear(ad, Wd[i % 4], None, mode=mode, path=path, out=zd), 200, graph=True)
+        report(f"2 decode M={M} K=4096 N=6144", f"linear {mode} path={path} (graph, 4 rotating W*)", us,
                byts=K * N * 2 + M * K * 2 + M * N * 2)
 del Wd
 
@@ -97,16 +97,21 @@ cs = torch.empty(N, device=dev)
 us = timed(lambda i: fn.fold_weights(W, g, b, c, out=Ws, c_out=cs), 5)
 report("3 prefill W fold", "fold_weights 28672x4096 (g, b, c)", us, byts=2 * N * K * 2 + 4 * (2 * K + 2 * N))
 z = torch.empty(M, N, dtype=torch.bfloat16, device=dev)
-for mode, path in (("rmsnorm", "auto"), ("none", "auto"), ("rmsnorm", "gemm1"), ("dyt", "auto")):
-    us = timed(lambda i: fn.linear(a, Ws, cs, mode=mode, path=path, out=z), 10 if not QUICK else 3)
-    report("3 prefill M=4096 K=4096 N=28672", f"linear {mode} path={path}", us, flops=2 * M * K * N)
+for mode, path, wsp in (("rmsnorm", "auto", "auto"), ("none", "auto", "auto"), ("rmsnorm", "gemm1", "auto"),
+                        ("dyt", "auto", "auto"), ("dyt", "auto", None)):
+    us = timed(lambda i: fn.linear(a, Ws, cs, mode=mode, path=path, out=z, workspace=wsp), 10 if not QUICK else 3)
+    tag = " (tanh prologue, no workspace)" if (mode == "dyt" and wsp is None) else (" (K8 pre-pass)" if mode == "dyt" else "")
+    report("3 prefill M=4096 K=4096 N=28672", f"linear {mode} path={path}{tag}", us, flops=2 * M * K * N)
 del W, Ws, z
 
 # ---------------- config 4: LayerNorm retrofit (V* fold + upstream GEMM + LN linear) and DyT
 M, d = 2048, 4096
 x, Vt, bp = SD.upstream(4, M, d, d, dev, torch.bfloat16)
-us = timed(lambda i: fn.fold_mean_center(Vt, bp), 5)
-report("4 LN V fold", "fold_mean_center 4096x4096 (+b_prev)", us, byts=2 * d * d * 2)
+Vs0 = torch.empty_like(Vt)
+wsv = torch.empty(fn.fold_mean_center_workspace_bytes(d, d) // 8 + 2, dtype=torch.float64, device=dev)
+us = timed(lambda i: fn.fold_mean_center(Vt, bp, out=Vs0, workspace=wsv), 20, graph=True)
+report("4 LN V fold", "fold_mean_center 4096x4096 (+b_prev), graph", us, byts=2 * d * d * 2)
+del Vs0, wsv
 Vs, bs = fn.fold_mean_center(Vt, bp)
 astar = torch.empty(M, d, dtype=torch.bfloat16, device=dev)
 us = timed(lambda i: fn.linear(x, Vs, bs, mode="none", out=astar), 20)

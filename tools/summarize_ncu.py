@@ -36,6 +36,18 @@ KEYS = [
 ]
 
 
+def raw_metrics_all(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    if len(rows) < 3:
+        return []
+    hdr, units = rows[0], rows[1]
+    res = []
+    for vals in rows[2:]:
+        res.append({h: (vals[i], units[i]) for i, h in enumerate(hdr) if i < len(vals)})
+    return res
+
+
 def raw_metrics(rep):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
@@ -59,13 +71,12 @@ def main(tag):
     lines = [f"# ncu summary — {tag}", ""]
     traffic_path = os.path.join(PROF, "traffic.json")
     traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
-    for name in ("gemm", "gemv"):
+    reps = []
+    for name in ("gemm", "gemv", "aux"):
         rep = os.path.join(OUT, f"prof_{name}_{tag}.ncu-rep")
-        if not os.path.exists(rep):
-            continue
-        d = raw_metrics(rep)
-        if d is None:
-            continue
+        if os.path.exists(rep):
+            reps += [(name, d) for d in raw_metrics_all(rep)]
+    for name, d in reps:
         kname = d.get("Kernel Name", ("?", ""))[0]
         lines += [f"## {name}: `{kname}`", "", "| metric | value | unit |", "|---|---|---|"]
         for key, label in KEYS:
