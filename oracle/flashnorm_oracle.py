@@ -227,6 +227,66 @@ def fold_mean_center(V, b_prev=None):
 
 
 # ---------------------------------------------------------------------------
+# FFN with a GLU variant (§2.2, Figs 3-4) — NEXT-1
+# ---------------------------------------------------------------------------
+
+GLU_ACTS = ("silu", "relu", "bilinear")
+
+
+def glu_act(x, act):
+    """The GLU variant's activation [reading c24]: SwiGLU silu(x) = x / (1 + e^-x),
+    ReGLU relu(x) = max(x, 0), bilinear GLU: identity (PAPER.md:70 names ReGLU and
+    bilinear GLU; the FFN "with a GLU variant" of Fig 3 is SwiGLU in Llama)."""
+    x = _f64(x)
+    if act == "silu":
+        return x / (1.0 + np.exp(-x))
+    if act == "relu":
+        return np.maximum(x, 0.0)
+    if act == "bilinear":
+        return x.copy()
+    raise ValueError(act)
+
+
+def glu_hidden(a, Wg, Wu, g=None, eps=0.0, act="silu"):
+    """Unoptimized Fig 3(a) / Fig 4(a): x = RMSNorm(a; g), h = act(x Wg) * (x Wu).
+
+    Bias-free FFN ("bias-free FFNs").  Wg, Wu are n x f (paper convention).
+    """
+    x = rmsnorm(a, g, None, eps)
+    return glu_act(x @ _f64(Wg), act) * (x @ _f64(Wu))
+
+
+def glu_ffn(a, Wg, Wu, Wd, g=None, eps=0.0, act="silu"):
+    """Full FFN output y = h Wd (Fig 3(a)), Wd is f x n."""
+    return glu_hidden(a, Wg, Wu, g, eps, act) @ _f64(Wd)
+
+
+def glu_hidden_deferred(a, Wg_star, Wu_star, eps=0.0, act="silu"):
+    """Optimized forms, step by step as the figures draw them [reading c25]:
+
+    Fig 3(b) (silu):  h' = act((a Wg*) / RMSe(a)) * (a Wu*),  output scale s = 1/RMSe(a)
+                      ("one set [of f multipliers] can be deferred to the FFN output").
+    Fig 4(b) (relu, bilinear): h'' = act(a Wg*) * (a Wu*),   s = 1/MSe(a) = 1/RMSe(a)^2
+                      ("eliminate the scaling before the activation function and
+                      combine it with the scaling at the output").
+    The FFN output is then y = (h Wd) * s.  Returns (h, s[M]).
+    """
+    a = _f64(a)
+    G = a @ _f64(Wg_star)
+    U = a @ _f64(Wu_star)
+    r = 1.0 / rmse(a, eps)
+    if act == "silu":
+        return glu_act(G * r[:, None], act) * U, r
+    return glu_act(G, act) * U, r * r
+
+
+def glu_ffn_deferred(a, Wg_star, Wu_star, Wd, eps=0.0, act="silu"):
+    """y = (h Wd) * s with (h, s) from glu_hidden_deferred (Fig 3(b) / Fig 4(b) output scaling)."""
+    h, s = glu_hidden_deferred(a, Wg_star, Wu_star, eps, act)
+    return (h @ _f64(Wd)) * s[:, None]
+
+
+# ---------------------------------------------------------------------------
 # Parity metric [reading c12]
 # ---------------------------------------------------------------------------
 

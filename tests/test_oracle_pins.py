@@ -19,7 +19,7 @@ from oracle import flashnorm_oracle as O
 
 
 def ev(expr):
-    return float(eval(str(expr), {"__builtins__": {}}, {k: getattr(math, k) for k in ("sqrt", "tanh")}))
+    return float(eval(str(expr), {"__builtins__": {}}, {k: getattr(math, k) for k in ("sqrt", "tanh", "exp")}))
 
 
 def evv(lst):
@@ -278,3 +278,85 @@ def test_faults_are_detected(golden):
     _, bs = O.fold_mean_center(np.array(fm["V"], float), None)
     assert bs is None  # dropping b_prev centering leaves b_prev un-centered: [1,3] != [-1,1]
     assert not np.allclose(fm["b_prev"], fm["b_prev_star"])
+
+
+# ---------------------------------------------------------------- GLU FFN (NEXT-1)
+
+def test_glu_worked(golden):
+    for ex in golden["glu"]:
+        a, g = np.array(ex["a"], float), np.array(ex["g"], float)
+        Wg, Wu, Wd = (np.array(ex[k], float) for k in ("Wg", "Wu", "Wd"))
+        h = O.glu_hidden(a, Wg, Wu, g, ex["eps"], ex["act"])
+        np.testing.assert_allclose(h[0], evv(ex["expect_h"]), rtol=1e-14, atol=1e-15)
+        if "expect_y" in ex:
+            np.testing.assert_allclose(O.glu_ffn(a, Wg, Wu, Wd, g, ex["eps"], ex["act"])[0], evv(ex["expect_y"]),
+                                       rtol=1e-14, atol=1e-15)
+        Wgs, Wus = O.merge_norm_weights(Wg, g), O.merge_norm_weights(Wu, g)
+        _, s = O.glu_hidden_deferred(a, Wgs, Wus, ex["eps"], ex["act"])
+        assert s[0] == pytest.approx(ev(ex["expect_s_deferred"]), rel=1e-14)
+
+
+def test_glu_act_textbook():
+    """silu against math.exp per element; relu/bilinear against their definitions"""
+    xs = np.linspace(-30, 30, 121)
+    np.testing.assert_allclose(O.glu_act(xs, "silu"), [x / (1 + math.exp(-x)) for x in xs], rtol=1e-15, atol=1e-300)
+    assert np.array_equal(O.glu_act(xs, "relu"), [max(x, 0.0) for x in xs])
+    assert np.array_equal(O.glu_act(xs, "bilinear"), xs)
+
+
+def _brute_glu_exact(a, Wg, Wu, Wd, g, eps, act):
+    """Fractions for every step except the one irrational value, 1/RMSe (sqrt)."""
+    out = []
+    for row in a:
+        n = len(row)
+        ms = sum(Fraction(x) ** 2 for x in row) / n + Fraction(eps)
+        r = 1 / math.sqrt(float(ms))
+        x = [Fraction(row[i]) * Fraction(g[i]) for i in range(n)]   # r applied in float at the end
+        G = [sum(x[i] * Fraction(Wg[i][j]) for i in range(n)) for j in range(len(Wg[0]))]
+        U = [sum(x[i] * Fraction(Wu[i][j]) for i in range(n)) for j in range(len(Wu[0]))]
+        if act == "relu":
+            h = [max(G[j], 0) * U[j] for j in range(len(G))]      # relu(G r) U r = relu(G) U r^2
+        else:
+            h = [G[j] * U[j] for j in range(len(G))]
+        y = [float(sum(h[j] * Fraction(Wd[j][k]) for j in range(len(h)))) * r * r for k in range(len(Wd[0]))]
+        out.append(y)
+    return np.array(out)
+
+
+@pytest.mark.parametrize("act", ["relu", "bilinear"])
+def test_glu_brute_force_tiny(act):
+    rng = np.random.default_rng(11)
+    M, n, f = 3, 5, 6
+    a = rng.integers(-9, 10, (M, n)) / 4.0
+    Wg = rng.integers(-9, 10, (n, f)) / 8.0
+    Wu = rng.integers(-9, 10, (n, f)) / 8.0
+    Wd = rng.integers(-9, 10, (f, n)) / 8.0
+    g = rng.integers(1, 9, n) / 4.0
+    ref = _brute_glu_exact(a.tolist(), Wg.tolist(), Wu.tolist(), Wd.tolist(), g, 0.0625, act)
+    np.testing.assert_allclose(O.glu_ffn(a, Wg, Wu, Wd, g, 0.0625, act), ref, rtol=1e-12, atol=1e-13)
+
+
+@pytest.mark.parametrize("act", ["silu", "relu", "bilinear"])
+@pytest.mark.parametrize("eps", [0.0, 1e-5])
+def test_glu_deferred_equals_unoptimized(act, eps):
+    """The paper's claim: Fig 3(b)/4(b) compute the same FFN output as Fig 3(a)/4(a)."""
+    rng = np.random.default_rng(3)
+    M, n, f = 6, 32, 40
+    a = rng.standard_normal((M, n)) * rng.uniform(0.1, 10, (M, 1))
+    Wg, Wu = rng.standard_normal((n, f)) / np.sqrt(n), rng.standard_normal((n, f)) / np.sqrt(n)
+    Wd = rng.standard_normal((f, n)) / np.sqrt(f)
+    g = rng.uniform(0.5, 1.5, n)
+    y = O.glu_ffn(a, Wg, Wu, Wd, g, eps, act)
+    y2 = O.glu_ffn_deferred(a, O.merge_norm_weights(Wg, g), O.merge_norm_weights(Wu, g), Wd, eps, act)
+    np.testing.assert_allclose(y2, y, rtol=1e-12, atol=1e-12)
+
+
+def test_glu_faults_detected():
+    """silu applied AFTER the deferred scale (wrong for a non-scale-invariant act) must fail"""
+    rng = np.random.default_rng(4)
+    a = rng.standard_normal((4, 16)) * 3
+    Wg, Wu = rng.standard_normal((16, 8)), rng.standard_normal((16, 8))
+    h = O.glu_hidden(a, Wg, Wu, None, 0.0, "silu")
+    r = 1.0 / O.rmse(a, 0.0)
+    wrong = O.glu_act(a @ Wg, "silu") * (a @ Wu) * (r * r)[:, None]   # Fig 4(b) form used for silu
+    assert not np.allclose(wrong, h, rtol=1e-3)
