@@ -411,6 +411,25 @@ def measure_secondary(args, fn, torch, dev, stream, peaks, a, Ws, cs, g):
                           "what": "dyt_prepass (tanh once per element) -> GEMM mode none; prologue = tanh in SMEM"}
     del ws_dyt
 
+    # NEXT-1: the same gate||up GEMM with the GLU epilogue (SwiGLU, Fig 3(b)): h [M, F] (half the
+    # output bytes) + s [M]; then the down projection F -> K scaled by s at its output
+    F = N // 2
+    Wgu = fn.fold_glu_weights(Ws[:F], Ws[F:], None)  # W* rows already carry g
+    h = torch.empty((M, F), dtype=torch.bfloat16, device=dev)
+    sg = torch.empty(M, dtype=torch.float32, device=dev)
+    ms_g = timed(lambda i: fn.glu_linear(a, Wgu, eps=1e-5, act="silu", out=h, s_out=sg), 10)
+    Wdn, _, _, _ = SD.layer(77, K, F, dev, torch.bfloat16)
+    yd = torch.empty((M, K), dtype=torch.bfloat16, device=dev)
+    ms_dn = timed(lambda i: fn.linear_scaled(h, Wdn, sg, out=yd), 10)
+    fl_g, fl_d = 2.0 * M * K * N, 2.0 * M * F * K
+    out["glu_ffn"] = {"workload": "llama3-8b FFN (SwiGLU) at config 3: gate||up 4096->2x14336 with the GLU "
+                                  "epilogue, then down 14336->4096 scaled by s (Figs 3(b))",
+                      "gate_up_ms": ms_g, "gate_up_TFLOP/s": fl_g / (ms_g * 1e-3) / 1e12,
+                      "gate_up_frac_bf16_peak": fl_g / (ms_g * 1e-3) / 1e12 / peaks.get("bf16_tflops", 1657.2),
+                      "down_ms": ms_dn, "down_TFLOP/s": fl_d / (ms_dn * 1e-3) / 1e12,
+                      "ffn_ms": ms_g + ms_dn, "ffn_TFLOP/s": (fl_g + fl_d) / ((ms_g + ms_dn) * 1e-3) / 1e12}
+    del Wgu, h, Wdn, yd
+
     # folds (offline, once per weight load): config-3 W (235 MB in + 235 MB out)
     Wf, gf, bf_, cf = SD.layer(5, N, K, dev, torch.bfloat16, with_b=True, with_c=True)
     Wo = torch.empty_like(Wf)

@@ -182,6 +182,38 @@ fn_status flashnorm_linear_ws(const void* a, const void* Wt_star, const float* c
                               fn_mode mode, fn_dtype dtype, void* z, fn_path path,
                               void* workspace, int64_t workspace_bytes, void* stream);
 
+/* --------------------------------------------------------------------------
+ * FFN with a GLU variant (NEXT-1, §2.2 Figs 3-4; readings c24, c25).
+ * Bias-free FFN: y = (act(x W_gate) ⊙ (x W_up)) W_down with x = RMSNorm(a; g).
+ *
+ * flashnorm_fold_glu_weights — W*_gate = diag(g) W_gate, W*_up = diag(g) W_up,
+ *   stored gate/up interleaved in 128-row blocks so one 256-row GEMM tile holds gate block
+ *   t and up block t:  Wgu_star[256 t + c] = W*_gate^T[128 t + c],
+ *                      Wgu_star[256 t + 128 + c] = W*_up^T[128 t + c],   c < 128.
+ *   Wgt, Wut   [F][K] storage dtype (transposed paper W_gate, W_up: n x f), F % 128 == 0.
+ *   g          [K] float32 or NULL (ones).   Wgu_star [2F][K] output (must not alias).
+ *   Numerics: each element exactly as flashnorm_fold_weights (RN_dtype(RN_f32(g w))).
+ *
+ * flashnorm_glu_linear — the gate||up GEMM with the GLU epilogue (bf16 only):
+ *   G = a W*_gate, U = a W*_up (fp32 accumulate), r_m = rsqrt(ssq_m/K + eps) (ssq beside the
+ *   contraction, as flashnorm_linear);
+ *   FN_GLU_SILU (SwiGLU, Fig 3(b)):     h = RN(silu(G r) * U),  s_m = r_m
+ *   FN_GLU_RELU / FN_GLU_BILINEAR (Fig 4(b)): h = RN(act(G) * U), s_m = r_m^2 = 1/MSe(a_m)
+ *   The FFN output is y = (h W_down) * s: pass s to flashnorm_linear_scaled (the deferred
+ *   scaling at the FFN output).  h [M][F] bf16 output, s [M] float32 output (16-B aligned).
+ *
+ * flashnorm_linear_scaled — z = RN((a W*) * row_scale_m + c*) (bf16 only): a plain linear
+ *   layer with a given per-row output scale (the down projection of Figs 3(b)/4(b)).
+ * -------------------------------------------------------------------------- */
+typedef enum { FN_GLU_SILU = 0, FN_GLU_RELU = 1, FN_GLU_BILINEAR = 2 } fn_glu_act;
+
+fn_status flashnorm_fold_glu_weights(const void* Wgt, const void* Wut, int64_t F, int64_t K, fn_dtype dtype,
+                                     const float* g, void* Wgu_star, void* stream);
+fn_status flashnorm_glu_linear(const void* a, const void* Wgu_star, int64_t M, int64_t K, int64_t F, float eps,
+                               fn_glu_act act, fn_dtype dtype, void* h, float* s, void* stream);
+fn_status flashnorm_linear_scaled(const void* a, const void* Wt_star, const float* c_star, const float* row_scale,
+                                  int64_t M, int64_t K, int64_t N, fn_dtype dtype, void* z, void* stream);
+
 /* End-to-end variant: a_host / z_host are HOST pointers (pinned memory for
  * asynchronous copies); a_dev / z_dev are caller-owned device scratch of
  * M*K / M*N elements.  Enqueues H2D(a) -> flashnorm_linear -> D2H(z) on

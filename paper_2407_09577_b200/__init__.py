@@ -22,13 +22,15 @@ from typing import Optional, Tuple
 __all__ = [
     "FlashNormError", "lib", "lib_path", "fold_weights", "fold_mean_center", "fold_mean_center_workspace_bytes",
     "linear", "linear_from_host", "baseline_norm", "gather_columns", "launch_count", "reset_launch_count",
-    "version", "linear_workspace_bytes", "MODES", "PATHS", "EXPORTS",
+    "version", "linear_workspace_bytes", "fold_glu_weights", "glu_linear", "linear_scaled", "glu_ffn",
+    "MODES", "GLU_ACTS", "PATHS", "EXPORTS",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 lib_path = os.path.join(_HERE, "libflashnorm.so")
 
 MODES = {"rmsnorm": 0, "layernorm": 1, "dyt": 2, "none": 3}
+GLU_ACTS = {"silu": 0, "relu": 1, "bilinear": 2}
 PATHS = {"auto": 0, "gemm": 1, "gemv": 2, "simt": 3, "gemm1": 4, "gemv_mma": 5}
 _DT_BF16, _DT_F32 = 0, 1
 
@@ -36,7 +38,7 @@ _DT_BF16, _DT_F32 = 0, 1
 EXPORTS = [
     "flashnorm_fold_weights", "flashnorm_fold_mean_center_workspace_bytes", "flashnorm_fold_mean_center",
     "flashnorm_linear", "flashnorm_linear_ex", "flashnorm_linear_workspace_bytes", "flashnorm_linear_ws",
-    "flashnorm_linear_from_host", "flashnorm_baseline_norm",
+    "flashnorm_linear_from_host", "flashnorm_fold_glu_weights", "flashnorm_glu_linear", "flashnorm_linear_scaled", "flashnorm_baseline_norm",
     "flashnorm_gather_columns", "flashnorm_status_string", "flashnorm_last_error", "flashnorm_launch_count",
     "flashnorm_reset_launch_count", "flashnorm_version",
 ]
@@ -71,6 +73,9 @@ def lib() -> ctypes.CDLL:
         "flashnorm_linear_ex": [_vp, _vp, _vp, _i64, _i64, _i64, _f32, _f32, _int, _int, _vp, _int, _vp],
         "flashnorm_linear_workspace_bytes": [_i64, _i64, _i64, _int, _int, _int],
         "flashnorm_linear_ws": [_vp, _vp, _vp, _i64, _i64, _i64, _f32, _f32, _int, _int, _vp, _int, _vp, _i64, _vp],
+        "flashnorm_fold_glu_weights": [_vp, _vp, _i64, _i64, _int, _vp, _vp, _vp],
+        "flashnorm_glu_linear": [_vp, _vp, _i64, _i64, _i64, _f32, _int, _int, _vp, _vp, _vp],
+        "flashnorm_linear_scaled": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _vp, _vp],
         "flashnorm_linear_from_host": [_vp, _vp, _vp, _i64, _i64, _i64, _f32, _f32, _int, _int, _vp, _vp, _vp,
                                        _vp],
         "flashnorm_baseline_norm": [_vp, _vp, _vp, _i64, _i64, _f32, _int, _f32, _int, _vp, _vp],
@@ -238,6 +243,59 @@ def linear_workspace_bytes(M: int, K: int, N: int, mode: str = "rmsnorm", dtype=
     torch = _torch()
     dt = _DT_F32 if dtype == torch.float32 else _DT_BF16
     return int(lib().flashnorm_linear_workspace_bytes(M, K, N, MODES[mode], dt, PATHS[path]))
+
+
+def fold_glu_weights(Wg_t, Wu_t, g=None, out=None):
+    """Gate/up folds for a GLU FFN: returns Wgu_star [2F, K], gate/up
+    interleaved in 128-row blocks (include/flashnorm.h).  Wg_t, Wu_t: [F, K]."""
+    torch = _torch()
+    _dev(Wg_t, "Wg_t")
+    _dev(Wu_t, "Wu_t")
+    if Wg_t.shape != Wu_t.shape or Wg_t.dim() != 2 or Wg_t.dtype != Wu_t.dtype:
+        raise FlashNormError(2, "fold_glu_weights", f"Wg_t{list(Wg_t.shape)} / Wu_t{list(Wu_t.shape)}: need two [F, K]")
+    F, K = Wg_t.shape
+    g = _vec(g, "g", K)
+    W = out if out is not None else torch.empty((2 * F, K), dtype=Wg_t.dtype, device=Wg_t.device)
+    _check(lib().flashnorm_fold_glu_weights(_ptr(Wg_t), _ptr(Wu_t), F, K, _dtype_code(Wg_t), _ptr(g), _ptr(W),
+                                            _stream(Wg_t)), "fold_glu_weights")
+    return W
+
+
+def glu_linear(a, Wgu_star, eps: float = 1e-5, act: str = "silu", out=None, s_out=None):
+    """Gate||up GEMM with the GLU epilogue: returns (h [M, F], s [M]) with y = (h W_down) * s
+    (Figs 3(b)/4(b), readings c24-c25)."""
+    torch = _torch()
+    _dev(a, "a")
+    _dev(Wgu_star, "Wgu_star")
+    M, K = a.shape
+    F = Wgu_star.shape[0] // 2
+    h = out if out is not None else torch.empty((M, F), dtype=a.dtype, device=a.device)
+    s = s_out if s_out is not None else torch.empty(M, dtype=torch.float32, device=a.device)
+    _check(lib().flashnorm_glu_linear(_ptr(a), _ptr(Wgu_star), M, K, F, float(eps), GLU_ACTS[act], _dtype_code(a),
+                                      _ptr(h), _ptr(s), _stream(a)), "glu_linear")
+    return h, s
+
+
+def linear_scaled(a, Wt_star, row_scale, c_star=None, out=None):
+    """z = (a W*) * row_scale[m] + c*: the down projection with the deferred FFN-output scale."""
+    torch = _torch()
+    _dev(a, "a")
+    _dev(Wt_star, "Wt_star")
+    _dev(row_scale, "row_scale")
+    M, K = a.shape
+    N = Wt_star.shape[0]
+    c_star = _vec(c_star, "c_star", N)
+    z = out if out is not None else torch.empty((M, N), dtype=a.dtype, device=a.device)
+    _check(lib().flashnorm_linear_scaled(_ptr(a), _ptr(Wt_star), _ptr(c_star), _ptr(row_scale), M, K, N,
+                                         _dtype_code(a), _ptr(z), _stream(a)), "linear_scaled")
+    return z
+
+
+def glu_ffn(a, Wgu_star, Wd_t, eps: float = 1e-5, act: str = "silu"):
+    """The whole FlashNorm GLU FFN: two launches (gate||up with the GLU epilogue, then the down
+    projection scaled at its output)."""
+    h, s = glu_linear(a, Wgu_star, eps=eps, act=act)
+    return linear_scaled(h, Wd_t, s)
 
 
 def linear_from_host(a_host, Wt_star, c_star, a_dev, z_dev, z_host, eps: float = 1e-5, mode: str = "rmsnorm",

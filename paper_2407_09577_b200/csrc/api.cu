@@ -141,9 +141,17 @@ int kernel_mode(fn_mode m) {
   }
 }
 
+// Extras beyond flashnorm_linear: the GLU epilogue (NEXT-1) and a given per-row output scale.
+struct LinearExtras {
+  int glu_act = -1;                 // >= 0: gate||up GEMM with the GLU epilogue, z = h [M][N/2]
+  float* s_out = nullptr;           // GLU: output scale per row
+  const float* row_scale = nullptr; // FN_NONE: z = RN(acc * row_scale[m] + c*)
+};
+
 fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, int64_t M, int64_t K, int64_t N,
                       float eps, float alpha, fn_mode mode, fn_dtype dtype, void* z, fn_path path,
-                      void* workspace, int64_t workspace_bytes, cudaStream_t stream) {
+                      void* workspace, int64_t workspace_bytes, cudaStream_t stream,
+                      const LinearExtras& ex = LinearExtras()) {
   fn_status s;
   if ((s = check_dtype(dtype)) != FN_OK) return s;
   if (mode < FN_RMSNORM || mode > FN_NONE) return fail(FN_ERR_VALUE, "unknown fn_mode %d", (int)mode);
@@ -182,8 +190,9 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
     return FN_OK;
   }
 
-  const bool tc_ok = fn::gemv_tc_supported((int)M, (int)N, num_sms());
-  const bool mma_ok = fn::gemv_supported((int)M, (int)K);
+  // the GLU epilogue lives in the GEMM kernels; a given row scale in the GEMM and tcgen05 decode kernels
+  const bool tc_ok = ex.glu_act < 0 && fn::gemv_tc_supported((int)M, (int)N, num_sms());
+  const bool mma_ok = ex.glu_act < 0 && ex.row_scale == nullptr && fn::gemv_supported((int)M, (int)K);
   const bool gemv_ok = tc_ok || mma_ok;
   if (path == FN_PATH_SIMT) return fail(FN_ERR_UNSUPPORTED, "SIMT path is f32-only");
   if ((path == FN_PATH_GEMV && !gemv_ok) || (path == FN_PATH_GEMV_MMA && !mma_ok))
@@ -195,7 +204,7 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
     if ((s = get_tmap(Wt_star, N, K, fn::gemv_tc_tile_rows(km, (int)K, (int)N, num_sms()), &tw)) != FN_OK) return s;
     if ((s = get_tmap(a, M, K, 16, &ta)) != FN_OK) return s;
     cudaError_t e = fn::launch_gemv_tc(tw, ta, c_star, static_cast<__nv_bfloat16*>(z), (int)M, (int)K, (int)N, eps,
-                                       alpha, km, num_sms(), stream);
+                                       alpha, km, num_sms(), stream, ex.row_scale);
     if (e != cudaSuccess) return cuda_fail(e, "gemv_tc");
     ++g_launches;
     return FN_OK;
@@ -248,6 +257,9 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
   p.cstar = c_star;
   p.z = static_cast<__nv_bfloat16*>(z);
   p.a = static_cast<const __nv_bfloat16*>(a);
+  p.glu_act = ex.glu_act;
+  p.s_out = ex.s_out;
+  p.row_scale = ex.row_scale;
   cudaError_t e = pair ? fn::launch_gemm2(ta, tb, p, km, num_sms(), stream)
                        : fn::launch_gemm(ta, tb, p, km, num_sms(), stream);
   if (e != cudaSuccess) return cuda_fail(e, pair ? "gemm2_sm100" : "gemm_sm100");
@@ -344,6 +356,59 @@ fn_status flashnorm_linear_ws(const void* a, const void* Wt_star, const float* c
     return fail(FN_ERR_NULL, "workspace is NULL but workspace_bytes = %lld", (long long)workspace_bytes);
   return linear_impl(a, Wt_star, c_star, M, K, N, eps, alpha, mode, dtype, z, path, workspace, workspace_bytes,
                      static_cast<cudaStream_t>(stream));
+}
+
+fn_status flashnorm_linear_scaled(const void* a, const void* Wt_star, const float* c_star, const float* row_scale,
+                                  int64_t M, int64_t K, int64_t N, fn_dtype dtype, void* z, void* stream) {
+  if (dtype != FN_BF16) return fail(FN_ERR_UNSUPPORTED, "flashnorm_linear_scaled is bf16-only");
+  if (row_scale == nullptr && M > 0) return fail(FN_ERR_NULL, "row_scale is NULL");
+  fn_status s;
+  if ((s = check_ptr16("row_scale", row_scale)) != FN_OK) return s;
+  LinearExtras ex;
+  ex.row_scale = row_scale;
+  return linear_impl(a, Wt_star, c_star, M, K, N, 0.0f, 0.0f, FN_NONE, dtype, z, FN_PATH_AUTO, nullptr, 0,
+                     static_cast<cudaStream_t>(stream), ex);
+}
+
+fn_status flashnorm_fold_glu_weights(const void* Wgt, const void* Wut, int64_t F, int64_t K, fn_dtype dtype,
+                                     const float* g, void* Wgu_star, void* stream) {
+  fn_status s;
+  if ((s = check_dtype(dtype)) != FN_OK) return s;
+  if (F <= 0 || K <= 0) return fail(FN_ERR_SHAPE, "Wgt/Wut[%lld x %lld]: sizes must be positive", (long long)F,
+                                    (long long)K);
+  if (F % 128 != 0) return fail(FN_ERR_SHAPE, "F = %lld must be a multiple of 128 (gate/up interleave)", (long long)F);
+  if (Wgt == nullptr || Wut == nullptr || Wgu_star == nullptr)
+    return fail(FN_ERR_NULL, "Wgt=%p Wut=%p Wgu_star=%p: NULL", Wgt, Wut, Wgu_star);
+  if ((s = check_vec("K", K, dtype)) != FN_OK) return s;
+  if ((s = check_ptr16("Wgt", Wgt)) != FN_OK || (s = check_ptr16("Wut", Wut)) != FN_OK ||
+      (s = check_ptr16("Wgu_star", Wgu_star)) != FN_OK || (s = check_ptr16("g", g)) != FN_OK)
+    return s;
+  if (Wgu_star == Wgt || Wgu_star == Wut) return fail(FN_ERR_VALUE, "Wgu_star must not alias Wgt / Wut");
+  const int dt = dtype == FN_BF16 ? 0 : 1;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = fn::launch_fold_weights(Wgt, F, K, dt, g, nullptr, nullptr, Wgu_star, nullptr, st, 0);
+  if (e == cudaSuccess) e = fn::launch_fold_weights(Wut, F, K, dt, g, nullptr, nullptr, Wgu_star, nullptr, st, 1);
+  if (e != cudaSuccess) return cuda_fail(e, "fold_glu_weights");
+  g_launches += 2;
+  return FN_OK;
+}
+
+fn_status flashnorm_glu_linear(const void* a, const void* Wgu_star, int64_t M, int64_t K, int64_t F, float eps,
+                               fn_glu_act act, fn_dtype dtype, void* h, float* s_out, void* stream) {
+  if (dtype != FN_BF16) return fail(FN_ERR_UNSUPPORTED, "flashnorm_glu_linear is bf16-only");
+  if (act < FN_GLU_SILU || act > FN_GLU_BILINEAR) return fail(FN_ERR_VALUE, "unknown fn_glu_act %d", (int)act);
+  if (F <= 0 || F % 128 != 0)
+    return fail(FN_ERR_SHAPE, "F = %lld must be a positive multiple of 128 (gate/up interleave)", (long long)F);
+  if (s_out == nullptr && M > 0) return fail(FN_ERR_NULL, "s_out is NULL");
+  fn_status s;
+  if ((s = check_ptr16("s_out", s_out)) != FN_OK) return s;
+  if (h != nullptr && (h == a || h == Wgu_star)) return fail(FN_ERR_VALUE, "h must not alias a or Wgu_star");
+  LinearExtras ex;
+  ex.glu_act = (int)act;
+  ex.s_out = s_out;
+  // the GEMM over the interleaved [2F][K] weights; z = h is [M][F]
+  return linear_impl(a, Wgu_star, nullptr, M, K, 2 * F, eps, 0.0f, FN_RMSNORM, dtype, h, FN_PATH_AUTO, nullptr, 0,
+                     static_cast<cudaStream_t>(stream), ex);
 }
 
 fn_status flashnorm_linear_from_host(const void* a_host, const void* Wt_star, const float* c_star, int64_t M,

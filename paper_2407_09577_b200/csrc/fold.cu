@@ -140,7 +140,7 @@ template <int DT, bool HAS_G, bool HAS_B>
 __global__ void __launch_bounds__(fold::WARPS_PER_CTA * 32)
     fold_weights_kernel(const uint8_t* __restrict__ Wt, int64_t N, int64_t K, const float* __restrict__ g,
                         const float* __restrict__ b, const float* __restrict__ c, uint8_t* __restrict__ Wt_star,
-                        float* __restrict__ c_star) {
+                        float* __restrict__ c_star, int glu_half) {
   // One warp per RPW consecutive rows: each lane loads its g/b chunk once and applies
   // it to RPW rows (RPW independent 16-byte W loads in flight per chunk); the c* sum of
   // every row keeps the contract order (lane l: its chunks ascending, then butterfly).
@@ -227,7 +227,9 @@ __global__ void __launch_bounds__(fold::WARPS_PER_CTA * 32)
         if (DT == 0) ow[e >> 1] = pack_bf16(ws[e], ws[e + 1]);  // packed RNE (F2FP, not XU)
         else { ow[e] = __float_as_uint(ws[e]); ow[e + 1] = __float_as_uint(ws[e + 1]); }
       }
-      *reinterpret_cast<uint4*>(Wt_star + ((j0 + r) * K + q * E) * ES) = o;
+      const int64_t jr = j0 + r;
+      const int64_t jo = glu_half < 0 ? jr : (jr >> 7) * 256 + glu_half * 128 + (jr & 127);  // GLU interleave
+      *reinterpret_cast<uint4*>(Wt_star + (jo * K + q * E) * ES) = o;
     }
    }
   }
@@ -251,14 +253,14 @@ __global__ void __launch_bounds__(fold::WARPS_PER_CTA * 32)
 }
 
 cudaError_t launch_fold_weights(const void* Wt, int64_t N, int64_t K, int dtype, const float* g, const float* b,
-                                const float* c, void* Wt_star, float* c_star, cudaStream_t stream) {
+                                const float* c, void* Wt_star, float* c_star, cudaStream_t stream, int glu_half) {
   const int64_t rows_per_cta = fold::WARPS_PER_CTA * fold::ROWS_PER_WARP;
   const dim3 grid((unsigned)((N + rows_per_cta - 1) / rows_per_cta));
   const dim3 block(fold::WARPS_PER_CTA * 32);
   const uint8_t* src = static_cast<const uint8_t*>(Wt);
   uint8_t* dst = static_cast<uint8_t*>(Wt_star);
   const bool hg = g != nullptr, hb = b != nullptr;
-#define FN_FOLD_LAUNCH(DT, G, B) fold_weights_kernel<DT, G, B><<<grid, block, 0, stream>>>(src, N, K, g, b, c, dst, c_star)
+#define FN_FOLD_LAUNCH(DT, G, B) fold_weights_kernel<DT, G, B><<<grid, block, 0, stream>>>(src, N, K, g, b, c, dst, c_star, glu_half)
   if (dtype == 0) {
     if (hg && hb) FN_FOLD_LAUNCH(0, true, true);
     else if (hg) FN_FOLD_LAUNCH(0, true, false);

@@ -242,8 +242,38 @@ __global__ void __launch_bounds__(gemm::THREADS, 1)
       mbar_wait_warp(&tfull[as], aphase);
       tc_fence_after();
       const int row = m_blk * BM + ew * 32 + lane;
-      const int n_base = n_blk * BN;
       const uint32_t taddr = tmem_base + ((ew * 32u) << 16) + as * BN;
+      if (MODE == MODE_RMS && p.glu_act >= 0) {
+        // GLU epilogue: TMEM columns [0,128) = gate block n_blk, [128,256) = up block n_blk
+        const int F = p.N / 2;
+        const float s_row = p.glu_act == GLU_SILU ? r : r * r;  // output scale (reading c25)
+        if (n_blk == 0 && row < p.M && p.s_out != nullptr) p.s_out[row] = s_row;
+        __nv_bfloat16* hrow = p.z + static_cast<size_t>(row) * F + n_blk * (BN / 2);
+#pragma unroll 1
+        for (int j = 0; j < BN / 64; ++j) {
+          uint32_t vg[32], vu[32];
+          tmem_ld_32x32b_x32(taddr + j * 32, vg);
+          tmem_ld_32x32b_x32(taddr + BN / 2 + j * 32, vu);
+          tmem_wait_ld();
+          uint32_t packed[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            packed[q] = pack_bf16(glu_apply(p.glu_act, __uint_as_float(vg[2 * q]), __uint_as_float(vu[2 * q]), r),
+                                  glu_apply(p.glu_act, __uint_as_float(vg[2 * q + 1]), __uint_as_float(vu[2 * q + 1]), r));
+          if (row < p.M) {
+            uint4* dst = reinterpret_cast<uint4*>(hrow + j * 32);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              dst[q] = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[as]);
+        continue;
+      }
+      if (MODE == MODE_NONE && p.row_scale != nullptr) r = row < p.M ? __ldg(p.row_scale + row) : 1.0f;
+      const int n_base = n_blk * BN;
       __nv_bfloat16* zrow = p.z + static_cast<size_t>(row) * p.N + n_base;
 #pragma unroll 1
       for (int j = 0; j < BN / 32; ++j) {

@@ -98,7 +98,8 @@ template <int MODE, int R>
 __global__ void __launch_bounds__(dtc::THREADS, 1)
     flashnorm_gemv_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_a,
                              const float* __restrict__ cstar, __nv_bfloat16* __restrict__ z, int M, int K, int N,
-                             float eps, float alpha, int S, int slot, int use_cluster) {
+                             float eps, float alpha, int S, int slot, int use_cluster,
+                             const float* __restrict__ row_scale) {
   using namespace dtc;
   constexpr int W_STAGE = Cfg<R>::W_STAGE;
   constexpr int STAGES = Cfg<R>::STAGES;
@@ -383,7 +384,9 @@ __global__ void __launch_bounds__(dtc::THREADS, 1)
       const float invK = 1.0f / (float)K;
       float rr[TOK];
 #pragma unroll
-      for (int m = 0; m < TOK; ++m) rr[m] = MODE == MODE_RMS ? rsqrtf(fmaf(ssq[m], invK, eps)) : 1.0f;
+      for (int m = 0; m < TOK; ++m)
+        rr[m] = MODE == MODE_RMS ? rsqrtf(fmaf(ssq[m], invK, eps))
+                                 : (MODE == MODE_NONE && row_scale != nullptr && m < M ? __ldg(row_scale + m) : 1.0f);
       pdl_wait_prior_grid();  // z may still be read by the previous kernel of the stream
 #pragma unroll
       for (int j = 0; j < R; ++j) {
@@ -505,7 +508,8 @@ bool gemv_tc_supported(int M, int N, int num_sms) {
 }
 
 cudaError_t launch_gemv_tc(const CUtensorMap& tw, const CUtensorMap& ta, const float* cstar, __nv_bfloat16* z,
-                           int M, int K, int N, float eps, float alpha, int mode, int num_sms, cudaStream_t stream) {
+                           int M, int K, int N, float eps, float alpha, int mode, int num_sms, cudaStream_t stream,
+                           const float* row_scale) {
   using namespace dtc;
   const DtcPlan p = dtc_plan(mode, K, N, num_sms);
   dtc_set_attr(mode, p.R);
@@ -530,7 +534,7 @@ cudaError_t launch_gemv_tc(const CUtensorMap& tw, const CUtensorMap& ta, const f
   cfg.attrs = at;
   cfg.numAttrs = 2;
   void* args[] = {(void*)&tw, (void*)&ta, (void*)&cstar, (void*)&z, (void*)&M, (void*)&K, (void*)&N,
-                  (void*)&eps, (void*)&alpha, (void*)&S, (void*)&slot, (void*)&use_cluster};
+                  (void*)&eps, (void*)&alpha, (void*)&S, (void*)&slot, (void*)&use_cluster, (void*)&row_scale};
   return cudaLaunchKernelExC(&cfg, fptr, args);
 }
 

@@ -17,7 +17,25 @@ struct GemmParams {
   __nv_bfloat16* z;
   const __nv_bfloat16* a;  // activations (the DyT prologue of the pair kernel reads them directly)
   int group_m;  // M blocks per tile group (L2 locality: A of a group stays resident while W* streams)
+  // GLU epilogue (MODE_RMS only, NEXT-1, reading c25): -1 = off, else GLU_SILU/GLU_RELU/GLU_BILINEAR.
+  // W* rows are gate/up interleaved in 128-row blocks; z is [M][N/2] and s_out[M] the output scale.
+  int glu_act;
+  float* s_out;
+  // MODE_NONE: optional per-row output scale z = RN(acc * row_scale[m] + c*) (the GLU down projection)
+  const float* row_scale;
 };
+enum GluAct { GLU_SILU = 0, GLU_RELU = 1, GLU_BILINEAR = 2 };
+
+// the GLU epilogue's element op (reading c25): SwiGLU scales the gate before the activation,
+// ReGLU / bilinear leave both scales to the output (s = r^2)
+static __device__ __forceinline__ float glu_apply(int act, float gate, float up, float r) {
+  if (act == GLU_SILU) {
+    const float x = gate * r;
+    return __fdividef(x, 1.0f + __expf(-x)) * up;
+  }
+  if (act == GLU_RELU) return fmaxf(gate, 0.0f) * up;
+  return gate * up;
+}
 
 // Persistent tile order: groups of `group_m` M blocks, M fastest inside a group, so the
 // tiles in flight at any time share a few W* column blocks (each streamed from HBM
@@ -51,7 +69,8 @@ bool gemv_tc_supported(int M, int N, int num_sms);
 int gemv_tc_split(int K, int N, int num_sms);      // K splits per tile
 int gemv_tc_tile_rows(int mode, int K, int N, int num_sms);  // W* rows per tile (128 or 256; the TMA box)
 cudaError_t launch_gemv_tc(const CUtensorMap& tw, const CUtensorMap& ta, const float* cstar, __nv_bfloat16* z,
-                           int M, int K, int N, float eps, float alpha, int mode, int num_sms, cudaStream_t stream);
+                           int M, int K, int N, float eps, float alpha, int mode, int num_sms, cudaStream_t stream,
+                           const float* row_scale = nullptr);
 size_t gemv_smem_bytes(int M, int K);
 cudaError_t launch_gemv(const __nv_bfloat16* a, const __nv_bfloat16* Wt, const float* cstar, __nv_bfloat16* z,
                         int M, int K, int N, float eps, float alpha, int mode, int num_sms, cudaStream_t stream);
@@ -61,8 +80,10 @@ cudaError_t launch_linear_f32(const float* a, const float* Wt, const float* csta
                               float eps, float alpha, int mode, cudaStream_t stream);
 
 // K1/K2: folds (fold.cu).  dtype: 0 = bf16, 1 = f32
+// glu_half: -1 = rows as given; 0 / 1 = write row j to (j/128)*256 + glu_half*128 + j%128 (the
+// gate / up half of the 128-row-block interleave of flashnorm_fold_glu_weights)
 cudaError_t launch_fold_weights(const void* Wt, int64_t N, int64_t K, int dtype, const float* g, const float* b,
-                                const float* c, void* Wt_star, float* c_star, cudaStream_t stream);
+                                const float* c, void* Wt_star, float* c_star, cudaStream_t stream, int glu_half = -1);
 int64_t fold_mean_center_workspace(int64_t n_out, int64_t d_in);
 // tm_v: plain (no swizzle) 2-D map of Vt [n_out][d_in], box FOLD_BOX_BYTES wide x 32 rows.
 constexpr int FOLD_BOX_BYTES = 512;

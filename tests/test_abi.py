@@ -99,6 +99,22 @@ def test_linear_ws_validation_codes(L):
     assert wb(300, 64, 64, 2, 1, 0) == 0                              # f32: none
 
 
+def test_glu_validation_codes(L):
+    gl = L.flashnorm_glu_linear
+    assert gl(P(0x1000), P(0x2000), 4, 64, 100, 1e-5, 0, 0, P(0x3000), P(0x4000), None) == 2   # F % 128
+    assert gl(P(0x1000), P(0x2000), 4, 64, 128, 1e-5, 7, 0, P(0x3000), P(0x4000), None) == 5   # act
+    assert gl(P(0x1000), P(0x2000), 4, 64, 128, 1e-5, 0, 1, P(0x3000), P(0x4000), None) == 6   # f32
+    assert gl(P(0x1000), P(0x2000), 4, 64, 128, 1e-5, 0, 0, P(0x3000), None, None) == 1        # s
+    assert gl(P(0x1000), P(0x2000), 4, 64, 128, 1e-5, 0, 0, P(0x1000), P(0x4000), None) == 5   # h aliases a
+    fg = L.flashnorm_fold_glu_weights
+    assert fg(P(0x1000), P(0x2000), 100, 64, 0, None, P(0x3000), None) == 2                    # F % 128
+    assert fg(P(0x1000), P(0x2000), 128, 60, 0, None, P(0x3000), None) == 4                    # K % 8
+    assert fg(P(0x1000), P(0x2000), 128, 64, 0, None, P(0x1000), None) == 5                    # aliasing
+    ls = L.flashnorm_linear_scaled
+    assert ls(P(0x1000), P(0x2000), None, None, 4, 64, 64, 0, P(0x3000), None) == 1            # no scale
+    assert ls(P(0x1000), P(0x2000), None, P(0x4000), 4, 64, 64, 1, P(0x3000), None) == 6       # f32
+
+
 def test_fold_validation_codes(L):
     f = L.flashnorm_fold_weights
     assert f(P(0x1000), 8, 64, 0, None, P(0x4000), None, P(0x2000), None, None) == 1   # b without c_star

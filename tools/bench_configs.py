@@ -102,6 +102,20 @@ for mode, path, wsp in (("rmsnorm", "auto", "auto"), ("none", "auto", "auto"), (
     us = timed(lambda i: fn.linear(a, Ws, cs, mode=mode, path=path, out=z, workspace=wsp), 10 if not QUICK else 3)
     tag = " (tanh prologue, no workspace)" if (mode == "dyt" and wsp is None) else (" (K8 pre-pass)" if mode == "dyt" else "")
     report("3 prefill M=4096 K=4096 N=28672", f"linear {mode} path={path}{tag}", us, flops=2 * M * K * N)
+# NEXT-1: SwiGLU FFN at config 3 (gate||up with the GLU epilogue + scaled down projection)
+F = N // 2
+Wgu = fn.fold_glu_weights(Ws[:F], Ws[F:], None)
+h = torch.empty((M, F), dtype=torch.bfloat16, device=dev)
+sg = torch.empty(M, dtype=torch.float32, device=dev)
+for act in ("silu", "relu"):
+    us = timed(lambda i: fn.glu_linear(a, Wgu, eps=1e-5, act=act, out=h, s_out=sg), 10 if not QUICK else 3)
+    report("NEXT-1 GLU FFN M=4096 K=4096 F=14336", f"glu_linear {act} (gate||up GEMM + GLU epilogue)", us,
+           flops=2 * M * K * N)
+Wdn, _, _, _ = SD.layer(77, K, F, dev, torch.bfloat16)
+yd = torch.empty((M, K), dtype=torch.bfloat16, device=dev)
+us = timed(lambda i: fn.linear_scaled(h, Wdn, sg, out=yd), 10 if not QUICK else 3)
+report("NEXT-1 GLU FFN M=4096 K=4096 F=14336", "linear_scaled down 14336->4096 (x s)", us, flops=2 * M * F * K)
+del Wgu, h, Wdn, yd
 del W, Ws, z
 
 # ---------------- config 4: LayerNorm retrofit (V* fold + upstream GEMM + LN linear) and DyT
