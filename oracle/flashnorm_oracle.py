@@ -287,6 +287,60 @@ def glu_ffn_deferred(a, Wg_star, Wu_star, Wd, eps=0.0, act="silu"):
 
 
 # ---------------------------------------------------------------------------
+# Q/K/V projection with RoPE (§3, Fig 5) — NEXT-2
+# ---------------------------------------------------------------------------
+
+def rope_permute(x):
+    """permute(x) = (-x2, x1, -x4, x3, ..., -x_h, x_{h-1}) over the last axis."""
+    x = _f64(x)
+    y = np.empty_like(x)
+    y[..., 0::2] = -x[..., 1::2]
+    y[..., 1::2] = x[..., 0::2]
+    return y
+
+
+def rope_cos_sin(pos, cos_tab, sin_tab):
+    """cos_m = (cos m t1, cos m t1, cos m t2, cos m t2, ...) for each row's position m
+    (PAPER.md:87-88); the tables hold cos(m t_i) / sin(m t_i) as [max_pos, h/2] [reading c26]."""
+    c = _f64(cos_tab)[np.asarray(pos)]
+    s = _f64(sin_tab)[np.asarray(pos)]
+    return np.repeat(c, 2, axis=-1), np.repeat(s, 2, axis=-1)
+
+
+def rope(x, pos, cos_tab, sin_tab):
+    """y = x * cos_m + permute(x) * sin_m for one head x[M, h]."""
+    c, s = rope_cos_sin(pos, cos_tab, sin_tab)
+    return _f64(x) * c + rope_permute(x) * s
+
+
+def qkv_rope_unfused(a, W, g, eps, n_rope, h, pos, cos_tab, sin_tab, qk_scale=1.0):
+    """Fig 5(a): x = RMSNorm(a; g); [Q | K | V] = x W (W is n x N, Q and K in the first n_rope
+    columns, h columns per head); RoPE on every Q/K head; Q and K times qk_scale (the paper folds
+    sqrt(1/sqrt(h)) of the scaled dot-product into both); V unchanged."""
+    y = rmsnorm(a, g, None, eps) @ _f64(W)
+    out = y.copy()
+    for h0 in range(0, n_rope, h):
+        out[:, h0:h0 + h] = rope(y[:, h0:h0 + h], pos, cos_tab, sin_tab) * qk_scale
+    return out
+
+
+def qkv_rope_deferred(a, Wstar, eps, n_rope, h, pos, cos_tab, sin_tab, qk_scale=1.0):
+    """Fig 5(b), step by step: acc = a W*; the cos/sin vectors are scaled ONCE per token by
+    1/RMSe(a) (and by qk_scale) and shared by all heads; V keeps the explicit 1/RMSe scale
+    (PAPER.md:89-93)."""
+    acc = _f64(a) @ _f64(Wstar)
+    r = 1.0 / rmse(a, eps)
+    c, s = rope_cos_sin(pos, cos_tab, sin_tab)
+    c = c * (r * qk_scale)[:, None]
+    s = s * (r * qk_scale)[:, None]
+    out = acc * r[:, None]
+    for h0 in range(0, n_rope, h):
+        x = acc[:, h0:h0 + h]
+        out[:, h0:h0 + h] = x * c + rope_permute(x) * s
+    return out
+
+
+# ---------------------------------------------------------------------------
 # Parity metric [reading c12]
 # ---------------------------------------------------------------------------
 

@@ -360,3 +360,76 @@ def test_glu_faults_detected():
     r = 1.0 / O.rmse(a, 0.0)
     wrong = O.glu_act(a @ Wg, "silu") * (a @ Wu) * (r * r)[:, None]   # Fig 4(b) form used for silu
     assert not np.allclose(wrong, h, rtol=1e-3)
+
+
+# ---------------------------------------------------------------- RoPE / QKV (NEXT-2)
+
+def _tables(max_pos, h, base=10000.0):
+    i = np.arange(h // 2)
+    theta = base ** (-2.0 * i / h)
+    ang = np.arange(max_pos)[:, None] * theta[None, :]
+    return np.cos(ang), np.sin(ang)
+
+
+def test_rope_worked_quarter_turn():
+    """m*theta = pi/2: cos = 0, sin = 1 -> (x1, x2) -> (-x2, x1), the paper's permute"""
+    cos_tab = np.array([[1.0], [0.0]])
+    sin_tab = np.array([[0.0], [1.0]])
+    y = O.rope(np.array([[3.0, 4.0], [3.0, 4.0]]), [0, 1], cos_tab, sin_tab)
+    np.testing.assert_array_equal(y, [[3.0, 4.0], [-4.0, 3.0]])
+    np.testing.assert_array_equal(O.rope_permute(np.array([1.0, 2.0, 3.0, 4.0])), [-2.0, 1.0, -4.0, 3.0])
+
+
+def test_rope_is_a_rotation_and_relative():
+    """Each pair is rotated by m*theta_i: norms are preserved and q.k after RoPE depends only on
+    the relative position (RoPE's defining property) — checked with math.cos/sin per pair."""
+    rng = np.random.default_rng(6)
+    h, max_pos = 16, 64
+    cos_tab, sin_tab = _tables(max_pos, h)
+    q, k = rng.standard_normal((1, h)), rng.standard_normal((1, h))
+    for m, n in ((5, 3), (40, 1), (7, 7)):
+        qm = O.rope(q, [m], cos_tab, sin_tab)
+        kn = O.rope(k, [n], cos_tab, sin_tab)
+        np.testing.assert_allclose(np.linalg.norm(qm), np.linalg.norm(q), rtol=1e-14)
+        rel = O.rope(q, [m - n], cos_tab, sin_tab)
+        assert float((qm @ kn.T)[0, 0]) == pytest.approx(float((rel @ k.T)[0, 0]), rel=1e-12, abs=1e-12)
+        # explicit 2x2 rotation per pair with math
+        for i in range(h // 2):
+            ang = m * 10000.0 ** (-2.0 * i / h)
+            x1, x2 = q[0, 2 * i], q[0, 2 * i + 1]
+            assert qm[0, 2 * i] == pytest.approx(x1 * math.cos(ang) - x2 * math.sin(ang), abs=1e-13)
+            assert qm[0, 2 * i + 1] == pytest.approx(x2 * math.cos(ang) + x1 * math.sin(ang), abs=1e-13)
+
+
+@pytest.mark.parametrize("eps", [0.0, 1e-5])
+@pytest.mark.parametrize("qk_scale", [1.0, 1.0 / math.sqrt(math.sqrt(128.0))])
+def test_qkv_rope_deferred_equals_unfused(eps, qk_scale):
+    """The paper's claim: Fig 5(b) (cos/sin scaled by 1/RMS once per token) == Fig 5(a)"""
+    rng = np.random.default_rng(7)
+    M, n, h = 5, 48, 8
+    n_q, n_k, n_v = 4 * h, 2 * h, 2 * h
+    N = n_q + n_k + n_v
+    a = rng.standard_normal((M, n)) * rng.uniform(0.1, 5, (M, 1))
+    W = rng.standard_normal((n, N)) / np.sqrt(n)
+    g = rng.uniform(0.5, 1.5, n)
+    cos_tab, sin_tab = _tables(32, h)
+    pos = rng.integers(0, 32, M)
+    ref = O.qkv_rope_unfused(a, W, g, eps, n_q + n_k, h, pos, cos_tab, sin_tab, qk_scale)
+    got = O.qkv_rope_deferred(a, O.merge_norm_weights(W, g), eps, n_q + n_k, h, pos, cos_tab, sin_tab, qk_scale)
+    np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-12)
+    # the scaled dot product: (q' . k') == (rope(q) . rope(k)) / sqrt(h) when qk_scale = h^-1/4
+    if qk_scale != 1.0:
+        plain = O.qkv_rope_unfused(a, W, g, eps, n_q + n_k, h, pos, cos_tab, sin_tab, 1.0)
+        qd = ref[:, :h] @ ref[:, n_q:n_q + h].T
+        np.testing.assert_allclose(qd, plain[:, :h] @ plain[:, n_q:n_q + h].T / math.sqrt(128.0), rtol=1e-12)
+
+
+def test_rope_fault_detected():
+    """rotate-half pairing (i, i+h/2) instead of the paper's adjacent pairs must differ"""
+    rng = np.random.default_rng(8)
+    x = rng.standard_normal((1, 8))
+    cos_tab, sin_tab = _tables(4, 8)
+    y = O.rope(x, [3], cos_tab, sin_tab)
+    c, s = O.rope_cos_sin([3], cos_tab, sin_tab)
+    half = np.concatenate([-x[:, 4:], x[:, :4]], axis=1)
+    assert not np.allclose(x * c + half * s, y)
