@@ -214,6 +214,29 @@ fn_status flashnorm_glu_linear(const void* a, const void* Wgu_star, int64_t M, i
 fn_status flashnorm_linear_scaled(const void* a, const void* Wt_star, const float* c_star, const float* row_scale,
                                   int64_t M, int64_t K, int64_t N, fn_dtype dtype, void* z, void* stream);
 
+/* --------------------------------------------------------------------------
+ * flashnorm_qkv_rope_linear — the Q/K/V projection with RoPE (NEXT-2, PAPER.md:80-94,
+ * §3 Fig 5(b); readings c26, c27), bias-free, bf16 only:
+ *   acc = a W*^T (W* = folded [Q|K|V] weights, N rows: Q and K heads in the first n_rope rows,
+ *   head_dim rows per head, V after), r_m = rsqrt(ssq_m/K + eps) reduced beside the contraction;
+ *   Q/K columns: pairs (2i, 2i+1) of each head rotate with the per-token cos/sin scaled ONCE by
+ *   r_m * qk_scale (shared by every head):
+ *     z[m][2i]   = RN(acc_2i * c - acc_2i+1 * s),  z[m][2i+1] = RN(acc_2i+1 * c + acc_2i * s),
+ *     c = cos_tab[pos_m][i'] * r_m * qk_scale,  s = sin_tab[pos_m][i'] * r_m * qk_scale,
+ *     i' = (column mod head_dim) / 2;
+ *   V columns (>= n_rope): z = RN(acc * r_m)  ("the V linear layer still needs the
+ *   normalization at its output").
+ *   positions [M] int32 (device), cos_tab / sin_tab [max_pos][head_dim/2] float32 (device;
+ *   the caller guarantees 0 <= positions[m] < max_pos).  qk_scale: pass sqrt(1/sqrt(head_dim))
+ *   to fold the scaled dot-product's 1/sqrt(head_dim), or 1.
+ *   n_rope % head_dim == 0, n_rope % 32 == 0, head_dim even.  Decode (M <= 16) runs on the
+ *   tcgen05 split-K kernel, prefill on the tcgen05 GEMM.
+ * -------------------------------------------------------------------------- */
+fn_status flashnorm_qkv_rope_linear(const void* a, const void* Wt_star, int64_t M, int64_t K, int64_t N,
+                                    int64_t n_rope, int64_t head_dim, const int32_t* positions,
+                                    const float* cos_tab, const float* sin_tab, float qk_scale, float eps,
+                                    fn_dtype dtype, void* z, void* stream);
+
 /* End-to-end variant: a_host / z_host are HOST pointers (pinned memory for
  * asynchronous copies); a_dev / z_dev are caller-owned device scratch of
  * M*K / M*N elements.  Enqueues H2D(a) -> flashnorm_linear -> D2H(z) on

@@ -22,7 +22,7 @@ from typing import Optional, Tuple
 __all__ = [
     "FlashNormError", "lib", "lib_path", "fold_weights", "fold_mean_center", "fold_mean_center_workspace_bytes",
     "linear", "linear_from_host", "baseline_norm", "gather_columns", "launch_count", "reset_launch_count",
-    "version", "linear_workspace_bytes", "fold_glu_weights", "glu_linear", "linear_scaled", "glu_ffn",
+    "version", "linear_workspace_bytes", "fold_glu_weights", "glu_linear", "linear_scaled", "glu_ffn", "qkv_rope_linear",
     "MODES", "GLU_ACTS", "PATHS", "EXPORTS",
 ]
 
@@ -38,7 +38,8 @@ _DT_BF16, _DT_F32 = 0, 1
 EXPORTS = [
     "flashnorm_fold_weights", "flashnorm_fold_mean_center_workspace_bytes", "flashnorm_fold_mean_center",
     "flashnorm_linear", "flashnorm_linear_ex", "flashnorm_linear_workspace_bytes", "flashnorm_linear_ws",
-    "flashnorm_linear_from_host", "flashnorm_fold_glu_weights", "flashnorm_glu_linear", "flashnorm_linear_scaled", "flashnorm_baseline_norm",
+    "flashnorm_linear_from_host", "flashnorm_fold_glu_weights", "flashnorm_glu_linear", "flashnorm_linear_scaled",
+    "flashnorm_qkv_rope_linear", "flashnorm_baseline_norm",
     "flashnorm_gather_columns", "flashnorm_status_string", "flashnorm_last_error", "flashnorm_launch_count",
     "flashnorm_reset_launch_count", "flashnorm_version",
 ]
@@ -75,6 +76,8 @@ def lib() -> ctypes.CDLL:
         "flashnorm_linear_ws": [_vp, _vp, _vp, _i64, _i64, _i64, _f32, _f32, _int, _int, _vp, _int, _vp, _i64, _vp],
         "flashnorm_fold_glu_weights": [_vp, _vp, _i64, _i64, _int, _vp, _vp, _vp],
         "flashnorm_glu_linear": [_vp, _vp, _i64, _i64, _i64, _f32, _int, _int, _vp, _vp, _vp],
+        "flashnorm_qkv_rope_linear": [_vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _f32, _f32, _int, _vp,
+                                      _vp],
         "flashnorm_linear_scaled": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _vp, _vp],
         "flashnorm_linear_from_host": [_vp, _vp, _vp, _i64, _i64, _i64, _f32, _f32, _int, _int, _vp, _vp, _vp,
                                        _vp],
@@ -296,6 +299,26 @@ def glu_ffn(a, Wgu_star, Wd_t, eps: float = 1e-5, act: str = "silu"):
     projection scaled at its output)."""
     h, s = glu_linear(a, Wgu_star, eps=eps, act=act)
     return linear_scaled(h, Wd_t, s)
+
+
+def qkv_rope_linear(a, Wt_star, n_rope: int, head_dim: int, positions, cos_tab, sin_tab, qk_scale: float = 1.0,
+                    eps: float = 1e-5, out=None):
+    """[Q | K | V] = RoPE-fused FlashNorm projection (Fig 5(b)).
+    positions: int32 [M]; cos_tab / sin_tab: float32 [max_pos, head_dim // 2]."""
+    torch = _torch()
+    _dev(a, "a")
+    _dev(Wt_star, "Wt_star")
+    for t, nm in ((positions, "positions"), (cos_tab, "cos_tab"), (sin_tab, "sin_tab")):
+        _dev(t, nm)
+    if positions.dtype != torch.int32 or cos_tab.dtype != torch.float32 or sin_tab.dtype != torch.float32:
+        raise FlashNormError(3, "qkv_rope_linear", "positions must be int32, cos_tab / sin_tab float32")
+    M, K = a.shape
+    N = Wt_star.shape[0]
+    z = out if out is not None else torch.empty((M, N), dtype=a.dtype, device=a.device)
+    _check(lib().flashnorm_qkv_rope_linear(_ptr(a), _ptr(Wt_star), M, K, N, n_rope, head_dim, _ptr(positions),
+                                           _ptr(cos_tab), _ptr(sin_tab), float(qk_scale), float(eps),
+                                           _dtype_code(a), _ptr(z), _stream(a)), "qkv_rope_linear")
+    return z
 
 
 def linear_from_host(a_host, Wt_star, c_star, a_dev, z_dev, z_host, eps: float = 1e-5, mode: str = "rmsnorm",

@@ -146,6 +146,7 @@ struct LinearExtras {
   int glu_act = -1;                 // >= 0: gate||up GEMM with the GLU epilogue, z = h [M][N/2]
   float* s_out = nullptr;           // GLU: output scale per row
   const float* row_scale = nullptr; // FN_NONE: z = RN(acc * row_scale[m] + c*)
+  fn::RopeParams rope{nullptr, nullptr, nullptr, 0, 0, 1.0f};  // FN_RMSNORM: RoPE on [0, rope.n)
 };
 
 fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, int64_t M, int64_t K, int64_t N,
@@ -192,7 +193,8 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
 
   // the GLU epilogue lives in the GEMM kernels; a given row scale in the GEMM and tcgen05 decode kernels
   const bool tc_ok = ex.glu_act < 0 && fn::gemv_tc_supported((int)M, (int)N, num_sms());
-  const bool mma_ok = ex.glu_act < 0 && ex.row_scale == nullptr && fn::gemv_supported((int)M, (int)K);
+  const bool mma_ok = ex.glu_act < 0 && ex.row_scale == nullptr && ex.rope.pos == nullptr &&
+                      fn::gemv_supported((int)M, (int)K);
   const bool gemv_ok = tc_ok || mma_ok;
   if (path == FN_PATH_SIMT) return fail(FN_ERR_UNSUPPORTED, "SIMT path is f32-only");
   if ((path == FN_PATH_GEMV && !gemv_ok) || (path == FN_PATH_GEMV_MMA && !mma_ok))
@@ -204,7 +206,7 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
     if ((s = get_tmap(Wt_star, N, K, fn::gemv_tc_tile_rows(km, (int)K, (int)N, num_sms()), &tw)) != FN_OK) return s;
     if ((s = get_tmap(a, M, K, 16, &ta)) != FN_OK) return s;
     cudaError_t e = fn::launch_gemv_tc(tw, ta, c_star, static_cast<__nv_bfloat16*>(z), (int)M, (int)K, (int)N, eps,
-                                       alpha, km, num_sms(), stream, ex.row_scale);
+                                       alpha, km, num_sms(), stream, ex.row_scale, ex.rope);
     if (e != cudaSuccess) return cuda_fail(e, "gemv_tc");
     ++g_launches;
     return FN_OK;
@@ -260,6 +262,7 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
   p.glu_act = ex.glu_act;
   p.s_out = ex.s_out;
   p.row_scale = ex.row_scale;
+  p.rope = ex.rope;
   cudaError_t e = pair ? fn::launch_gemm2(ta, tb, p, km, num_sms(), stream)
                        : fn::launch_gemm(ta, tb, p, km, num_sms(), stream);
   if (e != cudaSuccess) return cuda_fail(e, pair ? "gemm2_sm100" : "gemm_sm100");
@@ -367,6 +370,26 @@ fn_status flashnorm_linear_scaled(const void* a, const void* Wt_star, const floa
   LinearExtras ex;
   ex.row_scale = row_scale;
   return linear_impl(a, Wt_star, c_star, M, K, N, 0.0f, 0.0f, FN_NONE, dtype, z, FN_PATH_AUTO, nullptr, 0,
+                     static_cast<cudaStream_t>(stream), ex);
+}
+
+fn_status flashnorm_qkv_rope_linear(const void* a, const void* Wt_star, int64_t M, int64_t K, int64_t N,
+                                    int64_t n_rope, int64_t head_dim, const int32_t* positions, const float* cos_tab,
+                                    const float* sin_tab, float qk_scale, float eps, fn_dtype dtype, void* z,
+                                    void* stream) {
+  if (dtype != FN_BF16) return fail(FN_ERR_UNSUPPORTED, "flashnorm_qkv_rope_linear is bf16-only");
+  if (head_dim <= 0 || head_dim % 2 != 0 || head_dim > 65536)
+    return fail(FN_ERR_SHAPE, "head_dim = %lld must be even and positive", (long long)head_dim);
+  if (n_rope < 0 || n_rope > N || n_rope % head_dim != 0 || n_rope % 32 != 0)
+    return fail(FN_ERR_SHAPE, "n_rope = %lld must be a multiple of head_dim (%lld) and of 32, <= N = %lld",
+                (long long)n_rope, (long long)head_dim, (long long)N);
+  if (M > 0 && n_rope > 0 && (positions == nullptr || cos_tab == nullptr || sin_tab == nullptr))
+    return fail(FN_ERR_NULL, "positions=%p cos_tab=%p sin_tab=%p: NULL", (const void*)positions,
+                (const void*)cos_tab, (const void*)sin_tab);
+  if (!std::isfinite(qk_scale)) return fail(FN_ERR_VALUE, "qk_scale = %g must be finite", (double)qk_scale);
+  LinearExtras ex;
+  if (n_rope > 0) ex.rope = fn::RopeParams{positions, cos_tab, sin_tab, (int)n_rope, (int)head_dim, qk_scale};
+  return linear_impl(a, Wt_star, nullptr, M, K, N, eps, 0.0f, FN_RMSNORM, dtype, z, FN_PATH_AUTO, nullptr, 0,
                      static_cast<cudaStream_t>(stream), ex);
 }
 

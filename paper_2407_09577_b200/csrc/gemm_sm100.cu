@@ -295,11 +295,41 @@ __global__ void __launch_bounds__(gemm::THREADS, 1)
           for (int q = 0; q < 32; ++q) cb[q] = 0.f;
         }
         uint32_t packed[16];
+        if (MODE == MODE_RMS && p.rope.pos != nullptr && n_base + j * 32 < p.rope.n) {
+          // Fig 5(b): cos/sin scaled once per token by r (and sqrt(1/sqrt h)), shared by all heads
+          const int pos = row < p.M ? __ldg(p.rope.pos + row) : 0;
+          const int hh = p.rope.h >> 1;
+          const float rq = r * p.rope.qk;
+          const int i0 = ((n_base + j * 32) % p.rope.h) >> 1;  // 16 consecutive pair indices
+          float cs[16], sn[16];
+          if ((hh & 3) == 0 && i0 + 16 <= hh) {  // one head, 16-byte aligned: 4 x float4 each
+            const float4* c4 = reinterpret_cast<const float4*>(p.rope.cos_tab + (size_t)pos * hh + i0);
+            const float4* s4 = reinterpret_cast<const float4*>(p.rope.sin_tab + (size_t)pos * hh + i0);
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const float z0 = fmaf(__uint_as_float(v[2 * q]), r, cb[2 * q]);
-          const float z1 = fmaf(__uint_as_float(v[2 * q + 1]), r, cb[2 * q + 1]);
-          packed[q] = pack_bf16(z0, z1);
+            for (int q = 0; q < 4; ++q) {
+              const float4 c = __ldg(c4 + q), sv = __ldg(s4 + q);
+              cs[4 * q] = c.x; cs[4 * q + 1] = c.y; cs[4 * q + 2] = c.z; cs[4 * q + 3] = c.w;
+              sn[4 * q] = sv.x; sn[4 * q + 1] = sv.y; sn[4 * q + 2] = sv.z; sn[4 * q + 3] = sv.w;
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              const int i = ((n_base + j * 32 + 2 * q) % p.rope.h) >> 1;
+              cs[q] = __ldg(p.rope.cos_tab + (size_t)pos * hh + i);
+              sn[q] = __ldg(p.rope.sin_tab + (size_t)pos * hh + i);
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const float c = cs[q] * rq, s = sn[q] * rq;
+            const float x0 = __uint_as_float(v[2 * q]), x1 = __uint_as_float(v[2 * q + 1]);
+            packed[q] = pack_bf16(fmaf(x0, c, -x1 * s), fmaf(x1, c, x0 * s));
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            packed[q] = pack_bf16(fmaf(__uint_as_float(v[2 * q]), r, cb[2 * q]),
+                                  fmaf(__uint_as_float(v[2 * q + 1]), r, cb[2 * q + 1]));
         }
         if (row < p.M) {
           uint4* dst = reinterpret_cast<uint4*>(zrow + j * 32);

@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(dtc::THREADS, 1)
     flashnorm_gemv_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_a,
                              const float* __restrict__ cstar, __nv_bfloat16* __restrict__ z, int M, int K, int N,
                              float eps, float alpha, int S, int slot, int use_cluster,
-                             const float* __restrict__ row_scale) {
+                             const float* __restrict__ row_scale, const RopeParams rope) {
   using namespace dtc;
   constexpr int W_STAGE = Cfg<R>::W_STAGE;
   constexpr int STAGES = Cfg<R>::STAGES;
@@ -270,6 +270,25 @@ __global__ void __launch_bounds__(dtc::THREADS, 1)
     const uint32_t q4 = warp & 3u;  // TMEM lane quarter this warp may access
     const int row = (int)(q4 * 32 + lane);
     named_bar_sync(1, 128);         // ssq_own written by the side warp
+    // RoPE: fetch this thread's cos/sin (per token) while the accumulator is still being built;
+    // only block 0 of the tile (R = 1 covers it whole) is used below
+    const bool rope_blk = R == 1 && MODE == MODE_RMS && rope.pos != nullptr && n0 < rope.n;
+    float rc[TOK], rs[TOK];
+    if (rope_blk) {
+      const int n = n0 + row;
+      const int hh = rope.h >> 1;
+      const int i = (n % rope.h) >> 1;
+#pragma unroll
+      for (int m = 0; m < TOK; ++m) {
+        rc[m] = 0.f;
+        rs[m] = 0.f;
+        if (m < M) {
+          const int pos = __ldg(rope.pos + m);
+          rc[m] = __ldg(rope.cos_tab + (size_t)pos * hh + i);
+          rs[m] = __ldg(rope.sin_tab + (size_t)pos * hh + i);
+        }
+      }
+    }
     mbar_wait_warp(tfull, 0);
     if (warp == 2 && lane == 0) TC_TRACE(2);
     tc_fence_after();
@@ -391,6 +410,44 @@ __global__ void __launch_bounds__(dtc::THREADS, 1)
 #pragma unroll
       for (int j = 0; j < R; ++j) {
         const int n = n0 + j * ROWS + row;
+        if (R == 1 && rope_blk) {
+          // RoPE (Fig 5(b)): the pair partner of W* row n is row n^1, held by lane^1; cos/sin are
+          // scaled once per token by r * qk (shared by every head)
+          float pv[TOK];
+#pragma unroll
+          for (int m = 0; m < TOK; ++m) pv[m] = __shfl_xor_sync(0xffffffffu, acc[j][m], 1);
+          if (n < N && n < rope.n) {
+            const float sgn = (n & 1) ? 1.0f : -1.0f;  // y0 = x0 c - x1 s, y1 = x1 c + x0 s
+#pragma unroll
+            for (int m = 0; m < TOK; ++m) {
+              if (m < M) {
+                const float rq = rr[m] * rope.qk;
+                z[(size_t)m * N + n] = __float2bfloat16_rn(fmaf(acc[j][m], rc[m] * rq, sgn * pv[m] * (rs[m] * rq)));
+              }
+            }
+            continue;
+          }
+        } else if (R == 2 && MODE == MODE_RMS && rope.pos != nullptr && n0 + j * ROWS < rope.n) {
+          float pv[TOK];
+#pragma unroll
+          for (int m = 0; m < TOK; ++m) pv[m] = __shfl_xor_sync(0xffffffffu, acc[j][m], 1);
+          if (n < N && n < rope.n) {
+            const int hh = rope.h >> 1;
+            const int i = (n % rope.h) >> 1;
+            const float sgn = (n & 1) ? 1.0f : -1.0f;
+#pragma unroll
+            for (int m = 0; m < TOK; ++m) {
+              if (m < M) {
+                const int pos = __ldg(rope.pos + m);
+                const float rq = rr[m] * rope.qk;
+                const float c = __ldg(rope.cos_tab + (size_t)pos * hh + i) * rq;
+                const float sn = __ldg(rope.sin_tab + (size_t)pos * hh + i) * rq;
+                z[(size_t)m * N + n] = __float2bfloat16_rn(fmaf(acc[j][m], c, sgn * pv[m] * sn));
+              }
+            }
+            continue;
+          }
+        }
         if (n < N) {
           const float cb = cstar != nullptr ? __ldg(cstar + n) : 0.0f;
 #pragma unroll
@@ -509,7 +566,7 @@ bool gemv_tc_supported(int M, int N, int num_sms) {
 
 cudaError_t launch_gemv_tc(const CUtensorMap& tw, const CUtensorMap& ta, const float* cstar, __nv_bfloat16* z,
                            int M, int K, int N, float eps, float alpha, int mode, int num_sms, cudaStream_t stream,
-                           const float* row_scale) {
+                           const float* row_scale, RopeParams rope) {
   using namespace dtc;
   const DtcPlan p = dtc_plan(mode, K, N, num_sms);
   dtc_set_attr(mode, p.R);
@@ -534,7 +591,8 @@ cudaError_t launch_gemv_tc(const CUtensorMap& tw, const CUtensorMap& ta, const f
   cfg.attrs = at;
   cfg.numAttrs = 2;
   void* args[] = {(void*)&tw, (void*)&ta, (void*)&cstar, (void*)&z, (void*)&M, (void*)&K, (void*)&N,
-                  (void*)&eps, (void*)&alpha, (void*)&S, (void*)&slot, (void*)&use_cluster, (void*)&row_scale};
+                  (void*)&eps, (void*)&alpha, (void*)&S, (void*)&slot, (void*)&use_cluster, (void*)&row_scale,
+                  (void*)&rope};
   return cudaLaunchKernelExC(&cfg, fptr, args);
 }
 

@@ -9,6 +9,18 @@ namespace fn {
 
 enum KernelMode { MODE_RMS = 0, MODE_DYT = 1, MODE_NONE = 2 };
 
+// RoPE epilogue (NEXT-2, Fig 5(b), readings c26-c27): output columns [0, n) are
+// Q/K heads of h columns; for token m at position pos[m], adjacent pairs (2i, 2i+1) of a head
+// rotate with cos'/sin' = table[pos][i] * r_m * qk (the 1/RMS and sqrt(1/sqrt h) folded into
+// cos/sin once per token); the V columns >= n keep acc * r_m.  pos == nullptr: off.
+struct RopeParams {
+  const int* pos;
+  const float* cos_tab;  // [max_pos][h/2]
+  const float* sin_tab;
+  int n, h;
+  float qk;
+};
+
 struct GemmParams {
   int M, N, K;
   int num_m_blocks, num_n_blocks, num_tiles, num_k_blocks;
@@ -23,6 +35,7 @@ struct GemmParams {
   float* s_out;
   // MODE_NONE: optional per-row output scale z = RN(acc * row_scale[m] + c*) (the GLU down projection)
   const float* row_scale;
+  RopeParams rope;
 };
 enum GluAct { GLU_SILU = 0, GLU_RELU = 1, GLU_BILINEAR = 2 };
 
@@ -70,7 +83,7 @@ int gemv_tc_split(int K, int N, int num_sms);      // K splits per tile
 int gemv_tc_tile_rows(int mode, int K, int N, int num_sms);  // W* rows per tile (128 or 256; the TMA box)
 cudaError_t launch_gemv_tc(const CUtensorMap& tw, const CUtensorMap& ta, const float* cstar, __nv_bfloat16* z,
                            int M, int K, int N, float eps, float alpha, int mode, int num_sms, cudaStream_t stream,
-                           const float* row_scale = nullptr);
+                           const float* row_scale = nullptr, RopeParams rope = RopeParams{nullptr, nullptr, nullptr, 0, 0, 1.f});
 size_t gemv_smem_bytes(int M, int K);
 cudaError_t launch_gemv(const __nv_bfloat16* a, const __nv_bfloat16* Wt, const float* cstar, __nv_bfloat16* z,
                         int M, int K, int N, float eps, float alpha, int mode, int num_sms, cudaStream_t stream);

@@ -86,6 +86,18 @@ for M in (1, 16):
         us = timed(lambda i: fn.linear(ad, Wd[i % 4], None, mode=mode, path=path, out=zd), 200, graph=True)
         report(f"2 decode M={M} K=4096 N=6144", f"linear {mode} path={path} (graph, 4 rotating W*)", us,
                byts=K * N * 2 + M * K * 2 + M * N * 2)
+# NEXT-2: the same QKV projection with RoPE fused (32 Q + 8 K heads of 128 rotated, V plain)
+i_ = torch.arange(64, device=dev, dtype=torch.float64)
+ang = torch.arange(8192, device=dev, dtype=torch.float64)[:, None] * (500000.0 ** (-2.0 * i_ / 128))[None, :]
+cos_t, sin_t = torch.cos(ang).float(), torch.sin(ang).float()
+for M in (1, 16):
+    ad = SD.activations(7, M, K, dev, torch.bfloat16)
+    zd = torch.empty(M, N, dtype=torch.bfloat16, device=dev)
+    posd = torch.arange(M, device=dev, dtype=torch.int32) + 1000
+    us = timed(lambda i: fn.qkv_rope_linear(ad, Wd[i % 4], 5120, 128, posd, cos_t, sin_t, qk_scale=128 ** -0.25,
+                                            out=zd), 200, graph=True)
+    report(f"NEXT-2 decode M={M} K=4096 N=6144", "qkv_rope_linear (graph, 4 rotating W*)", us,
+           byts=K * N * 2 + M * K * 2 + M * N * 2)
 del Wd
 
 # ---------------- config 3: prefill + folds
@@ -102,6 +114,12 @@ for mode, path, wsp in (("rmsnorm", "auto", "auto"), ("none", "auto", "auto"), (
     us = timed(lambda i: fn.linear(a, Ws, cs, mode=mode, path=path, out=z, workspace=wsp), 10 if not QUICK else 3)
     tag = " (tanh prologue, no workspace)" if (mode == "dyt" and wsp is None) else (" (K8 pre-pass)" if mode == "dyt" else "")
     report("3 prefill M=4096 K=4096 N=28672", f"linear {mode} path={path}{tag}", us, flops=2 * M * K * N)
+# NEXT-2 prefill: the RoPE epilogue on the same GEMM (Q/K = the first 5120 of 28672 columns)
+pos3 = (torch.arange(M, device=dev, dtype=torch.int32) % 8192)
+us = timed(lambda i: fn.qkv_rope_linear(a, Ws, 5120, 128, pos3, cos_t, sin_t, qk_scale=128 ** -0.25, out=z),
+           10 if not QUICK else 3)
+report("NEXT-2 prefill M=4096 K=4096 N=28672", "qkv_rope_linear (RoPE on 5120 columns)", us, flops=2 * M * K * N)
+
 # NEXT-1: SwiGLU FFN at config 3 (gate||up with the GLU epilogue + scaled down projection)
 F = N // 2
 Wgu = fn.fold_glu_weights(Ws[:F], Ws[F:], None)
