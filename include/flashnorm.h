@@ -207,6 +207,14 @@ fn_status flashnorm_linear_ws(const void* a, const void* Wt_star, const float* c
  * -------------------------------------------------------------------------- */
 typedef enum { FN_GLU_SILU = 0, FN_GLU_RELU = 1, FN_GLU_BILINEAR = 2 } fn_glu_act;
 
+/* flashnorm_relu_ffn_up — FFN with ReLU (not gated), Fig 2(b): the whole
+ *   normalization is deferred to the FFN output because ReLU(s a) = s ReLU(a) for s >= 0:
+ *   h = RN(relu(a W*_up)) (no scale), s_m = r_m = rsqrt(ssq_m/K + eps); the FFN output is
+ *   y = (h W_down) * s via flashnorm_linear_scaled.  Wt_star [F][K] (W*_up^T), h [M][F] bf16,
+ *   s [M] float32.  bf16 only, tcgen05 GEMM. */
+fn_status flashnorm_relu_ffn_up(const void* a, const void* Wt_star, int64_t M, int64_t K, int64_t F, float eps,
+                                fn_dtype dtype, void* h, float* s, void* stream);
+
 fn_status flashnorm_fold_glu_weights(const void* Wgt, const void* Wut, int64_t F, int64_t K, fn_dtype dtype,
                                      const float* g, void* Wgu_star, void* stream);
 fn_status flashnorm_glu_linear(const void* a, const void* Wgu_star, int64_t M, int64_t K, int64_t F, float eps,

@@ -230,6 +230,19 @@ def fold_mean_center(V, b_prev=None):
 # FFN with a GLU variant (§2.2, Figs 3-4) — NEXT-1
 # ---------------------------------------------------------------------------
 
+def relu_ffn(a, Wu, Wd, g=None, eps=0.0):
+    """FFN with ReLU, unoptimized Fig 2(a): y = ReLU(RMSNorm(a; g) Wu) Wd (bias-free)."""
+    return np.maximum(rmsnorm(a, g, None, eps) @ _f64(Wu), 0.0) @ _f64(Wd)
+
+
+def relu_ffn_deferred(a, Wu_star, Wd, eps=0.0):
+    """Fig 2(b): the normalization deferred to the FFN output, y = (ReLU(a Wu*) Wd) / RMSe(a)
+    ("multiplying its argument by a non-negative scaling factor s is the same as scaling its
+    output by s").  Returns (h, s) with y = (h Wd) * s."""
+    h = np.maximum(_f64(a) @ _f64(Wu_star), 0.0)
+    return h, 1.0 / rmse(a, eps)
+
+
 GLU_ACTS = ("silu", "relu", "bilinear")
 
 

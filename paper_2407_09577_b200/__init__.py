@@ -22,7 +22,7 @@ from typing import Optional, Tuple
 __all__ = [
     "FlashNormError", "lib", "lib_path", "fold_weights", "fold_mean_center", "fold_mean_center_workspace_bytes",
     "linear", "linear_from_host", "baseline_norm", "gather_columns", "launch_count", "reset_launch_count",
-    "version", "linear_workspace_bytes", "fold_glu_weights", "glu_linear", "linear_scaled", "glu_ffn", "qkv_rope_linear",
+    "version", "linear_workspace_bytes", "fold_glu_weights", "glu_linear", "linear_scaled", "glu_ffn", "qkv_rope_linear", "relu_ffn_up",
     "MODES", "GLU_ACTS", "PATHS", "EXPORTS",
 ]
 
@@ -39,7 +39,7 @@ EXPORTS = [
     "flashnorm_fold_weights", "flashnorm_fold_mean_center_workspace_bytes", "flashnorm_fold_mean_center",
     "flashnorm_linear", "flashnorm_linear_ex", "flashnorm_linear_workspace_bytes", "flashnorm_linear_ws",
     "flashnorm_linear_from_host", "flashnorm_fold_glu_weights", "flashnorm_glu_linear", "flashnorm_linear_scaled",
-    "flashnorm_qkv_rope_linear", "flashnorm_baseline_norm",
+    "flashnorm_qkv_rope_linear", "flashnorm_relu_ffn_up", "flashnorm_baseline_norm",
     "flashnorm_gather_columns", "flashnorm_status_string", "flashnorm_last_error", "flashnorm_launch_count",
     "flashnorm_reset_launch_count", "flashnorm_version",
 ]
@@ -78,6 +78,7 @@ def lib() -> ctypes.CDLL:
         "flashnorm_glu_linear": [_vp, _vp, _i64, _i64, _i64, _f32, _int, _int, _vp, _vp, _vp],
         "flashnorm_qkv_rope_linear": [_vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _f32, _f32, _int, _vp,
                                       _vp],
+        "flashnorm_relu_ffn_up": [_vp, _vp, _i64, _i64, _i64, _f32, _int, _vp, _vp, _vp],
         "flashnorm_linear_scaled": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _vp, _vp],
         "flashnorm_linear_from_host": [_vp, _vp, _vp, _i64, _i64, _i64, _f32, _f32, _int, _int, _vp, _vp, _vp,
                                        _vp],
@@ -276,6 +277,20 @@ def glu_linear(a, Wgu_star, eps: float = 1e-5, act: str = "silu", out=None, s_ou
     s = s_out if s_out is not None else torch.empty(M, dtype=torch.float32, device=a.device)
     _check(lib().flashnorm_glu_linear(_ptr(a), _ptr(Wgu_star), M, K, F, float(eps), GLU_ACTS[act], _dtype_code(a),
                                       _ptr(h), _ptr(s), _stream(a)), "glu_linear")
+    return h, s
+
+
+def relu_ffn_up(a, Wt_star, eps: float = 1e-5, out=None, s_out=None):
+    """Fig 2(b): h = relu(a W*_up) (unscaled), s = 1/RMSe(a); y = (h W_down) * s via linear_scaled."""
+    torch = _torch()
+    _dev(a, "a")
+    _dev(Wt_star, "Wt_star")
+    M, K = a.shape
+    F = Wt_star.shape[0]
+    h = out if out is not None else torch.empty((M, F), dtype=a.dtype, device=a.device)
+    s = s_out if s_out is not None else torch.empty(M, dtype=torch.float32, device=a.device)
+    _check(lib().flashnorm_relu_ffn_up(_ptr(a), _ptr(Wt_star), M, K, F, float(eps), _dtype_code(a), _ptr(h), _ptr(s),
+                                       _stream(a)), "relu_ffn_up")
     return h, s
 
 

@@ -393,6 +393,19 @@ fn_status flashnorm_qkv_rope_linear(const void* a, const void* Wt_star, int64_t 
                      static_cast<cudaStream_t>(stream), ex);
 }
 
+fn_status flashnorm_relu_ffn_up(const void* a, const void* Wt_star, int64_t M, int64_t K, int64_t F, float eps,
+                                fn_dtype dtype, void* h, float* s_out, void* stream) {
+  if (dtype != FN_BF16) return fail(FN_ERR_UNSUPPORTED, "flashnorm_relu_ffn_up is bf16-only");
+  if (s_out == nullptr && M > 0) return fail(FN_ERR_NULL, "s_out is NULL");
+  fn_status s;
+  if ((s = check_ptr16("s_out", s_out)) != FN_OK) return s;
+  LinearExtras ex;
+  ex.glu_act = fn::RELU_FFN;
+  ex.s_out = s_out;
+  return linear_impl(a, Wt_star, nullptr, M, K, F, eps, 0.0f, FN_RMSNORM, dtype, h, FN_PATH_AUTO, nullptr, 0,
+                     static_cast<cudaStream_t>(stream), ex);
+}
+
 fn_status flashnorm_fold_glu_weights(const void* Wgt, const void* Wut, int64_t F, int64_t K, fn_dtype dtype,
                                      const float* g, void* Wgu_star, void* stream) {
   fn_status s;

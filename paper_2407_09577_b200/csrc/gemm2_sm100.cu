@@ -301,7 +301,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
       tc_fence_after();
       const int row = m_blk * 2 * BM + rank * BM + ew * 32 + lane;
       const uint32_t taddr = tmem_base + ((ew * 32u) << 16) + as * BN;
-      if (MODE == MODE_RMS && p.glu_act >= 0) {
+      if (MODE == MODE_RMS && p.glu_act >= 0 && p.glu_act != RELU_FFN) {
         // GLU epilogue: TMEM columns [0,128) = gate block n_blk, [128,256) = up block n_blk
         const int F = p.N / 2;
         const float s_row = p.glu_act == GLU_SILU ? r : r * r;  // output scale (reading c25)
@@ -331,6 +331,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
         continue;
       }
       if (MODE == MODE_NONE && p.row_scale != nullptr) r = row < p.M ? __ldg(p.row_scale + row) : 1.0f;
+      const bool relu_ffn = MODE == MODE_RMS && p.glu_act == RELU_FFN;  // Fig 2(b): relu(acc), s = r
+      if (relu_ffn) {
+        if (n_blk == 0 && row < p.M && p.s_out != nullptr) p.s_out[row] = r;
+      }
       const int n_base = n_blk * BN;
       __nv_bfloat16* zrow = p.z + static_cast<size_t>(row) * p.N + n_base;
 #pragma unroll 1
@@ -383,6 +387,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
             const float x0 = __uint_as_float(v[2 * q]), x1 = __uint_as_float(v[2 * q + 1]);
             packed[q] = pack_bf16(fmaf(x0, c, -x1 * s), fmaf(x1, c, x0 * s));
           }
+        } else if (relu_ffn) {
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            packed[q] = pack_bf16(fmaxf(__uint_as_float(v[2 * q]), 0.0f), fmaxf(__uint_as_float(v[2 * q + 1]), 0.0f));
         } else {
 #pragma unroll
           for (int q = 0; q < 16; ++q)

@@ -38,6 +38,9 @@ struct GemmParams {
   RopeParams rope;
 };
 enum GluAct { GLU_SILU = 0, GLU_RELU = 1, GLU_BILINEAR = 2 };
+// Fig 2(b) (ReLU FFN, not gated): z = RN(relu(acc)) unscaled, s_out = r — the scale is deferred
+// to the FFN output (ReLU(s a) = s ReLU(a), s >= 0)
+constexpr int RELU_FFN = 3;
 
 // the GLU epilogue's element op (reading c25): SwiGLU scales the gate before the activation,
 // ReGLU / bilinear leave both scales to the output (s = r^2)

@@ -152,3 +152,18 @@ def test_glu_validation():
     Wg = torch.zeros(100, 64, dtype=torch.bfloat16, device=DEV)
     with pytest.raises(fn.FlashNormError, match="multiple of 128"):
         fn.fold_glu_weights(Wg, Wg)
+
+
+@pytest.mark.parametrize("M,K,F", [(300, 1024, 1000), (8, 512, 256)])
+def test_relu_ffn_end_to_end(M, K, F):
+    """Fig 2(b): h = relu(a W*_up) unscaled, s = 1/RMSe(a); y = (h W_down) * s == oracle Fig 2(a)"""
+    a = gen_activations(13, M, K, "normal", "bf16")
+    Wu, g, _, _ = gen_layer(13, F, K, "bf16")
+    Wd, _, _, _ = gen_layer(14, K, F, "bf16")
+    Wus, _ = fn.fold_weights(T(Wu), T(g, "f32"))
+    h, s = fn.relu_ffn_up(T(a), Wus, eps=1e-5)
+    y = fn.linear_scaled(h, T(Wd), s)
+    torch.cuda.synchronize()
+    assert np.all(H(h) >= 0)
+    np.testing.assert_allclose(H(s), 1.0 / O.rmse(a, 1e-5), rtol=2e-6)
+    assert O.rowwise_rel_err(H(y), O.relu_ffn(a, Wu.T, Wd.T, g, 1e-5)) <= TOL_BF16

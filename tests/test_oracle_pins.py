@@ -433,3 +433,26 @@ def test_rope_fault_detected():
     c, s = O.rope_cos_sin([3], cos_tab, sin_tab)
     half = np.concatenate([-x[:, 4:], x[:, :4]], axis=1)
     assert not np.allclose(x * c + half * s, y)
+
+
+# ---------------------------------------------------------------- ReLU FFN (Fig 2)
+
+def test_relu_ffn_worked():
+    """a = [3, -4], g = 1, eps = 0: x = a/sqrt(12.5); Wu = I; relu keeps x1; Wd = [[1],[1]]:
+    y = 3/sqrt(12.5) (hand-worked, Fig 2(a))"""
+    a = np.array([[3.0, -4.0]])
+    y = O.relu_ffn(a, np.eye(2), np.array([[1.0], [1.0]]))
+    assert y[0, 0] == pytest.approx(3 / math.sqrt(12.5), rel=1e-15)
+    h, s = O.relu_ffn_deferred(a, np.eye(2), np.array([[1.0], [1.0]]))
+    np.testing.assert_array_equal(h, [[3.0, 0.0]])
+    assert s[0] == pytest.approx(1 / math.sqrt(12.5), rel=1e-15)
+
+
+@pytest.mark.parametrize("eps", [0.0, 1e-5])
+def test_relu_ffn_deferred_equals_unoptimized(eps):
+    rng = np.random.default_rng(12)
+    a = rng.standard_normal((6, 24)) * rng.uniform(0.1, 10, (6, 1))
+    Wu, Wd = rng.standard_normal((24, 40)), rng.standard_normal((40, 24))
+    g = rng.uniform(0.5, 1.5, 24)
+    h, s = O.relu_ffn_deferred(a, O.merge_norm_weights(Wu, g), Wd, eps)
+    np.testing.assert_allclose((h @ Wd) * s[:, None], O.relu_ffn(a, Wu, Wd, g, eps), rtol=1e-12, atol=1e-12)
