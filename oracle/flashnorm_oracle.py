@@ -354,6 +354,54 @@ def qkv_rope_deferred(a, Wstar, eps, n_rope, h, pos, cos_tab, sin_tab, qk_scale=
 
 
 # ---------------------------------------------------------------------------
+# QK-normalization with RoPE (§4, Figs 6-7) — NEXT-4 (part)
+# ---------------------------------------------------------------------------
+
+def permute_g(g):
+    """permuteg(g) = (g2, g1, g4, g3, ..., g_h, g_{h-1}) (PAPER.md:134)."""
+    g = _f64(g)
+    y = np.empty_like(g)
+    y[0::2] = g[1::2]
+    y[1::2] = g[0::2]
+    return y
+
+
+def qk_norm_rope_unfused(a, W, g, eps, n_q, n_k, h, g_q, g_k, eps_qk, pos, cos_tab, sin_tab, qk_scale=1.0):
+    """Fig 6(a) + Fig 7(a): x = RMSNorm(a; g, eps); [Q|K|V] = x W; every Q head
+    RMSNorm(q; g_q, eps_qk) then RoPE, every K head RMSNorm(k; g_k, eps_qk) then RoPE (OpenELM's
+    q_norm_weight / k_norm_weight, the same for all heads of the layer, PAPER.md:103-105);
+    Q, K times qk_scale; V unchanged."""
+    y = rmsnorm(a, g, None, eps) @ _f64(W)
+    out = y.copy()
+    for h0 in range(0, n_q + n_k, h):
+        gn = g_q if h0 < n_q else g_k
+        qh = rmsnorm(y[:, h0:h0 + h], gn, None, eps_qk)
+        out[:, h0:h0 + h] = rope(qh, pos, cos_tab, sin_tab) * qk_scale
+    return out
+
+
+def qk_norm_rope_deferred(a, Wstar, eps, n_q, n_k, h, g_q, g_k, eps_qk, pos, cos_tab, sin_tab, qk_scale=1.0):
+    """Fig 6(b) + Fig 7(b), step by step:
+    * acc = a W* (no 1/RMS(a) on the Q/K path: s_a cancels, "s_c = s_b / s_a", PAPER.md:117-123);
+    * s_b = 1/RMS of each Q/K head of acc — with eps kept exact as 1/sqrt(MS(acc_head) +
+      eps_qk * MSe(a)) [reading c28] (= the paper's 1/RMS(b) when eps_qk = 0);
+    * RoPE with the head norm weights fused into cos/sin, shared by all heads:
+      y = b s_b * (cos * g) + permute(b) s_b * (sin * permuteg(g));
+    * V: acc / RMSe(a)."""
+    a = _f64(a)
+    acc = a @ _f64(Wstar)
+    mse_a = rmse(a, eps) ** 2
+    out = acc / np.sqrt(mse_a)[:, None]
+    c, s = rope_cos_sin(pos, cos_tab, sin_tab)
+    for h0 in range(0, n_q + n_k, h):
+        gn = _f64(g_q if h0 < n_q else g_k)
+        b = acc[:, h0:h0 + h]
+        sb = 1.0 / np.sqrt(np.mean(b * b, axis=1) + eps_qk * mse_a)
+        out[:, h0:h0 + h] = (b * (c * gn) + rope_permute(b) * (s * permute_g(gn))) * (sb * qk_scale)[:, None]
+    return out
+
+
+# ---------------------------------------------------------------------------
 # Parity metric [reading c12]
 # ---------------------------------------------------------------------------
 

@@ -456,3 +456,51 @@ def test_relu_ffn_deferred_equals_unoptimized(eps):
     g = rng.uniform(0.5, 1.5, 24)
     h, s = O.relu_ffn_deferred(a, O.merge_norm_weights(Wu, g), Wd, eps)
     np.testing.assert_allclose((h @ Wd) * s[:, None], O.relu_ffn(a, Wu, Wd, g, eps), rtol=1e-12, atol=1e-12)
+
+
+# ---------------------------------------------------------------- QK-norm + RoPE (NEXT-4 part)
+
+def test_permute_g_definition():
+    np.testing.assert_array_equal(O.permute_g(np.array([1.0, 2.0, 3.0, 4.0])), [2.0, 1.0, 4.0, 3.0])
+
+
+def test_qk_norm_scale_invariance_worked():
+    """Fig 6: y = a W* s_a s_c g = a W* s_b g. Worked: head b = [3, 4] (RMS^2 = 12.5); any s_a
+    cancels; with g = [2, 1], position 0 (cos 1, sin 0): y = [6, 4] / sqrt(12.5)."""
+    a = np.array([[3.0, 4.0]])
+    cos_tab, sin_tab = np.array([[1.0]]), np.array([[0.0]])
+    for scale in (1.0, 1e-3, 7.0):   # scaling a scales acc; the QK-norm output must not change
+        y = O.qk_norm_rope_deferred(a * scale, np.eye(2), 0.0, 2, 0, 2, np.array([2.0, 1.0]), None, 0.0, [0],
+                                    cos_tab, sin_tab)
+        np.testing.assert_allclose(y[0], np.array([6.0, 4.0]) / math.sqrt(12.5), rtol=1e-14)
+
+
+@pytest.mark.parametrize("eps_qk", [0.0, 1e-6])
+@pytest.mark.parametrize("eps", [0.0, 1e-5])
+def test_qk_norm_rope_deferred_equals_unfused(eps, eps_qk):
+    """The paper's claim (exact with the eps reading c28): Figs 6(b)+7(b) == Figs 6(a)+7(a)"""
+    rng = np.random.default_rng(13)
+    M, n, h = 5, 40, 8
+    n_q, n_k, n_v = 3 * h, 2 * h, 2 * h
+    N = n_q + n_k + n_v
+    a = rng.standard_normal((M, n)) * rng.uniform(0.01, 10, (M, 1))
+    W = rng.standard_normal((n, N)) / np.sqrt(n)
+    g = rng.uniform(0.5, 1.5, n)
+    g_q, g_k = rng.uniform(0.5, 1.5, h), rng.uniform(0.5, 1.5, h)
+    cos_tab, sin_tab = _tables(16, h)
+    pos = rng.integers(0, 16, M)
+    ref = O.qk_norm_rope_unfused(a, W, g, eps, n_q, n_k, h, g_q, g_k, eps_qk, pos, cos_tab, sin_tab, 0.7)
+    got = O.qk_norm_rope_deferred(a, O.merge_norm_weights(W, g), eps, n_q, n_k, h, g_q, g_k, eps_qk, pos,
+                                  cos_tab, sin_tab, 0.7)
+    np.testing.assert_allclose(got, ref, rtol=1e-11, atol=1e-12)
+
+
+def test_qk_norm_head_rms_is_one():
+    """after the per-head RMSNorm with g = 1 and RoPE (a rotation), each head has RMS 1"""
+    rng = np.random.default_rng(14)
+    a = rng.standard_normal((3, 16))
+    W = rng.standard_normal((16, 32))
+    cos_tab, sin_tab = _tables(8, 8)
+    y = O.qk_norm_rope_unfused(a, W, None, 0.0, 16, 8, 8, np.ones(8), np.ones(8), 0.0, [1, 2, 3], cos_tab, sin_tab)
+    for h0 in range(0, 24, 8):
+        np.testing.assert_allclose(np.sqrt(np.mean(y[:, h0:h0 + 8] ** 2, axis=1)), 1.0, rtol=1e-13)
