@@ -245,6 +245,24 @@ fn_status flashnorm_qkv_rope_linear(const void* a, const void* Wt_star, int64_t 
                                     const float* cos_tab, const float* sin_tab, float qk_scale, float eps,
                                     fn_dtype dtype, void* z, void* stream);
 
+/* --------------------------------------------------------------------------
+ * flashnorm_qk_norm_rope_linear — Q/K/V projection with OpenELM-style QK-normalization and
+ * RoPE (NEXT-4 part, §4 Figs 6(b) + 7(b); reading c28), bf16 only:
+ *   acc = a W*^T; Q heads = columns [0, n_q), K heads = [n_q, n_q + n_k), head_dim each, V after.
+ *   Per token m and Q/K head b (head_dim values of acc; no 1/RMS(a) on this path, it cancels):
+ *     s_b = rsqrt(MS(b) + eps_qk * MSe(a_m)),  MSe(a_m) = ssq_m/K + eps  (exact for any eps_qk)
+ *     y_2i   = RN((b_2i cos_i g_2i - b_2i+1 sin_i g_2i+1) * s_b * qk_scale)
+ *     y_2i+1 = RN((b_2i+1 cos_i g_2i+1 + b_2i sin_i g_2i) * s_b * qk_scale)
+ *   with g = g_q (Q heads) or g_k (K heads) [head_dim] float32, cos_i / sin_i = table[pos_m][i];
+ *   V columns: RN(acc * r_m).  head_dim in {32, 64, 128, 256}; decode (M <= 16) runs on the
+ *   tcgen05 split-K kernel when head_dim divides 128, else on the tcgen05 GEMM.
+ * -------------------------------------------------------------------------- */
+fn_status flashnorm_qk_norm_rope_linear(const void* a, const void* Wt_star, int64_t M, int64_t K, int64_t N,
+                                       int64_t n_q, int64_t n_k, int64_t head_dim, const float* g_q,
+                                       const float* g_k, float eps_qk, const int32_t* positions,
+                                       const float* cos_tab, const float* sin_tab, float qk_scale, float eps,
+                                       fn_dtype dtype, void* z, void* stream);
+
 /* End-to-end variant: a_host / z_host are HOST pointers (pinned memory for
  * asynchronous copies); a_dev / z_dev are caller-owned device scratch of
  * M*K / M*N elements.  Enqueues H2D(a) -> flashnorm_linear -> D2H(z) on

@@ -22,7 +22,7 @@ from typing import Optional, Tuple
 __all__ = [
     "FlashNormError", "lib", "lib_path", "fold_weights", "fold_mean_center", "fold_mean_center_workspace_bytes",
     "linear", "linear_from_host", "baseline_norm", "gather_columns", "launch_count", "reset_launch_count",
-    "version", "linear_workspace_bytes", "fold_glu_weights", "glu_linear", "linear_scaled", "glu_ffn", "qkv_rope_linear", "relu_ffn_up",
+    "version", "linear_workspace_bytes", "fold_glu_weights", "glu_linear", "linear_scaled", "glu_ffn", "qkv_rope_linear", "relu_ffn_up", "qk_norm_rope_linear",
     "MODES", "GLU_ACTS", "PATHS", "EXPORTS",
 ]
 
@@ -39,7 +39,7 @@ EXPORTS = [
     "flashnorm_fold_weights", "flashnorm_fold_mean_center_workspace_bytes", "flashnorm_fold_mean_center",
     "flashnorm_linear", "flashnorm_linear_ex", "flashnorm_linear_workspace_bytes", "flashnorm_linear_ws",
     "flashnorm_linear_from_host", "flashnorm_fold_glu_weights", "flashnorm_glu_linear", "flashnorm_linear_scaled",
-    "flashnorm_qkv_rope_linear", "flashnorm_relu_ffn_up", "flashnorm_baseline_norm",
+    "flashnorm_qkv_rope_linear", "flashnorm_relu_ffn_up", "flashnorm_qk_norm_rope_linear", "flashnorm_baseline_norm",
     "flashnorm_gather_columns", "flashnorm_status_string", "flashnorm_last_error", "flashnorm_launch_count",
     "flashnorm_reset_launch_count", "flashnorm_version",
 ]
@@ -78,6 +78,8 @@ def lib() -> ctypes.CDLL:
         "flashnorm_glu_linear": [_vp, _vp, _i64, _i64, _i64, _f32, _int, _int, _vp, _vp, _vp],
         "flashnorm_qkv_rope_linear": [_vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _f32, _f32, _int, _vp,
                                       _vp],
+        "flashnorm_qk_norm_rope_linear": [_vp, _vp, _i64, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _f32, _vp, _vp,
+                                          _vp, _f32, _f32, _int, _vp, _vp],
         "flashnorm_relu_ffn_up": [_vp, _vp, _i64, _i64, _i64, _f32, _int, _vp, _vp, _vp],
         "flashnorm_linear_scaled": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _vp, _vp],
         "flashnorm_linear_from_host": [_vp, _vp, _vp, _i64, _i64, _i64, _f32, _f32, _int, _int, _vp, _vp, _vp,
@@ -278,6 +280,23 @@ def glu_linear(a, Wgu_star, eps: float = 1e-5, act: str = "silu", out=None, s_ou
     _check(lib().flashnorm_glu_linear(_ptr(a), _ptr(Wgu_star), M, K, F, float(eps), GLU_ACTS[act], _dtype_code(a),
                                       _ptr(h), _ptr(s), _stream(a)), "glu_linear")
     return h, s
+
+
+def qk_norm_rope_linear(a, Wt_star, n_q: int, n_k: int, head_dim: int, g_q, g_k, positions, cos_tab, sin_tab,
+                        eps_qk: float = 1e-6, qk_scale: float = 1.0, eps: float = 1e-5, out=None):
+    """[Q | K | V] with per-head QK-norm fused into RoPE (Figs 6(b)+7(b))."""
+    torch = _torch()
+    for t, nm in ((a, "a"), (Wt_star, "Wt_star"), (g_q, "g_q"), (g_k, "g_k"), (positions, "positions"),
+                  (cos_tab, "cos_tab"), (sin_tab, "sin_tab")):
+        _dev(t, nm)
+    M, K = a.shape
+    N = Wt_star.shape[0]
+    z = out if out is not None else torch.empty((M, N), dtype=a.dtype, device=a.device)
+    _check(lib().flashnorm_qk_norm_rope_linear(_ptr(a), _ptr(Wt_star), M, K, N, n_q, n_k, head_dim, _ptr(g_q),
+                                               _ptr(g_k), float(eps_qk), _ptr(positions), _ptr(cos_tab),
+                                               _ptr(sin_tab), float(qk_scale), float(eps), _dtype_code(a), _ptr(z),
+                                               _stream(a)), "qk_norm_rope_linear")
+    return z
 
 
 def relu_ffn_up(a, Wt_star, eps: float = 1e-5, out=None, s_out=None):

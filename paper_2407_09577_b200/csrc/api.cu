@@ -146,7 +146,7 @@ struct LinearExtras {
   int glu_act = -1;                 // >= 0: gate||up GEMM with the GLU epilogue, z = h [M][N/2]
   float* s_out = nullptr;           // GLU: output scale per row
   const float* row_scale = nullptr; // FN_NONE: z = RN(acc * row_scale[m] + c*)
-  fn::RopeParams rope{nullptr, nullptr, nullptr, 0, 0, 1.0f};  // FN_RMSNORM: RoPE on [0, rope.n)
+  fn::RopeParams rope{nullptr, nullptr, nullptr, 0, 0, 1.0f, nullptr, nullptr, 0, 0.f};  // RoPE on [0, rope.n)
 };
 
 fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, int64_t M, int64_t K, int64_t N,
@@ -192,7 +192,10 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
   }
 
   // the GLU epilogue lives in the GEMM kernels; a given row scale in the GEMM and tcgen05 decode kernels
-  const bool tc_ok = ex.glu_act < 0 && fn::gemv_tc_supported((int)M, (int)N, num_sms());
+  // QK-norm on the decode kernel needs whole heads inside its 128-row tiles (h | 128, R = 1)
+  const bool qkn_tc_ok = ex.rope.g_q == nullptr ||
+                         (128 % ex.rope.h == 0 && fn::gemv_tc_tile_rows(fn::MODE_RMS, (int)K, (int)N, num_sms()) == 128);
+  const bool tc_ok = ex.glu_act < 0 && qkn_tc_ok && fn::gemv_tc_supported((int)M, (int)N, num_sms());
   const bool mma_ok = ex.glu_act < 0 && ex.row_scale == nullptr && ex.rope.pos == nullptr &&
                       fn::gemv_supported((int)M, (int)K);
   const bool gemv_ok = tc_ok || mma_ok;
@@ -388,7 +391,37 @@ fn_status flashnorm_qkv_rope_linear(const void* a, const void* Wt_star, int64_t 
                 (const void*)cos_tab, (const void*)sin_tab);
   if (!std::isfinite(qk_scale)) return fail(FN_ERR_VALUE, "qk_scale = %g must be finite", (double)qk_scale);
   LinearExtras ex;
-  if (n_rope > 0) ex.rope = fn::RopeParams{positions, cos_tab, sin_tab, (int)n_rope, (int)head_dim, qk_scale};
+  if (n_rope > 0)
+    ex.rope = fn::RopeParams{positions, cos_tab, sin_tab, (int)n_rope, (int)head_dim, qk_scale, nullptr, nullptr, 0, 0.f};
+  return linear_impl(a, Wt_star, nullptr, M, K, N, eps, 0.0f, FN_RMSNORM, dtype, z, FN_PATH_AUTO, nullptr, 0,
+                     static_cast<cudaStream_t>(stream), ex);
+}
+
+fn_status flashnorm_qk_norm_rope_linear(const void* a, const void* Wt_star, int64_t M, int64_t K, int64_t N,
+                                       int64_t n_q, int64_t n_k, int64_t head_dim, const float* g_q,
+                                       const float* g_k, float eps_qk, const int32_t* positions,
+                                       const float* cos_tab, const float* sin_tab, float qk_scale, float eps,
+                                       fn_dtype dtype, void* z, void* stream) {
+  if (dtype != FN_BF16) return fail(FN_ERR_UNSUPPORTED, "flashnorm_qk_norm_rope_linear is bf16-only");
+  if (head_dim != 32 && head_dim != 64 && head_dim != 128 && head_dim != 256)
+    return fail(FN_ERR_SHAPE, "head_dim = %lld must be 32, 64, 128 or 256", (long long)head_dim);
+  if (n_q < 0 || n_k < 0 || n_q % head_dim != 0 || n_k % head_dim != 0 || n_q + n_k > N)
+    return fail(FN_ERR_SHAPE, "n_q = %lld, n_k = %lld must be multiples of head_dim (%lld) with n_q + n_k <= N = %lld",
+                (long long)n_q, (long long)n_k, (long long)head_dim, (long long)N);
+  if (M > 0 && n_q + n_k > 0 &&
+      (positions == nullptr || cos_tab == nullptr || sin_tab == nullptr || g_q == nullptr || g_k == nullptr))
+    return fail(FN_ERR_NULL, "positions / cos_tab / sin_tab / g_q / g_k must not be NULL");
+  fn_status s;
+  if ((s = check_ptr16("g_q", g_q)) != FN_OK || (s = check_ptr16("g_k", g_k)) != FN_OK ||
+      (s = check_ptr16("cos_tab", cos_tab)) != FN_OK || (s = check_ptr16("sin_tab", sin_tab)) != FN_OK)
+    return s;
+  if (!std::isfinite(qk_scale) || !(eps_qk >= 0.0f) || !std::isfinite(eps_qk))
+    return fail(FN_ERR_VALUE, "qk_scale = %g, eps_qk = %g: must be finite (eps_qk >= 0)", (double)qk_scale,
+                (double)eps_qk);
+  LinearExtras ex;
+  if (n_q + n_k > 0)
+    ex.rope = fn::RopeParams{positions, cos_tab, sin_tab, (int)(n_q + n_k), (int)head_dim, qk_scale,
+                             g_q, g_k, (int)n_q, eps_qk};
   return linear_impl(a, Wt_star, nullptr, M, K, N, eps, 0.0f, FN_RMSNORM, dtype, z, FN_PATH_AUTO, nullptr, 0,
                      static_cast<cudaStream_t>(stream), ex);
 }

@@ -279,6 +279,7 @@ __global__ void __launch_bounds__(gemm::THREADS, 1)
       }
       const int n_base = n_blk * BN;
       __nv_bfloat16* zrow = p.z + static_cast<size_t>(row) * p.N + n_base;
+      float head_sb = 1.0f;  // QK-norm: 1/RMS of the current Q/K head of this row (reading c28)
 #pragma unroll 1
       for (int j = 0; j < BN / 32; ++j) {
         if (n_base + j * 32 >= p.N) break;  // warp-uniform
@@ -303,7 +304,34 @@ __global__ void __launch_bounds__(gemm::THREADS, 1)
           // Fig 5(b): cos/sin scaled once per token by r (and sqrt(1/sqrt h)), shared by all heads
           const int pos = row < p.M ? __ldg(p.rope.pos + row) : 0;
           const int hh = p.rope.h >> 1;
-          const float rq = r * p.rope.qk;
+          const int col0 = n_base + j * 32;
+          const bool qkn = p.rope.g_q != nullptr;
+          if (qkn && col0 % p.rope.h == 0) {
+            // Fig 6(b): the head's own RMS from the unscaled accumulator (s_a cancels); the head's
+            // h / 32 chunks are read from TMEM once more for the sum of squares
+            float ss = 0.f;
+            for (int u = 0; u < p.rope.h / 32; ++u) {
+              uint32_t w[32];
+              tmem_ld_32x32b_x32(taddr + (j + u) * 32, w);
+              tmem_wait_ld();
+#pragma unroll
+              for (int q = 0; q < 32; ++q) ss = fmaf(__uint_as_float(w[q]), __uint_as_float(w[q]), ss);
+            }
+            head_sb = rsqrtf(fmaf(p.rope.eps_qk, 1.0f / (r * r), ss / (float)p.rope.h));
+          }
+          const float rq = (qkn ? head_sb : r) * p.rope.qk;
+          float gm[32];  // QK-norm weights of these 32 head dimensions (Fig 7(b)), else 1
+          if (qkn) {
+            const float* gsrc = (col0 < p.rope.n_q ? p.rope.g_q : p.rope.g_k) + (col0 % p.rope.h);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const float4 g4 = __ldg(reinterpret_cast<const float4*>(gsrc) + q);
+              gm[4 * q] = g4.x; gm[4 * q + 1] = g4.y; gm[4 * q + 2] = g4.z; gm[4 * q + 3] = g4.w;
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < 32; ++q) gm[q] = 1.0f;
+          }
           const int i0 = ((n_base + j * 32) % p.rope.h) >> 1;  // 16 consecutive pair indices
           float cs[16], sn[16];
           if ((hh & 3) == 0 && i0 + 16 <= hh) {  // one head, 16-byte aligned: 4 x float4 each
@@ -325,9 +353,11 @@ __global__ void __launch_bounds__(gemm::THREADS, 1)
           }
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
+            // y0 = x0 cos g0 - x1 sin g1, y1 = x1 cos g1 + x0 sin g0 (permuteg)
             const float c = cs[q] * rq, s = sn[q] * rq;
             const float x0 = __uint_as_float(v[2 * q]), x1 = __uint_as_float(v[2 * q + 1]);
-            packed[q] = pack_bf16(fmaf(x0, c, -x1 * s), fmaf(x1, c, x0 * s));
+            const float g0 = gm[2 * q], g1 = gm[2 * q + 1];
+            packed[q] = pack_bf16(fmaf(x0, c * g0, -x1 * (s * g1)), fmaf(x1, c * g1, x0 * (s * g0)));
           }
         } else if (relu_ffn) {
 #pragma unroll

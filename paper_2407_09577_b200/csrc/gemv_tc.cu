@@ -416,18 +416,49 @@ __global__ void __launch_bounds__(dtc::THREADS, 1)
           float pv[TOK];
 #pragma unroll
           for (int m = 0; m < TOK; ++m) pv[m] = __shfl_xor_sync(0xffffffffu, acc[j][m], 1);
+          float sc[TOK];  // per-token scale of this row's head: r (Fig 5(b)) or the head's s_b (Fig 6(b))
+#pragma unroll
+          for (int m = 0; m < TOK; ++m) sc[m] = rr[m];
+          float g_own = 1.0f, g_pair = 1.0f;
+          if (rope.g_q != nullptr) {
+            // QK-norm: MS of each token's head over the head's rows (h / 32 warps of this tile)
+            float* red = reinterpret_cast<float*>(smem + 65536);  // [4 warps][TOK], ring is free here
+#pragma unroll
+            for (int m = 0; m < TOK; ++m) {
+              float q = acc[j][m] * acc[j][m];
+#pragma unroll
+              for (int off = 16; off > 0; off >>= 1) q += __shfl_xor_sync(0xffffffffu, q, off);
+              if (lane == 0) red[q4 * TOK + m] = q;
+            }
+            named_bar_sync(3, 128);
+            const int wph = rope.h / 32;                 // warps per head (h = 32, 64 or 128)
+            const int w0 = (int)(q4 / (uint32_t)wph) * wph;
+#pragma unroll
+            for (int m = 0; m < TOK; ++m) {
+              float ss = 0.f;
+              for (int w = 0; w < wph; ++w) ss += red[(w0 + w) * TOK + m];
+              sc[m] = rsqrtf(fmaf(rope.eps_qk, 1.0f / (rr[m] * rr[m]), ss / (float)rope.h));
+            }
+            if (n < rope.n) {
+              const float* gsrc = n < rope.n_q ? rope.g_q : rope.g_k;
+              g_own = __ldg(gsrc + n % rope.h);
+              g_pair = __ldg(gsrc + (n ^ 1) % rope.h);
+            }
+          }
           if (n < N && n < rope.n) {
-            const float sgn = (n & 1) ? 1.0f : -1.0f;  // y0 = x0 c - x1 s, y1 = x1 c + x0 s
+            const float sgn = (n & 1) ? 1.0f : -1.0f;  // y0 = x0 c g0 - x1 s g1, y1 = x1 c g1 + x0 s g0
 #pragma unroll
             for (int m = 0; m < TOK; ++m) {
               if (m < M) {
-                const float rq = rr[m] * rope.qk;
-                z[(size_t)m * N + n] = __float2bfloat16_rn(fmaf(acc[j][m], rc[m] * rq, sgn * pv[m] * (rs[m] * rq)));
+                const float rq = sc[m] * rope.qk;
+                z[(size_t)m * N + n] =
+                    __float2bfloat16_rn(fmaf(acc[j][m], rc[m] * rq * g_own, sgn * pv[m] * (rs[m] * rq * g_pair)));
               }
             }
             continue;
           }
-        } else if (R == 2 && MODE == MODE_RMS && rope.pos != nullptr && n0 + j * ROWS < rope.n) {
+        } else if (R == 2 && MODE == MODE_RMS && rope.pos != nullptr && rope.g_q == nullptr &&
+                   n0 + j * ROWS < rope.n) {
           float pv[TOK];
 #pragma unroll
           for (int m = 0; m < TOK; ++m) pv[m] = __shfl_xor_sync(0xffffffffu, acc[j][m], 1);

@@ -19,6 +19,13 @@ struct RopeParams {
   const float* sin_tab;
   int n, h;
   float qk;
+  // QK-norm (NEXT-4, reading c28): g_q != nullptr -> each Q head (columns
+  // [0, n_q)) / K head ([n_q, n)) of acc is RMS-normalized on its own, s_b = rsqrt(MS(head) +
+  // eps_qk * MSe(a)) (no 1/RMS(a): it cancels), and g_q / g_k are fused into cos / sin.
+  const float* g_q;
+  const float* g_k;
+  int n_q;
+  float eps_qk;
 };
 
 struct GemmParams {
@@ -86,7 +93,8 @@ int gemv_tc_split(int K, int N, int num_sms);      // K splits per tile
 int gemv_tc_tile_rows(int mode, int K, int N, int num_sms);  // W* rows per tile (128 or 256; the TMA box)
 cudaError_t launch_gemv_tc(const CUtensorMap& tw, const CUtensorMap& ta, const float* cstar, __nv_bfloat16* z,
                            int M, int K, int N, float eps, float alpha, int mode, int num_sms, cudaStream_t stream,
-                           const float* row_scale = nullptr, RopeParams rope = RopeParams{nullptr, nullptr, nullptr, 0, 0, 1.f});
+                           const float* row_scale = nullptr,
+                           RopeParams rope = RopeParams{nullptr, nullptr, nullptr, 0, 0, 1.f, nullptr, nullptr, 0, 0.f});
 size_t gemv_smem_bytes(int M, int K);
 cudaError_t launch_gemv(const __nv_bfloat16* a, const __nv_bfloat16* Wt, const float* cstar, __nv_bfloat16* z,
                         int M, int K, int N, float eps, float alpha, int mode, int num_sms, cudaStream_t stream);

@@ -109,3 +109,32 @@ def test_qkv_rope_validation():
         fn.qkv_rope_linear(a, W, 100, 64, p, c, c)
     with pytest.raises(fn.FlashNormError, match="head_dim"):
         fn.qkv_rope_linear(a, W, 128, 63, p, c, c)
+
+
+# ---------------------------------------------------------------- QK-norm + RoPE (NEXT-4 part)
+
+def run_qkn(M, K, h, nq_heads, nk_heads, eps_qk, seed=5, max_pos=4096):
+    n_q, n_k = nq_heads * h, nk_heads * h
+    N = n_q + n_k + nk_heads * h
+    a = gen_activations(seed, M, K, "normal", "bf16")
+    Wt, g, _, _ = gen_layer(seed, N, K, "bf16")
+    rng = np.random.default_rng(seed)
+    g_q = rng.uniform(0.5, 1.5, h).astype(np.float32)
+    g_k = rng.uniform(0.5, 1.5, h).astype(np.float32)
+    cos_tab, sin_tab = tables(max_pos, h)
+    pos = rng.integers(0, max_pos, M).astype(np.int32)
+    Ws, _ = fn.fold_weights(T(Wt), T(g.astype(np.float32), "f32"))
+    z = fn.qk_norm_rope_linear(T(a), Ws, n_q, n_k, h, T(g_q, "f32"), T(g_k, "f32"), T(pos, "i32"),
+                               T(cos_tab, "f32"), T(sin_tab, "f32"), eps_qk=eps_qk, qk_scale=0.5, eps=1e-5)
+    torch.cuda.synchronize()
+    ref = O.qk_norm_rope_unfused(a, Wt.T, g, 1e-5, n_q, n_k, h, g_q, g_k, eps_qk, pos, cos_tab, sin_tab, 0.5)
+    return H(z), ref
+
+
+@pytest.mark.parametrize("M,K,h,nq,nk", [(1, 2048, 64, 16, 4), (16, 1024, 128, 8, 2), (5, 512, 32, 8, 8),
+                                         (300, 1024, 64, 8, 2), (100, 768, 128, 4, 4), (40, 512, 256, 2, 2)])
+@pytest.mark.parametrize("eps_qk", [0.0, 1e-6])
+def test_qk_norm_rope_parity(M, K, h, nq, nk, eps_qk):
+    """decode (tcgen05 split-K, h | 128) and GEMM paths vs the unfused Figs 6(a)+7(a)"""
+    z, ref = run_qkn(M, K, h, nq, nk, eps_qk)
+    assert O.rowwise_rel_err(z, ref) <= TOL_BF16
