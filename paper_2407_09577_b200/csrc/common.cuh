@@ -106,6 +106,14 @@ FN_DEVICE void tma_load_2d(void* dst, const CUtensorMap* m, uint64_t* bar, int32
       "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(x), "r"(y), "l"(policy)
       : "memory");
 }
+// 2D tiled prefetch global -> L2 only (no SMEM, no barrier): warms the lines a later
+// tma_load_2d of the same box will read.
+FN_DEVICE void tma_prefetch_l2_2d(const CUtensorMap* m, int32_t x, int32_t y) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(x), "r"(y)
+               : "memory");
+}
 // L2 eviction-priority policies (createpolicy encodings used by TMA cache hints)
 constexpr uint64_t kEvictFirst = 0x12F0000000000000ull;
 constexpr uint64_t kEvictLast = 0x14F0000000000000ull;
@@ -211,6 +219,34 @@ FN_DEVICE uint32_t mapa_shared(const void* p, uint32_t rank) {
 // arrive (release, cluster scope) on an mbarrier given by a shared::cluster address
 FN_DEVICE void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// split cluster barrier: arrive (relaxed; pairs with fence_mbar_init) / wait (acquire)
+FN_DEVICE void cluster_arrive_relaxed() { asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory"); }
+FN_DEVICE void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+// 16-byte / 4-byte stores into another CTA's shared memory (shared::cluster address)
+FN_DEVICE void st_cluster_v4(uint32_t cluster_addr, float4 v) {
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(cluster_addr), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+FN_DEVICE void st_cluster_f32(uint32_t cluster_addr, float v) {
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(cluster_addr), "f"(v) : "memory");
+}
+// whole-warp wait with cluster-scope acquire (pairs with remote release arrives)
+FN_DEVICE uint32_t mbar_try_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok;
+}
+FN_DEVICE void mbar_wait_warp_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = mbar_try_wait_cluster(bar, parity);
+  while (!__all_sync(0xffffffffu, ok)) ok = mbar_try_wait_cluster(bar, parity);
 }
 // 2-CTA TMA load into the local CTA's smem, completing tx bytes on the mbarrier at
 // `bar_cluster_addr` (the leader CTA's barrier, a shared::cluster address)

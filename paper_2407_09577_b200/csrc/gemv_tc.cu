@@ -49,12 +49,12 @@ constexpr int TMEM_COLS = 32;           // D of MMA j in columns [16j, 16j+16), 
 constexpr int MAX_S = 8;                // K splits per tile (portable cluster size)
 constexpr int MAX_CTAS = 160;           // tiles * S <= #SMs (148)
 constexpr int SLOTS = 4;                // global-mode partial buffers, round robin over launches
-constexpr size_t SMEM_MAX = 232448;     // opt-in dynamic SMEM per CTA
+constexpr size_t SMEM_MAX = 232448;     // opt-in dynamic SMEM per CTA (ring sizes stay below it)
 // tile = R x 128 W* rows (R MMAs per k step sharing the token operand)
 template <int R> struct Cfg {
   static constexpr int W_STAGE = R * ROWS * BK * 2;                  // 16 / 32 KiB
-  static constexpr int STAGES = R == 1 ? 12 : 6;                     // ~204-216 KiB ring
-  static constexpr size_t SMEM = 1024 + (size_t)STAGES * (W_STAGE + T_STAGE) + 1024;
+  static constexpr int STAGES = R == 1 ? 12 : 6;                     // default: ~204-216 KiB ring
+  static size_t smem(int stages) { return 1024 + (size_t)stages * (W_STAGE + T_STAGE) + 1024; }
 };
 }  // namespace dtc
 
@@ -82,7 +82,7 @@ FN_DEVICE float4 ld_cluster_v4(uint32_t cluster_addr) {
 }
 
 #ifdef FN_GEMV_TC_TRACE  // tools/micro/gemv_tc_trace.cu: per-CTA timeline (globaltimer, ns)
-__device__ unsigned long long g_tc_trace[2][160][8];
+__device__ unsigned long long g_tc_trace[2][160][16];
 __device__ unsigned g_tc_launch;
 FN_DEVICE unsigned long long tc_gtime() {
   unsigned long long t;
@@ -95,14 +95,15 @@ FN_DEVICE unsigned long long tc_gtime() {
 #endif
 
 template <int MODE, int R>
-__global__ void __launch_bounds__(dtc::THREADS, 1)
+__global__ void __launch_bounds__(dtc::THREADS, 2)  // <= 168 registers: two CTAs may share an SM
     flashnorm_gemv_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_a,
                              const float* __restrict__ cstar, __nv_bfloat16* __restrict__ z, int M, int K, int N,
                              float eps, float alpha, int S, int slot, int use_cluster,
-                             const float* __restrict__ row_scale, const RopeParams rope) {
+                             const float* __restrict__ row_scale, const RopeParams rope, int l2pf,
+                             int stages, int flags, const __nv_bfloat16* __restrict__ wptr) {
   using namespace dtc;
   constexpr int W_STAGE = Cfg<R>::W_STAGE;
-  constexpr int STAGES = Cfg<R>::STAGES;
+  const int STAGES = stages;  // ring depth (runtime: the host sizes it for 1 or 2 CTAs per SM)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sW = smem;                                  // [STAGES][R*128 x 64] SW128
@@ -116,8 +117,13 @@ __global__ void __launch_bounds__(dtc::THREADS, 1)
   float* ssq_own = reinterpret_cast<float*>(tmem_holder + 4);  // [16]
   float* side_fence = ssq_own + TOK;                           // [32] load-completion fence
   int* last_flag = reinterpret_cast<int*>(side_fence + 32);
+  uint64_t* recv_bar = reinterpret_cast<uint64_t*>(last_flag + 2);  // push mode: peers' partials landed
   // cluster mode: after the last MMA the ring is free; each CTA stages its partial there
   float* part = reinterpret_cast<float*>(smem);                // [R][128][16]
+  // push mode: the leader's receive slots, one per peer rank, beside the ring (a peer may finish
+  // before the leader's ring is drained): [S-1][R*128*16 + 16] fp32
+  constexpr int RECV_STRIDE = R * ROWS * TOK + TOK;
+  float* recv = reinterpret_cast<float*>(sT + STAGES * T_STAGE + 1024);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -147,6 +153,7 @@ __global__ void __launch_bounds__(dtc::THREADS, 1)
       mbar_init(&ready[s], 1);
     }
     mbar_init(tfull, 1);
+    mbar_init(recv_bar, (uint32_t)(S > 1 ? (S - 1) * 128 : 1));  // one release-arrive per peer epilogue thread
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -157,6 +164,8 @@ __global__ void __launch_bounds__(dtc::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  const bool push = S > 1 && use_cluster && (flags & 1);
+  if (push) cluster_arrive_relaxed();  // barrier inits published; the matching wait precedes any remote access
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -166,6 +175,20 @@ __global__ void __launch_bounds__(dtc::THREADS, 1)
       for (int i = 0; i < pre; ++i) {
         mbar_arrive_expect_tx(&full[i], W_STAGE + T_STAGE);
         tma_load_2d(sW + i * W_STAGE, &tmap_w, &full[i], (kb0 + i) * BK, n0, kEvictFirst);
+      }
+      // ... and the rest of this CTA's W* slice is pulled into L2 (up to l2pf boxes), so the
+      // HBM stream keeps going while this call waits for the previous one; the ring refills
+      // after the wait then hit L2
+      for (int i = pre; i < my_kb && i < pre + l2pf; ++i)
+        tma_prefetch_l2_2d(&tmap_w, (kb0 + i) * BK, n0);  // the box is the whole R x 128-row tile
+      if (flags & 2) {
+        // ... and the whole slice of the CTA half a grid away: CTAs start in blockIdx order as
+        // the previous call's CTAs leave, so the upper half typically starts late; its W* is
+        // then already in L2 when it does
+        const int pb = (int)((blockIdx.x + gridDim.x / 2) % gridDim.x);
+        const int prank = pb % S, pn0 = (pb / S) * R * ROWS;
+        const int pk0 = (int)(((long long)prank * nkb) / S), pk1 = (int)(((long long)(prank + 1) * nkb) / S);
+        for (int i = pk0; i < pk1; ++i) tma_prefetch_l2_2d(&tmap_w, i * BK, pn0);
       }
       pdl_wait_prior_grid();  // tokens may be the previous kernel's output
       TC_TRACE(1);
@@ -190,6 +213,11 @@ __global__ void __launch_bounds__(dtc::THREADS, 1)
       for (int i = 0; i < my_kb; ++i) {
         if (MODE == MODE_DYT) mbar_wait(&ready[stage], phase);
         else mbar_wait(&full[stage], phase);
+#ifdef FN_GEMV_TC_TRACE
+        if (i == 0) TC_TRACE(5);
+        if (i == STAGES) TC_TRACE(6);
+        if (i == my_kb - 1) TC_TRACE(7);
+#endif
         tc_fence_after();
         const uint64_t bdesc = make_sw128_desc(smem_u32(sT + stage * T_STAGE));
 #pragma unroll
@@ -266,6 +294,30 @@ __global__ void __launch_bounds__(dtc::THREADS, 1)
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
+    if (warp >= 3 && wptr != nullptr && (flags & 12)) {
+      // idle epilogue warps (3-5) pull W* lines beyond the ring into L2 with plain prefetches
+      // (LSU path; the TMA queue stays free for the producer): own slice (flag 4) and/or the
+      // slice of the CTA half a grid away (flag 8), one 128-byte line = one row x one k block
+      const int t = (int)threadIdx.x - 96;  // 0..95
+      const int rows = R * ROWS;
+      auto pf = [&](int nbase, int ka, int kb) {
+        const int nlines = (kb - ka) * rows;
+        for (int l = t; l < nlines; l += 96) {
+          const int n = nbase + l % rows, k = ka + l / rows;
+          if (n < N) {
+            if (flags & 16) asm volatile("prefetch.global.L2 [%0];" ::"l"(wptr + (size_t)n * K + (size_t)k * BK));
+            else asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(wptr + (size_t)n * K + (size_t)k * BK));
+          }
+        }
+      };
+      const int pre = my_kb < STAGES ? my_kb : STAGES;
+      if (flags & 4) pf(n0, kb0 + pre, kb1);
+      if (flags & 8) {
+        const int pb = (int)((blockIdx.x + gridDim.x / 2) % gridDim.x);
+        const int prank = pb % S, pn0 = (pb / S) * R * ROWS;
+        pf(pn0, (int)(((long long)prank * nkb) / S), (int)(((long long)(prank + 1) * nkb) / S));
+      }
+    }
     // ---------------------------------------------------------------- epilogue (warps 2-5)
     const uint32_t q4 = warp & 3u;  // TMEM lane quarter this warp may access
     const int row = (int)(q4 * 32 + lane);
@@ -305,7 +357,43 @@ __global__ void __launch_bounds__(dtc::THREADS, 1)
 #pragma unroll
     for (int m = 0; m < TOK; ++m) ssq[m] = MODE == MODE_RMS ? ssq_own[m] : 0.f;
     bool write_z = true;
-    if (S > 1 && use_cluster) {
+    if (push) {
+      // push mode: each peer stores its partial straight into its receive slot in the leader
+      // (DSMEM stores from registers), then every peer epilogue thread release-arrives on the
+      // leader's recv barrier; the leader sums the slots in fixed rank order (deterministic).
+      // No cluster-wide barrier: a peer leaves as soon as its stores are issued.
+      if (rank != 0) {
+        cluster_wait();  // the leader's recv barrier is initialised
+        float* slot_local = recv + (rank - 1) * RECV_STRIDE;
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          const uint32_t dst = mapa_shared(slot_local + (j * ROWS + row) * TOK, 0u);
+#pragma unroll
+          for (int m4 = 0; m4 < TOK / 4; ++m4)
+            st_cluster_v4(dst + m4 * 16, make_float4(acc[j][4 * m4], acc[j][4 * m4 + 1], acc[j][4 * m4 + 2],
+                                                     acc[j][4 * m4 + 3]));
+        }
+        if (MODE == MODE_RMS && warp == 2 && lane < TOK)
+          st_cluster_f32(mapa_shared(slot_local + R * ROWS * TOK + lane, 0u), ssq_own[lane]);
+        mbar_arrive_cluster(mapa_shared(recv_bar, 0u));
+        write_z = false;
+      } else {
+        mbar_wait_warp_cluster(recv_bar, 0);
+        for (int r = 1; r < S; ++r) {  // fixed rank order
+          const float* sl = recv + (r - 1) * RECV_STRIDE;
+#pragma unroll
+          for (int j = 0; j < R; ++j)
+#pragma unroll
+            for (int m4 = 0; m4 < TOK / 4; ++m4) {
+              const float4 p = reinterpret_cast<const float4*>(sl + (j * ROWS + row) * TOK)[m4];
+              acc[j][4 * m4] += p.x; acc[j][4 * m4 + 1] += p.y; acc[j][4 * m4 + 2] += p.z; acc[j][4 * m4 + 3] += p.w;
+            }
+          if (MODE == MODE_RMS)
+#pragma unroll
+            for (int m = 0; m < TOK; ++m) ssq[m] += sl[R * ROWS * TOK + m];
+        }
+      }
+    } else if (S > 1 && use_cluster) {
       // cluster mode: every CTA parks its partial in its own (now free) ring SMEM; after one
       // cluster barrier the leader reads ranks 1..S-1 over DSMEM in fixed rank order; a
       // second barrier keeps the other CTAs' SMEM alive until the leader is done
@@ -317,7 +405,9 @@ __global__ void __launch_bounds__(dtc::THREADS, 1)
               make_float4(acc[j][4 * m4], acc[j][4 * m4 + 1], acc[j][4 * m4 + 2], acc[j][4 * m4 + 3]);
       if (MODE == MODE_RMS && warp == 2 && lane < TOK)
         part[R * ROWS * TOK + lane] = ssq_own[lane];
+      if (warp == 2 && lane == 0) TC_TRACE(8);
       cluster_sync_all();  // (1) partials visible cluster-wide; warps 0 and 1 join below
+      if (warp == 2 && lane == 0) TC_TRACE(9);
       write_z = rank == 0;
       if (write_z) {
         for (int r = 1; r < S; ++r) {  // fixed rank order
@@ -340,7 +430,9 @@ __global__ void __launch_bounds__(dtc::THREADS, 1)
           }
         }
       }
+      if (warp == 2 && lane == 0) TC_TRACE(10);
       cluster_sync_all();  // (2) the leader has read every remote partial
+      if (warp == 2 && lane == 0) TC_TRACE(11);
     } else if (S > 1) {
       // global mode: publish this CTA's partial, count arrivals on the tile; the last reduces
       float4* mine = g_dtc_part[slot][blockIdx.x];
@@ -488,12 +580,16 @@ __global__ void __launch_bounds__(dtc::THREADS, 1)
       }
     }
   }
-  if (S > 1 && use_cluster && warp < 2) {
+  if (warp == 2 && lane == 0) TC_TRACE(12);
+  if (push) {
+    if (rank == 0 || warp < 2) cluster_wait();  // pairs with the arrive at the start (peer epilogue waited above)
+  } else if (S > 1 && use_cluster && warp < 2) {
     cluster_sync_all();
     cluster_sync_all();
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) TC_TRACE(13);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, TMEM_COLS);
@@ -522,11 +618,37 @@ const void* dtc_fptr(int mode, int R) {
   return mode == MODE_RMS ? dtc_kernel<MODE_RMS, 2>() : mode == MODE_DYT ? dtc_kernel<MODE_DYT, 2>()
                                                                          : dtc_kernel<MODE_NONE, 2>();
 }
-size_t dtc_smem(int R) { return R == 1 ? dtc::Cfg<1>::SMEM : dtc::Cfg<2>::SMEM; }
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e != nullptr ? atoi(e) : dflt;
+}
+// A/B knobs (defaults = the measured best): FN_DECODE_STAGES ring depth cap, FN_DECODE_PUSH
+// push-mode cluster reduction, FN_DECODE_PF2 partner-slice L2 prefetch
+int dtc_flags() {
+  static const int f = (env_int("FN_DECODE_PUSH", 1) ? 1 : 0) | (env_int("FN_DECODE_PF2", 0) ? 2 : 0) |
+                       (env_int("FN_DECODE_LSUPF", 1) & 7) << 2;  // bit 2 of LSUPF: evict_normal hint
+  return f;
+}
+size_t dtc_recv_bytes(int R, int S) {
+  return (dtc_flags() & 1) && S > 1 ? (size_t)(S - 1) * (R * dtc::ROWS * dtc::TOK + dtc::TOK) * 4 : 0;
+}
+size_t dtc_smem_for(int R, int stages, int S) {
+  const size_t ring = R == 1 ? dtc::Cfg<1>::smem(stages) : dtc::Cfg<2>::smem(stages);
+  return ring + dtc_recv_bytes(R, S);
+}
+// deepest ring (<= the default depth) that fits the SMEM budget beside the receive slots
+int dtc_stages(int R, int S) {
+  static const int cap = env_int("FN_DECODE_STAGES", 0);
+  int st = cap >= 4 ? cap : (R == 1 ? dtc::Cfg<1>::STAGES : dtc::Cfg<2>::STAGES);
+  while (st > 2 && dtc_smem_for(R, st, S) > dtc::SMEM_MAX - 256) --st;
+  return st;
+}
+size_t dtc_smem(int R, int S) { return dtc_smem_for(R, dtc_stages(R, S), S); }
 void dtc_set_attr(int mode, int R) {
   static bool done[3][3] = {};
   if (!done[mode][R]) {
-    cudaFuncSetAttribute(dtc_fptr(mode, R), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dtc::SMEM_MAX);
+    // budget less 256 B of static shared memory headroom (debug/trace builds add some)
+    cudaFuncSetAttribute(dtc_fptr(mode, R), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dtc::SMEM_MAX - 256);
     done[mode][R] = true;
   }
 }
@@ -536,7 +658,7 @@ bool cluster_fits(int mode, int R, int S, int clusters) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(clusters * S);
   cfg.blockDim = dim3(dtc::THREADS);
-  cfg.dynamicSmemBytes = dtc_smem(R);
+  cfg.dynamicSmemBytes = dtc_smem(R, S);
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = S;
@@ -574,7 +696,11 @@ DtcPlan dtc_plan(int mode, int K, int N, int num_sms) {
     const int tiles = (N + R * ROWS - 1) / (R * ROWS);
     if (tiles > cap) continue;
     if (R == 2 && best_ctas > 0) break;  // R = 2 only when R = 1 does not fit
-    const int smax = std::max(1, std::min(std::min(cap / tiles, MAX_S), nkb));
+    static const int s_env = [] {
+      const char* e = getenv("FN_DECODE_SMAX");  // A/B knob: cap on the K split
+      return e != nullptr ? atoi(e) : MAX_S;
+    }();
+    const int smax = std::max(1, std::min(std::min(cap / tiles, std::min(MAX_S, s_env)), nkb));
     int fit = 1;
     for (int c = smax; c > 1; --c)
       if (cluster_fits(mode, R, c, tiles)) { fit = c; break; }
@@ -597,7 +723,7 @@ bool gemv_tc_supported(int M, int N, int num_sms) {
 
 cudaError_t launch_gemv_tc(const CUtensorMap& tw, const CUtensorMap& ta, const float* cstar, __nv_bfloat16* z,
                            int M, int K, int N, float eps, float alpha, int mode, int num_sms, cudaStream_t stream,
-                           const float* row_scale, RopeParams rope) {
+                           const float* row_scale, RopeParams rope, const __nv_bfloat16* wptr) {
   using namespace dtc;
   const DtcPlan p = dtc_plan(mode, K, N, num_sms);
   dtc_set_attr(mode, p.R);
@@ -610,7 +736,7 @@ cudaError_t launch_gemv_tc(const CUtensorMap& tw, const CUtensorMap& ta, const f
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(tiles * S);
   cfg.blockDim = dim3(THREADS);
-  cfg.dynamicSmemBytes = dtc_smem(p.R);
+  cfg.dynamicSmemBytes = dtc_smem(p.R, S);
   cfg.stream = stream;
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -621,9 +747,15 @@ cudaError_t launch_gemv_tc(const CUtensorMap& tw, const CUtensorMap& ta, const f
   at[1].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 2;
+  static const int l2pf = [] {
+    const char* e = getenv("FN_DECODE_L2PF");  // A/B knob: W* boxes per CTA prefetched to L2 pre-wait
+    return e != nullptr ? atoi(e) : 0;  // measured: TMA prefetches queue behind/ahead of the ring loads
+  }();
+  int stages = dtc_stages(p.R, S);
+  int flags = dtc_flags();
   void* args[] = {(void*)&tw, (void*)&ta, (void*)&cstar, (void*)&z, (void*)&M, (void*)&K, (void*)&N,
                   (void*)&eps, (void*)&alpha, (void*)&S, (void*)&slot, (void*)&use_cluster, (void*)&row_scale,
-                  (void*)&rope};
+                  (void*)&rope, (void*)&l2pf, (void*)&stages, (void*)&flags, (void*)&wptr};
   return cudaLaunchKernelExC(&cfg, fptr, args);
 }
 
