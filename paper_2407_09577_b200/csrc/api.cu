@@ -210,7 +210,7 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
     if ((s = get_tmap(a, M, K, 16, &ta)) != FN_OK) return s;
     cudaError_t e = fn::launch_gemv_tc(tw, ta, c_star, static_cast<__nv_bfloat16*>(z), (int)M, (int)K, (int)N, eps,
                                        alpha, km, num_sms(), stream, ex.row_scale, ex.rope,
-                                       static_cast<const __nv_bfloat16*>(Wt_star));
+                                       static_cast<const __nv_bfloat16*>(Wt_star), static_cast<const __nv_bfloat16*>(a));
     if (e != cudaSuccess) return cuda_fail(e, "gemv_tc");
     ++g_launches;
     return FN_OK;

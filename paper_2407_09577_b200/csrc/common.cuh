@@ -269,6 +269,17 @@ FN_DEVICE void dsmem_signal16(uint32_t dst_cluster_addr, const void* src_local, 
                "r"(smem_u32(src_local)), "r"(bar_cluster_addr)
                : "memory");
 }
+// bulk copy of `bytes` (multiple of 16) from this CTA's SMEM into a peer CTA's SMEM, completing
+// on the peer's mbarrier (complete_tx); the source may be reused after bulk_wait_read()
+FN_DEVICE void dsmem_bulk_copy(uint32_t dst_cluster_addr, const void* src_local, uint32_t bytes,
+                               uint32_t bar_cluster_addr) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   dst_cluster_addr),
+               "r"(smem_u32(src_local)), "r"(bytes), "r"(bar_cluster_addr)
+               : "memory");
+}
+FN_DEVICE void bulk_commit_group() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+FN_DEVICE void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 FN_DEVICE void tmem_alloc_pair(uint32_t* dst_smem, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
                "r"(ncols)

@@ -32,6 +32,8 @@
 #include "kernels.h"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <atomic>
 #include <map>
 #include <mutex>
@@ -90,8 +92,17 @@ FN_DEVICE unsigned long long tc_gtime() {
   return t;
 }
 #define TC_TRACE(ev) g_tc_trace[trace_par][blockIdx.x < 160 ? blockIdx.x : 159][(ev)] = tc_gtime()
+// per-stage SM-clock stamps of CTA 0 (launch parity 1): [0] MMA saw full, [1] producer issued,
+// [2] side warp released, [3] producer saw empty
+__device__ long long g_tc_stage[4][64];
+#define TC_STAGE(w, i) do { if (trace_par == 1 && blockIdx.x == 0 && (i) < 64) g_tc_stage[w][i] = clock64(); } while (0)
+// epilogue SM-clock stamps of CTAs 0 (leader) and 1 (peer), launch parity 1, warp 2 lane 0
+__device__ long long g_tc_epi[2][8];
+#define TC_EPI(e) do { if (trace_par == 1 && blockIdx.x < 2 && warp == 2 && lane == 0) g_tc_epi[blockIdx.x][e] = clock64(); } while (0)
 #else
+#define TC_EPI(e)
 #define TC_TRACE(ev)
+#define TC_STAGE(w, i)
 #endif
 
 template <int MODE, int R>
@@ -100,7 +111,8 @@ __global__ void __launch_bounds__(dtc::THREADS, 2)  // <= 168 registers: two CTA
                              const float* __restrict__ cstar, __nv_bfloat16* __restrict__ z, int M, int K, int N,
                              float eps, float alpha, int S, int slot, int use_cluster,
                              const float* __restrict__ row_scale, const RopeParams rope, int l2pf,
-                             int stages, int flags, const __nv_bfloat16* __restrict__ wptr) {
+                             int stages, int flags, const __nv_bfloat16* __restrict__ wptr,
+                             const __nv_bfloat16* __restrict__ aptr) {
   using namespace dtc;
   constexpr int W_STAGE = Cfg<R>::W_STAGE;
   const int STAGES = stages;  // ring depth (runtime: the host sizes it for 1 or 2 CTAs per SM)
@@ -114,9 +126,9 @@ __global__ void __launch_bounds__(dtc::THREADS, 2)  // <= 168 registers: two CTA
   uint64_t* ready = bars + 2 * STAGES; // [STAGES] DyT: tokens transformed
   uint64_t* tfull = bars + 3 * STAGES; // accumulator complete
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tfull + 1);
-  float* ssq_own = reinterpret_cast<float*>(tmem_holder + 4);  // [16]
-  float* side_fence = ssq_own + TOK;                           // [32] load-completion fence
-  int* last_flag = reinterpret_cast<int*>(side_fence + 32);
+  float* ssq_own = reinterpret_cast<float*>(tmem_holder + 4);  // [16] this CTA's partial ssq per token
+  float* ssq_red = ssq_own + TOK;                              // [4 warps][16]
+  int* last_flag = reinterpret_cast<int*>(ssq_red + 4 * TOK);
   uint64_t* recv_bar = reinterpret_cast<uint64_t*>(last_flag + 2);  // push mode: peers' partials landed
   // cluster mode: after the last MMA the ring is free; each CTA stages its partial there
   float* part = reinterpret_cast<float*>(smem);                // [R][128][16]
@@ -149,12 +161,14 @@ __global__ void __launch_bounds__(dtc::THREADS, 2)  // <= 168 registers: two CTA
     prefetch_tmap(&tmap_a);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], MODE == MODE_RMS ? 2 : 1);  // MMA commit (+ side warp)
+      mbar_init(&empty[s], 1);  // MMA commit
       mbar_init(&ready[s], 1);
     }
     mbar_init(tfull, 1);
-    mbar_init(recv_bar, (uint32_t)(S > 1 ? (S - 1) * 128 : 1));  // one release-arrive per peer epilogue thread
+    mbar_init(recv_bar, 1);  // push mode: the leader's expect_tx + each peer's bulk copy (complete_tx)
     fence_mbar_init();
+    if (S > 1 && use_cluster && (flags & 1) && rank == 0)
+      mbar_arrive_expect_tx(recv_bar, (uint32_t)((S - 1) * RECV_STRIDE * 4));
   }
   if (warp == 1) {
     tmem_alloc(tmem_holder, TMEM_COLS);
@@ -196,8 +210,10 @@ __global__ void __launch_bounds__(dtc::THREADS, 2)  // <= 168 registers: two CTA
         tma_load_2d(sT + i * T_STAGE, &tmap_a, &full[i], (kb0 + i) * BK, 0, kEvictLast);
       int stage = pre == STAGES ? 0 : pre;
       uint32_t phase = pre == STAGES ? 1u : 0u;
+      for (int i = 0; i < pre; ++i) TC_STAGE(1, i);
       for (int i = pre; i < my_kb; ++i) {
         mbar_wait(&empty[stage], phase ^ 1);
+        TC_STAGE(1, i);
         mbar_arrive_expect_tx(&full[stage], W_STAGE + T_STAGE);
         tma_load_2d(sW + stage * W_STAGE, &tmap_w, &full[stage], (kb0 + i) * BK, n0, kEvictFirst);
         tma_load_2d(sT + stage * T_STAGE, &tmap_a, &full[stage], (kb0 + i) * BK, 0, kEvictLast);
@@ -214,6 +230,7 @@ __global__ void __launch_bounds__(dtc::THREADS, 2)  // <= 168 registers: two CTA
         if (MODE == MODE_DYT) mbar_wait(&ready[stage], phase);
         else mbar_wait(&full[stage], phase);
 #ifdef FN_GEMV_TC_TRACE
+        TC_STAGE(0, i);
         if (i == 0) TC_TRACE(5);
         if (i == STAGES) TC_TRACE(6);
         if (i == my_kb - 1) TC_TRACE(7);
@@ -234,41 +251,6 @@ __global__ void __launch_bounds__(dtc::THREADS, 2)  // <= 168 registers: two CTA
     }
   } else {
     // ------------------------------------------------------------ side warp (warp 2), then epilogue
-    if (warp == 2) {
-      if (MODE == MODE_RMS) {
-        // lane l: token row l/2, 16-byte chunks 4*(l&1) .. +3 of each stage (swizzled position)
-        const int trow = (int)lane >> 1;
-        float s0 = 0.f, s1 = 0.f;
-        int stage = 0;
-        uint32_t phase = 0;
-        for (int i = 0; i < my_kb; ++i) {
-          mbar_wait_warp(&full[stage], phase);
-          const uint4* row = reinterpret_cast<const uint4*>(sT + stage * T_STAGE + trow * 128);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const uint4 v = row[(4 * (lane & 1) + q) ^ (trow & 7)];
-            float x;
-            x = bf16lo(v.x); s0 = fmaf(x, x, s0);
-            x = bf16hi(v.x); s1 = fmaf(x, x, s1);
-            x = bf16lo(v.y); s0 = fmaf(x, x, s0);
-            x = bf16hi(v.y); s1 = fmaf(x, x, s1);
-            x = bf16lo(v.z); s0 = fmaf(x, x, s0);
-            x = bf16hi(v.z); s1 = fmaf(x, x, s1);
-            x = bf16lo(v.w); s0 = fmaf(x, x, s0);
-            x = bf16hi(v.w); s1 = fmaf(x, x, s1);
-          }
-          // the store consumes every loaded value: it (and the arrive after it) issue only
-          // once this warp's LDS of the stage have returned (WAR vs the TMA refill)
-          side_fence[lane] = s0 + s1;
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[stage]);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
-        }
-        float s = s0 + s1;
-        s += __shfl_xor_sync(0xffffffffu, s, 1);  // lanes 2r, 2r+1 -> token row r (fixed order)
-        if ((lane & 1) == 0) ssq_own[lane >> 1] = s;
-      }
-    }
     if (MODE == MODE_DYT) {
       // tanh(alpha a) in place on each token stage before its MMA: warps 2-5, one 16-byte
       // chunk per thread (2 KiB per stage), so the transform keeps ahead of the W* stream
@@ -318,10 +300,62 @@ __global__ void __launch_bounds__(dtc::THREADS, 2)  // <= 168 registers: two CTA
         pf(pn0, (int)(((long long)prank * nkb) / S), (int)(((long long)(prank + 1) * nkb) / S));
       }
     }
+    if (MODE == MODE_RMS) {
+      // per-token partial ssq over this CTA's K range, read by warps 2-5 straight from global
+      // (L2) after the dependency wait: beside the contraction and OFF the
+      // W* ring — a side warp squaring each ring stage gated its release and paced the whole
+      // ring at ~400 cycles per stage (tools/micro/gemv_tc_trace.cu, per-stage clocks)
+      pdl_wait_prior_grid();  // tokens may be the previous kernel's output
+      const int t = (int)threadIdx.x - 64;  // 0..127
+      const int k0 = kb0 * BK;
+      const int nch = (min(kb1 * BK, K) - k0) / 8;  // 16-byte chunks (K % 8 == 0)
+      constexpr int CPT = 2;                        // chunks per thread per token per round
+      float sm[TOK];
+#pragma unroll
+      for (int m = 0; m < TOK; ++m) sm[m] = 0.f;
+      for (int c0 = t; c0 < nch; c0 += 128 * CPT) {
+        uint4 v[TOK][CPT];
+#pragma unroll
+        for (int m = 0; m < TOK; ++m)
+#pragma unroll
+          for (int u = 0; u < CPT; ++u) {
+            const int c = c0 + u * 128;
+            v[m][u] = (m < M && c < nch) ? __ldg(reinterpret_cast<const uint4*>(aptr + (size_t)m * K + k0) + c)
+                                         : make_uint4(0u, 0u, 0u, 0u);
+          }
+#pragma unroll
+        for (int m = 0; m < TOK; ++m)
+#pragma unroll
+          for (int u = 0; u < CPT; ++u) {
+            float x, s0 = 0.f, s1 = 0.f;
+            x = bf16lo(v[m][u].x); s0 = fmaf(x, x, s0);
+            x = bf16hi(v[m][u].x); s1 = fmaf(x, x, s1);
+            x = bf16lo(v[m][u].y); s0 = fmaf(x, x, s0);
+            x = bf16hi(v[m][u].y); s1 = fmaf(x, x, s1);
+            x = bf16lo(v[m][u].z); s0 = fmaf(x, x, s0);
+            x = bf16hi(v[m][u].z); s1 = fmaf(x, x, s1);
+            x = bf16lo(v[m][u].w); s0 = fmaf(x, x, s0);
+            x = bf16hi(v[m][u].w); s1 = fmaf(x, x, s1);
+            sm[m] += s0 + s1;
+          }
+      }
+#pragma unroll
+      for (int m = 0; m < TOK; ++m) {
+        float x = sm[m];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+        sm[m] = x;
+      }
+      if (lane == 0)
+#pragma unroll
+        for (int m = 0; m < TOK; ++m) ssq_red[(warp - 2) * TOK + m] = sm[m];
+      named_bar_sync(1, 128);
+      if (t < TOK) ssq_own[t] = (ssq_red[t] + ssq_red[TOK + t]) + (ssq_red[2 * TOK + t] + ssq_red[3 * TOK + t]);
+    }
     // ---------------------------------------------------------------- epilogue (warps 2-5)
     const uint32_t q4 = warp & 3u;  // TMEM lane quarter this warp may access
     const int row = (int)(q4 * 32 + lane);
-    named_bar_sync(1, 128);         // ssq_own written by the side warp
+    named_bar_sync(1, 128);         // ssq_own complete
     // RoPE: fetch this thread's cos/sin (per token) while the accumulator is still being built;
     // only block 0 of the tile (R = 1 covers it whole) is used below
     const bool rope_blk = R == 1 && MODE == MODE_RMS && rope.pos != nullptr && n0 < rope.n;
@@ -341,7 +375,11 @@ __global__ void __launch_bounds__(dtc::THREADS, 2)  // <= 168 registers: two CTA
         }
       }
     }
+    // z (written below) may still be read by the previous kernel of the stream: wait for it here,
+    // while the contraction runs (RMS mode already waited before reading the tokens)
+    if (MODE != MODE_RMS) pdl_wait_prior_grid();
     mbar_wait_warp(tfull, 0);
+    TC_EPI(0);
     if (warp == 2 && lane == 0) TC_TRACE(2);
     tc_fence_after();
     float acc[R][TOK];
@@ -353,6 +391,7 @@ __global__ void __launch_bounds__(dtc::THREADS, 2)  // <= 168 registers: two CTA
 #pragma unroll
       for (int m = 0; m < TOK; ++m) acc[j][m] = __uint_as_float(v[m]);
     }
+    TC_EPI(1);
     float ssq[TOK];
 #pragma unroll
     for (int m = 0; m < TOK; ++m) ssq[m] = MODE == MODE_RMS ? ssq_own[m] : 0.f;
@@ -363,22 +402,35 @@ __global__ void __launch_bounds__(dtc::THREADS, 2)  // <= 168 registers: two CTA
       // leader's recv barrier; the leader sums the slots in fixed rank order (deterministic).
       // No cluster-wide barrier: a peer leaves as soon as its stores are issued.
       if (rank != 0) {
-        cluster_wait();  // the leader's recv barrier is initialised
-        float* slot_local = recv + (rank - 1) * RECV_STRIDE;
+        // stage the partial (+ ssq) in this CTA's own SMEM (the ring is free once tfull fired),
+        // then ONE bulk copy moves it into the leader's receive slot and completes on the leader's
+        // recv barrier (a release-arrive per thread after DSMEM stores measured ~1500 cycles)
 #pragma unroll
-        for (int j = 0; j < R; ++j) {
-          const uint32_t dst = mapa_shared(slot_local + (j * ROWS + row) * TOK, 0u);
+        for (int j = 0; j < R; ++j)
 #pragma unroll
           for (int m4 = 0; m4 < TOK / 4; ++m4)
-            st_cluster_v4(dst + m4 * 16, make_float4(acc[j][4 * m4], acc[j][4 * m4 + 1], acc[j][4 * m4 + 2],
-                                                     acc[j][4 * m4 + 3]));
+            reinterpret_cast<float4*>(part)[(j * ROWS + row) * (TOK / 4) + m4] =
+                make_float4(acc[j][4 * m4], acc[j][4 * m4 + 1], acc[j][4 * m4 + 2], acc[j][4 * m4 + 3]);
+        if (MODE == MODE_RMS && warp == 2 && lane < TOK) part[R * ROWS * TOK + lane] = ssq_own[lane];
+        fence_proxy_async_smem();  // generic-proxy writes -> visible to the bulk-copy engine
+        named_bar_sync(1, 128);
+        TC_EPI(2);
+        if (warp == 2) {
+          cluster_wait();  // the leader's recv barrier is initialised (arrive at kernel start)
+          if (lane == 0) {
+            dsmem_bulk_copy(mapa_shared(recv + (rank - 1) * RECV_STRIDE, 0u), part, RECV_STRIDE * 4,
+                            mapa_shared(recv_bar, 0u));
+            bulk_commit_group();
+            bulk_wait_read();  // the source (this CTA's SMEM) stays valid until read
+          }
+          __syncwarp();
         }
-        if (MODE == MODE_RMS && warp == 2 && lane < TOK)
-          st_cluster_f32(mapa_shared(slot_local + R * ROWS * TOK + lane, 0u), ssq_own[lane]);
-        mbar_arrive_cluster(mapa_shared(recv_bar, 0u));
+        TC_EPI(3);
         write_z = false;
       } else {
+        TC_EPI(2);
         mbar_wait_warp_cluster(recv_bar, 0);
+        TC_EPI(3);
         for (int r = 1; r < S; ++r) {  // fixed rank order
           const float* sl = recv + (r - 1) * RECV_STRIDE;
 #pragma unroll
@@ -491,6 +543,7 @@ __global__ void __launch_bounds__(dtc::THREADS, 2)  // <= 168 registers: two CTA
         }
       }
     }
+    TC_EPI(7);
     if (write_z) {
       const float invK = 1.0f / (float)K;
       float rr[TOK];
@@ -498,7 +551,6 @@ __global__ void __launch_bounds__(dtc::THREADS, 2)  // <= 168 registers: two CTA
       for (int m = 0; m < TOK; ++m)
         rr[m] = MODE == MODE_RMS ? rsqrtf(fmaf(ssq[m], invK, eps))
                                  : (MODE == MODE_NONE && row_scale != nullptr && m < M ? __ldg(row_scale + m) : 1.0f);
-      pdl_wait_prior_grid();  // z may still be read by the previous kernel of the stream
 #pragma unroll
       for (int j = 0; j < R; ++j) {
         const int n = n0 + j * ROWS + row;
@@ -581,8 +633,9 @@ __global__ void __launch_bounds__(dtc::THREADS, 2)  // <= 168 registers: two CTA
     }
   }
   if (warp == 2 && lane == 0) TC_TRACE(12);
+  TC_EPI(4);
   if (push) {
-    if (rank == 0 || warp < 2) cluster_wait();  // pairs with the arrive at the start (peer epilogue waited above)
+    if (rank == 0 || warp != 2) cluster_wait();  // pairs with the arrive at the start (peer warp 2 waited above)
   } else if (S > 1 && use_cluster && warp < 2) {
     cluster_sync_all();
     cluster_sync_all();
@@ -590,10 +643,12 @@ __global__ void __launch_bounds__(dtc::THREADS, 2)  // <= 168 registers: two CTA
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) TC_TRACE(13);
+  TC_EPI(5);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, TMEM_COLS);
   }
+  TC_EPI(6);
 #ifdef FN_GEMV_TC_TRACE
   if (threadIdx.x == 0) {
     unsigned smid;
@@ -639,7 +694,7 @@ size_t dtc_smem_for(int R, int stages, int S) {
 // deepest ring (<= the default depth) that fits the SMEM budget beside the receive slots
 int dtc_stages(int R, int S) {
   static const int cap = env_int("FN_DECODE_STAGES", 0);
-  int st = cap >= 4 ? cap : (R == 1 ? dtc::Cfg<1>::STAGES : dtc::Cfg<2>::STAGES);
+  int st = cap >= 2 ? cap : (R == 1 ? dtc::Cfg<1>::STAGES : dtc::Cfg<2>::STAGES);
   while (st > 2 && dtc_smem_for(R, st, S) > dtc::SMEM_MAX - 256) --st;
   return st;
 }
@@ -709,6 +764,9 @@ DtcPlan dtc_plan(int mode, int K, int N, int num_sms) {
     const int ctas = tiles * p.S;
     if (ctas > best_ctas) { best = p; best_ctas = ctas; }
   }
+  if (env_int("FN_DECODE_VERBOSE", 0))
+    fprintf(stderr, "[flashnorm] decode plan K=%d N=%d: R=%d S=%d cluster=%d stages=%d smem=%zu\n", K, N, best.R,
+            best.S, best.cluster, dtc_stages(best.R, best.S), dtc_smem(best.R, best.S));
   std::lock_guard<std::mutex> lk(mu);
   cache.emplace(key, best);
   return best;
@@ -723,7 +781,8 @@ bool gemv_tc_supported(int M, int N, int num_sms) {
 
 cudaError_t launch_gemv_tc(const CUtensorMap& tw, const CUtensorMap& ta, const float* cstar, __nv_bfloat16* z,
                            int M, int K, int N, float eps, float alpha, int mode, int num_sms, cudaStream_t stream,
-                           const float* row_scale, RopeParams rope, const __nv_bfloat16* wptr) {
+                           const float* row_scale, RopeParams rope, const __nv_bfloat16* wptr,
+                           const __nv_bfloat16* aptr) {
   using namespace dtc;
   const DtcPlan p = dtc_plan(mode, K, N, num_sms);
   dtc_set_attr(mode, p.R);
@@ -755,7 +814,8 @@ cudaError_t launch_gemv_tc(const CUtensorMap& tw, const CUtensorMap& ta, const f
   int flags = dtc_flags();
   void* args[] = {(void*)&tw, (void*)&ta, (void*)&cstar, (void*)&z, (void*)&M, (void*)&K, (void*)&N,
                   (void*)&eps, (void*)&alpha, (void*)&S, (void*)&slot, (void*)&use_cluster, (void*)&row_scale,
-                  (void*)&rope, (void*)&l2pf, (void*)&stages, (void*)&flags, (void*)&wptr};
+                  (void*)&rope, (void*)&l2pf, (void*)&stages, (void*)&flags, (void*)&wptr,
+                  (void*)&aptr};
   return cudaLaunchKernelExC(&cfg, fptr, args);
 }
 

@@ -95,7 +95,8 @@ cudaError_t launch_gemv_tc(const CUtensorMap& tw, const CUtensorMap& ta, const f
                            int M, int K, int N, float eps, float alpha, int mode, int num_sms, cudaStream_t stream,
                            const float* row_scale = nullptr,
                            RopeParams rope = RopeParams{nullptr, nullptr, nullptr, 0, 0, 1.f, nullptr, nullptr, 0, 0.f},
-                           const __nv_bfloat16* wptr = nullptr);  // W* base (L2 prefetch hints only)
+                           const __nv_bfloat16* wptr = nullptr,   // W* base (L2 prefetch hints only)
+                           const __nv_bfloat16* aptr = nullptr);  // tokens [M x K] (RMS: ssq read from global)
 size_t gemv_smem_bytes(int M, int K);
 cudaError_t launch_gemv(const __nv_bfloat16* a, const __nv_bfloat16* Wt, const float* cstar, __nv_bfloat16* z,
                         int M, int K, int N, float eps, float alpha, int mode, int num_sms, cudaStream_t stream);

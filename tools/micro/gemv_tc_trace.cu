@@ -33,11 +33,11 @@ int main(int argc, char** argv) {
   for (int i = 0; i < 4; ++i) tw[i] = tmap(W[i], N, K, tr_rows);
   auto launch = [&](int i) {
     unsigned v = (unsigned)i; cudaMemcpyToSymbolAsync(fn::g_tc_launch, &v, 4, 0, cudaMemcpyHostToDevice, 0);
-    fn::launch_gemv_tc(tw[i % 4], ta, nullptr, z, M, K, N, 1e-5f, 0.5f, 0, 148, 0);
+    fn::launch_gemv_tc(tw[i % 4], ta, nullptr, z, M, K, N, 1e-5f, 0.5f, 0, 148, 0, nullptr, fn::RopeParams{nullptr, nullptr, nullptr, 0, 0, 1.f, nullptr, nullptr, 0, 0.f}, nullptr, a);
   };
-  auto launch_plain = [&](int i) { fn::launch_gemv_tc(tw[i % 4], ta, nullptr, z, M, K, N, 1e-5f, 0.5f, 0, 148, 0); };
+  auto launch_plain = [&](int i) { fn::launch_gemv_tc(tw[i % 4], ta, nullptr, z, M, K, N, 1e-5f, 0.5f, 0, 148, 0, nullptr, fn::RopeParams{nullptr, nullptr, nullptr, 0, 0, 1.f, nullptr, nullptr, 0, 0.f}, nullptr, a); };
   {
-    cudaError_t le = fn::launch_gemv_tc(tw[0], ta, nullptr, z, M, K, N, 1e-5f, 0.5f, 0, 148, 0);
+    cudaError_t le = fn::launch_gemv_tc(tw[0], ta, nullptr, z, M, K, N, 1e-5f, 0.5f, 0, 148, 0, nullptr, fn::RopeParams{nullptr, nullptr, nullptr, 0, 0, 1.f, nullptr, nullptr, 0, 0.f}, nullptr, a);
     printf("launch: %s\n", cudaGetErrorString(le));
     int n = -1;
     cudaLaunchConfig_t cfg = {};
@@ -100,6 +100,20 @@ int main(int argc, char** argv) {
                 T(2), T(8), T(9), T(10), T(11), T(12), T(13), T(3));
       }
     fclose(f);
+  }
+  {
+    static long long st[4][64];
+    cudaMemcpyFromSymbol(st, fn::g_tc_stage, sizeof(st));
+    printf("CTA0 per-stage clocks (relative to stage-0 MMA): i, mma_full, prod_issue, side_rel\n");
+    for (int i = 0; i < 40; ++i)
+      if (st[0][i]) printf("  %2d %8lld %8lld %8lld\n", i, st[0][i] - st[0][0], st[1][i] - st[0][0], st[2][i] - st[0][0]);
+  }
+  {
+    static long long ep[2][8];
+    cudaMemcpyFromSymbol(ep, fn::g_tc_epi, sizeof(ep));
+    printf("epilogue clocks rel. to tfull (CTA0 leader / CTA1 peer): tmem_ld, push/recv start, push/recv done, z stored, joined, dealloc\n");
+    for (int c = 0; c < 2; ++c) printf("  CTA%d: %lld %lld %lld %lld %lld %lld\n", c, ep[c][1] - ep[c][0], ep[c][2] - ep[c][0], ep[c][3] - ep[c][0], ep[c][4] - ep[c][0], ep[c][5] - ep[c][0], ep[c][6] - ep[c][0]);
+    printf("  reduced (before z): CTA0 %lld CTA1 %lld\n", ep[0][7] - ep[0][0], ep[1][7] - ep[1][0]);
   }
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   cudaEventRecord(e0); for (int i = 0; i < 200; ++i) launch_plain(i); cudaEventRecord(e1); cudaEventSynchronize(e1);
