@@ -402,6 +402,58 @@ def qk_norm_rope_deferred(a, Wstar, eps, n_q, n_k, h, g_q, g_k, eps_qk, pos, cos
 
 
 # ---------------------------------------------------------------------------
+# LayerNorm deferred past the contraction without a foldable V (NEXT-4) and
+# the App. B 1/n elimination
+# ---------------------------------------------------------------------------
+
+def column_sums(Wstar):
+    """u_j = sum_i W*_{i,j}: the sum of column j of the FOLLOWING layer's weights.
+
+    The §1.2 derivation moves the mean through a linear layer by summing
+    weights over the dimension the mean runs over; applied to the layer AFTER the centering,
+    (a - mu 1) W* = a W* - mu (1^T W*), the sums run over W*'s input index i [reading c29]."""
+    return np.sum(_f64(Wstar), axis=0)
+
+
+def layernorm_deferred(a, Wstar, u, cstar=None, eps=0.0):
+    """LayerNorm -> linear with BOTH the mean centering and the normalization deferred past the
+    contraction [reading c29], step by step:
+      mu   = (1/n) sum_i a_i                         (the mean)
+      acc  = a W*                                    (raw a: nothing before the contraction)
+      MS   = (1/n) sum_i (a_i - mu)^2 = (1/n) sum_i a_i^2 - mu^2
+                                                     (LayerNorm = mean centering then RMSNorm)
+      z    = (acc - mu u) / sqrt(MS + eps) + c*      (u = column_sums(W*); scale before bias)
+    """
+    a = _f64(a)
+    n = a.shape[-1]
+    mu = np.sum(a, axis=-1) / n
+    acc = a @ _f64(Wstar)
+    ms = np.sum(a * a, axis=-1) / n - mu * mu
+    z = (acc - mu[:, None] * _f64(u)[None, :]) / np.sqrt(ms + eps)[:, None]
+    if cstar is not None:
+        z = z + _f64(cstar)
+    return z
+
+
+def fold_weights_rss(W, g=None, b=None, c=None):
+    """App. B (PAPER.md:189-192): g* = sqrt(n) g merged into W: W*_{i,j} = sqrt(n) g_i W_{i,j};
+    c* = c + b W as in Fig A (the bias is unaffected by the 1/n elimination)."""
+    W = _f64(W)
+    n = W.shape[0]
+    gs = np.sqrt(n) * (np.ones(n) if g is None else _f64(g))
+    return gs[:, None] * W, eliminate_norm_bias(W, b, c)
+
+
+def deferred_linear_rss(a, Wstar_rss, cstar=None, eps=0.0):
+    """z = (a W*_rss) / RSSe(a) + c*, RSSe(a) = sqrt(n eps + sum a_i^2)."""
+    a = _f64(a)
+    z = (a @ _f64(Wstar_rss)) / rsse(a, eps)[..., None]
+    if cstar is not None:
+        z = z + _f64(cstar)
+    return z
+
+
+# ---------------------------------------------------------------------------
 # Parity metric [reading c12]
 # ---------------------------------------------------------------------------
 

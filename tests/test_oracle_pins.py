@@ -504,3 +504,87 @@ def test_qk_norm_head_rms_is_one():
     y = O.qk_norm_rope_unfused(a, W, None, 0.0, 16, 8, 8, np.ones(8), np.ones(8), 0.0, [1, 2, 3], cos_tab, sin_tab)
     for h0 in range(0, 24, 8):
         np.testing.assert_allclose(np.sqrt(np.mean(y[:, h0:h0 + 8] ** 2, axis=1)), 1.0, rtol=1e-13)
+
+
+# ---------------------------------------------------------------- NEXT-4: LayerNorm deferred without a foldable V
+
+def _ln_case(seed, M=6, n=64, k=40, mean_scale=3.0):
+    rng = np.random.default_rng(seed)
+    a = rng.standard_normal((M, n)) + rng.uniform(-mean_scale, mean_scale, (M, 1))
+    W = rng.standard_normal((n, k)) / np.sqrt(n)
+    g = rng.uniform(0.5, 1.5, n)
+    b = rng.uniform(-0.1, 0.1, n)
+    c = rng.uniform(-0.1, 0.1, k)
+    return a, W, g, b, c
+
+
+def test_layernorm_deferred_worked():
+    """LayerNorm([1, 3]) = [-1, 1]: with W* = I, u = [1, 1], eps = 0 the deferred
+    form gives ([1,3] - 2 [1,1]) / sqrt((1+9)/2 - 2^2) = [-1, 1]."""
+    z = O.layernorm_deferred(np.array([[1.0, 3.0]]), np.eye(2), O.column_sums(np.eye(2)), None, 0.0)
+    np.testing.assert_array_equal(z, [[-1.0, 1.0]])
+    np.testing.assert_array_equal(O.column_sums(np.array([[1.0, 2.0], [3.0, 5.0]])), [4.0, 7.0])
+
+
+@pytest.mark.parametrize("eps", [0.0, 1e-5])
+def test_layernorm_deferred_equals_unfused(eps):
+    """(a - mu 1) W* = a W* - mu u: the deferred LayerNorm equals the unfused LayerNorm -> linear
+    (PAPER.md:33), which test_layernorm_matches_torch_f64 pins to torch.layer_norm."""
+    a, W, g, b, c = _ln_case(21)
+    ref = O.norm_linear(a, W, g, b, c, eps, "layernorm")
+    Ws, cs = O.fold_weights(W, g, b, c)
+    assert O.rowwise_rel_err(O.layernorm_deferred(a, Ws, O.column_sums(Ws), cs, eps), ref) < 1e-11
+
+
+def test_layernorm_deferred_shift_invariant_and_constant_rows():
+    """LayerNorm is invariant to adding a constant to every input (the -mu u term removes it),
+    and a constant row (zero variance) with eps > 0 maps to c* exactly."""
+    a, W, g, b, c = _ln_case(22)
+    Ws, cs = O.fold_weights(W, g, b, c)
+    u = O.column_sums(Ws)
+    z0 = O.layernorm_deferred(a, Ws, u, cs, 1e-5)
+    z1 = O.layernorm_deferred(a + 2.5, Ws, u, cs, 1e-5)
+    assert O.rowwise_rel_err(z1, z0) < 1e-10
+    zc = O.layernorm_deferred(np.full((2, a.shape[1]), 0.75), Ws, u, cs, 1e-5)
+    np.testing.assert_allclose(zc, np.broadcast_to(cs, zc.shape), rtol=0, atol=1e-12)
+
+
+def test_layernorm_deferred_faults_detected():
+    """Plausible mistakes fail the pins above: u from the original W (not W*), mu^2 dropped from
+    the variance, the correction sign flipped."""
+    a, W, g, b, c = _ln_case(23)
+    ref = O.norm_linear(a, W, g, b, c, 1e-5, "layernorm")
+    Ws, cs = O.fold_weights(W, g, b, c)
+    u = O.column_sums(Ws)
+    assert O.rowwise_rel_err(O.layernorm_deferred(a, Ws, O.column_sums(W), cs, 1e-5), ref) > 1e-2
+    n = a.shape[1]
+    mu = a.mean(axis=1)
+    no_mu2 = (a @ Ws - mu[:, None] * u) / np.sqrt((a * a).sum(axis=1) / n + 1e-5)[:, None] + cs
+    assert O.rowwise_rel_err(no_mu2, ref) > 1e-2
+    flipped = (a @ Ws + mu[:, None] * u) / np.sqrt((a * a).sum(axis=1) / n - mu * mu + 1e-5)[:, None] + cs
+    assert O.rowwise_rel_err(flipped, ref) > 1e-2
+
+
+# ---------------------------------------------------------------- App. B: eliminating 1/n
+
+def test_rss_worked():
+    """n = 4, a = [1,1,1,1], W = I, g = 1, eps = 0: RSS = 2, g* = sqrt(4) = 2, z = 2a/2 = a,
+    which is RMSNorm(a) = a / RMS(a) = a / 1 (PAPER.md:185-192)."""
+    Ws, cs = O.fold_weights_rss(np.eye(4))
+    np.testing.assert_array_equal(Ws, 2.0 * np.eye(4))
+    np.testing.assert_array_equal(O.deferred_linear_rss(np.ones((1, 4)), Ws, cs, 0.0), np.ones((1, 4)))
+
+
+@pytest.mark.parametrize("eps", [0.0, 1e-5, 1e-2])
+def test_rss_equals_rms_path(eps):
+    """(a W*_rss)/RSSe(a) = (a W*)/RMSe(a) with g* = sqrt(n) g and RSSe = sqrt(n eps + sum a^2)
+    (PAPER.md:196-200), including low-energy rows where eps matters; a fault (eps instead of
+    n eps under the root) fails."""
+    a, W, g, b, c = _ln_case(24, mean_scale=0.0)
+    a[1] *= 1e-3
+    ref = O.deferred_linear(a, *O.fold_weights(W, g, b, c)[:1], O.fold_weights(W, g, b, c)[1], eps)
+    Wr, cr = O.fold_weights_rss(W, g, b, c)
+    assert O.rowwise_rel_err(O.deferred_linear_rss(a, Wr, cr, eps), ref) < 1e-12
+    if eps >= 1e-5:
+        wrong = (a @ Wr) / np.sqrt(eps + (a * a).sum(axis=1))[:, None] + cr
+        assert O.rowwise_rel_err(wrong, ref) > 1e-3
