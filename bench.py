@@ -430,6 +430,28 @@ def measure_secondary(args, fn, torch, dev, stream, peaks, a, Ws, cs, g):
                       "ffn_ms": ms_g + ms_dn, "ffn_TFLOP/s": (fl_g + fl_d) / ((ms_g + ms_dn) * 1e-3) / 1e12}
     del Wgu, h, Wdn, yd
 
+    # NEXT-4: exact LayerNorm deferred past the contraction (mean via u = 1^T W*, reading c29) at the
+    # config-3 shape (same CTA-pair kernel as the headline) and at config 4 (2048 x 4096 -> 4096)
+    u3 = fn.fold_colsum(Ws)
+    ms_ln = timed(lambda i: fn.layernorm_linear(a, Ws, u3, cs, eps=1e-5, out=z), 10)
+    a4 = SD.activations(9, 2048, 4096, dev, torch.bfloat16)
+    W4, g4, _, _ = SD.layer(9, 4096, 4096, dev, torch.bfloat16)
+    W4s, c4s = fn.fold_weights(W4, g4)
+    u4 = fn.fold_colsum(W4s)
+    z4 = torch.empty((2048, 4096), dtype=torch.bfloat16, device=dev)
+    ms_ln4 = timed(lambda i: fn.layernorm_linear(a4, W4s, u4, c4s, eps=1e-5, out=z4), 20)
+    ms_rms4 = timed(lambda i: fn.linear(a4, W4s, c4s, eps=1e-5, out=z4), 20)
+    ms_cs = timed(lambda i: fn.fold_colsum(Ws, out=u3), 10)
+    fl4 = 2.0 * 2048 * 4096 * 4096
+    out["layernorm_exact"] = {
+        "what": "flashnorm_layernorm_linear: z = (a W* - mu u) rsqrt(var + eps) + c*, mu/var beside the MMA",
+        "config3_ms": ms_ln, "config3_TFLOP/s": fl / (ms_ln * 1e-3) / 1e12,
+        "config3_frac_bf16_peak": fl / (ms_ln * 1e-3) / 1e12 / peaks.get("bf16_tflops", 1657.2),
+        "config4_ms": ms_ln4, "config4_TFLOP/s": fl4 / (ms_ln4 * 1e-3) / 1e12,
+        "config4_rmsnorm_ms": ms_rms4,
+        "fold_colsum_us": ms_cs * 1e3, "fold_colsum_GB/s": N * K * 2 / (ms_cs * 1e-3) / 1e9}
+    del a4, W4, W4s, z4, u3, u4
+
     # folds (offline, once per weight load): config-3 W (235 MB in + 235 MB out)
     Wf, gf, bf_, cf = SD.layer(5, N, K, dev, torch.bfloat16, with_b=True, with_c=True)
     Wo = torch.empty_like(Wf)

@@ -263,6 +263,36 @@ fn_status flashnorm_qk_norm_rope_linear(const void* a, const void* Wt_star, int6
                                        const float* cos_tab, const float* sin_tab, float qk_scale, float eps,
                                        fn_dtype dtype, void* z, void* stream);
 
+/* --------------------------------------------------------------------------
+ * LayerNorm deferred past the contraction WITHOUT a foldable preceding layer
+ * (NEXT-4; reading c29).  LayerNorm = mean centering then RMSNorm
+ * (PAPER.md:33); the §1.2 derivation moves the mean through a
+ * linear layer by summing weights — applied to the layer AFTER the norm:
+ *   (a - mu 1) W* = a W* - mu u,   u = 1^T W*  (u_j = sum_k W*t[j][k]).
+ *
+ * flashnorm_fold_colsum — offline: u[j] = RN_f32( fp64 sum_k W*t[j][k] ) in the
+ *   c* order of "fold_weights numerics" above (lane l: 16-byte chunks l, l+32, ...
+ *   ascending, elements ascending; xor butterfly 16,8,4,2,1), i.e. exactly the c*
+ *   that flashnorm_fold_weights computes for b = 1, c = NULL on Wt_star.
+ *   Wt_star [N][K] storage dtype (16-B aligned, K % 8 == 0); u [N] float32 output.
+ *
+ * flashnorm_layernorm_linear — per token, with the row statistics reduced beside
+ *   the contraction from the same A tiles (shift a0 = a[m][0] against cancellation):
+ *     mu_m  = a0 + S1/K,  var_m = max(S2/K - (S1/K)^2, 0),
+ *     S1 = sum_k (a[m][k] - a0),  S2 = sum_k (a[m][k] - a0)^2     (fp32)
+ *     z[m][j] = RN( fma( fma(-mu_m, u_j, acc[m][j]), rsqrt(var_m + eps), c*_j ) )
+ *   with W* = diag(g) W and c* = c + b W from flashnorm_fold_weights (LayerNorm's g
+ *   and b) and u from flashnorm_fold_colsum(W*).  a [M][K], z [M][N]; eps >= 0.
+ *   bf16: tcgen05 GEMM kernels for every M (decode shapes run the 1-CTA kernel);
+ *   f32: the FFMA kernel.  The correction subtracts mu u_j from acc, so rows with
+ *   |mean| >> std lose relative accuracy in fp32 accumulation (reading c9).
+ * -------------------------------------------------------------------------- */
+fn_status flashnorm_fold_colsum(const void* Wt_star, int64_t N, int64_t K, fn_dtype dtype, float* u,
+                                void* stream);
+fn_status flashnorm_layernorm_linear(const void* a, const void* Wt_star, const float* u, const float* c_star,
+                                     int64_t M, int64_t K, int64_t N, float eps, fn_dtype dtype, void* z,
+                                     void* stream);
+
 /* End-to-end variant: a_host / z_host are HOST pointers (pinned memory for
  * asynchronous copies); a_dev / z_dev are caller-owned device scratch of
  * M*K / M*N elements.  Enqueues H2D(a) -> flashnorm_linear -> D2H(z) on

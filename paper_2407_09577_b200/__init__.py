@@ -23,6 +23,7 @@ __all__ = [
     "FlashNormError", "lib", "lib_path", "fold_weights", "fold_mean_center", "fold_mean_center_workspace_bytes",
     "linear", "linear_from_host", "baseline_norm", "gather_columns", "launch_count", "reset_launch_count",
     "version", "linear_workspace_bytes", "fold_glu_weights", "glu_linear", "linear_scaled", "glu_ffn", "qkv_rope_linear", "relu_ffn_up", "qk_norm_rope_linear",
+    "fold_colsum", "layernorm_linear",
     "MODES", "GLU_ACTS", "PATHS", "EXPORTS",
 ]
 
@@ -39,6 +40,7 @@ EXPORTS = [
     "flashnorm_fold_weights", "flashnorm_fold_mean_center_workspace_bytes", "flashnorm_fold_mean_center",
     "flashnorm_linear", "flashnorm_linear_ex", "flashnorm_linear_workspace_bytes", "flashnorm_linear_ws",
     "flashnorm_linear_from_host", "flashnorm_fold_glu_weights", "flashnorm_glu_linear", "flashnorm_linear_scaled",
+    "flashnorm_fold_colsum", "flashnorm_layernorm_linear",
     "flashnorm_qkv_rope_linear", "flashnorm_relu_ffn_up", "flashnorm_qk_norm_rope_linear", "flashnorm_baseline_norm",
     "flashnorm_gather_columns", "flashnorm_status_string", "flashnorm_last_error", "flashnorm_launch_count",
     "flashnorm_reset_launch_count", "flashnorm_version",
@@ -82,6 +84,8 @@ def lib() -> ctypes.CDLL:
                                           _vp, _f32, _f32, _int, _vp, _vp],
         "flashnorm_relu_ffn_up": [_vp, _vp, _i64, _i64, _i64, _f32, _int, _vp, _vp, _vp],
         "flashnorm_linear_scaled": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _vp, _vp],
+        "flashnorm_fold_colsum": [_vp, _i64, _i64, _int, _vp, _vp],
+        "flashnorm_layernorm_linear": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _f32, _int, _vp, _vp],
         "flashnorm_linear_from_host": [_vp, _vp, _vp, _i64, _i64, _i64, _f32, _f32, _int, _int, _vp, _vp, _vp,
                                        _vp],
         "flashnorm_baseline_norm": [_vp, _vp, _vp, _i64, _i64, _f32, _int, _f32, _int, _vp, _vp],
@@ -325,6 +329,35 @@ def linear_scaled(a, Wt_star, row_scale, c_star=None, out=None):
     z = out if out is not None else torch.empty((M, N), dtype=a.dtype, device=a.device)
     _check(lib().flashnorm_linear_scaled(_ptr(a), _ptr(Wt_star), _ptr(c_star), _ptr(row_scale), M, K, N,
                                          _dtype_code(a), _ptr(z), _stream(a)), "linear_scaled")
+    return z
+
+
+def fold_colsum(Wt_star, out=None):
+    """u = 1^T W*: u[j] = sum_k W*t[j][k] (fp64 sum, one f32 rounding) — the correction vector of
+    the deferred LayerNorm (NEXT-4, reading c29)."""
+    torch = _torch()
+    _dev(Wt_star, "Wt_star")
+    N, K = Wt_star.shape
+    u = out if out is not None else torch.empty(N, dtype=torch.float32, device=Wt_star.device)
+    _check(lib().flashnorm_fold_colsum(_ptr(Wt_star), N, K, _dtype_code(Wt_star), _ptr(u), _stream(Wt_star)),
+           "fold_colsum")
+    return u
+
+
+def layernorm_linear(a, Wt_star, u, c_star=None, eps: float = 1e-5, out=None):
+    """LayerNorm -> linear with the mean AND the normalization deferred past the contraction:
+    z = (a W* - mu u) / sqrt(var + eps) + c*, mu / var reduced beside the contraction (PAPER.md:33,
+    42-46; reading c29).  W*, c* from fold_weights(W, g, b, c); u from fold_colsum(W*)."""
+    torch = _torch()
+    _dev(a, "a")
+    _dev(Wt_star, "Wt_star")
+    M, K = a.shape
+    N = Wt_star.shape[0]
+    u = _vec(u, "u", N)
+    c_star = _vec(c_star, "c_star", N)
+    z = out if out is not None else torch.empty((M, N), dtype=a.dtype, device=a.device)
+    _check(lib().flashnorm_layernorm_linear(_ptr(a), _ptr(Wt_star), _ptr(u), _ptr(c_star), M, K, N, float(eps),
+                                            _dtype_code(a), _ptr(z), _stream(a)), "layernorm_linear")
     return z
 
 

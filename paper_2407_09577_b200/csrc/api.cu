@@ -147,6 +147,7 @@ struct LinearExtras {
   float* s_out = nullptr;           // GLU: output scale per row
   const float* row_scale = nullptr; // FN_NONE: z = RN(acc * row_scale[m] + c*)
   fn::RopeParams rope{nullptr, nullptr, nullptr, 0, 0, 1.0f, nullptr, nullptr, 0, 0.f};  // RoPE on [0, rope.n)
+  const float* ln_u = nullptr;      // exact deferred LayerNorm (rmsnorm mode): u = 1^T W* [N]
 };
 
 fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, int64_t M, int64_t K, int64_t N,
@@ -185,7 +186,8 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
     if (path != FN_PATH_AUTO && path != FN_PATH_SIMT)
       return fail(FN_ERR_UNSUPPORTED, "f32 supports only the SIMT path (path=%d)", (int)path);
     cudaError_t e = fn::launch_linear_f32(static_cast<const float*>(a), static_cast<const float*>(Wt_star), c_star,
-                                          static_cast<float*>(z), (int)M, (int)K, (int)N, eps, alpha, km, stream);
+                                          static_cast<float*>(z), (int)M, (int)K, (int)N, eps, alpha, km, stream,
+                                          ex.ln_u);
     if (e != cudaSuccess) return cuda_fail(e, "linear_f32");
     ++g_launches;
     return FN_OK;
@@ -195,8 +197,11 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
   // QK-norm on the decode kernel needs whole heads inside its 128-row tiles (h | 128, R = 1)
   const bool qkn_tc_ok = ex.rope.g_q == nullptr ||
                          (128 % ex.rope.h == 0 && fn::gemv_tc_tile_rows(fn::MODE_RMS, (int)K, (int)N, num_sms()) == 128);
-  const bool tc_ok = ex.glu_act < 0 && qkn_tc_ok && fn::gemv_tc_supported((int)M, (int)N, num_sms());
-  const bool mma_ok = ex.glu_act < 0 && ex.row_scale == nullptr && ex.rope.pos == nullptr &&
+  // the exact deferred LayerNorm (ln_u) lives in the GEMM kernels only: decode shapes run the
+  // 1-CTA tcgen05 kernel
+  const bool tc_ok = ex.glu_act < 0 && ex.ln_u == nullptr && qkn_tc_ok &&
+                     fn::gemv_tc_supported((int)M, (int)N, num_sms());
+  const bool mma_ok = ex.glu_act < 0 && ex.ln_u == nullptr && ex.row_scale == nullptr && ex.rope.pos == nullptr &&
                       fn::gemv_supported((int)M, (int)K);
   const bool gemv_ok = tc_ok || mma_ok;
   if (path == FN_PATH_SIMT) return fail(FN_ERR_UNSUPPORTED, "SIMT path is f32-only");
@@ -267,6 +272,7 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
   p.s_out = ex.s_out;
   p.row_scale = ex.row_scale;
   p.rope = ex.rope;
+  p.ln_u = ex.ln_u;
   cudaError_t e = pair ? fn::launch_gemm2(ta, tb, p, km, num_sms(), stream)
                        : fn::launch_gemm(ta, tb, p, km, num_sms(), stream);
   if (e != cudaSuccess) return cuda_fail(e, pair ? "gemm2_sm100" : "gemm_sm100");
@@ -363,6 +369,32 @@ fn_status flashnorm_linear_ws(const void* a, const void* Wt_star, const float* c
     return fail(FN_ERR_NULL, "workspace is NULL but workspace_bytes = %lld", (long long)workspace_bytes);
   return linear_impl(a, Wt_star, c_star, M, K, N, eps, alpha, mode, dtype, z, path, workspace, workspace_bytes,
                      static_cast<cudaStream_t>(stream));
+}
+
+fn_status flashnorm_fold_colsum(const void* Wt_star, int64_t N, int64_t K, fn_dtype dtype, float* u, void* stream) {
+  fn_status s;
+  if ((s = check_dtype(dtype)) != FN_OK) return s;
+  if (N <= 0 || K <= 0)
+    return fail(FN_ERR_SHAPE, "Wt_star[%lld x %lld]: sizes must be positive", (long long)N, (long long)K);
+  if (Wt_star == nullptr || u == nullptr) return fail(FN_ERR_NULL, "Wt_star=%p u=%p: NULL", Wt_star, (void*)u);
+  if ((s = check_vec("K", K, dtype)) != FN_OK) return s;
+  if ((s = check_ptr16("Wt_star", Wt_star)) != FN_OK) return s;
+  cudaError_t e = fn::launch_fold_colsum(Wt_star, N, K, dtype == FN_BF16 ? 0 : 1, u, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fold_colsum");
+  ++g_launches;
+  return FN_OK;
+}
+
+fn_status flashnorm_layernorm_linear(const void* a, const void* Wt_star, const float* u, const float* c_star,
+                                     int64_t M, int64_t K, int64_t N, float eps, fn_dtype dtype, void* z,
+                                     void* stream) {
+  if (u == nullptr) return fail(FN_ERR_NULL, "u (column sums of W*) is NULL");
+  fn_status s;
+  if ((s = check_ptr16("u", u)) != FN_OK) return s;
+  LinearExtras ex;
+  ex.ln_u = u;
+  return linear_impl(a, Wt_star, c_star, M, K, N, eps, 0.0f, FN_RMSNORM, dtype, z, FN_PATH_AUTO, nullptr, 0,
+                     static_cast<cudaStream_t>(stream), ex);
 }
 
 fn_status flashnorm_linear_scaled(const void* a, const void* Wt_star, const float* c_star, const float* row_scale,

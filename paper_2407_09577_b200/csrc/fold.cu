@@ -276,6 +276,45 @@ cudaError_t launch_fold_weights(const void* Wt, int64_t N, int64_t K, int dtype,
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ K1u: column sums of W*
+// u_j = RN_f32( fp64 sum_k W*t[j][k] ) in the c* contract order of K1 (lane l: chunks l, l+32, ...
+// ascending, elements ascending; xor butterfly 16..1) — u = 1^T W* for the deferred LayerNorm
+// (NEXT-4, reading c29): z = (acc - mu u) r + c*.  One warp per row, 4 chunks in flight per lane.
+template <int DT>
+__global__ void __launch_bounds__(256)
+    colsum_rows_kernel(const uint8_t* __restrict__ Wt, int64_t N, int64_t K, float* __restrict__ u) {
+  constexpr int E = DT == 0 ? 8 : 4;
+  constexpr int ES = DT == 0 ? 2 : 4;
+  constexpr int U = 4;
+  const int lane = threadIdx.x & 31;
+  const int64_t j = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (j >= N) return;
+  const int64_t nchunks = K / E;
+  double acc = 0.0;
+  for (int64_t q0 = lane; q0 < nchunks; q0 += 32 * U) {
+    uint4 vv[U];
+#pragma unroll
+    for (int v = 0; v < U; ++v)
+      if (q0 + v * 32 < nchunks) vv[v] = ld_nc_v4(Wt + (j * K + (q0 + v * 32) * E) * ES);
+#pragma unroll
+    for (int v = 0; v < U; ++v) {
+      if (q0 + v * 32 >= nchunks) break;
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc = __dadd_rn(acc, (double)chunk_elem<DT>(vv[v], e));
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, off));
+  if (lane == 0) u[j] = __double2float_rn(acc);
+}
+
+cudaError_t launch_fold_colsum(const void* Wt_star, int64_t N, int64_t K, int dtype, float* u, cudaStream_t stream) {
+  const dim3 grid((unsigned)((N + 7) / 8));
+  if (dtype == 0) colsum_rows_kernel<0><<<grid, 256, 0, stream>>>(static_cast<const uint8_t*>(Wt_star), N, K, u);
+  else colsum_rows_kernel<1><<<grid, 256, 0, stream>>>(static_cast<const uint8_t*>(Wt_star), N, K, u);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ K2
 
 int64_t fold_mean_center_workspace(int64_t n_out, int64_t d_in) {

@@ -46,7 +46,8 @@ constexpr int THREADS = 384;
 constexpr int TMEM_COLS = 2 * BN;
 constexpr int BAR_BYTES = 1024;
 constexpr int SSQ_SLOTS = 16;          // per-CTA cache of reduced row ssq, by M block
-constexpr int SMEM_BYTES = 1024 + STAGES * (A_STAGE + B_STAGE) + BAR_BYTES + (4 + SSQ_SLOTS) * BM * 4 + 32;
+constexpr int SMEM_BYTES = 1024 + STAGES * (A_STAGE + B_STAGE) + BAR_BYTES + (4 + SSQ_SLOTS) * BM * 4 + 32 +
+                             (2 + SSQ_SLOTS) * BM * 4;  // + LayerNorm mean buffers
 }  // namespace gemm2
 
 template <int MODE>
@@ -75,6 +76,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
   float* ssq_cache = epi_fence + BM;  // [SSQ_SLOTS][BM]
   uint8_t* sig_dst = reinterpret_cast<uint8_t*>(ssq_cache + SSQ_SLOTS * BM);  // 16 B: DyT peer signal landing
   const uint8_t* sig_src = sig_dst + 16;                                      // 16 B: its (unused) source
+  float* mu_buf = reinterpret_cast<float*>(sig_dst + 32);  // [2][BM] LayerNorm (ln_u): row means
+  float* mu_cache = mu_buf + 2 * BM;                       // [SSQ_SLOTS][BM]
+  const bool ln = MODE == MODE_RMS && p.ln_u != nullptr;   // exact deferred LayerNorm (reading c29)
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -198,12 +202,46 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
 #pragma unroll
         for (int i = 0; i < SSQ_SLOTS; ++i)
           if (i == slot) { cached = tag[i] == m_blk; tag[i] = m_blk; }
-        float ssq;
+        float ssq, mu = 0.f;
         if (cached) {
           // this CTA already reduced these 128 rows for an earlier N tile: the ring
           // stages of this tile are released by the MMA commit alone
           stage = (stage + nkb) % STAGES;
           ssq = ssq_cache[slot * BM + t];
+          if (ln) mu = mu_cache[slot * BM + t];
+        } else if (ln) {
+          // LayerNorm: sum(a - a0) and sum((a - a0)^2) with the shift a0 = a[m][0] (logical chunk 0
+          // of stage kb = 0), so var = S2/K - (S1/K)^2 does not cancel for rows with a large mean;
+          // ssq := K var (the epilogue's rsqrt(ssq/K + eps) is then LayerNorm's 1/sqrt(var + eps))
+          float s0 = 0.f, s1 = 0.f, q0 = 0.f, q1 = 0.f, a0 = 0.f;
+          for (int kb = 0; kb < nkb; ++kb) {
+            mbar_wait_warp(&mma_done[stage], (md_phase >> stage) & 1u);
+            md_phase ^= 1u << stage;
+            const uint4* row = reinterpret_cast<const uint4*>(sA + stage * A_STAGE + t * 128);
+            if (kb == 0) a0 = bf16lo(row[t & 7].x);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const uint4 v = row[c ^ (t & 7)];
+              float d;
+              d = bf16lo(v.x) - a0; s0 += d; q0 = fmaf(d, d, q0);
+              d = bf16hi(v.x) - a0; s1 += d; q1 = fmaf(d, d, q1);
+              d = bf16lo(v.y) - a0; s0 += d; q0 = fmaf(d, d, q0);
+              d = bf16hi(v.y) - a0; s1 += d; q1 = fmaf(d, d, q1);
+              d = bf16lo(v.z) - a0; s0 += d; q0 = fmaf(d, d, q0);
+              d = bf16hi(v.z) - a0; s1 += d; q1 = fmaf(d, d, q1);
+              d = bf16lo(v.w) - a0; s0 += d; q0 = fmaf(d, d, q0);
+              d = bf16hi(v.w) - a0; s1 += d; q1 = fmaf(d, d, q1);
+            }
+            ssq_fence[t] = (s0 + s1) + (q0 + q1);  // issues only after every LDS above returned
+            named_bar_sync(1, 128);
+            if (t == 0) mbar_arrive(&empty[stage]);
+            if (++stage == STAGES) stage = 0;
+          }
+          const float S1 = s0 + s1, S2 = q0 + q1, invK = 1.0f / (float)p.K;
+          ssq = fmaxf(S2 - S1 * (S1 * invK), 0.0f);
+          mu = fmaf(S1, invK, a0);
+          ssq_cache[slot * BM + t] = ssq;
+          mu_cache[slot * BM + t] = mu;
         } else {
           float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
           for (int kb = 0; kb < nkb; ++kb) {
@@ -235,6 +273,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
         const uint32_t aphase = (local >> 1) & 1;
         mbar_wait_warp(&sempty[as], aphase ^ 1);
         ssq_buf[as * BM + t] = ssq;
+        if (ln) mu_buf[as * BM + t] = mu;
         named_bar_sync(1, 128);
         if (t == 0) mbar_arrive(&sfull[as]);
       }
@@ -288,11 +327,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
       tile_coords(tile, p, m_blk, n_blk);
       const int as = local & 1;
       const uint32_t aphase = (local >> 1) & 1;
-      float r = 1.0f;
+      float r = 1.0f, mu = 0.f;
       if (MODE == MODE_RMS) {
         mbar_wait_warp(&sfull[as], aphase);
         const float ssq = ssq_buf[as * BM + ew * 32 + lane];
-        epi_fence[ew * 32 + lane] = ssq;
+        if (ln) mu = mu_buf[as * BM + ew * 32 + lane];
+        epi_fence[ew * 32 + lane] = ssq + mu;  // consumes both loads before the buffer is released
         named_bar_sync(2, 128);
         if (ew == 0 && lane == 0) mbar_arrive(&sempty[as]);
         r = rsqrtf(fmaf(ssq, invK, p.eps));
@@ -421,6 +461,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
 #pragma unroll
           for (int q = 0; q < 16; ++q)
             packed[q] = pack_bf16(fmaxf(__uint_as_float(v[2 * q]), 0.0f), fmaxf(__uint_as_float(v[2 * q + 1]), 0.0f));
+        } else if (ln) {
+          // z = (acc - mu u_j) r + c*_j: the mean moved through the contraction (reading c29)
+          float uu[32];
+          const float4* u4 = reinterpret_cast<const float4*>(p.ln_u + n_base + j * 32);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (n_base + j * 32 + q * 4 < p.N) x = __ldg(u4 + q);
+            uu[4 * q + 0] = x.x; uu[4 * q + 1] = x.y; uu[4 * q + 2] = x.z; uu[4 * q + 3] = x.w;
+          }
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            packed[q] = pack_bf16(fmaf(fmaf(-mu, uu[2 * q], __uint_as_float(v[2 * q])), r, cb[2 * q]),
+                                  fmaf(fmaf(-mu, uu[2 * q + 1], __uint_as_float(v[2 * q + 1])), r, cb[2 * q + 1]));
         } else {
 #pragma unroll
           for (int q = 0; q < 16; ++q)

@@ -36,7 +36,7 @@ constexpr int B_STAGE = BN * BK * 2;  // 32 KiB
 constexpr int THREADS = 384;
 constexpr int TMEM_COLS = 2 * BN;  // double-buffered fp32 accumulator
 constexpr int BAR_BYTES = 1024;
-constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * (A_STAGE + B_STAGE) + BAR_BYTES + 4 * BM * 4;
+constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * (A_STAGE + B_STAGE) + BAR_BYTES + 6 * BM * 4;
 }  // namespace gemm
 
 template <int MODE>
@@ -60,6 +60,8 @@ __global__ void __launch_bounds__(gemm::THREADS, 1)
   float* ssq_buf = reinterpret_cast<float*>(smem + STAGES * (A_STAGE + B_STAGE) + BAR_BYTES);  // [2][BM]
   float* ssq_fence = ssq_buf + 2 * BM;  // [BM] scratch: load-completion fence of the side group
   float* epi_fence = ssq_fence + BM;    // [BM] scratch: load-completion fence of the epilogue
+  float* mu_buf = epi_fence + BM;       // [2][BM] LayerNorm (ln_u): row means
+  const bool ln = MODE == MODE_RMS && p.ln_u != nullptr;  // exact deferred LayerNorm (reading c29)
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -150,9 +152,32 @@ __global__ void __launch_bounds__(gemm::THREADS, 1)
       int local = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
         float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+        float a0 = 0.f;  // LayerNorm: shift a[m][0] (see gemm2_sm100.cu)
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait_warp(&full[stage], phase);
           const uint4* row = reinterpret_cast<const uint4*>(sA + stage * A_STAGE + t * 128);
+          if (ln) {
+            // s0, s1: sum(a - a0);  s2, s3: sum((a - a0)^2)
+            if (kb == 0) a0 = bf16lo(row[t & 7].x);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const uint4 v = row[c ^ (t & 7)];
+              float d;
+              d = bf16lo(v.x) - a0; s0 += d; s2 = fmaf(d, d, s2);
+              d = bf16hi(v.x) - a0; s1 += d; s3 = fmaf(d, d, s3);
+              d = bf16lo(v.y) - a0; s0 += d; s2 = fmaf(d, d, s2);
+              d = bf16hi(v.y) - a0; s1 += d; s3 = fmaf(d, d, s3);
+              d = bf16lo(v.z) - a0; s0 += d; s2 = fmaf(d, d, s2);
+              d = bf16hi(v.z) - a0; s1 += d; s3 = fmaf(d, d, s3);
+              d = bf16lo(v.w) - a0; s0 += d; s2 = fmaf(d, d, s2);
+              d = bf16hi(v.w) - a0; s1 += d; s3 = fmaf(d, d, s3);
+            }
+            ssq_fence[t] = (s0 + s1) + (s2 + s3);
+            named_bar_sync(1, 128);
+            if (t == 0) mbar_arrive(&empty[stage]);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            continue;
+          }
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
             const uint4 v = row[c ^ (t & 7)];  // swizzled order: conflict-free, sum is order-free
@@ -183,7 +208,13 @@ __global__ void __launch_bounds__(gemm::THREADS, 1)
         const int as = local & 1;
         const uint32_t aphase = (local >> 1) & 1;
         mbar_wait_warp(&sempty[as], aphase ^ 1);
-        ssq_buf[as * BM + t] = (s0 + s1) + (s2 + s3);
+        if (ln) {
+          const float S1 = s0 + s1, S2 = s2 + s3, invK = 1.0f / (float)p.K;
+          ssq_buf[as * BM + t] = fmaxf(S2 - S1 * (S1 * invK), 0.0f);  // K var
+          mu_buf[as * BM + t] = fmaf(S1, invK, a0);
+        } else {
+          ssq_buf[as * BM + t] = (s0 + s1) + (s2 + s3);
+        }
         named_bar_sync(1, 128);  // all 128 ssq values written (bar.sync drains the STS)
         if (t == 0) mbar_arrive(&sfull[as]);
       }
@@ -230,11 +261,12 @@ __global__ void __launch_bounds__(gemm::THREADS, 1)
       tile_coords(tile, p, m_blk, n_blk);
       const int as = local & 1;
       const uint32_t aphase = (local >> 1) & 1;
-      float r = 1.0f;
+      float r = 1.0f, mu = 0.f;
       if (MODE == MODE_RMS) {
         mbar_wait_warp(&sfull[as], aphase);
         const float ssq = ssq_buf[as * BM + ew * 32 + lane];
-        epi_fence[ew * 32 + lane] = ssq;  // issues only once the LDS above has returned
+        if (ln) mu = mu_buf[as * BM + ew * 32 + lane];
+        epi_fence[ew * 32 + lane] = ssq + mu;  // issues only once the LDS above have returned
         named_bar_sync(2, 128);           // ... and bar.sync drains it: ssq_buf[as] is free
         if (ew == 0 && lane == 0) mbar_arrive(&sempty[as]);
         r = rsqrtf(fmaf(ssq, invK, p.eps));
@@ -363,6 +395,20 @@ __global__ void __launch_bounds__(gemm::THREADS, 1)
 #pragma unroll
           for (int q = 0; q < 16; ++q)
             packed[q] = pack_bf16(fmaxf(__uint_as_float(v[2 * q]), 0.0f), fmaxf(__uint_as_float(v[2 * q + 1]), 0.0f));
+        } else if (ln) {
+          // z = (acc - mu u_j) r + c*_j: the mean moved through the contraction (reading c29)
+          float uu[32];
+          const float4* u4 = reinterpret_cast<const float4*>(p.ln_u + n_base + j * 32);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (n_base + j * 32 + q * 4 < p.N) x = __ldg(u4 + q);
+            uu[4 * q + 0] = x.x; uu[4 * q + 1] = x.y; uu[4 * q + 2] = x.z; uu[4 * q + 3] = x.w;
+          }
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            packed[q] = pack_bf16(fmaf(fmaf(-mu, uu[2 * q], __uint_as_float(v[2 * q])), r, cb[2 * q]),
+                                  fmaf(fmaf(-mu, uu[2 * q + 1], __uint_as_float(v[2 * q + 1])), r, cb[2 * q + 1]));
         } else {
 #pragma unroll
           for (int q = 0; q < 16; ++q)

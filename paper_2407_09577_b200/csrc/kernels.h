@@ -43,6 +43,10 @@ struct GemmParams {
   // MODE_NONE: optional per-row output scale z = RN(acc * row_scale[m] + c*) (the GLU down projection)
   const float* row_scale;
   RopeParams rope;
+  // MODE_RMS: exact LayerNorm deferred past the contraction (NEXT-4, reading c29) when non-null:
+  // u = 1^T W* [N]; the side group reduces sum(a - a0) and sum((a - a0)^2) per row (shift a0 =
+  // a[m][0]) and the epilogue writes z = RN(fma(fma(-mu, u_j, acc), rsqrt(var + eps), c*_j))
+  const float* ln_u;
 };
 enum GluAct { GLU_SILU = 0, GLU_RELU = 1, GLU_BILINEAR = 2 };
 // Fig 2(b) (ReLU FFN, not gated): z = RN(relu(acc)) unscaled, s_out = r — the scale is deferred
@@ -103,11 +107,12 @@ cudaError_t launch_gemv(const __nv_bfloat16* a, const __nv_bfloat16* Wt, const f
 
 // K5: fp32 SIMT path (simt_f32.cu)
 cudaError_t launch_linear_f32(const float* a, const float* Wt, const float* cstar, float* z, int M, int K, int N,
-                              float eps, float alpha, int mode, cudaStream_t stream);
+                              float eps, float alpha, int mode, cudaStream_t stream, const float* u = nullptr);
 
 // K1/K2: folds (fold.cu).  dtype: 0 = bf16, 1 = f32
 // glu_half: -1 = rows as given; 0 / 1 = write row j to (j/128)*256 + glu_half*128 + j%128 (the
 // gate / up half of the 128-row-block interleave of flashnorm_fold_glu_weights)
+cudaError_t launch_fold_colsum(const void* Wt_star, int64_t N, int64_t K, int dtype, float* u, cudaStream_t stream);
 cudaError_t launch_fold_weights(const void* Wt, int64_t N, int64_t K, int dtype, const float* g, const float* b,
                                 const float* c, void* Wt_star, float* c_star, cudaStream_t stream, int glu_half = -1);
 int64_t fold_mean_center_workspace(int64_t n_out, int64_t d_in);

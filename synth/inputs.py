@@ -71,6 +71,8 @@ def gen_activations(seed: int, M: int, K: int, mode: str = "normal", dtype: str 
     uniform   : a ~ U[-1, 1] (tiny config)
     outlier   : N(0,1) with 4 fixed channels scaled x200 (Llama massive-activation structure)
     lowenergy : each row scaled by 10^u, u ~ U[-3, 3] -> exercises eps (App. A)
+    shifted   : N(0,1) plus a per-row offset ~ U[-3, 3]: LayerNorm inputs with non-zero means
+                (the deferred LayerNorm without a foldable V, reading c29)
     """
     g = rng(seed, TENSOR_IDS[name])
     if mode == "uniform":
@@ -83,6 +85,9 @@ def gen_activations(seed: int, M: int, K: int, mode: str = "normal", dtype: str 
         elif mode == "lowenergy":
             u = rng(seed, 200 + TENSOR_IDS[name]).uniform(-3.0, 3.0, size=(M, 1))
             x = (x * np.power(10.0, u)).astype(np.float32)
+        elif mode == "shifted":
+            off = rng(seed, 300 + TENSOR_IDS[name]).uniform(-3.0, 3.0, size=(M, 1))
+            x = (x + off).astype(np.float32)
         elif mode != "normal":
             raise ValueError(mode)
     return _finish(x, dtype)

@@ -127,6 +127,20 @@ def test_fold_validation_codes(L):
     assert g(P(0x1000), 8, 12, 0, None, P(0x2000), None, P(0x3000), None) == 4
 
 
+def test_layernorm_exact_validation_codes(L):
+    cs = L.flashnorm_fold_colsum
+    assert cs(P(0x1000), 8, 64, 0, None, None) == 1                                   # no u
+    assert cs(P(0x1000), 0, 64, 0, P(0x2000), None) == 2
+    assert cs(P(0x1000), 8, 60, 0, P(0x2000), None) == 4                              # K % 8
+    assert cs(P(0x1000), 8, 64, 5, P(0x2000), None) == 3                              # dtype
+    ln = L.flashnorm_layernorm_linear
+    assert ln(P(0x1000), P(0x2000), None, None, 4, 64, 64, 1e-5, 0, P(0x3000), None) == 1   # no u
+    assert ln(P(0x1000), P(0x2000), P(0x4000), None, 4, 60, 64, 1e-5, 0, P(0x3000), None) == 4
+    assert ln(P(0x1000), P(0x2000), P(0x4000), None, 4, 64, 64, -1.0, 0, P(0x3000), None) == 5  # eps < 0
+    assert ln(P(0x1000), P(0x2000), P(0x4004), None, 4, 64, 64, 1e-5, 0, P(0x3000), None) == 4  # u align
+    assert ln(P(0x1000), P(0x2000), P(0x4000), None, 0, 64, 64, 1e-5, 0, P(0x3000), None) == 0  # M = 0
+
+
 def test_python_binding_refuses_cpu_tensors():
     import torch
     a = torch.zeros(4, 64, dtype=torch.bfloat16)
