@@ -356,7 +356,9 @@ def measure_secondary(args, fn, torch, dev, stream, peaks, a, Ws, cs, g):
         torch.cuda.synchronize(dev)
         return s.elapsed_time(e) / steps
 
-    # decode: rotate 4 W* buffers (4 x 50 MB > L2) so every call streams from HBM
+    # decode: rotate 4 W* buffers (4 x 50 MB > L2) so every call streams from HBM.  The decode
+    # chain is latency-bound, so let the SM clock recover from the prefill's power cap first
+    time.sleep(1.0)
     Wd = []
     for r in range(4):
         w, gd, _, _ = SD.layer(100 + r, DECODE_N, DECODE_K, dev, torch.bfloat16)

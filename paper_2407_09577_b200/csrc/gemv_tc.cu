@@ -757,7 +757,8 @@ DtcPlan dtc_plan(int mode, int K, int N, int num_sms) {
     }();
     const int smax = std::max(1, std::min(std::min(cap / tiles, std::min(MAX_S, s_env)), nkb));
     int fit = 1;
-    for (int c = smax; c > 1; --c)
+    static const int force_global = env_int("FN_DECODE_GLOBAL", 0);  // A/B knob: global-memory split-K reduction
+    for (int c = smax; c > 1 && !force_global; --c)
       if (cluster_fits(mode, R, c, tiles)) { fit = c; break; }
     DtcPlan p{R, fit, fit > 1 ? 1 : 0};
     if (fit == 1 && smax > 1) p = DtcPlan{R, smax, 0};  // no cluster fits: global-memory reduction
