@@ -20,6 +20,8 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <cstdlib>
+
 #include <algorithm>
 
 namespace fn {
@@ -27,7 +29,7 @@ namespace fn {
 namespace fold {
 constexpr int WARPS_PER_CTA = 8;  // K1
 constexpr int ROWS_PER_WARP = 2;  // K1: rows sharing one g/b chunk load
-constexpr int CHUNK_UNROLL = 4;   // K1: chunks per lane in flight
+constexpr int CHUNK_UNROLL = 2;   // K1: chunks per lane in flight (x ROWS_PER_WARP loads, 3 CTAs/SM)
 constexpr int COLSUM_ROWS = 32;  // rows per fp64 partial in K2 (contract constant)
 constexpr int BPREV_THREADS = 256;
 constexpr int K2_THREADS = 256;               // K2 passes 1/2: one 4-byte column group per thread
@@ -136,8 +138,8 @@ FN_DEVICE float chunk_elem(const uint4& v, int e) {
   return __uint_as_float(w[e]);
 }
 
-template <int DT, bool HAS_G, bool HAS_B>
-__global__ void __launch_bounds__(fold::WARPS_PER_CTA * 32)
+template <int DT, bool HAS_G, bool HAS_B, int RPW = fold::ROWS_PER_WARP, int U = fold::CHUNK_UNROLL, int MINB = 1>
+__global__ void __launch_bounds__(fold::WARPS_PER_CTA * 32, MINB)
     fold_weights_kernel(const uint8_t* __restrict__ Wt, int64_t N, int64_t K, const float* __restrict__ g,
                         const float* __restrict__ b, const float* __restrict__ c, uint8_t* __restrict__ Wt_star,
                         float* __restrict__ c_star, int glu_half) {
@@ -146,7 +148,6 @@ __global__ void __launch_bounds__(fold::WARPS_PER_CTA * 32)
   // every row keeps the contract order (lane l: its chunks ascending, then butterfly).
   constexpr int E = DT == 0 ? 8 : 4;       // elements per 16-byte chunk
   constexpr int ES = DT == 0 ? 2 : 4;      // element size
-  constexpr int RPW = fold::ROWS_PER_WARP;
   const int lane = threadIdx.x & 31;
   const int64_t j0 = ((int64_t)blockIdx.x * fold::WARPS_PER_CTA + (threadIdx.x >> 5)) * RPW;
   if (j0 >= N) return;
@@ -154,7 +155,6 @@ __global__ void __launch_bounds__(fold::WARPS_PER_CTA * 32)
   double acc[RPW];
 #pragma unroll
   for (int r = 0; r < RPW; ++r) acc[r] = 0.0;
-  constexpr int U = fold::CHUNK_UNROLL;
   for (int64_t q0 = lane; q0 < nchunks; q0 += 32 * U) {
    uint4 vv[U][RPW];
 #pragma unroll
@@ -252,15 +252,36 @@ __global__ void __launch_bounds__(fold::WARPS_PER_CTA * 32)
   }
 }
 
+template <int DT, bool G, bool B, int RPW, int U, int MINB>
+static void fold_launch_v(const uint8_t* src, int64_t N, int64_t K, const float* g, const float* b, const float* c,
+                          uint8_t* dst, float* c_star, cudaStream_t stream, int glu_half) {
+  const int64_t rows_per_cta = fold::WARPS_PER_CTA * RPW;
+  const dim3 grid((unsigned)((N + rows_per_cta - 1) / rows_per_cta));
+  fold_weights_kernel<DT, G, B, RPW, U, MINB><<<grid, fold::WARPS_PER_CTA * 32, 0, stream>>>(src, N, K, g, b, c, dst,
+                                                                                          c_star, glu_half);
+}
+// variants (rows per warp, chunks in flight per lane, min CTAs per SM): the c* contract order does
+// not depend on them.  A/B knob FN_FOLD_VARIANT; default = the measured best.
+template <int DT, bool G, bool B>
+static void fold_launch(int variant, const uint8_t* src, int64_t N, int64_t K, const float* g, const float* b,
+                        const float* c, uint8_t* dst, float* c_star, cudaStream_t stream, int glu_half) {
+  // measured (tools/bench_folds.py, config-3 W with g, b, c): (2 rows, 2 chunks, 3 CTAs/SM) 97 us;
+  // (2, 4, 1) 103 us (122 registers, 2 CTAs/SM); (1, 4, 3) 103; (2, 1, 4) 121; (1, 8, 2) 112
+  if (variant == 1) fold_launch_v<DT, G, B, 2, 4, 1>(src, N, K, g, b, c, dst, c_star, stream, glu_half);
+  else fold_launch_v<DT, G, B, fold::ROWS_PER_WARP, fold::CHUNK_UNROLL, 3>(src, N, K, g, b, c, dst, c_star, stream,
+                                                                           glu_half);
+}
+
 cudaError_t launch_fold_weights(const void* Wt, int64_t N, int64_t K, int dtype, const float* g, const float* b,
                                 const float* c, void* Wt_star, float* c_star, cudaStream_t stream, int glu_half) {
-  const int64_t rows_per_cta = fold::WARPS_PER_CTA * fold::ROWS_PER_WARP;
-  const dim3 grid((unsigned)((N + rows_per_cta - 1) / rows_per_cta));
-  const dim3 block(fold::WARPS_PER_CTA * 32);
+  static const int variant = [] {
+    const char* e = getenv("FN_FOLD_VARIANT");
+    return e != nullptr ? atoi(e) : 0;
+  }();
   const uint8_t* src = static_cast<const uint8_t*>(Wt);
   uint8_t* dst = static_cast<uint8_t*>(Wt_star);
   const bool hg = g != nullptr, hb = b != nullptr;
-#define FN_FOLD_LAUNCH(DT, G, B) fold_weights_kernel<DT, G, B><<<grid, block, 0, stream>>>(src, N, K, g, b, c, dst, c_star, glu_half)
+#define FN_FOLD_LAUNCH(DT, G, B) fold_launch<DT, G, B>(variant, src, N, K, g, b, c, dst, c_star, stream, glu_half)
   if (dtype == 0) {
     if (hg && hb) FN_FOLD_LAUNCH(0, true, true);
     else if (hg) FN_FOLD_LAUNCH(0, true, false);
