@@ -22,6 +22,7 @@ static CUtensorMap tmap(void* ptr, int rows, int cols, int box_rows) {
 int main(int argc, char** argv) {
   setvbuf(stdout, nullptr, _IONBF, 0);
   const int K = 4096, N = 6144, M = argc > 1 ? atoi(argv[1]) : 1;
+  const int MODE = argc > 3 ? atoi(argv[3]) : 0;  // fn::MODE_RMS = 0, MODE_DYT = 1
   std::vector<__nv_bfloat16*> W(4);
   for (auto& w : W) { cudaMalloc(&w, (size_t)K * N * 2); cudaMemset(w, 0, (size_t)K * N * 2); }
   __nv_bfloat16 *a, *z; cudaMalloc(&a, K * 2 * 16); cudaMalloc(&z, N * 2 * 16); cudaMemset(a, 0, K * 32);
@@ -33,11 +34,11 @@ int main(int argc, char** argv) {
   for (int i = 0; i < 4; ++i) tw[i] = tmap(W[i], N, K, tr_rows);
   auto launch = [&](int i) {
     unsigned v = (unsigned)i; cudaMemcpyToSymbolAsync(fn::g_tc_launch, &v, 4, 0, cudaMemcpyHostToDevice, 0);
-    fn::launch_gemv_tc(tw[i % 4], ta, nullptr, z, M, K, N, 1e-5f, 0.5f, 0, 148, 0, nullptr, fn::RopeParams{nullptr, nullptr, nullptr, 0, 0, 1.f, nullptr, nullptr, 0, 0.f}, nullptr, a);
+    fn::launch_gemv_tc(tw[i % 4], ta, nullptr, z, M, K, N, 1e-5f, 0.5f, MODE, 148, 0, nullptr, fn::RopeParams{nullptr, nullptr, nullptr, 0, 0, 1.f, nullptr, nullptr, 0, 0.f}, nullptr, a);
   };
-  auto launch_plain = [&](int i) { fn::launch_gemv_tc(tw[i % 4], ta, nullptr, z, M, K, N, 1e-5f, 0.5f, 0, 148, 0, nullptr, fn::RopeParams{nullptr, nullptr, nullptr, 0, 0, 1.f, nullptr, nullptr, 0, 0.f}, nullptr, a); };
+  auto launch_plain = [&](int i) { fn::launch_gemv_tc(tw[i % 4], ta, nullptr, z, M, K, N, 1e-5f, 0.5f, MODE, 148, 0, nullptr, fn::RopeParams{nullptr, nullptr, nullptr, 0, 0, 1.f, nullptr, nullptr, 0, 0.f}, nullptr, a); };
   {
-    cudaError_t le = fn::launch_gemv_tc(tw[0], ta, nullptr, z, M, K, N, 1e-5f, 0.5f, 0, 148, 0, nullptr, fn::RopeParams{nullptr, nullptr, nullptr, 0, 0, 1.f, nullptr, nullptr, 0, 0.f}, nullptr, a);
+    cudaError_t le = fn::launch_gemv_tc(tw[0], ta, nullptr, z, M, K, N, 1e-5f, 0.5f, MODE, 148, 0, nullptr, fn::RopeParams{nullptr, nullptr, nullptr, 0, 0, 1.f, nullptr, nullptr, 0, 0.f}, nullptr, a);
     printf("launch: %s\n", cudaGetErrorString(le));
     int n = -1;
     cudaLaunchConfig_t cfg = {};
