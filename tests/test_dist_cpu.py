@@ -91,3 +91,23 @@ def test_column_parallel_world2_gloo():
     assert [r[1] for r in res] == [True, True], res
     assert [r[2] for r in res] == [True, True], res
     assert res[0][3] == (5, 24) and res[0][4] == (0, 24) and res[1][4] == (24, 48)
+
+
+def test_layernorm_exact_shards_are_row_local():
+    """The deferred LayerNorm (reading c29) column-shards like the RMS path: u = 1^T W* and c* are
+    per output column, mu / var are per token over the full K that every rank holds, so the
+    concatenated shard outputs equal the unsharded result (no collective on the data path)."""
+    from oracle import flashnorm_oracle as O
+    rng = np.random.default_rng(5)
+    M, K, N, world = 6, 64, 64, 4
+    a = rng.standard_normal((M, K)) + rng.uniform(-3, 3, (M, 1))
+    Wt = rng.standard_normal((N, K)) / np.sqrt(K)
+    g, b, c = rng.uniform(0.5, 1.5, K), rng.uniform(-0.1, 0.1, K), rng.uniform(-0.1, 0.1, N)
+    Ws, cs = O.fold_weights(Wt.T, g, b, c)
+    full = O.layernorm_deferred(a, Ws, O.column_sums(Ws), cs, 1e-5)
+    parts = []
+    for rank in range(world):
+        lo, hi = shard_bounds(N, world, rank)
+        Wl, cl = O.fold_weights(Wt[lo:hi].T, g, b, c[lo:hi])
+        parts.append(O.layernorm_deferred(a, Wl, O.column_sums(Wl), cl, 1e-5))
+    np.testing.assert_allclose(np.concatenate(parts, axis=1), full, rtol=1e-12, atol=1e-12)
