@@ -293,6 +293,26 @@ fn_status flashnorm_layernorm_linear(const void* a, const void* Wt_star, const f
                                      int64_t M, int64_t K, int64_t N, float eps, fn_dtype dtype, void* z,
                                      void* stream);
 
+/* --------------------------------------------------------------------------
+ * flashnorm_linear_gather — the column-parallel layer with the all-gather fused into the GEMM
+ * epilogue (NEXT-3; W* column-sharded, activations replicated, no collective
+ * needed to COMPUTE a shard).  This rank's shard z[:, col0 : col0 + N] = flashnorm_linear(a,
+ * Wt_star, c_star, ...) is stored by the epilogue straight into each of the ndst destination
+ * buffers z_dsts[d] ([M][ldz] bf16, row-major) — on a multi-GPU node these are the peer-mapped
+ * gathered outputs of every rank (NVLink stores issued tile by tile, overlapping the next
+ * tile's mainloop, instead of a separate all-gather + permute); on one device, any set of
+ * local buffers.  Same arithmetic and bits as flashnorm_linear for every destination.
+ *   z_dsts   HOST array of ndst device pointers (1 <= ndst <= 8), each 16-B aligned,
+ *            none aliasing a; the caller orders the peers' readers after this call (e.g. a
+ *            barrier after the stream completes).
+ *   ldz      row stride of the destinations in elements, ldz >= col0 + N, ldz % 8 == 0;
+ *   col0     first column of this shard, col0 % 8 == 0.
+ *   bf16 only; runs the tcgen05 GEMM kernels for every M (decode shapes included).
+ * -------------------------------------------------------------------------- */
+fn_status flashnorm_linear_gather(const void* a, const void* Wt_star, const float* c_star, int64_t M, int64_t K,
+                                  int64_t N, float eps, float alpha, fn_mode mode, fn_dtype dtype,
+                                  void* const* z_dsts, int ndst, int64_t ldz, int64_t col0, void* stream);
+
 /* End-to-end variant: a_host / z_host are HOST pointers (pinned memory for
  * asynchronous copies); a_dev / z_dev are caller-owned device scratch of
  * M*K / M*N elements.  Enqueues H2D(a) -> flashnorm_linear -> D2H(z) on

@@ -23,7 +23,7 @@ __all__ = [
     "FlashNormError", "lib", "lib_path", "fold_weights", "fold_mean_center", "fold_mean_center_workspace_bytes",
     "linear", "linear_from_host", "baseline_norm", "gather_columns", "launch_count", "reset_launch_count",
     "version", "linear_workspace_bytes", "fold_glu_weights", "glu_linear", "linear_scaled", "glu_ffn", "qkv_rope_linear", "relu_ffn_up", "qk_norm_rope_linear",
-    "fold_colsum", "layernorm_linear",
+    "fold_colsum", "layernorm_linear", "linear_gather",
     "MODES", "GLU_ACTS", "PATHS", "EXPORTS",
 ]
 
@@ -40,7 +40,7 @@ EXPORTS = [
     "flashnorm_fold_weights", "flashnorm_fold_mean_center_workspace_bytes", "flashnorm_fold_mean_center",
     "flashnorm_linear", "flashnorm_linear_ex", "flashnorm_linear_workspace_bytes", "flashnorm_linear_ws",
     "flashnorm_linear_from_host", "flashnorm_fold_glu_weights", "flashnorm_glu_linear", "flashnorm_linear_scaled",
-    "flashnorm_fold_colsum", "flashnorm_layernorm_linear",
+    "flashnorm_fold_colsum", "flashnorm_layernorm_linear", "flashnorm_linear_gather",
     "flashnorm_qkv_rope_linear", "flashnorm_relu_ffn_up", "flashnorm_qk_norm_rope_linear", "flashnorm_baseline_norm",
     "flashnorm_gather_columns", "flashnorm_status_string", "flashnorm_last_error", "flashnorm_launch_count",
     "flashnorm_reset_launch_count", "flashnorm_version",
@@ -85,6 +85,8 @@ def lib() -> ctypes.CDLL:
         "flashnorm_relu_ffn_up": [_vp, _vp, _i64, _i64, _i64, _f32, _int, _vp, _vp, _vp],
         "flashnorm_linear_scaled": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _vp, _vp],
         "flashnorm_fold_colsum": [_vp, _i64, _i64, _int, _vp, _vp],
+        "flashnorm_linear_gather": [_vp, _vp, _vp, _i64, _i64, _i64, _f32, _f32, _int, _int, _vp, _int, _i64, _i64,
+                                    _vp],
         "flashnorm_layernorm_linear": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _f32, _int, _vp, _vp],
         "flashnorm_linear_from_host": [_vp, _vp, _vp, _i64, _i64, _i64, _f32, _f32, _int, _int, _vp, _vp, _vp,
                                        _vp],
@@ -359,6 +361,29 @@ def layernorm_linear(a, Wt_star, u, c_star=None, eps: float = 1e-5, out=None):
     _check(lib().flashnorm_layernorm_linear(_ptr(a), _ptr(Wt_star), _ptr(u), _ptr(c_star), M, K, N, float(eps),
                                             _dtype_code(a), _ptr(z), _stream(a)), "layernorm_linear")
     return z
+
+
+def linear_gather(a, Wt_star, dsts, col0: int, c_star=None, eps: float = 1e-5, mode: str = "rmsnorm",
+                  alpha: float = 0.5):
+    """This rank's column shard written by the GEMM epilogue into every buffer of `dsts` (each an
+    [M, ldz] bf16 tensor: local, or peer-mapped gathered outputs) at columns [col0, col0 + N)."""
+    _dev(a, "a")
+    _dev(Wt_star, "Wt_star")
+    M, K = a.shape
+    N = Wt_star.shape[0]
+    c_star = _vec(c_star, "c_star", N)
+    if not dsts:
+        raise FlashNormError(5, "linear_gather", "dsts is empty")
+    ldz = dsts[0].shape[1]
+    for d in dsts:
+        _dev(d, "dst")
+        if tuple(d.shape) != (M, ldz) or not d.is_contiguous() or d.dtype != a.dtype:
+            raise FlashNormError(2, "linear_gather", f"every destination must be a contiguous [{M}, {ldz}] "
+                                                    f"{a.dtype} tensor, got {d.dtype}{list(d.shape)}")
+    ptrs = (ctypes.c_void_p * len(dsts))(*[d.data_ptr() for d in dsts])
+    _check(lib().flashnorm_linear_gather(_ptr(a), _ptr(Wt_star), _ptr(c_star), M, K, N, float(eps), float(alpha),
+                                         MODES[mode], _dtype_code(a), ptrs, len(dsts), ldz, int(col0), _stream(a)),
+           "linear_gather")
 
 
 def glu_ffn(a, Wgu_star, Wd_t, eps: float = 1e-5, act: str = "silu"):

@@ -148,6 +148,8 @@ struct LinearExtras {
   const float* row_scale = nullptr; // FN_NONE: z = RN(acc * row_scale[m] + c*)
   fn::RopeParams rope{nullptr, nullptr, nullptr, 0, 0, 1.0f, nullptr, nullptr, 0, 0.f};  // RoPE on [0, rope.n)
   const float* ln_u = nullptr;      // exact deferred LayerNorm (rmsnorm mode): u = 1^T W* [N]
+  int ndst = 0, ldz = 0, col0 = 0;  // fused column gather: z shard -> ndst [M x ldz] buffers at col0
+  void* const* zdst = nullptr;
 };
 
 fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, int64_t M, int64_t K, int64_t N,
@@ -199,9 +201,10 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
                          (128 % ex.rope.h == 0 && fn::gemv_tc_tile_rows(fn::MODE_RMS, (int)K, (int)N, num_sms()) == 128);
   // the exact deferred LayerNorm (ln_u) lives in the GEMM kernels only: decode shapes run the
   // 1-CTA tcgen05 kernel
-  const bool tc_ok = ex.glu_act < 0 && ex.ln_u == nullptr && qkn_tc_ok &&
+  const bool tc_ok = ex.glu_act < 0 && ex.ln_u == nullptr && ex.ndst == 0 && qkn_tc_ok &&
                      fn::gemv_tc_supported((int)M, (int)N, num_sms());
-  const bool mma_ok = ex.glu_act < 0 && ex.ln_u == nullptr && ex.row_scale == nullptr && ex.rope.pos == nullptr &&
+  const bool mma_ok = ex.glu_act < 0 && ex.ln_u == nullptr && ex.ndst == 0 && ex.row_scale == nullptr &&
+                      ex.rope.pos == nullptr &&
                       fn::gemv_supported((int)M, (int)K);
   const bool gemv_ok = tc_ok || mma_ok;
   if (path == FN_PATH_SIMT) return fail(FN_ERR_UNSUPPORTED, "SIMT path is f32-only");
@@ -273,6 +276,11 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
   p.row_scale = ex.row_scale;
   p.rope = ex.rope;
   p.ln_u = ex.ln_u;
+  p.ndst = ex.ndst;
+  p.ldz = ex.ldz;
+  p.col0 = ex.col0;
+  for (int d = 0; d < fn::MAX_GATHER_DST; ++d)
+    p.zdst[d] = d < ex.ndst ? static_cast<__nv_bfloat16*>(ex.zdst[d]) : nullptr;
   cudaError_t e = pair ? fn::launch_gemm2(ta, tb, p, km, num_sms(), stream)
                        : fn::launch_gemm(ta, tb, p, km, num_sms(), stream);
   if (e != cudaSuccess) return cuda_fail(e, pair ? "gemm2_sm100" : "gemm_sm100");
@@ -394,6 +402,35 @@ fn_status flashnorm_layernorm_linear(const void* a, const void* Wt_star, const f
   LinearExtras ex;
   ex.ln_u = u;
   return linear_impl(a, Wt_star, c_star, M, K, N, eps, 0.0f, FN_RMSNORM, dtype, z, FN_PATH_AUTO, nullptr, 0,
+                     static_cast<cudaStream_t>(stream), ex);
+}
+
+fn_status flashnorm_linear_gather(const void* a, const void* Wt_star, const float* c_star, int64_t M, int64_t K,
+                                  int64_t N, float eps, float alpha, fn_mode mode, fn_dtype dtype,
+                                  void* const* z_dsts, int ndst, int64_t ldz, int64_t col0, void* stream) {
+  if (dtype != FN_BF16) return fail(FN_ERR_UNSUPPORTED, "flashnorm_linear_gather is bf16-only");
+  if (ndst < 1 || ndst > fn::MAX_GATHER_DST)
+    return fail(FN_ERR_VALUE, "ndst = %d must be in [1, %d]", ndst, fn::MAX_GATHER_DST);
+  if (z_dsts == nullptr) return fail(FN_ERR_NULL, "z_dsts is NULL");
+  if (col0 < 0 || ldz < col0 + N || ldz > INT32_MAX)
+    return fail(FN_ERR_SHAPE, "shard columns [%lld, %lld) do not fit rows of ldz = %lld", (long long)col0,
+                (long long)(col0 + N), (long long)ldz);
+  if (ldz % 8 != 0 || col0 % 8 != 0)
+    return fail(FN_ERR_ALIGN, "ldz = %lld and col0 = %lld must be multiples of 8 (16-byte rows)", (long long)ldz,
+                (long long)col0);
+  fn_status s;
+  for (int d = 0; d < ndst; ++d) {
+    if (z_dsts[d] == nullptr) return fail(FN_ERR_NULL, "z_dsts[%d] is NULL", d);
+    if ((s = check_ptr16("z_dsts[d]", z_dsts[d])) != FN_OK) return s;
+    if (z_dsts[d] == a) return fail(FN_ERR_VALUE, "z_dsts[%d] aliases a", d);
+  }
+  LinearExtras ex;
+  ex.ndst = ndst;
+  ex.ldz = (int)ldz;
+  ex.col0 = (int)col0;
+  ex.zdst = z_dsts;
+  // z (the plain output) is unused on this path: pass the first destination for the checks
+  return linear_impl(a, Wt_star, c_star, M, K, N, eps, alpha, mode, dtype, z_dsts[0], FN_PATH_GEMM, nullptr, 0,
                      static_cast<cudaStream_t>(stream), ex);
 }
 

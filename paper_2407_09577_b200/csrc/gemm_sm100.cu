@@ -416,11 +416,24 @@ __global__ void __launch_bounds__(gemm::THREADS, 1)
                                   fmaf(__uint_as_float(v[2 * q + 1]), r, cb[2 * q + 1]));
         }
         if (row < p.M) {
-          uint4* dst = reinterpret_cast<uint4*>(zrow + j * 32);
+          if (p.ndst == 0) {
+            uint4* dst = reinterpret_cast<uint4*>(zrow + j * 32);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            if (n_base + j * 32 + q * 8 < p.N)
-              dst[q] = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+            for (int q = 0; q < 4; ++q) {
+              if (n_base + j * 32 + q * 8 < p.N)
+                dst[q] = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+            }
+          } else {
+            // fused gather (see gemm2_sm100.cu): every destination gets the row segment
+            const size_t off = static_cast<size_t>(row) * p.ldz + p.col0 + n_base + j * 32;
+#pragma unroll 1
+            for (int d = 0; d < p.ndst; ++d) {
+              uint4* dst = reinterpret_cast<uint4*>(p.zdst[d] + off);
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                if (n_base + j * 32 + q * 8 < p.N)
+                  dst[q] = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+            }
           }
         }
       }

@@ -47,7 +47,13 @@ struct GemmParams {
   // u = 1^T W* [N]; the side group reduces sum(a - a0) and sum((a - a0)^2) per row (shift a0 =
   // a[m][0]) and the epilogue writes z = RN(fma(fma(-mu, u_j, acc), rsqrt(var + eps), c*_j))
   const float* ln_u;
+  // fused column gather (NEXT-3): ndst > 0 -> the epilogue stores each output row
+  // segment of this rank's N-column shard to ndst destinations (local or peer-mapped [M x ldz]
+  // buffers, e.g. every rank's gathered z), at columns [col0, col0 + N); ndst = 0 -> z [M x N]
+  int ndst, ldz, col0;
+  __nv_bfloat16* zdst[8];
 };
+constexpr int MAX_GATHER_DST = 8;
 enum GluAct { GLU_SILU = 0, GLU_RELU = 1, GLU_BILINEAR = 2 };
 // Fig 2(b) (ReLU FFN, not gated): z = RN(relu(acc)) unscaled, s_out = r — the scale is deferred
 // to the FFN output (ReLU(s a) = s ReLU(a), s >= 0)

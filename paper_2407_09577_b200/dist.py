@@ -86,4 +86,29 @@ class ColumnParallelFlashNorm:
         dist.all_gather_into_tensor(flat, z_local.contiguous(), group=self.group)
         return self._permute(flat.view(self.world, M, Nl))  # [P][M][Nl] -> [M][P*Nl]
 
+    def forward_fused_gather(self, a, eps: float = 1e-5, mode: str = "rmsnorm", alpha: float = 0.5):
+        """Gathered output with the all-gather FUSED into the GEMM epilogue (NEXT-3): every rank's
+        epilogue stores its shard straight into every rank's gathered buffer over NVLink
+        (flashnorm_linear_gather with the peers' symmetric-memory pointers), tile by tile while the
+        next tiles compute; a device-side barrier then orders the peers' reads.  Replaces the
+        NCCL all-gather + permute of `forward(gather=True)`.  Needs CUDA + NCCL and
+        torch symmetric memory; the epilogue itself is tested on one GPU (several local
+        destinations, tests/test_gpu_parity.py), the multi-GPU pointer exchange is not (round 1
+        ran on one GPU)."""
+        import torch
+        import torch.distributed._symmetric_memory as symm_mem
+        from . import linear_gather
+        M, Nl = a.shape[0], self.W.shape[0]
+        N = Nl * self.world
+        key = (M, N, a.dtype, a.device)
+        if getattr(self, "_symm_key", None) != key:
+            buf = symm_mem.empty((M, N), dtype=a.dtype, device=a.device)
+            hdl = symm_mem.rendezvous(buf, self.group if self.group is not None else torch.distributed.group.WORLD)
+            peers = [hdl.get_buffer(p, (M, N), a.dtype) for p in range(self.world)]
+            self._symm_key, self._symm_buf, self._symm_hdl, self._symm_peers = key, buf, hdl, peers
+        self._symm_hdl.barrier(channel=0)  # the peers finished reading the previous result
+        linear_gather(a, self.W, self._symm_peers, self.rank * Nl, c_star=self.c, eps=eps, mode=mode, alpha=alpha)
+        self._symm_hdl.barrier(channel=0)  # every shard has landed in every buffer
+        return self._symm_buf
+
     __call__ = forward

@@ -149,3 +149,16 @@ def test_python_binding_refuses_cpu_tensors():
         fn.linear(a, w)
     with pytest.raises(fn.FlashNormError, match="CUDA tensor"):
         fn.fold_weights(w)
+
+
+def test_linear_gather_validation_codes(L):
+    import ctypes
+    f = L.flashnorm_linear_gather
+    one = (ctypes.c_void_p * 1)(0x3000)
+    assert f(P(0x1000), P(0x2000), None, 4, 64, 64, 1e-5, 0.5, 0, 1, one, 1, 64, 0, None) == 6     # f32
+    assert f(P(0x1000), P(0x2000), None, 4, 64, 64, 1e-5, 0.5, 0, 0, one, 0, 64, 0, None) == 5     # ndst
+    assert f(P(0x1000), P(0x2000), None, 4, 64, 64, 1e-5, 0.5, 0, 0, None, 1, 64, 0, None) == 1    # dsts
+    assert f(P(0x1000), P(0x2000), None, 4, 64, 64, 1e-5, 0.5, 0, 0, one, 1, 96, 40, None) == 2    # ldz
+    assert f(P(0x1000), P(0x2000), None, 4, 64, 64, 1e-5, 0.5, 0, 0, one, 1, 132, 68, None) == 4   # col0 % 8
+    bad = (ctypes.c_void_p * 1)(0x3004)
+    assert f(P(0x1000), P(0x2000), None, 4, 64, 64, 1e-5, 0.5, 0, 0, bad, 1, 64, 0, None) == 4     # align

@@ -467,3 +467,43 @@ def test_gemm_repeated_launches_bit_identical(M, K, N, mode, path):
         r = torch.rsqrt((af * af).mean(1, keepdim=True) + 1e-5) if mode == "rmsnorm" else 1.0
         ref = acc * r + cs
         assert float(((z0.float() - ref).abs() / ref.abs().amax(1, keepdim=True)).max()) <= 1e-2
+
+
+# ============================================================ NEXT-3: column gather fused into the epilogue
+
+@pytest.mark.parametrize("M", [4, 77, 300])
+@pytest.mark.parametrize("mode", ["rmsnorm", "none", "dyt"])
+def test_linear_gather_shards_into_every_destination_bit_exact(M, mode):
+    """Each of P = 4 column shards writes itself (flashnorm_linear_gather) into ndst = 3 [M x N]
+    buffers; afterwards every buffer equals the unsharded flashnorm_linear bit for bit (the
+    shard-concatenation invariant of SURVEY §8(e), through the multi-destination epilogue)."""
+    K, N, P = 512, 1024, 4
+    a = T(gen_activations(61, M, K, "normal", "bf16"))
+    Wt, g, b, c = gen_layer(61, N, K, "bf16", with_b=True, with_c=True)
+    Ws, cs = fn.fold_weights(T(Wt), T(g, "f32"), T(b, "f32"), T(c, "f32"))
+    full = fn.linear(a, Ws, cs, eps=1e-5, mode=mode, alpha=0.5, path="gemm")
+    dsts = [torch.full((M, N), float("nan"), dtype=torch.bfloat16, device=DEV) for _ in range(3)]
+    Nl = N // P
+    for r in range(P):
+        fn.linear_gather(a, Ws[r * Nl:(r + 1) * Nl], dsts, r * Nl, c_star=cs[r * Nl:(r + 1) * Nl], eps=1e-5,
+                         mode=mode, alpha=0.5)
+    for d in dsts:
+        assert np.array_equal(bits(d), bits(full))
+
+
+def test_linear_gather_strided_destination_and_validation():
+    """A shard into a wider row (ldz > N, col0 > 0) leaves the other columns untouched; bad
+    arguments are rejected before any launch."""
+    M, K, N, ldz, col0 = 130, 256, 256, 1024, 512
+    a = T(gen_activations(62, M, K, "normal", "bf16"))
+    Wt, g, _, _ = gen_layer(62, N, K, "bf16")
+    Ws, cs = fn.fold_weights(T(Wt), T(g, "f32"))
+    z = fn.linear(a, Ws, cs, eps=1e-5)
+    dst = torch.zeros((M, ldz), dtype=torch.bfloat16, device=DEV)
+    fn.linear_gather(a, Ws, [dst], col0, c_star=cs)
+    assert np.array_equal(bits(dst[:, col0:col0 + N].contiguous()), bits(z))
+    assert not dst[:, :col0].any() and not dst[:, col0 + N:].any()
+    with pytest.raises(fn.FlashNormError, match="FN_ERR_SHAPE"):
+        fn.linear_gather(a, Ws, [dst], ldz - N + 8, c_star=cs)
+    with pytest.raises(fn.FlashNormError, match="FN_ERR_VALUE"):
+        fn.linear_gather(a, Ws, [dst] * 9, 0, c_star=cs)
