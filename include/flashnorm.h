@@ -315,9 +315,14 @@ fn_status flashnorm_linear_gather(const void* a, const void* Wt_star, const floa
 
 /* End-to-end variant: a_host / z_host are HOST pointers (pinned memory for
  * asynchronous copies); a_dev / z_dev are caller-owned device scratch of
- * M*K / M*N elements.  Enqueues H2D(a) -> flashnorm_linear -> D2H(z) on
- * `stream` and returns without synchronizing (the caller synchronizes the
- * stream before reading z_host). */
+ * M*K / M*N elements.  Enqueues H2D(a) -> flashnorm_linear -> D2H(z) and
+ * returns without synchronizing (the caller synchronizes `stream` before
+ * reading z_host).  For M >= 1024 the rows are pipelined in ~8 chunks over
+ * two library-owned copy streams (per device) joined to `stream` by events:
+ * H2D of chunk c+1 || the linear of chunk c on `stream` || D2H of chunk c-1.
+ * Rows are independent, so z is identical to the unchunked call.  All work
+ * of the call is ordered after earlier work on `stream` and before later
+ * work on it. */
 fn_status flashnorm_linear_from_host(const void* a_host, const void* Wt_star, const float* c_star,
                                      int64_t M, int64_t K, int64_t N, float eps, float alpha,
                                      fn_mode mode, fn_dtype dtype, void* a_dev, void* z_dev,

@@ -17,6 +17,7 @@
 
 #include "../../include/flashnorm.h"
 #include "kernels.h"
+#include <algorithm>
 
 namespace {
 
@@ -550,6 +551,38 @@ fn_status flashnorm_glu_linear(const void* a, const void* Wgu_star, int64_t M, i
                      static_cast<cudaStream_t>(stream), ex);
 }
 
+namespace {
+// copy streams + events of the end-to-end entry, one set per device (created once)
+struct E2EPipe {
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t start = nullptr, done = nullptr;
+  cudaEvent_t h[16] = {}, g[16] = {};
+};
+std::mutex g_e2e_mu;
+std::map<int, E2EPipe> g_e2e;
+cudaError_t e2e_pipe(E2EPipe** out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(g_e2e_mu);
+  auto it = g_e2e.find(dev);
+  if (it == g_e2e.end()) {
+    E2EPipe p;
+    if ((e = cudaStreamCreateWithFlags(&p.h2d, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    if ((e = cudaStreamCreateWithFlags(&p.d2h, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&p.start, cudaEventDisableTiming)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&p.done, cudaEventDisableTiming)) != cudaSuccess) return e;
+    for (int c = 0; c < 16; ++c) {
+      if ((e = cudaEventCreateWithFlags(&p.h[c], cudaEventDisableTiming)) != cudaSuccess) return e;
+      if ((e = cudaEventCreateWithFlags(&p.g[c], cudaEventDisableTiming)) != cudaSuccess) return e;
+    }
+    it = g_e2e.emplace(dev, p).first;
+  }
+  *out = &it->second;
+  return cudaSuccess;
+}
+}  // namespace
+
 fn_status flashnorm_linear_from_host(const void* a_host, const void* Wt_star, const float* c_star, int64_t M,
                                      int64_t K, int64_t N, float eps, float alpha, fn_mode mode, fn_dtype dtype,
                                      void* a_dev, void* z_dev, void* z_host, void* stream) {
@@ -560,13 +593,54 @@ fn_status flashnorm_linear_from_host(const void* a_host, const void* Wt_star, co
   if (M < 0 || K <= 0 || N <= 0) return fail(FN_ERR_SHAPE, "M=%lld K=%lld N=%lld", (long long)M, (long long)K, (long long)N);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t eb = (size_t)elem_bytes(dtype);
-  cudaError_t e = cudaMemcpyAsync(a_dev, a_host, (size_t)M * K * eb, cudaMemcpyHostToDevice, st);
-  if (e != cudaSuccess) return cuda_fail(e, "H2D a");
-  if ((s = linear_impl(a_dev, Wt_star, c_star, M, K, N, eps, alpha, mode, dtype, z_dev, FN_PATH_AUTO, nullptr, 0,
-                       st)) != FN_OK)
-    return s;
-  e = cudaMemcpyAsync(z_host, z_dev, (size_t)M * N * eb, cudaMemcpyDeviceToHost, st);
-  if (e != cudaSuccess) return cuda_fail(e, "D2H z");
+  // Row chunks pipelined over three engines: H2D of chunk c+1 (copy stream) || the FlashNorm
+  // linear of chunk c (the caller's stream) || D2H of chunk c-1 (second copy stream).  Rows are
+  // independent (RMS is per token), so chunking changes nothing in z.  Decode-sized calls and
+  // tiny problems take one chunk.
+  int64_t MC = M;
+  if (M >= 1024) MC = ((M / 8 + 255) / 256) * 256;  // ~8 chunks of a multiple of 256 rows
+  const int nc = (int)((M + MC - 1) / MC);
+  if (nc <= 1) {
+    cudaError_t e = cudaMemcpyAsync(a_dev, a_host, (size_t)M * K * eb, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(e, "H2D a");
+    if ((s = linear_impl(a_dev, Wt_star, c_star, M, K, N, eps, alpha, mode, dtype, z_dev, FN_PATH_AUTO, nullptr, 0,
+                         st)) != FN_OK)
+      return s;
+    e = cudaMemcpyAsync(z_host, z_dev, (size_t)M * N * eb, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return cuda_fail(e, "D2H z");
+    return FN_OK;
+  }
+  E2EPipe* pp = nullptr;
+  cudaError_t e = e2e_pipe(&pp);
+  if (e != cudaSuccess) return cuda_fail(e, "e2e streams");
+  // everything earlier on the caller's stream (e.g. the previous call reading a_dev / z_dev)
+  // precedes this call's copies
+  if ((e = cudaEventRecord(pp->start, st)) != cudaSuccess) return cuda_fail(e, "event");
+  if ((e = cudaStreamWaitEvent(pp->h2d, pp->start, 0)) != cudaSuccess) return cuda_fail(e, "event wait");
+  if ((e = cudaStreamWaitEvent(pp->d2h, pp->start, 0)) != cudaSuccess) return cuda_fail(e, "event wait");
+  const uint8_t* ah = static_cast<const uint8_t*>(a_host);
+  uint8_t* ad = static_cast<uint8_t*>(a_dev);
+  uint8_t* zd = static_cast<uint8_t*>(z_dev);
+  uint8_t* zh = static_cast<uint8_t*>(z_host);
+  for (int c = 0; c < nc; ++c) {
+    const int64_t r0 = c * MC, mc = std::min(MC, M - r0);
+    if ((e = cudaMemcpyAsync(ad + r0 * K * eb, ah + r0 * K * eb, (size_t)(mc * K) * eb, cudaMemcpyHostToDevice,
+                             pp->h2d)) != cudaSuccess)
+      return cuda_fail(e, "H2D a");
+    if ((e = cudaEventRecord(pp->h[c], pp->h2d)) != cudaSuccess) return cuda_fail(e, "event");
+    if ((e = cudaStreamWaitEvent(st, pp->h[c], 0)) != cudaSuccess) return cuda_fail(e, "event wait");
+    if ((s = linear_impl(ad + r0 * K * eb, Wt_star, c_star, mc, K, N, eps, alpha, mode, dtype, zd + r0 * N * eb,
+                         FN_PATH_AUTO, nullptr, 0, st)) != FN_OK)
+      return s;
+    if ((e = cudaEventRecord(pp->g[c], st)) != cudaSuccess) return cuda_fail(e, "event");
+    if ((e = cudaStreamWaitEvent(pp->d2h, pp->g[c], 0)) != cudaSuccess) return cuda_fail(e, "event wait");
+    if ((e = cudaMemcpyAsync(zh + r0 * N * eb, zd + r0 * N * eb, (size_t)(mc * N) * eb, cudaMemcpyDeviceToHost,
+                             pp->d2h)) != cudaSuccess)
+      return cuda_fail(e, "D2H z");
+  }
+  // the caller's stream completes only after the last copy
+  if ((e = cudaEventRecord(pp->done, pp->d2h)) != cudaSuccess) return cuda_fail(e, "event");
+  if ((e = cudaStreamWaitEvent(st, pp->done, 0)) != cudaSuccess) return cuda_fail(e, "event wait");
   return FN_OK;
 }
 

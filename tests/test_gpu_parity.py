@@ -507,3 +507,22 @@ def test_linear_gather_strided_destination_and_validation():
         fn.linear_gather(a, Ws, [dst], ldz - N + 8, c_star=cs)
     with pytest.raises(fn.FlashNormError, match="FN_ERR_VALUE"):
         fn.linear_gather(a, Ws, [dst] * 9, 0, c_star=cs)
+
+
+@pytest.mark.parametrize("M", [8, 300, 2500])
+def test_linear_from_host_matches_device_path(M):
+    """The end-to-end entry (pinned host buffers; M >= 1024 pipelined in row chunks over copy
+    streams) returns exactly the device path's z, also when called back to back."""
+    K, N = 512, 1024
+    a = T(gen_activations(71, M, K, "normal", "bf16"))
+    Wt, g, b, c = gen_layer(71, N, K, "bf16", with_b=True, with_c=True)
+    Ws, cs = fn.fold_weights(T(Wt), T(g, "f32"), T(b, "f32"), T(c, "f32"))
+    ref = bits(fn.linear(a, Ws, cs, eps=1e-5))
+    a_host = a.cpu().pin_memory()
+    z_host = torch.empty((M, N), dtype=torch.bfloat16).pin_memory()
+    a_dev, z_dev = torch.empty_like(a), torch.empty((M, N), dtype=torch.bfloat16, device=DEV)
+    for _ in range(3):
+        z_host.zero_()
+        fn.linear_from_host(a_host, Ws, cs, a_dev, z_dev, z_host)
+        torch.cuda.current_stream().synchronize()
+        assert np.array_equal(z_host.view(torch.int16).numpy().view(np.uint16), ref)
