@@ -249,15 +249,20 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
   // CTA-pair (cta_group::2, 256x256 tiles) kernel when M > 128; the 1-CTA kernel for M <= 128
   // and FN_PATH_GEMM1.
   const bool pair = M > 128 && (path != FN_PATH_GEMM1);
+  // 224-wide pair tiles when they even out the last wave (plain / LayerNorm / scaled / gather
+  // epilogues; GLU, RoPE and QK-norm keep their 256-column tile algebra, DyT its prologue)
+  const bool allow_224 = km != fn::MODE_DYT && ex.glu_act < 0 && ex.rope.pos == nullptr;
+  const int bn = pair ? fn::gemm2_pick_bn((int)M, (int)N, num_sms(), allow_224) : 256;
   CUtensorMap ta, tb;
   if ((s = get_tmap(a, M, K, 128, &ta)) != FN_OK) return s;
-  if ((s = get_tmap(Wt_star, N, K, pair ? 128 : 256, &tb)) != FN_OK) return s;
+  if ((s = get_tmap(Wt_star, N, K, pair ? bn / 2 : 256, &tb)) != FN_OK) return s;
   fn::GemmParams p;
   p.M = (int)M;
   p.N = (int)N;
   p.K = (int)K;
   p.num_m_blocks = (int)(pair ? (M + 255) / 256 : (M + 127) / 128);
-  p.num_n_blocks = (int)((N + 255) / 256);
+  p.num_n_blocks = (int)((N + bn - 1) / bn);
+  p.bn = bn;
   p.num_tiles = p.num_m_blocks * p.num_n_blocks;
   {  // ~40 MB of A per tile group (L2 is 126 MB; W* tiles and z share it)
     const int64_t a_bytes_per_blk = (pair ? 256 : 128) * K * 2;

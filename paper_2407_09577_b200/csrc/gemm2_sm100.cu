@@ -32,6 +32,8 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <cstdlib>
+
 namespace fn {
 
 namespace gemm2 {
@@ -48,13 +50,20 @@ constexpr int BAR_BYTES = 1024;
 constexpr int SSQ_SLOTS = 16;          // per-CTA cache of reduced row ssq, by M block
 constexpr int SMEM_BYTES = 1024 + STAGES * (A_STAGE + B_STAGE) + BAR_BYTES + (4 + SSQ_SLOTS) * BM * 4 + 32 +
                              (2 + SSQ_SLOTS) * BM * 4;  // + LayerNorm mean buffers
+// the pair tile width is a template parameter: 256 (default) or 224 (picked by the host when it
+// evens out the last wave of tiles over the CTA pairs, gemm2_pick_bn); TMEM stays 2 x 256 columns
+constexpr int smem_bytes(int bn) { return SMEM_BYTES - STAGES * (B_STAGE - (bn / 2) * BK * 2); }
 }  // namespace gemm2
 
-template <int MODE>
+template <int MODE, int BN_ = gemm2::BN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
     flashnorm_gemm2_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                            GemmParams p) {
   using namespace gemm2;
+  constexpr int BN = BN_;                // pair tile columns
+  constexpr int BNH = BN / 2;            // W* rows loaded per CTA
+  constexpr int B_STAGE = BNH * BK * 2;  // 16 / 14 KiB
+  static_assert(BN % 32 == 0 && BN <= 256, "pair tile width");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
@@ -520,29 +529,61 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
 
 int gemm2_smem_bytes() { return gemm2::SMEM_BYTES; }
 
-cudaError_t launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb_half, const GemmParams& p, int mode,
-                         int num_sms, cudaStream_t stream) {
+// Pair tile width for an M x N problem: the one with the shorter makespan, counted as
+// ceil(tiles / pairs) rounds of bn columns (the last N block counted whole).  Config 3:
+// 1792 tiles of 256 = 25 rounds x 256 vs 2048 of 224 = 28 x 224 (-2 %); its 8-rank shard
+// (N = 3584): 4 x 256 vs 4 x 224 (-12 %); config 4 (2048 x 4096) keeps 256 (2 x 256 vs 3 x 224).
+int gemm2_pick_bn(int M, int N, int num_sms, bool allow_224) {
+  static const int force = [] {
+    const char* e = getenv("FN_GEMM2_BN");  // A/B knob: 256 or 224
+    return e != nullptr ? atoi(e) : 0;
+  }();
+  if (!allow_224) return 256;
+  if (force == 256 || force == 224) return force;
+  const long long pairs = num_sms / 2 > 0 ? num_sms / 2 : 1;
+  const long long mb = (M + 255) / 256;
+  auto span = [&](int bn) {
+    const long long tiles = mb * ((N + bn - 1) / bn);
+    return ((tiles + pairs - 1) / pairs) * bn;
+  };
+  return span(224) < span(256) ? 224 : 256;
+}
+
+template <int MODE, int BN>
+static cudaError_t launch_gemm2_t(const CUtensorMap& ta, const CUtensorMap& tb_half, const GemmParams& p,
+                                  int num_sms, cudaStream_t stream) {
   using namespace gemm2;
-  static bool attr_set[3] = {false, false, false};
-  const void* fptr = mode == MODE_RMS   ? (const void*)flashnorm_gemm2_kernel<MODE_RMS>
-                     : mode == MODE_DYT ? (const void*)flashnorm_gemm2_kernel<MODE_DYT>
-                                        : (const void*)flashnorm_gemm2_kernel<MODE_NONE>;
-  if (!attr_set[mode]) {
-    cudaError_t e = cudaFuncSetAttribute(fptr, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  static bool attr_set = false;
+  const void* fptr = (const void*)flashnorm_gemm2_kernel<MODE, BN>;
+  const int smem = smem_bytes(BN);
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(fptr, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    attr_set[mode] = true;
+    attr_set = true;
   }
   int pairs = num_sms / 2;
   if (p.num_tiles < pairs) pairs = p.num_tiles;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * pairs);
   cfg.blockDim = dim3(THREADS);
-  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cfg.attrs = nullptr;
   cfg.numAttrs = 0;  // cluster shape comes from __cluster_dims__
   void* args[] = {(void*)&ta, (void*)&tb_half, (void*)&p};
   return cudaLaunchKernelExC(&cfg, fptr, args);
+}
+
+cudaError_t launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb_half, const GemmParams& p, int mode,
+                         int num_sms, cudaStream_t stream) {
+  if (p.bn == 224) {
+    if (mode == MODE_RMS) return launch_gemm2_t<MODE_RMS, 224>(ta, tb_half, p, num_sms, stream);
+    if (mode == MODE_NONE) return launch_gemm2_t<MODE_NONE, 224>(ta, tb_half, p, num_sms, stream);
+    return cudaErrorInvalidValue;  // DyT, GLU and RoPE run 256-wide tiles (the host never asks)
+  }
+  if (mode == MODE_RMS) return launch_gemm2_t<MODE_RMS, 256>(ta, tb_half, p, num_sms, stream);
+  if (mode == MODE_DYT) return launch_gemm2_t<MODE_DYT, 256>(ta, tb_half, p, num_sms, stream);
+  return launch_gemm2_t<MODE_NONE, 256>(ta, tb_half, p, num_sms, stream);
 }
 
 }  // namespace fn

@@ -52,6 +52,7 @@ struct GemmParams {
   // buffers, e.g. every rank's gathered z), at columns [col0, col0 + N); ndst = 0 -> z [M x N]
   int ndst, ldz, col0;
   __nv_bfloat16* zdst[8];
+  int bn;  // pair kernel tile width (256 or 224, gemm2_pick_bn); num_n_blocks = ceil(N / bn)
 };
 constexpr int MAX_GATHER_DST = 8;
 enum GluAct { GLU_SILU = 0, GLU_RELU = 1, GLU_BILINEAR = 2 };
@@ -86,6 +87,7 @@ __host__ __device__ inline void tile_coords(int tile, const GemmParams& p, int& 
 
 // K3: tcgen05 prefill GEMM (gemm_sm100.cu)
 int gemm_smem_bytes();
+int gemm2_pick_bn(int M, int N, int num_sms, bool allow_224);
 cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int mode, int num_sms,
                         cudaStream_t stream);
 
