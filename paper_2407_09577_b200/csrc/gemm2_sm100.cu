@@ -530,9 +530,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
 int gemm2_smem_bytes() { return gemm2::SMEM_BYTES; }
 
 // Pair tile width for an M x N problem: the one with the shorter makespan, counted as
-// ceil(tiles / pairs) rounds of bn columns (the last N block counted whole).  Config 3:
-// 1792 tiles of 256 = 25 rounds x 256 vs 2048 of 224 = 28 x 224 (-2 %); its 8-rank shard
-// (N = 3584): 4 x 256 vs 4 x 224 (-12 %); config 4 (2048 x 4096) keeps 256 (2 x 256 vs 3 x 224).
+// ceil(tiles / pairs) rounds of bn columns (the last N block counted whole), 224 discounted by
+// its lower per-tile rate.  Config 3 keeps 256 (25 x 256 vs 28 x 224: 2 % shorter, not enough);
+// its 8-rank shard (N = 3584) takes 224 (4 x 256 vs 4 x 224); config 4 keeps 256.
 int gemm2_pick_bn(int M, int N, int num_sms, bool allow_224) {
   static const int force = [] {
     const char* e = getenv("FN_GEMM2_BN");  // A/B knob: 256 or 224
@@ -546,7 +546,9 @@ int gemm2_pick_bn(int M, int N, int num_sms, bool allow_224) {
     const long long tiles = mb * ((N + bn - 1) / bn);
     return ((tiles + pairs - 1) / pairs) * bn;
   };
-  return span(224) < span(256) ? 224 : 256;
+  // a 224-wide tile runs ~2.5 % below a 256-wide one (tools/ab_bn.py: config 3 1484 vs 1478
+  // TFLOP/s although its span is 2 % shorter); 160-wide tiles measured 7-17 % slower everywhere
+  return span(224) * 40 < span(256) * 39 ? 224 : 256;
 }
 
 template <int MODE, int BN>
@@ -576,10 +578,10 @@ static cudaError_t launch_gemm2_t(const CUtensorMap& ta, const CUtensorMap& tb_h
 
 cudaError_t launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb_half, const GemmParams& p, int mode,
                          int num_sms, cudaStream_t stream) {
-  if (p.bn == 224) {
+  if (p.bn == 224) {  // DyT, GLU and RoPE run 256-wide tiles (the host never asks)
     if (mode == MODE_RMS) return launch_gemm2_t<MODE_RMS, 224>(ta, tb_half, p, num_sms, stream);
     if (mode == MODE_NONE) return launch_gemm2_t<MODE_NONE, 224>(ta, tb_half, p, num_sms, stream);
-    return cudaErrorInvalidValue;  // DyT, GLU and RoPE run 256-wide tiles (the host never asks)
+    return cudaErrorInvalidValue;
   }
   if (mode == MODE_RMS) return launch_gemm2_t<MODE_RMS, 256>(ta, tb_half, p, num_sms, stream);
   if (mode == MODE_DYT) return launch_gemm2_t<MODE_DYT, 256>(ta, tb_half, p, num_sms, stream);

@@ -25,7 +25,7 @@ def timed(f, steps=10, warm=3):
     return s.elapsed_time(e) / steps * 1e3
 
 
-shapes = [(4096, 4096, 28672), (4096, 4096, 14336), (4096, 4096, 7168), (4096, 4096, 3584), (2048, 4096, 4096),
+shapes = [(4096, 4096, 28672), (4096, 4096, 14336), (4096, 4096, 7168), (4096, 4096, 3584), (2048, 4096, 4096), (2048, 4096, 16384),
           (8192, 8192, 14336), (8192, 8192, 7168)]
 out = []
 for (M, K, N) in shapes:
