@@ -263,6 +263,11 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
   p.num_m_blocks = (int)(pair ? (M + 255) / 256 : (M + 127) / 128);
   p.num_n_blocks = (int)((N + bn - 1) / bn);
   p.bn = bn;
+  static const int rms_local = [] {
+    const char* e = getenv("FN_GEMM2_RMS_LOCAL");  // A/B knob (DESIGN.md §12 item 1)
+    return e != nullptr ? atoi(e) : 0;
+  }();
+  p.rms_local = rms_local;
   p.num_tiles = p.num_m_blocks * p.num_n_blocks;
   {  // ~40 MB of A per tile group (L2 is 126 MB; W* tiles and z share it)
     const int64_t a_bytes_per_blk = (pair ? 256 : 128) * K * 2;

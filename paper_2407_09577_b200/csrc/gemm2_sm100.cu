@@ -88,6 +88,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
   float* mu_buf = reinterpret_cast<float*>(sig_dst + 32);  // [2][BM] LayerNorm (ln_u): row means
   float* mu_cache = mu_buf + 2 * BM;                       // [SSQ_SLOTS][BM]
   const bool ln = MODE == MODE_RMS && p.ln_u != nullptr;   // exact deferred LayerNorm (reading c29)
+  // RMS with LOCAL A completion (p.rms_local): each CTA's A half lands on its own `afull`, the
+  // ssq group reads it there while the MMA runs (release `empty` = MMA commit + ssq group), and
+  // warp 3 relays "A landed" to the leader's `ready` (the peer with a 16-byte DSMEM bulk copy)
+  const bool la = MODE == MODE_RMS && p.rms_local != 0;
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -103,7 +107,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);     // RMS: ssq group;  NONE/DyT: MMA commit
+      mbar_init(&empty[s], la ? 2 : 1);  // RMS: ssq group (la: + MMA commit);  NONE/DyT: MMA commit
       mbar_init(&mma_done[s], 1);
       mbar_init(&afull[s], 1);
       mbar_init(&ready[s], 1);
@@ -140,8 +144,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           const uint32_t fb = full0 + stage * 8;
-          if (MODE == MODE_DYT) {
-            // raw A lands on a LOCAL barrier (this CTA's prologue warps transform it);
+          if (MODE == MODE_DYT || la) {
+            // raw A lands on a LOCAL barrier (DyT: this CTA's prologue warps transform it;
+            // la: the ssq group reads it and warp 3 relays its arrival to the leader);
             // B still completes on the leader's `full`
             if (leader) mbar_arrive_expect_tx(&full[stage], 2 * B_STAGE);
             mbar_arrive_expect_tx(&afull[stage], A_STAGE);
@@ -175,13 +180,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
 #pragma unroll
         for (int i = 0; i < SSQ_SLOTS; ++i)
           if (i == slot) { cached = tag[i] == m_blk; tag[i] = m_blk; }
-        uint64_t* release = (MODE == MODE_RMS && !cached) ? mma_done : empty;
+        uint64_t* release = (MODE == MODE_RMS && !cached && !la) ? mma_done : empty;
         mbar_wait(&tempty[as], aphase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + as * BN;
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&full[stage], phase);
-          if (MODE == MODE_DYT) mbar_wait(&ready[stage], phase);  // both CTAs' tanh(alpha a) written
+          if (MODE == MODE_DYT || la) mbar_wait(&ready[stage], phase);  // both CTAs' A ready (DyT: transformed)
           tc_fence_after();
           const uint64_t adesc = make_sw128_desc(smem_u32(sA + stage * A_STAGE));
           const uint64_t bdesc = make_sw128_desc(smem_u32(sB + stage * B_STAGE));
@@ -193,6 +198,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
         umma_commit_pair_mc(&tfull[as], 0x3);
       }
     }
+  } else if (warp == 3) {
+    // ------------------------------------------------------------ la relay (both CTAs)
+    if (la && elect_one()) {
+      const uint32_t ready0 = mapa_shared(&ready[0], 0);
+      const uint32_t sig0 = mapa_shared(sig_dst, 0);  // 16-byte landing slot in the leader
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&afull[stage], phase);
+          if (leader) mbar_arrive_expect_tx(&ready[stage], 16);  // + the peer's 16-byte signal
+          else dsmem_signal16(sig0, sig_src, ready0 + stage * 8);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
   } else if (warp >= 4 && warp < 8) {
     // ------------------------------------------------------------ ssq group (both CTAs)
     if (MODE == MODE_RMS) {
@@ -200,7 +221,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
       int tag[SSQ_SLOTS];
 #pragma unroll
       for (int i = 0; i < SSQ_SLOTS; ++i) tag[i] = -1;
-      uint32_t md_phase = 0;  // per-stage parity of mma_done (used only on uncached tiles)
+      uint32_t md_phase = 0;  // per-stage parity of mma_done (uncached tiles) / afull (la: every tile)
+      // the barrier that says "this stage's A may be read": mma_done (consumed by the MMA, so it
+      // has landed in both CTAs) or, with la, this CTA's own afull (landed; read beside the MMA)
+      auto wait_a = [&](int st) {
+        mbar_wait_warp(la ? &afull[st] : &mma_done[st], (md_phase >> st) & 1u);
+        md_phase ^= 1u << st;
+      };
       int stage = 0;
       int local = 0;
       for (int tile = cluster; tile < num_tiles; tile += nclusters, ++local) {
@@ -214,8 +241,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
         float ssq, mu = 0.f;
         if (cached) {
           // this CTA already reduced these 128 rows for an earlier N tile: the ring
-          // stages of this tile are released by the MMA commit alone
-          stage = (stage + nkb) % STAGES;
+          // stages of this tile are released by the MMA commit alone (la: plus this group's
+          // arrival, after the stage landed, which keeps the group within one ring phase)
+          if (la) {
+            for (int kb = 0; kb < nkb; ++kb) {
+              wait_a(stage);
+              if (t == 0) mbar_arrive(&empty[stage]);
+              if (++stage == STAGES) stage = 0;
+            }
+          } else {
+            stage = (stage + nkb) % STAGES;
+          }
           ssq = ssq_cache[slot * BM + t];
           if (ln) mu = mu_cache[slot * BM + t];
         } else if (ln) {
@@ -224,8 +260,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
           // ssq := K var (the epilogue's rsqrt(ssq/K + eps) is then LayerNorm's 1/sqrt(var + eps))
           float s0 = 0.f, s1 = 0.f, q0 = 0.f, q1 = 0.f, a0 = 0.f;
           for (int kb = 0; kb < nkb; ++kb) {
-            mbar_wait_warp(&mma_done[stage], (md_phase >> stage) & 1u);
-            md_phase ^= 1u << stage;
+            wait_a(stage);
             const uint4* row = reinterpret_cast<const uint4*>(sA + stage * A_STAGE + t * 128);
             if (kb == 0) a0 = bf16lo(row[t & 7].x);
 #pragma unroll
@@ -254,8 +289,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
         } else {
           float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
           for (int kb = 0; kb < nkb; ++kb) {
-            mbar_wait_warp(&mma_done[stage], (md_phase >> stage) & 1u);
-            md_phase ^= 1u << stage;
+            wait_a(stage);
             const uint4* row = reinterpret_cast<const uint4*>(sA + stage * A_STAGE + t * 128);
 #pragma unroll
             for (int c = 0; c < 8; ++c) {

@@ -53,6 +53,7 @@ struct GemmParams {
   int ndst, ldz, col0;
   __nv_bfloat16* zdst[8];
   int bn;  // pair kernel tile width (256 or 224, gemm2_pick_bn); num_n_blocks = ceil(N / bn)
+  int rms_local;  // pair kernel, RMS: A completes on each CTA's own barrier (see gemm2_sm100.cu)
 };
 constexpr int MAX_GATHER_DST = 8;
 enum GluAct { GLU_SILU = 0, GLU_RELU = 1, GLU_BILINEAR = 2 };
