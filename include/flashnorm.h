@@ -49,7 +49,8 @@ typedef enum {
     FN_ERR_ALIGN = 4,        /* pointer not 16-B aligned / K, N not multiple of 8 */
     FN_ERR_VALUE = 5,        /* eps < 0, non-finite eps/alpha, bad mode           */
     FN_ERR_UNSUPPORTED = 6,  /* valid request this build does not implement       */
-    FN_ERR_CUDA = 7          /* CUDA runtime/driver failure (text has the reason) */
+    FN_ERR_CUDA = 7,         /* CUDA runtime/driver failure (text has the reason) */
+    FN_ERR_NCCL = 8          /* NCCL missing or failed (text has the reason)       */
 } fn_status;
 
 typedef enum {
@@ -312,6 +313,33 @@ fn_status flashnorm_layernorm_linear(const void* a, const void* Wt_star, const f
 fn_status flashnorm_linear_gather(const void* a, const void* Wt_star, const float* c_star, int64_t M, int64_t K,
                                   int64_t N, float eps, float alpha, fn_mode mode, fn_dtype dtype,
                                   void* const* z_dsts, int ndst, int64_t ldz, int64_t col0, void* stream);
+
+/* --------------------------------------------------------------------------
+ * Opt-in multi-GPU plumbing.  W* is column-sharded, the
+ * activations replicated: every rank computes its shard z_local [M][N_local]
+ * with flashnorm_linear and NO collective; only a caller that wants the
+ * gathered z [M][P * N_local] on every rank calls flashnorm_allgather_columns.
+ * NCCL is loaded at run time (libnccl.so.2; the instance PyTorch loaded, if
+ * any); without it these calls return FN_ERR_NCCL.
+ *
+ *   flashnorm_comm_unique_id   writes an ncclUniqueId (FN_NCCL_UNIQUE_ID_BYTES)
+ *                              on one rank; the caller broadcasts it.
+ *   flashnorm_comm_init        ncclCommInitRank(nranks, id, rank) -> *comm
+ *                              (one GPU per rank: call with that GPU current).
+ *   flashnorm_comm_destroy     ncclCommDestroy (NULL is a no-op).
+ *   flashnorm_allgather_columns  ncclAllGather(z_local -> workspace [P][M][N_local])
+ *                              then the permute into z_full [M][P * N_local], both on
+ *                              `stream`; workspace = flashnorm_allgather_workspace_bytes().
+ *                              bf16 or f32; workspace must not alias z_local / z_full.
+ * The epilogue-fused alternative is flashnorm_linear_gather (peer-mapped outputs).
+ * -------------------------------------------------------------------------- */
+#define FN_NCCL_UNIQUE_ID_BYTES 128
+fn_status flashnorm_comm_unique_id(void* id_out);
+fn_status flashnorm_comm_init(const void* nccl_unique_id, int nranks, int rank, void** comm);
+fn_status flashnorm_comm_destroy(void* comm);
+int64_t flashnorm_allgather_workspace_bytes(int64_t P, int64_t M, int64_t N_local, fn_dtype dtype);
+fn_status flashnorm_allgather_columns(const void* z_local, int64_t M, int64_t N_local, fn_dtype dtype,
+                                      void* z_full, void* workspace, void* comm, void* stream);
 
 /* End-to-end variant: a_host / z_host are HOST pointers (pinned memory for
  * asynchronous copies); a_dev / z_dev are caller-owned device scratch of

@@ -23,7 +23,8 @@ __all__ = [
     "FlashNormError", "lib", "lib_path", "fold_weights", "fold_mean_center", "fold_mean_center_workspace_bytes",
     "linear", "linear_from_host", "baseline_norm", "gather_columns", "launch_count", "reset_launch_count",
     "version", "linear_workspace_bytes", "fold_glu_weights", "glu_linear", "linear_scaled", "glu_ffn", "qkv_rope_linear", "relu_ffn_up", "qk_norm_rope_linear",
-    "fold_colsum", "layernorm_linear", "linear_gather",
+    "fold_colsum", "layernorm_linear", "linear_gather", "comm_unique_id", "comm_init", "comm_destroy",
+    "allgather_columns",
     "MODES", "GLU_ACTS", "PATHS", "EXPORTS",
 ]
 
@@ -41,6 +42,8 @@ EXPORTS = [
     "flashnorm_linear", "flashnorm_linear_ex", "flashnorm_linear_workspace_bytes", "flashnorm_linear_ws",
     "flashnorm_linear_from_host", "flashnorm_fold_glu_weights", "flashnorm_glu_linear", "flashnorm_linear_scaled",
     "flashnorm_fold_colsum", "flashnorm_layernorm_linear", "flashnorm_linear_gather",
+    "flashnorm_comm_unique_id", "flashnorm_comm_init", "flashnorm_comm_destroy",
+    "flashnorm_allgather_workspace_bytes", "flashnorm_allgather_columns",
     "flashnorm_qkv_rope_linear", "flashnorm_relu_ffn_up", "flashnorm_qk_norm_rope_linear", "flashnorm_baseline_norm",
     "flashnorm_gather_columns", "flashnorm_status_string", "flashnorm_last_error", "flashnorm_launch_count",
     "flashnorm_reset_launch_count", "flashnorm_version",
@@ -85,6 +88,11 @@ def lib() -> ctypes.CDLL:
         "flashnorm_relu_ffn_up": [_vp, _vp, _i64, _i64, _i64, _f32, _int, _vp, _vp, _vp],
         "flashnorm_linear_scaled": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _vp, _vp],
         "flashnorm_fold_colsum": [_vp, _i64, _i64, _int, _vp, _vp],
+        "flashnorm_comm_unique_id": [_vp],
+        "flashnorm_comm_init": [_vp, _int, _int, ctypes.POINTER(ctypes.c_void_p)],
+        "flashnorm_comm_destroy": [_vp],
+        "flashnorm_allgather_workspace_bytes": [_i64, _i64, _i64, _int],
+        "flashnorm_allgather_columns": [_vp, _i64, _i64, _int, _vp, _vp, _vp, _vp],
         "flashnorm_linear_gather": [_vp, _vp, _vp, _i64, _i64, _i64, _f32, _f32, _int, _int, _vp, _int, _i64, _i64,
                                     _vp],
         "flashnorm_layernorm_linear": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _f32, _int, _vp, _vp],
@@ -104,6 +112,7 @@ def lib() -> ctypes.CDLL:
         f.restype = _int
     L.flashnorm_fold_mean_center_workspace_bytes.restype = _i64
     L.flashnorm_linear_workspace_bytes.restype = _i64
+    L.flashnorm_allgather_workspace_bytes.restype = _i64
     L.flashnorm_launch_count.restype = _i64
     L.flashnorm_reset_launch_count.restype = None
     for name in ("flashnorm_status_string", "flashnorm_last_error", "flashnorm_version"):
@@ -384,6 +393,41 @@ def linear_gather(a, Wt_star, dsts, col0: int, c_star=None, eps: float = 1e-5, m
     _check(lib().flashnorm_linear_gather(_ptr(a), _ptr(Wt_star), _ptr(c_star), M, K, N, float(eps), float(alpha),
                                          MODES[mode], _dtype_code(a), ptrs, len(dsts), ldz, int(col0), _stream(a)),
            "linear_gather")
+
+
+def comm_unique_id() -> bytes:
+    """An NCCL unique id (128 bytes) for flashnorm_comm_init; create on one rank, share it."""
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().flashnorm_comm_unique_id(buf), "comm_unique_id")
+    return buf.raw
+
+
+def comm_init(unique_id: bytes, nranks: int, rank: int) -> int:
+    """NCCL communicator of this rank (call with this rank's GPU current); returns the handle."""
+    if len(unique_id) != 128:
+        raise FlashNormError(5, "comm_init", "unique_id must be 128 bytes")
+    out = ctypes.c_void_p()
+    _check(lib().flashnorm_comm_init(ctypes.create_string_buffer(unique_id, 128), int(nranks), int(rank),
+                                     ctypes.byref(out)), "comm_init")
+    return out.value
+
+
+def comm_destroy(comm: int) -> None:
+    _check(lib().flashnorm_comm_destroy(ctypes.c_void_p(comm)), "comm_destroy")
+
+
+def allgather_columns(z_local, comm: int, nranks: int, out=None, workspace=None):
+    """z [M, P*N_local] from every rank's column shard z_local [M, N_local] (NCCL all-gather through the
+    C ABI, then the library's permute), on the current stream."""
+    torch = _torch()
+    _dev(z_local, "z_local")
+    M, Nl = z_local.shape
+    z = out if out is not None else torch.empty((M, nranks * Nl), dtype=z_local.dtype, device=z_local.device)
+    if workspace is None:
+        workspace = torch.empty((nranks, M, Nl), dtype=z_local.dtype, device=z_local.device)
+    _check(lib().flashnorm_allgather_columns(_ptr(z_local), M, Nl, _dtype_code(z_local), _ptr(z), _ptr(workspace),
+                                             ctypes.c_void_p(comm), _stream(z_local)), "allgather_columns")
+    return z
 
 
 def glu_ffn(a, Wgu_star, Wd_t, eps: float = 1e-5, act: str = "silu"):

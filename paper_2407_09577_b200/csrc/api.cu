@@ -301,6 +301,17 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
 
 }  // namespace
 
+namespace fn {
+// error text for the other translation units of the C ABI (comm.cu)
+fn_status api_fail(fn_status st, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return st;
+}
+}  // namespace fn
+
 extern "C" {
 
 fn_status flashnorm_fold_weights(const void* Wt, int64_t N, int64_t K, fn_dtype dtype, const float* g,
@@ -699,6 +710,7 @@ const char* flashnorm_status_string(fn_status s) {
     case FN_ERR_VALUE: return "FN_ERR_VALUE";
     case FN_ERR_UNSUPPORTED: return "FN_ERR_UNSUPPORTED";
     case FN_ERR_CUDA: return "FN_ERR_CUDA";
+    case FN_ERR_NCCL: return "FN_ERR_NCCL";
   }
   return "FN_ERR_UNKNOWN";
 }

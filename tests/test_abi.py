@@ -162,3 +162,17 @@ def test_linear_gather_validation_codes(L):
     assert f(P(0x1000), P(0x2000), None, 4, 64, 64, 1e-5, 0.5, 0, 0, one, 1, 132, 68, None) == 4   # col0 % 8
     bad = (ctypes.c_void_p * 1)(0x3004)
     assert f(P(0x1000), P(0x2000), None, 4, 64, 64, 1e-5, 0.5, 0, 0, bad, 1, 64, 0, None) == 4     # align
+
+
+def test_nccl_entry_validation_codes(L):
+    assert L.flashnorm_status_string(8) == b"FN_ERR_NCCL"
+    assert L.flashnorm_comm_unique_id(None) == 1
+    assert L.flashnorm_comm_init(None, 1, 0, None) == 1
+    assert L.flashnorm_comm_init(P(0x1000), 2, 2, None) in (1, 5)
+    assert L.flashnorm_comm_destroy(None) == 0
+    assert L.flashnorm_allgather_workspace_bytes(4, 8, 64, 0) == 4 * 8 * 64 * 2
+    f = L.flashnorm_allgather_columns
+    assert f(P(0x1000), 8, 64, 0, P(0x2000), P(0x3000), None, None) == 1        # comm
+    assert f(P(0x1000), 8, 0, 0, P(0x2000), P(0x3000), P(0x4000), None) == 2    # N_local
+    assert f(P(0x1000), 8, 64, 7, P(0x2000), P(0x3000), P(0x4000), None) == 3   # dtype
+    assert f(P(0x1000), 8, 64, 0, P(0x2000), P(0x2000), P(0x4000), None) == 5   # workspace aliases z

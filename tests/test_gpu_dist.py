@@ -55,3 +55,33 @@ def test_fused_gather_symmetric_memory_world1():
     env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
     r = subprocess.run([sys.executable, "-c", SCRIPT, ROOT], env=env, capture_output=True, text=True, timeout=300)
     assert "FUSED_GATHER_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
+SCRIPT_ABI = r'''
+import sys
+sys.path.insert(0, sys.argv[1])
+import torch
+import paper_2407_09577_b200 as fn
+from synth import device as SD
+torch.cuda.set_device(0)
+uid = fn.comm_unique_id()
+comm = fn.comm_init(uid, 1, 0)
+a = SD.activations(4, 200, 512, "cuda", torch.bfloat16)
+W, g, _, _ = SD.layer(4, 512, 512, "cuda", torch.bfloat16)
+Ws, cs = fn.fold_weights(W, g)
+zl = fn.linear(a, Ws, cs)
+z = fn.allgather_columns(zl, comm, 1)
+torch.cuda.synchronize()
+assert torch.equal(z.view(torch.int16), zl.view(torch.int16))
+fn.comm_destroy(comm)
+print("NCCL_ABI_OK")
+'''
+
+
+def test_nccl_allgather_through_the_c_abi_world1():
+    """flashnorm_comm_unique_id / comm_init / allgather_columns / comm_destroy with one rank:
+    NCCL loaded by the library (dlopen), the all-gather + permute returns the shard itself."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    r = subprocess.run([sys.executable, "-c", SCRIPT_ABI, ROOT], capture_output=True, text=True, timeout=300)
+    assert "NCCL_ABI_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
