@@ -401,6 +401,12 @@ def measure_secondary(args, fn, torch, dev, stream, peaks, a, Ws, cs, g):
     out["unfused_prefill"] = {"fused_ms": ms_f, "unfused_ms": ms_u, "fusion_gain": ms_u / ms_f,
                               "what": "baseline_norm (y=RN(a*r*g)) -> flashnorm_linear(mode=none)"}
 
+    # context only (not part of the library): the vendor GEMM (cuBLAS via torch.matmul) on the same
+    # operands, plain bf16 a @ W*^T with no normalization
+    ms_cb = timed(lambda i: torch.matmul(a, Ws.t(), out=z), 10)
+    out["vendor_gemm_context"] = {"what": "torch.matmul (cuBLAS) a @ W*^T, bf16, no norm — not part of the library",
+                                  "ms": ms_cb, "TFLOP/s": 2.0 * M * K * N / (ms_cb * 1e-3) / 1e12}
+
     # DyT variant of the same shape: tanh pre-pass (K8) into a workspace + the GEMM in mode none,
     # and the in-kernel tanh prologue (MUFU-bound) for comparison
     ws_dyt = torch.empty(M * K * 2, dtype=torch.uint8, device=dev)
