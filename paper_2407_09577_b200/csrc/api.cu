@@ -268,6 +268,11 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
     return e != nullptr ? atoi(e) : 0;
   }();
   p.rms_local = rms_local;
+  static const int tile_rot = [] {
+    const char* e = getenv("FN_GEMM2_TILE_ROT");  // A/B knob: 0 = plain grid-stride wave order
+    return e != nullptr ? atoi(e) : 1;
+  }();
+  p.tile_rot = tile_rot;
   p.num_tiles = p.num_m_blocks * p.num_n_blocks;
   {  // ~40 MB of A per tile group (L2 is 126 MB; W* tiles and z share it)
     const int64_t a_bytes_per_blk = (pair ? 256 : 128) * K * 2;

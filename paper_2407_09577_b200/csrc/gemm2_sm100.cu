@@ -131,6 +131,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
 
   const int num_tiles = p.num_tiles;  // pair tiles: num_m_blocks (of 256) x num_n_blocks
   const int nkb = p.num_k_blocks;
+  const int rot = pair_tile_rotation(p, nclusters);
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
@@ -138,7 +139,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
       const uint32_t full0 = mapa_shared(&full[0], 0);  // leader's barrier array
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+      for (int jw = 0, tile = next_pair_tile(jw, cluster, nclusters, rot, num_tiles); tile >= 0;
+         tile = next_pair_tile(jw, cluster, nclusters, rot, num_tiles)) {
         int m_blk, n_blk;
         tile_coords(tile, p, m_blk, n_blk);
         for (int kb = 0; kb < nkb; ++kb) {
@@ -170,7 +172,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      for (int tile = cluster; tile < num_tiles; tile += nclusters, ++local) {
+      for (int jw = 0, tile = next_pair_tile(jw, cluster, nclusters, rot, num_tiles); tile >= 0;
+         tile = next_pair_tile(jw, cluster, nclusters, rot, num_tiles), ++local) {
         const int as = local & 1;
         const uint32_t aphase = (local >> 1) & 1;
         int m_blk, n_blk_unused;
@@ -205,7 +208,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
       const uint32_t sig0 = mapa_shared(sig_dst, 0);  // 16-byte landing slot in the leader
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+      for (int jw = 0, tile = next_pair_tile(jw, cluster, nclusters, rot, num_tiles); tile >= 0;
+         tile = next_pair_tile(jw, cluster, nclusters, rot, num_tiles)) {
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&afull[stage], phase);
           if (leader) mbar_arrive_expect_tx(&ready[stage], 16);  // + the peer's 16-byte signal
@@ -230,7 +234,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
       };
       int stage = 0;
       int local = 0;
-      for (int tile = cluster; tile < num_tiles; tile += nclusters, ++local) {
+      for (int jw = 0, tile = next_pair_tile(jw, cluster, nclusters, rot, num_tiles); tile >= 0;
+         tile = next_pair_tile(jw, cluster, nclusters, rot, num_tiles), ++local) {
         int m_blk, n_blk_unused;
         tile_coords(tile, p, m_blk, n_blk_unused);
         const int slot = m_blk % SSQ_SLOTS;
@@ -330,7 +335,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
       const uint32_t sig0 = mapa_shared(sig_dst, 0);  // 16-byte landing slot in the leader
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+      for (int jw = 0, tile = next_pair_tile(jw, cluster, nclusters, rot, num_tiles); tile >= 0;
+         tile = next_pair_tile(jw, cluster, nclusters, rot, num_tiles)) {
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait_warp(&afull[stage], phase);
           uint4* row = reinterpret_cast<uint4*>(sA + stage * A_STAGE + t * 128);
@@ -365,7 +371,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
     const uint32_t tempty0 = mapa_shared(&tempty[0], 0);
     int local = 0;
     const float invK = 1.0f / static_cast<float>(p.K);
-    for (int tile = cluster; tile < num_tiles; tile += nclusters, ++local) {
+    for (int jw = 0, tile = next_pair_tile(jw, cluster, nclusters, rot, num_tiles); tile >= 0;
+         tile = next_pair_tile(jw, cluster, nclusters, rot, num_tiles), ++local) {
       int m_blk, n_blk;
       tile_coords(tile, p, m_blk, n_blk);
       const int as = local & 1;

@@ -54,6 +54,7 @@ struct GemmParams {
   __nv_bfloat16* zdst[8];
   int bn;  // pair kernel tile width (256 or 224, gemm2_pick_bn); num_n_blocks = ceil(N / bn)
   int rms_local;  // pair kernel, RMS: A completes on each CTA's own barrier (see gemm2_sm100.cu)
+  int tile_rot;   // pair kernel: rotated wave order (pair_tile_rotation); 0 = plain grid stride
 };
 constexpr int MAX_GATHER_DST = 8;
 enum GluAct { GLU_SILU = 0, GLU_RELU = 1, GLU_BILINEAR = 2 };
@@ -84,6 +85,30 @@ __host__ __device__ inline void tile_coords(int tile, const GemmParams& p, int& 
   const int gm = (p.num_m_blocks - m0) < G ? (p.num_m_blocks - m0) : G;
   m_blk = m0 + idx % gm;
   n_blk = idx / gm;
+}
+
+// Pair kernel wave order (DESIGN.md §12 item 1).  Wave j holds tiles [C j, C j + C) of the
+// order above, exactly as a plain grid stride would (same W* column blocks in flight), but pair
+// `cluster` takes tile C j + (cluster + rot j) mod C.  With s = C mod gm, rot = gm - s (or C - s,
+// whichever moves the M block more slowly) keeps m_blk = cluster mod gm for ~C / min(s, gm - s)
+// waves, so a pair meets ~3 M blocks instead of gm / gcd(s, gm) (config 3: 8) and the RMS side
+// group computes far fewer uncached ssq blocks.  rot = 0 is the plain grid stride.
+__host__ __device__ inline int pair_tile_rotation(const GemmParams& p, int C) {
+  if (!p.tile_rot) return 0;
+  const int gm = p.group_m < p.num_m_blocks ? p.group_m : p.num_m_blocks;
+  const int s = C % gm;
+  if (s == 0) return 0;
+  return (gm - s <= s) ? gm - s : C - s;
+}
+// the pair's next tile (-1 when done); j counts waves and is advanced past the returned tile
+__host__ __device__ inline int next_pair_tile(int& j, int cluster, int C, int rot, int num_tiles) {
+  for (;;) {
+    const int base = C * j;
+    if (base >= num_tiles) return -1;
+    const int t = base + (cluster + rot * j) % C;
+    ++j;
+    if (t < num_tiles) return t;
+  }
 }
 
 // K3: tcgen05 prefill GEMM (gemm_sm100.cu)
