@@ -269,8 +269,8 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
   }();
   p.rms_local = rms_local;
   static const int tile_rot = [] {
-    const char* e = getenv("FN_GEMM2_TILE_ROT");  // A/B knob: 0 = plain grid-stride wave order
-    return e != nullptr ? atoi(e) : 1;
+    const char* e = getenv("FN_GEMM2_TILE_ROT");  // A/B knob: 0 plain stride, 1 rotated, 2 matched table
+    return e != nullptr ? atoi(e) : 2;
   }();
   p.tile_rot = tile_rot;
   p.num_tiles = p.num_m_blocks * p.num_n_blocks;

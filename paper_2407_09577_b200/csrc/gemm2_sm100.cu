@@ -33,6 +33,10 @@
 #include "kernels.h"
 
 #include <cstdlib>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <tuple>
 
 namespace fn {
 
@@ -48,6 +52,7 @@ constexpr int THREADS = 384;
 constexpr int TMEM_COLS = 2 * BN;
 constexpr int BAR_BYTES = 1024;
 constexpr int SSQ_SLOTS = 16;          // per-CTA cache of reduced row ssq, by M block
+static_assert(SSQ_SLOTS == PAIR_SSQ_SLOTS, "the host schedule mirrors this cache");
 constexpr int SMEM_BYTES = 1024 + STAGES * (A_STAGE + B_STAGE) + BAR_BYTES + (4 + SSQ_SLOTS) * BM * 4 + 32 +
                              (2 + SSQ_SLOTS) * BM * 4;  // + LayerNorm mean buffers
 // the pair tile width is a template parameter: 256 (default) or 224 (picked by the host when it
@@ -58,7 +63,7 @@ constexpr int smem_bytes(int bn) { return SMEM_BYTES - STAGES * (B_STAGE - (bn /
 template <int MODE, int BN_ = gemm2::BN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
     flashnorm_gemm2_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                           GemmParams p) {
+                           GemmParams p, const __grid_constant__ PairSchedule sched) {
   using namespace gemm2;
   constexpr int BN = BN_;                // pair tile columns
   constexpr int BNH = BN / 2;            // W* rows loaded per CTA
@@ -132,6 +137,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
   const int num_tiles = p.num_tiles;  // pair tiles: num_m_blocks (of 256) x num_n_blocks
   const int nkb = p.num_k_blocks;
   const int rot = pair_tile_rotation(p, nclusters);
+  auto next_tile = [&](int& j) -> int {
+    return sched.waves > 0 ? next_sched_tile(j, sched, cluster, nclusters)
+                           : next_pair_tile(j, cluster, nclusters, rot, num_tiles);
+  };
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
@@ -139,8 +148,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
       const uint32_t full0 = mapa_shared(&full[0], 0);  // leader's barrier array
       int stage = 0;
       uint32_t phase = 0;
-      for (int jw = 0, tile = next_pair_tile(jw, cluster, nclusters, rot, num_tiles); tile >= 0;
-         tile = next_pair_tile(jw, cluster, nclusters, rot, num_tiles)) {
+      for (int jw = 0, tile = next_tile(jw); tile >= 0;
+         tile = next_tile(jw)) {
         int m_blk, n_blk;
         tile_coords(tile, p, m_blk, n_blk);
         for (int kb = 0; kb < nkb; ++kb) {
@@ -172,8 +181,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      for (int jw = 0, tile = next_pair_tile(jw, cluster, nclusters, rot, num_tiles); tile >= 0;
-         tile = next_pair_tile(jw, cluster, nclusters, rot, num_tiles), ++local) {
+      for (int jw = 0, tile = next_tile(jw); tile >= 0;
+         tile = next_tile(jw), ++local) {
         const int as = local & 1;
         const uint32_t aphase = (local >> 1) & 1;
         int m_blk, n_blk_unused;
@@ -208,8 +217,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
       const uint32_t sig0 = mapa_shared(sig_dst, 0);  // 16-byte landing slot in the leader
       int stage = 0;
       uint32_t phase = 0;
-      for (int jw = 0, tile = next_pair_tile(jw, cluster, nclusters, rot, num_tiles); tile >= 0;
-         tile = next_pair_tile(jw, cluster, nclusters, rot, num_tiles)) {
+      for (int jw = 0, tile = next_tile(jw); tile >= 0;
+         tile = next_tile(jw)) {
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&afull[stage], phase);
           if (leader) mbar_arrive_expect_tx(&ready[stage], 16);  // + the peer's 16-byte signal
@@ -234,8 +243,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
       };
       int stage = 0;
       int local = 0;
-      for (int jw = 0, tile = next_pair_tile(jw, cluster, nclusters, rot, num_tiles); tile >= 0;
-         tile = next_pair_tile(jw, cluster, nclusters, rot, num_tiles), ++local) {
+      for (int jw = 0, tile = next_tile(jw); tile >= 0;
+         tile = next_tile(jw), ++local) {
         int m_blk, n_blk_unused;
         tile_coords(tile, p, m_blk, n_blk_unused);
         const int slot = m_blk % SSQ_SLOTS;
@@ -335,8 +344,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
       const uint32_t sig0 = mapa_shared(sig_dst, 0);  // 16-byte landing slot in the leader
       int stage = 0;
       uint32_t phase = 0;
-      for (int jw = 0, tile = next_pair_tile(jw, cluster, nclusters, rot, num_tiles); tile >= 0;
-         tile = next_pair_tile(jw, cluster, nclusters, rot, num_tiles)) {
+      for (int jw = 0, tile = next_tile(jw); tile >= 0;
+         tile = next_tile(jw)) {
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait_warp(&afull[stage], phase);
           uint4* row = reinterpret_cast<uint4*>(sA + stage * A_STAGE + t * 128);
@@ -371,8 +380,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
     const uint32_t tempty0 = mapa_shared(&tempty[0], 0);
     int local = 0;
     const float invK = 1.0f / static_cast<float>(p.K);
-    for (int jw = 0, tile = next_pair_tile(jw, cluster, nclusters, rot, num_tiles); tile >= 0;
-         tile = next_pair_tile(jw, cluster, nclusters, rot, num_tiles), ++local) {
+    for (int jw = 0, tile = next_tile(jw); tile >= 0;
+         tile = next_tile(jw), ++local) {
       int m_blk, n_blk;
       tile_coords(tile, p, m_blk, n_blk);
       const int as = local & 1;
@@ -592,6 +601,24 @@ int gemm2_pick_bn(int M, int N, int num_sms, bool allow_224) {
   return span(224) * 40 < span(256) * 39 ? 224 : 256;
 }
 
+// host cache of matched schedules (tile_rot == 2), keyed by the tile grid and the pair count;
+// any other case gets the empty table (waves = 0: the kernel computes its order itself)
+static const PairSchedule* pair_schedule(const GemmParams& p, int pairs) {
+  static const PairSchedule none = {};
+  if (p.tile_rot != 2) return &none;
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, int, int>, std::unique_ptr<PairSchedule>> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto key = std::make_tuple(p.num_m_blocks, p.num_n_blocks, p.group_m, pairs);
+  auto it = cache.find(key);
+  if (it == cache.end()) {
+    std::unique_ptr<PairSchedule> s(new PairSchedule());
+    if (!build_pair_schedule(p, pairs, *s)) s->waves = 0;
+    it = cache.emplace(key, std::move(s)).first;
+  }
+  return it->second.get();
+}
+
 template <int MODE, int BN>
 static cudaError_t launch_gemm2_t(const CUtensorMap& ta, const CUtensorMap& tb_half, const GemmParams& p,
                                   int num_sms, cudaStream_t stream) {
@@ -613,7 +640,8 @@ static cudaError_t launch_gemm2_t(const CUtensorMap& ta, const CUtensorMap& tb_h
   cfg.stream = stream;
   cfg.attrs = nullptr;
   cfg.numAttrs = 0;  // cluster shape comes from __cluster_dims__
-  void* args[] = {(void*)&ta, (void*)&tb_half, (void*)&p};
+  const PairSchedule* sched = pair_schedule(p, pairs);
+  void* args[] = {(void*)&ta, (void*)&tb_half, (void*)&p, (void*)sched};
   return cudaLaunchKernelExC(&cfg, fptr, args);
 }
 

@@ -54,7 +54,7 @@ struct GemmParams {
   __nv_bfloat16* zdst[8];
   int bn;  // pair kernel tile width (256 or 224, gemm2_pick_bn); num_n_blocks = ceil(N / bn)
   int rms_local;  // pair kernel, RMS: A completes on each CTA's own barrier (see gemm2_sm100.cu)
-  int tile_rot;   // pair kernel: rotated wave order (pair_tile_rotation); 0 = plain grid stride
+  int tile_rot;   // pair kernel wave order: 0 plain grid stride, 1 rotated (pair_tile_rotation), 2 matched table
 };
 constexpr int MAX_GATHER_DST = 8;
 enum GluAct { GLU_SILU = 0, GLU_RELU = 1, GLU_BILINEAR = 2 };
@@ -109,6 +109,66 @@ __host__ __device__ inline int next_pair_tile(int& j, int cluster, int C, int ro
     ++j;
     if (t < num_tiles) return t;
   }
+}
+
+// Matched wave order (tile_rot = 2): the same per-wave tile sets, but the host assigns each
+// wave's tiles to pairs so that a pair whose ssq cache already holds a tile's M block takes it
+// (a per-wave greedy matching), which brings config 3 from 218 uncached tiles (rotation) to
+// near the one-per-pair floor.  The table rides in the kernel's parameter space (<= 16 KiB).
+constexpr int PAIR_SSQ_SLOTS = 16;  // mirrors the pair kernel's per-CTA ssq cache (slot = m % 16)
+constexpr int SCHED_MAX = 8192;
+constexpr int SCHED_MAX_PAIRS = 160;
+struct PairSchedule {
+  int waves;                // 0: no table (rotation / plain stride)
+  uint16_t t[SCHED_MAX];    // [waves][C]: tile of pair c in wave j, 0xFFFF = idle
+};
+__host__ __device__ inline int next_sched_tile(int& j, const PairSchedule& s, int cluster, int C) {
+  while (j < s.waves) {
+    const int t = s.t[j * C + cluster];
+    ++j;
+    if (t != 0xFFFF) return t;
+  }
+  return -1;
+}
+// greedy per-wave matching (a pair on the same M block, then one holding it in its ssq cache,
+// then any); false when the table does not fit (the caller keeps the rotation)
+inline bool build_pair_schedule(const GemmParams& p, int C, PairSchedule& s) {
+  const int nt = p.num_tiles;
+  s.waves = 0;
+  if (C <= 0 || C > SCHED_MAX_PAIRS || nt <= 0 || nt >= 0xFFFF) return false;
+  const int waves = (nt + C - 1) / C;
+  if ((long long)waves * C > SCHED_MAX) return false;
+  int tag[PAIR_SSQ_SLOTS * SCHED_MAX_PAIRS];
+  int cur[SCHED_MAX_PAIRS];
+  for (int i = 0; i < C * PAIR_SSQ_SLOTS; ++i) tag[i] = -1;
+  for (int c = 0; c < C; ++c) cur[c] = -1;
+  for (int j = 0; j < waves; ++j) {
+    const int t0 = j * C, n = (nt - t0) < C ? (nt - t0) : C;
+    bool used[SCHED_MAX_PAIRS] = {};
+    bool done[SCHED_MAX_PAIRS] = {};
+    for (int c = 0; c < C; ++c) s.t[t0 + c] = 0xFFFF;
+    for (int pass = 0; pass < 3; ++pass) {
+      for (int i = 0; i < n; ++i) {
+        if (done[i]) continue;
+        int m, nb;
+        tile_coords(t0 + i, p, m, nb);
+        for (int c = 0; c < C; ++c) {
+          if (used[c]) continue;
+          const bool ok = pass == 0   ? cur[c] == m
+                          : pass == 1 ? tag[c * PAIR_SSQ_SLOTS + m % PAIR_SSQ_SLOTS] == m
+                                      : true;
+          if (!ok) continue;
+          used[c] = done[i] = true;
+          s.t[t0 + c] = (uint16_t)(t0 + i);
+          cur[c] = m;
+          tag[c * PAIR_SSQ_SLOTS + m % PAIR_SSQ_SLOTS] = m;
+          break;
+        }
+      }
+    }
+  }
+  s.waves = waves;
+  return true;
 }
 
 // K3: tcgen05 prefill GEMM (gemm_sm100.cu)

@@ -23,17 +23,22 @@ int main() {
           if (G < 1) G = 1;
           if (G > mb) G = mb;
           p.group_m = (int)G;
-          long long visits[2] = {0, 0};
-          int maxtiles[2] = {0, 0};
-          for (int r = 0; r < 2; ++r) {
+          long long visits[3] = {0, 0, 0};
+          int maxtiles[3] = {0, 0, 0};
+          for (int r = 0; r < 3; ++r) {
             p.tile_rot = r;
             const int rot = fn::pair_tile_rotation(p, C);
+            static fn::PairSchedule sched;
+            sched.waves = 0;
+            if (r == 2) fn::build_pair_schedule(p, C, sched);
             std::vector<int> seen(p.num_tiles, 0);
             for (int cl = 0; cl < C; ++cl) {
               std::set<int> ms;
               int n = 0;
-              for (int j = 0, t = fn::next_pair_tile(j, cl, C, rot, p.num_tiles); t >= 0;
-                   t = fn::next_pair_tile(j, cl, C, rot, p.num_tiles)) {
+              auto nxt = [&](int& j) {
+                return sched.waves > 0 ? fn::next_sched_tile(j, sched, cl, C) : fn::next_pair_tile(j, cl, C, rot, p.num_tiles);
+              };
+              for (int j = 0, t = nxt(j); t >= 0; t = nxt(j)) {
                 if (t >= p.num_tiles) { printf("FAIL out of range C=%d mb=%d nb=%d\n", C, mb, nb); return 1; }
                 ++seen[t];
                 ++n;
@@ -47,19 +52,26 @@ int main() {
             for (int t = 0; t < p.num_tiles; ++t)
               if (seen[t] != 1) { printf("FAIL tile %d seen %d times C=%d mb=%d nb=%d rot=%d\n", t, seen[t], C, mb, nb, rot); return 1; }
           }
-          if (maxtiles[1] > maxtiles[0]) { printf("FAIL makespan C=%d mb=%d nb=%d\n", C, mb, nb); return 1; }
+          if (maxtiles[1] > maxtiles[0] || maxtiles[2] > maxtiles[0]) { printf("FAIL makespan C=%d mb=%d nb=%d\n", C, mb, nb); return 1; }
+          if (visits[2] > visits[0]) { printf("FAIL matched visits C=%d mb=%d nb=%d\n", C, mb, nb); return 1; }
           ++shapes;
         }
   // config 3 (M = K = 4096, N = 28672, 256-wide tiles) on 74 pairs: the figure DESIGN.md quotes
   fn::GemmParams p{};
   p.num_m_blocks = 16; p.num_n_blocks = 112; p.num_tiles = 16 * 112; p.group_m = 16;
-  long long v[2] = {0, 0};
-  for (int r = 0; r < 2; ++r) {
+  long long v[3] = {0, 0, 0};
+  static fn::PairSchedule sched;
+  for (int r = 0; r < 3; ++r) {
     p.tile_rot = r;
     const int rot = fn::pair_tile_rotation(p, 74);
+    sched.waves = 0;
+    if (r == 2 && !fn::build_pair_schedule(p, 74, sched)) { printf("FAIL config3 table\n"); return 1; }
     for (int cl = 0; cl < 74; ++cl) {
       std::set<int> ms;
-      for (int j = 0, t = fn::next_pair_tile(j, cl, 74, rot, p.num_tiles); t >= 0; t = fn::next_pair_tile(j, cl, 74, rot, p.num_tiles)) {
+      auto nxt = [&](int& j) {
+        return sched.waves > 0 ? fn::next_sched_tile(j, sched, cl, 74) : fn::next_pair_tile(j, cl, 74, rot, p.num_tiles);
+      };
+      for (int j = 0, t = nxt(j); t >= 0; t = nxt(j)) {
         int m, n;
         fn::tile_coords(t, p, m, n);
         ms.insert(m);
@@ -67,6 +79,6 @@ int main() {
       v[r] += (long long)ms.size();
     }
   }
-  printf("OK %d config3_first_visits plain=%lld rotated=%lld\n", shapes, v[0], v[1]);
+  printf("OK %d config3_first_visits plain=%lld rotated=%lld matched=%lld\n", shapes, v[0], v[1], v[2]);
   return 0;
 }

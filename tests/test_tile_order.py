@@ -21,5 +21,5 @@ def test_pair_tile_order_partitions(tmp_path):
     out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
     assert out.returncode == 0, out.stdout + out.stderr
     assert out.stdout.startswith("OK"), out.stdout
-    # config 3 on 74 pairs: 592 first visits of an M block with the plain stride, 218 rotated
-    assert "plain=592 rotated=218" in out.stdout, out.stdout
+    # config 3 on 74 pairs: 592 first visits of an M block with the plain stride, 218 rotated, 102 matched
+    assert "plain=592 rotated=218 matched=102" in out.stdout, out.stdout
