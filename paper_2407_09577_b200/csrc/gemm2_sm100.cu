@@ -37,6 +37,7 @@
 #include <memory>
 #include <mutex>
 #include <tuple>
+#include <type_traits>
 
 namespace fn {
 
@@ -60,10 +61,11 @@ constexpr int SMEM_BYTES = 1024 + STAGES * (A_STAGE + B_STAGE) + BAR_BYTES + (4 
 constexpr int smem_bytes(int bn) { return SMEM_BYTES - STAGES * (B_STAGE - (bn / 2) * BK * 2); }
 }  // namespace gemm2
 
-template <int MODE, int BN_ = gemm2::BN>
+template <int MODE, int BN_ = gemm2::BN, bool TBL = true>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
     flashnorm_gemm2_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                           GemmParams p, const __grid_constant__ PairSchedule sched) {
+                           GemmParams p,
+                           const __grid_constant__ std::conditional_t<TBL, PairSchedule, PairScheduleNone> sched) {
   using namespace gemm2;
   constexpr int BN = BN_;                // pair tile columns
   constexpr int BNH = BN / 2;            // W* rows loaded per CTA
@@ -138,8 +140,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
   const int nkb = p.num_k_blocks;
   const int rot = pair_tile_rotation(p, nclusters);
   auto next_tile = [&](int& j) -> int {
-    return sched.waves > 0 ? next_sched_tile(j, sched, cluster, nclusters)
-                           : next_pair_tile(j, cluster, nclusters, rot, num_tiles);
+    if constexpr (TBL) {
+      if (sched.waves > 0) return next_sched_tile(j, sched, cluster, nclusters);
+    }
+    return next_pair_tile(j, cluster, nclusters, rot, num_tiles);
   };
 
   if (warp == 0) {
@@ -619,20 +623,18 @@ static const PairSchedule* pair_schedule(const GemmParams& p, int pairs) {
   return it->second.get();
 }
 
-template <int MODE, int BN>
-static cudaError_t launch_gemm2_t(const CUtensorMap& ta, const CUtensorMap& tb_half, const GemmParams& p,
-                                  int num_sms, cudaStream_t stream) {
+template <int MODE, int BN, bool TBL>
+static cudaError_t launch_gemm2_k(const CUtensorMap& ta, const CUtensorMap& tb_half, const GemmParams& p, int pairs,
+                                  const void* sched, cudaStream_t stream) {
   using namespace gemm2;
   static bool attr_set = false;
-  const void* fptr = (const void*)flashnorm_gemm2_kernel<MODE, BN>;
+  const void* fptr = (const void*)flashnorm_gemm2_kernel<MODE, BN, TBL>;
   const int smem = smem_bytes(BN);
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(fptr, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  int pairs = num_sms / 2;
-  if (p.num_tiles < pairs) pairs = p.num_tiles;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * pairs);
   cfg.blockDim = dim3(THREADS);
@@ -640,9 +642,21 @@ static cudaError_t launch_gemm2_t(const CUtensorMap& ta, const CUtensorMap& tb_h
   cfg.stream = stream;
   cfg.attrs = nullptr;
   cfg.numAttrs = 0;  // cluster shape comes from __cluster_dims__
-  const PairSchedule* sched = pair_schedule(p, pairs);
-  void* args[] = {(void*)&ta, (void*)&tb_half, (void*)&p, (void*)sched};
+  void* args[] = {(void*)&ta, (void*)&tb_half, (void*)&p, const_cast<void*>(sched)};
   return cudaLaunchKernelExC(&cfg, fptr, args);
+}
+
+template <int MODE, int BN>
+static cudaError_t launch_gemm2_t(const CUtensorMap& ta, const CUtensorMap& tb_half, const GemmParams& p,
+                                  int num_sms, cudaStream_t stream) {
+  int pairs = num_sms / 2;
+  if (p.num_tiles < pairs) pairs = p.num_tiles;
+  // one wave or less: the order cannot matter, and the table-free instance skips the 16 KiB
+  // parameter upload (measured ~0.4 us per call on small shapes)
+  const PairSchedule* sched = p.num_tiles > pairs ? pair_schedule(p, pairs) : nullptr;
+  if (sched != nullptr && sched->waves > 0) return launch_gemm2_k<MODE, BN, true>(ta, tb_half, p, pairs, sched, stream);
+  static const PairScheduleNone none = {0};
+  return launch_gemm2_k<MODE, BN, false>(ta, tb_half, p, pairs, &none, stream);
 }
 
 cudaError_t launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb_half, const GemmParams& p, int mode,

@@ -122,6 +122,10 @@ struct PairSchedule {
   int waves;                // 0: no table (rotation / plain stride)
   uint16_t t[SCHED_MAX];    // [waves][C]: tile of pair c in wave j, 0xFFFF = idle
 };
+// launches with at most one wave use this parameter instead (no 16 KiB parameter upload)
+struct PairScheduleNone {
+  int waves;
+};
 __host__ __device__ inline int next_sched_tile(int& j, const PairSchedule& s, int cluster, int C) {
   while (j < s.waves) {
     const int t = s.t[j * C + cluster];
