@@ -616,6 +616,9 @@ static const PairSchedule* pair_schedule(const GemmParams& p, int pairs) {
   auto key = std::make_tuple(p.num_m_blocks, p.num_n_blocks, p.group_m, pairs);
   auto it = cache.find(key);
   if (it == cache.end()) {
+    // bounded (16 KiB per entry); entries are never freed, so a returned table stays valid while
+    // other threads launch — past the bound new shapes take the closed-form rotation instead
+    if (cache.size() >= 512) return &none;
     std::unique_ptr<PairSchedule> s(new PairSchedule());
     if (!build_pair_schedule(p, pairs, *s)) s->waves = 0;
     it = cache.emplace(key, std::move(s)).first;
