@@ -279,6 +279,14 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
     int64_t G = (40ll << 20) / a_bytes_per_blk;
     if (G < 1) G = 1;
     if (G > p.num_m_blocks) G = p.num_m_blocks;
+    static const int balance = [] {
+      const char* e = getenv("FN_GEMM2_GROUP_BAL");  // A/B knob: equal-sized tile groups
+      return e != nullptr ? atoi(e) : 1;
+    }();
+    if (balance) {  // same group count, sizes differing by at most one block (no short last group)
+      const int64_t ngroups = (p.num_m_blocks + G - 1) / G;
+      G = (p.num_m_blocks + ngroups - 1) / ngroups;
+    }
     p.group_m = (int)G;
   }
   p.num_k_blocks = (int)((K + 63) / 64);

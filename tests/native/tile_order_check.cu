@@ -22,6 +22,10 @@ int main() {
           long long G = (40ll << 20) / (256ll * K * 2);
           if (G < 1) G = 1;
           if (G > mb) G = mb;
+          if ((nb & 1) != 0) {  // balanced groups (api.cu, FN_GEMM2_GROUP_BAL) on half the shapes
+            const long long ng = (mb + G - 1) / G;
+            G = (mb + ng - 1) / ng;
+          }
           p.group_m = (int)G;
           long long visits[3] = {0, 0, 0};
           int maxtiles[3] = {0, 0, 0};
