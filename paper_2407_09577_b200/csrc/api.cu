@@ -276,7 +276,11 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
   p.num_tiles = p.num_m_blocks * p.num_n_blocks;
   {  // ~40 MB of A per tile group (L2 is 126 MB; W* tiles and z share it)
     const int64_t a_bytes_per_blk = (pair ? 256 : 128) * K * 2;
-    int64_t G = (40ll << 20) / a_bytes_per_blk;
+    static const int64_t group_mb = [] {
+      const char* e = getenv("FN_GEMM2_GROUP_MB");  // A/B knob: A bytes per tile group, MiB
+      return (int64_t)(e != nullptr ? atoi(e) : 40);
+    }();
+    int64_t G = (group_mb << 20) / a_bytes_per_blk;
     if (G < 1) G = 1;
     if (G > p.num_m_blocks) G = p.num_m_blocks;
     static const int balance = [] {
