@@ -58,6 +58,28 @@ def dist_env():
     return ws, rank, local
 
 
+def _free_port():
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_cmd(argv, gpus, port):
+    """The torchrun command bench.py re-executes itself under for `--gpus N` (N > 1) when it was
+    started as a plain process: one rank per GPU over NCCL on this node (the driver's contract)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+
+
+def spawn_env(env):
+    """NCCL init logging stays on (INIT subsystem only) so the rank count is visible in the log."""
+    env = dict(env)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    return env
+
+
 # ------------------------------------------------------------------ clocks sampler
 
 class ClockSampler:
@@ -256,24 +278,33 @@ def run_ours(args, ws, rank, local):
     launches = fn.launch_count()
     barrier_sync()
     total_ms = max_over_ranks(t_start.elapsed_time(t_end))
-    kern_ms = statistics.mean(s.elapsed_time(e) for s, e in ev)
+    kern_ms = max_over_ranks(statistics.mean(s.elapsed_time(e) for s, e in ev))  # slowest rank's shard
     flops_rank = 2.0 * M * K * Nl
     value = flops_rank * ws * args.steps / (total_ms * 1e-3) / 1e12
     achieved = flops_rank / (kern_ms * 1e-3) / 1e12
     peak_tf = peaks.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"])
     # the kernel flashnorm_linear dispatches for this shape (include/flashnorm.h fn_path)
     kname = "flashnorm_gemm2_kernel" if M > 128 else "flashnorm_gemm_kernel"
-    traffic = None
+    # DRAM bytes per launch of this kernel from the latest committed `ncu --set full` capture
+    # (profiles/traffic.json names the capture it came from); not re-measured inside this run
+    traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(kname)
+            tj = json.load(open(tp))
+            traffic = tj.get(kname)
+            traffic_src = tj.get("source")
         except Exception:
             traffic = None
 
     extra = {}
     if rank == 0 and ws == 1:
         extra = measure_secondary(args, fn, torch, dev, stream, peaks, a, Ws, cs, g)
+    if ws > 1:
+        extra["multi_gpu"] = measure_multi_gpu(args, fn, torch, dev, stream, a, Ws, cs, z, ws, rank,
+                                               barrier_sync, max_over_ranks)
+    extra["config5"] = measure_config5(args, fn, torch, dev, stream, peaks, ws, rank, barrier_sync,
+                                       max_over_ranks)
 
     # ---- e2e: through the C ABI with HOST buffers, copies inside the timed region
     a_host = a.cpu().pin_memory()
@@ -309,7 +340,8 @@ def run_ours(args, ws, rank, local):
                    "parallelism": f"column-sharded W* x{ws}" if ws > 1 else "single GPU",
                    "l2": "inputs > L2 (W* 235 MB), no flush"},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
-                     "frac": achieved / peak_tf, "traffic": traffic,
+                     "frac": achieved / peak_tf, "traffic": traffic, "traffic_source": traffic_src,
+                     "algorithmic_bytes": (M * K + Nl * K + M * Nl) * 2,
                      "kernel": f"{kname}<MODE_RMS> (tcgen05{' cta_group::2' if M > 128 else ''})",
                      "peak_source": f"{peaks_src} bf16_tflops (burst, cuBLAS)"},
         "cpu_baseline": cpu,
@@ -320,6 +352,85 @@ def run_ours(args, ws, rank, local):
     }
     line.update(extra)
     print(json.dumps(line), flush=True)
+
+
+def _events_ms(torch, stream, fnc, steps):
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record(stream)
+    for i in range(steps):
+        fnc(i)
+    e.record(stream)
+    e.synchronize()
+    return s.elapsed_time(e) / steps
+
+
+def measure_multi_gpu(args, fn, torch, dev, stream, a, Ws, cs, z, ws, rank, barrier_sync, max_over_ranks):
+    """N > 1 only: how many ranks NCCL sees, and the OPT-IN output gathers timed apart from the
+    metric (the shard needs no collective; the gather runs only when asked for).
+      * nccl_gather: torch.distributed all_gather_into_tensor (NCCL over NVLink) + the library's
+        [P][M][N/P] -> [M][N] permute, after the shard's linear;
+      * fused_gather: flashnorm_linear_gather into every rank's symmetric-memory buffer (peer
+        stores from the GEMM epilogue) + the device barriers (dist.ColumnParallelFlashNorm).
+    Times are device events, max over ranks; each also reports a bit-exact check against the
+    NCCL result on this rank."""
+    import torch.distributed as dist
+    from paper_2407_09577_b200.dist import ColumnParallelFlashNorm
+    one = torch.ones(1, device=dev)
+    dist.all_reduce(one)
+    out = {"world_size": dist.get_world_size(), "gpus_active": int(one.item()), "backend": dist.get_backend()}
+    layer = ColumnParallelFlashNorm(Ws, cs, world=ws, rank=rank)
+    steps = max(3, min(args.steps, 10))
+    try:
+        for _ in range(2):
+            zg = layer(a, gather=True)
+        barrier_sync()
+        ms_lin = max_over_ranks(_events_ms(torch, stream, lambda i: fn.linear(a, Ws, cs, eps=1e-5, out=z), steps))
+        ms_g = max_over_ranks(_events_ms(torch, stream, lambda i: layer(a, gather=True), steps))
+        out["nccl_gather"] = {"linear_ms": ms_lin, "linear_plus_gather_ms": ms_g, "gather_ms": ms_g - ms_lin,
+                              "gathered_bytes_per_rank": (ws - 1) * z.numel() * 2}
+    except Exception as e:  # reported, never fatal for the metric line
+        out["nccl_gather"] = {"error": repr(e)[:300]}
+        zg = None
+    try:
+        for _ in range(2):
+            zf = layer.forward_fused_gather(a, eps=1e-5)
+        barrier_sync()
+        ms_f = max_over_ranks(_events_ms(torch, stream, lambda i: layer.forward_fused_gather(a, eps=1e-5), steps))
+        zf = layer.forward_fused_gather(a, eps=1e-5, copy=True)
+        barrier_sync()
+        same = bool(zg is not None and torch.equal(zf.view(torch.int16), zg.view(torch.int16)))
+        out["fused_gather"] = {"ms": ms_f, "bit_exact_vs_nccl": same}
+    except Exception as e:
+        out["fused_gather"] = {"error": repr(e)[:300]}
+    return out
+
+
+def measure_config5(args, fn, torch, dev, stream, peaks, ws, rank, barrier_sync, max_over_ranks):
+    """BASELINE config 5 (Llama-3-70B FFN shapes: 8192 tokens, RMSNorm + FFN gate||up 8192 ->
+    2 x 28672) with W* column-sharded over the ws ranks: this rank's N/ws columns, activations
+    replicated, no collective.  TFLOP/s per rank (slowest rank) and for the whole job."""
+    from synth import device as SD
+    M, K, N = 8192, 8192, 57344
+    Nl = N // ws
+    a5 = SD.activations(5, M, K, dev, torch.bfloat16)
+    W5, g5, _, _ = SD.layer(5, N, K, dev, torch.bfloat16)
+    W5s = fn.fold_weights(W5[rank * Nl:(rank + 1) * Nl].contiguous(), g5)[0]
+    del W5
+    z5 = torch.empty((M, Nl), dtype=torch.bfloat16, device=dev)
+    for _ in range(2):
+        fn.linear(a5, W5s, None, eps=1e-5, out=z5)
+    barrier_sync()
+    steps = 5
+    ms = max_over_ranks(_events_ms(torch, stream, lambda i: fn.linear(a5, W5s, None, eps=1e-5, out=z5), steps))
+    fl = 2.0 * M * K * Nl
+    peak = peaks.get("bf16_tflops", FALLBACK_PEAKS["bf16_tflops"])
+    res = {"workload": f"llama3-70b FFN gate||up M={M} K={K} N={N}, column shard N/{ws} = {Nl} per rank",
+           "ms_per_step": ms, "TFLOP/s_per_rank": fl / (ms * 1e-3) / 1e12,
+           "frac_bf16_peak_per_rank": fl / (ms * 1e-3) / 1e12 / peak,
+           "TFLOP/s_job": fl * ws / (ms * 1e-3) / 1e12, "steps": steps}
+    del a5, W5s, z5
+    torch.cuda.empty_cache()
+    return res
 
 
 def measure_secondary(args, fn, torch, dev, stream, peaks, a, Ws, cs, g):
@@ -356,11 +467,13 @@ def measure_secondary(args, fn, torch, dev, stream, peaks, a, Ws, cs, g):
         torch.cuda.synchronize(dev)
         return s.elapsed_time(e) / steps
 
-    # decode: rotate 4 W* buffers (4 x 50 MB > L2) so every call streams from HBM.  The decode
-    # chain is latency-bound, so let the SM clock recover from the prefill's power cap first
+    # decode: rotate 8 W* buffers (8 x 50.3 MB = 403 MB >= 3 x the 126 MB L2) so every call
+    # streams from HBM.  The decode chain is latency-bound, so let the SM clock recover from the
+    # prefill's power cap first
     time.sleep(1.0)
+    NB = 8
     Wd = []
-    for r in range(4):
+    for r in range(NB):
         w, gd, _, _ = SD.layer(100 + r, DECODE_N, DECODE_K, dev, torch.bfloat16)
         Wd.append(fn.fold_weights(w, gd)[0])
         del w
@@ -368,8 +481,8 @@ def measure_secondary(args, fn, torch, dev, stream, peaks, a, Ws, cs, g):
     for Mdec in (1, 16):
         ad = SD.activations(7, Mdec, DECODE_K, dev, torch.bfloat16)
         zd = torch.empty((Mdec, DECODE_N), dtype=torch.bfloat16, device=dev)
-        ms = timed(lambda i: fn.linear(ad, Wd[i % 4], None, eps=1e-5, out=zd), args.secondary_iters, graph=True)
-        ms_eager = timed(lambda i: fn.linear(ad, Wd[i % 4], None, eps=1e-5, out=zd), args.secondary_iters)
+        ms = timed(lambda i: fn.linear(ad, Wd[i % NB], None, eps=1e-5, out=zd), args.secondary_iters, graph=True)
+        ms_eager = timed(lambda i: fn.linear(ad, Wd[i % NB], None, eps=1e-5, out=zd), args.secondary_iters)
         byts = DECODE_K * DECODE_N * 2 + Mdec * DECODE_K * 2 + Mdec * DECODE_N * 2
         gbs = byts / (ms * 1e-3) / 1e9
         # unfused: norm kernel + plain GEMV on the original weights (same W stream)
@@ -377,13 +490,16 @@ def measure_secondary(args, fn, torch, dev, stream, peaks, a, Ws, cs, g):
 
         def unf(i):
             fn.baseline_norm(ad, g, None, eps=1e-5, out=yd)
-            fn.linear(yd, Wd[i % 4], None, mode="none", out=zd)
+            fn.linear(yd, Wd[i % NB], None, mode="none", out=zd)
         ms_u = timed(unf, args.secondary_iters, graph=True)
+        gbs_e = byts / (ms_eager * 1e-3) / 1e9
         dec[f"M{Mdec}"] = {"us": ms * 1e3, "GB/s": gbs, "frac_hbm": gbs / hbm, "bytes": byts,
-                           "eager_us": ms_eager * 1e3, "unfused_us": ms_u * 1e3, "fusion_gain": ms_u / ms}
+                           "eager_us": ms_eager * 1e3, "eager_GB/s": gbs_e, "eager_frac_hbm": gbs_e / hbm,
+                           "unfused_us": ms_u * 1e3, "fusion_gain": ms_u / ms}
     out["decode"] = {"workload": "llama3-8b decode: RMSNorm + QKV 4096->6144 (BASELINE config 2)",
-                     "unit": "GB/s", "peak_hbm_gbs": hbm, "l2": "4 rotating W* buffers (200 MB > L2)",
-                     "timing": "CUDA graph of 200 back-to-back calls (PDL-chained launches), events",
+                     "unit": "GB/s", "peak_hbm_gbs": hbm, "l2": f"{NB} rotating W* buffers ({NB * 50.3:.0f} MB >= 3x L2)",
+                     "timing": "us/frac_hbm: CUDA graph of back-to-back calls (PDL-chained launches); "
+                               "eager_*: the same calls launched one by one from Python; events",
                      "kernel": "flashnorm_gemv_tc_kernel (tcgen05 swap-AB split-K, DSMEM cluster reduction)",
                      **dec}
     del Wd
@@ -469,15 +585,24 @@ def measure_secondary(args, fn, torch, dev, stream, peaks, a, Ws, cs, g):
     out["fold"] = {"fold_weights_us": ms_fold * 1e3, "GB/s": fb / (ms_fold * 1e-3) / 1e9,
                    "frac_hbm": fb / (ms_fold * 1e-3) / 1e9 / hbm, "bytes": fb, "shape": [N, K]}
     del Wf, Wo
-    # LayerNorm retrofit fold (config 4 V: 4096 x 4096 bf16 + b_prev), 3 kernels, CUDA graph
-    _, Vt, bp = SD.upstream(4, 16, 4096, 4096, dev, torch.bfloat16)
-    Vs = torch.empty_like(Vt)
+    # LayerNorm retrofit fold (config 4 V: 4096 x 4096 bf16 + b_prev), CUDA graph over 6 rotating
+    # V / V* pairs (6 x 67 MB = 403 MB >= 3 x L2): every call reads V from HBM and writes V* to it
+    NV = 6
+    Vts, bps, Vss = [], [], []
+    for r in range(NV):
+        _, Vt, bp = SD.upstream(4 + r, 16, 4096, 4096, dev, torch.bfloat16)
+        Vts.append(Vt)
+        bps.append(bp)
+        Vss.append(torch.empty_like(Vt))
     wsv = torch.empty(fn.fold_mean_center_workspace_bytes(4096, 4096) // 8 + 2, dtype=torch.float64, device=dev)
-    ms_mc = timed(lambda i: fn.fold_mean_center(Vt, bp, out=Vs, workspace=wsv), 20, graph=True)
+    ms_mc = timed(lambda i: fn.fold_mean_center(Vts[i % NV], bps[i % NV], out=Vss[i % NV], workspace=wsv), 24,
+                  graph=True)
     vb = 2 * 4096 * 4096 * 2
     out["fold"].update({"fold_mean_center_us": ms_mc * 1e3, "fold_mean_center_GB/s": vb / (ms_mc * 1e-3) / 1e9,
                         "fold_mean_center_frac_hbm": vb / (ms_mc * 1e-3) / 1e9 / hbm,
-                        "fold_mean_center_shape": [4096, 4096]})
+                        "fold_mean_center_shape": [4096, 4096],
+                        "fold_mean_center_l2": f"{NV} rotating V/V* pairs ({NV * 67} MB >= 3x L2), CUDA graph"})
+    del Vts, Vss
     return out
 
 
@@ -496,8 +621,17 @@ def main():
         args.warmup = 3
     ws, rank, local = dist_env()
     if args.impl == "reference":
-        run_reference(args, ws, rank)
+        run_reference(args, max(ws, args.gpus) if "WORLD_SIZE" not in os.environ else ws, rank)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N` as a plain process: become N ranks (one per GPU) under torchrun
+        import torch
+        n = torch.cuda.device_count()
+        if n < args.gpus:
+            raise SystemExit(f"bench.py --gpus {args.gpus}: only {n} CUDA device(s) visible")
+        sys.exit(subprocess.call(spawn_cmd(sys.argv[1:], args.gpus, _free_port()), env=spawn_env(os.environ)))
+    if ws != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={ws} but --gpus {args.gpus} (one rank per GPU)")
     run_ours(args, ws, rank, local)
     if ws > 1:
         import torch.distributed as dist

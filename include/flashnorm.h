@@ -149,6 +149,22 @@ fn_status flashnorm_fold_mean_center(const void* Vt, int64_t n_out, int64_t d_in
  *   IEEE inf/NaN in that row (documented; not reported per row).
  *   bf16: tcgen05 GEMM (prefill) or decode GEMV, chosen by M (FN_PATH_AUTO);
  *   f32:  FFMA SIMT kernel (no TF32).
+ *   FN_LAYERNORM trusts that `a` was mean-centered upstream: release builds do
+ *   not check it.  With the environment variable FN_DEBUG_LAYERNORM=1 the call first
+ *   measures max_m |mean(a_m)| / rms(a_m) on the device (one extra kernel and a stream
+ *   synchronization) and returns FN_ERR_VALUE, naming the value, if it exceeds 1e-2.
+ *
+ *   Programmatic dependent launch (decode path, M <= 16): the decode kernels are launched
+ *   with programmatic stream serialization and start streaming Wt_star (and c_star) into
+ *   shared memory BEFORE waiting for the preceding kernel on `stream`; `a` is read only
+ *   after that wait and `z` written only after it.  Precondition: Wt_star and c_star are not
+ *   written by a kernel that is still running on `stream` when this call is enqueued
+ *   (weights are written once, offline: the fold kernels of this library, torch copies and
+ *   cuBLAS all complete and flush before a dependent launch may start, because none of them
+ *   triggers early).  The only kernels of this library that trigger early
+ *   (griddepcontrol.launch_dependents) are the decode kernels themselves, which write z; a
+ *   decode call whose Wt_star is the z of the immediately preceding decode call must put an
+ *   event or a plain kernel between them.
  * -------------------------------------------------------------------------- */
 fn_status flashnorm_linear(const void* a, const void* Wt_star, const float* c_star,
                            int64_t M, int64_t K, int64_t N, float eps, float alpha,
@@ -163,7 +179,8 @@ fn_status flashnorm_linear_ex(const void* a, const void* Wt_star, const float* c
  * For mode == FN_DYT on a bf16 GEMM path (M > 16 or an explicit GEMM path) a
  * workspace of flashnorm_linear_workspace_bytes() = M*K*2 bytes lets the
  * library compute RN_bf16(tanh(alpha a)) ONCE per element (kernel K8, an
- * HBM-bound pre-pass) and then run the GEMM in mode FN_NONE
+ * HBM-bound pre-pass; DyT is named at PAPER.md:5 and its bias at PAPER.md:25,
+ * the elementwise formula is reading c10) and then run the GEMM in mode FN_NONE
  * on it, instead of recomputing tanh in the A-tile prologue of every N tile
  * (MUFU tanh: ~16 values/clk/SM on sm_100a, the same rate at which the tensor
  * core consumes A at BN = 256, DESIGN.md §6 K8).  z is bit-identical to the
@@ -327,9 +344,13 @@ fn_status flashnorm_linear_gather(const void* a, const void* Wt_star, const floa
  *   flashnorm_comm_init        ncclCommInitRank(nranks, id, rank) -> *comm
  *                              (one GPU per rank: call with that GPU current).
  *   flashnorm_comm_destroy     ncclCommDestroy (NULL is a no-op).
+ *   flashnorm_comm_count       ncclCommCount: *nranks = the communicator's rank count P
+ *                              (callers size z_full / workspace from it).
  *   flashnorm_allgather_columns  ncclAllGather(z_local -> workspace [P][M][N_local])
  *                              then the permute into z_full [M][P * N_local], both on
- *                              `stream`; workspace = flashnorm_allgather_workspace_bytes().
+ *                              `stream`; P is the communicator's rank count (not an
+ *                              argument); z_full must hold M*P*N_local elements and the
+ *                              workspace flashnorm_allgather_workspace_bytes(P, ...) bytes.
  *                              bf16 or f32; workspace must not alias z_local / z_full.
  * The epilogue-fused alternative is flashnorm_linear_gather (peer-mapped outputs).
  * -------------------------------------------------------------------------- */
@@ -337,6 +358,7 @@ fn_status flashnorm_linear_gather(const void* a, const void* Wt_star, const floa
 fn_status flashnorm_comm_unique_id(void* id_out);
 fn_status flashnorm_comm_init(const void* nccl_unique_id, int nranks, int rank, void** comm);
 fn_status flashnorm_comm_destroy(void* comm);
+fn_status flashnorm_comm_count(void* comm, int* nranks);
 int64_t flashnorm_allgather_workspace_bytes(int64_t P, int64_t M, int64_t N_local, fn_dtype dtype);
 fn_status flashnorm_allgather_columns(const void* z_local, int64_t M, int64_t N_local, fn_dtype dtype,
                                       void* z_full, void* workspace, void* comm, void* stream);

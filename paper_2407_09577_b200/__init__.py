@@ -24,7 +24,7 @@ __all__ = [
     "linear", "linear_from_host", "baseline_norm", "gather_columns", "launch_count", "reset_launch_count",
     "version", "linear_workspace_bytes", "fold_glu_weights", "glu_linear", "linear_scaled", "glu_ffn", "qkv_rope_linear", "relu_ffn_up", "qk_norm_rope_linear",
     "fold_colsum", "layernorm_linear", "linear_gather", "comm_unique_id", "comm_init", "comm_destroy",
-    "allgather_columns",
+    "allgather_columns", "comm_count",
     "MODES", "GLU_ACTS", "PATHS", "EXPORTS",
 ]
 
@@ -42,7 +42,7 @@ EXPORTS = [
     "flashnorm_linear", "flashnorm_linear_ex", "flashnorm_linear_workspace_bytes", "flashnorm_linear_ws",
     "flashnorm_linear_from_host", "flashnorm_fold_glu_weights", "flashnorm_glu_linear", "flashnorm_linear_scaled",
     "flashnorm_fold_colsum", "flashnorm_layernorm_linear", "flashnorm_linear_gather",
-    "flashnorm_comm_unique_id", "flashnorm_comm_init", "flashnorm_comm_destroy",
+    "flashnorm_comm_unique_id", "flashnorm_comm_init", "flashnorm_comm_destroy", "flashnorm_comm_count",
     "flashnorm_allgather_workspace_bytes", "flashnorm_allgather_columns",
     "flashnorm_qkv_rope_linear", "flashnorm_relu_ffn_up", "flashnorm_qk_norm_rope_linear", "flashnorm_baseline_norm",
     "flashnorm_gather_columns", "flashnorm_status_string", "flashnorm_last_error", "flashnorm_launch_count",
@@ -91,6 +91,7 @@ def lib() -> ctypes.CDLL:
         "flashnorm_comm_unique_id": [_vp],
         "flashnorm_comm_init": [_vp, _int, _int, ctypes.POINTER(ctypes.c_void_p)],
         "flashnorm_comm_destroy": [_vp],
+        "flashnorm_comm_count": [_vp, ctypes.POINTER(ctypes.c_int)],
         "flashnorm_allgather_workspace_bytes": [_i64, _i64, _i64, _int],
         "flashnorm_allgather_columns": [_vp, _i64, _i64, _int, _vp, _vp, _vp, _vp],
         "flashnorm_linear_gather": [_vp, _vp, _vp, _i64, _i64, _i64, _f32, _f32, _int, _int, _vp, _int, _i64, _i64,
@@ -164,6 +165,47 @@ def _vec(t, name: str, n: int):
     return t
 
 
+def _mat(t, name: str, rows: Optional[int] = None, cols: Optional[int] = None, dtype=None):
+    """A contiguous 2-D CUDA tensor, optionally of a given shape / dtype (the C side trusts the
+    sizes it is given: a wrong shape here would read or write out of bounds on the GPU)."""
+    _dev(t, name)
+    if t.dim() != 2:
+        raise FlashNormError(2, name, f"{name} must be 2-D, got {list(t.shape)}")
+    if (rows is not None and t.shape[0] != rows) or (cols is not None and t.shape[1] != cols):
+        want = f"[{'*' if rows is None else rows}, {'*' if cols is None else cols}]"
+        raise FlashNormError(2, name, f"{name} must be {want}, got {list(t.shape)}")
+    if dtype is not None and t.dtype != dtype:
+        raise FlashNormError(3, name, f"{name} must be {dtype}, got {t.dtype}")
+    return t
+
+
+def _operands(a, Wt, name: str, w_name: str = "Wt_star"):
+    """a [M, K] and W [N, K]: both CUDA, contiguous, 2-D, same dtype, same device, same K.
+    Returns (M, K, N)."""
+    _mat(a, "a")
+    _mat(Wt, w_name)
+    if a.shape[1] != Wt.shape[1]:
+        raise FlashNormError(2, name, f"a{list(a.shape)} and {w_name}{list(Wt.shape)}: need a[M,K], {w_name}[N,K]")
+    if a.dtype != Wt.dtype:
+        raise FlashNormError(3, name, f"a is {a.dtype} but {w_name} is {Wt.dtype}")
+    if a.device != Wt.device:
+        raise FlashNormError(5, name, f"a is on {a.device} but {w_name} on {Wt.device}")
+    _dtype_code(a)
+    return a.shape[0], a.shape[1], Wt.shape[0]
+
+
+def _out(t, name: str, shape, dtype, device):
+    """A caller-supplied output buffer: exact shape, dtype and device, contiguous; else a new one."""
+    torch = _torch()
+    if t is None:
+        return torch.empty(tuple(shape), dtype=dtype, device=device)
+    _dev(t, name)
+    if tuple(t.shape) != tuple(shape) or t.dtype != dtype or t.device != device:
+        raise FlashNormError(2, name, f"{name} must be {dtype}{list(shape)} on {device}, "
+                                      f"got {t.dtype}{list(t.shape)} on {t.device}")
+    return t
+
+
 def _ptr(t):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
@@ -182,15 +224,14 @@ def fold_weights(Wt, g=None, b=None, c=None, out=None, c_out=None):
     Returns (Wt_star [N, K] same dtype, c_star float32[N] or None).
     """
     torch = _torch()
-    _dev(Wt, "Wt")
-    if Wt.dim() != 2:
-        raise FlashNormError(2, "fold_weights", f"Wt must be 2-D [N, K], got {list(Wt.shape)}")
+    _mat(Wt, "Wt")
+    _dtype_code(Wt)
     N, K = Wt.shape
     g, b, c = _vec(g, "g", K), _vec(b, "b", K), _vec(c, "c", N)
-    Ws = out if out is not None else torch.empty_like(Wt)
-    cs = c_out
-    if cs is None and (b is not None or c is not None):
-        cs = torch.empty(N, dtype=torch.float32, device=Wt.device)
+    Ws = _out(out, "out", (N, K), Wt.dtype, Wt.device)
+    cs = None
+    if c_out is not None or b is not None or c is not None:
+        cs = _out(c_out, "c_out", (N,), torch.float32, Wt.device)
     _check(lib().flashnorm_fold_weights(_ptr(Wt), N, K, _dtype_code(Wt), _ptr(g), _ptr(b), _ptr(c), _ptr(Ws),
                                         _ptr(cs), _stream(Wt)), "fold_weights")
     return Ws, cs
@@ -207,15 +248,21 @@ def fold_mean_center(Vt, b_prev=None, out=None, workspace=None):
     Returns (Vt_star, b_prev_star or None).
     """
     torch = _torch()
-    _dev(Vt, "Vt")
+    _mat(Vt, "Vt")
+    _dtype_code(Vt)
     n_out, d_in = Vt.shape
     b_prev = _vec(b_prev, "b_prev", n_out)
-    Vs = out if out is not None else torch.empty_like(Vt)
+    Vs = _out(out, "out", (n_out, d_in), Vt.dtype, Vt.device)
     bs = torch.empty(n_out, dtype=torch.float32, device=Vt.device) if b_prev is not None else None
     ws = workspace
+    nbytes = fold_mean_center_workspace_bytes(n_out, d_in)
     if ws is None:
-        nbytes = fold_mean_center_workspace_bytes(n_out, d_in)
         ws = torch.empty((nbytes + 15) // 16 * 2, dtype=torch.float64, device=Vt.device)
+    else:
+        _dev(ws, "workspace")
+        if ws.numel() * ws.element_size() < nbytes:
+            raise FlashNormError(2, "fold_mean_center", f"workspace holds {ws.numel() * ws.element_size()} bytes, "
+                                                        f"needs {nbytes}")
     _check(lib().flashnorm_fold_mean_center(_ptr(Vt), n_out, d_in, _dtype_code(Vt), _ptr(b_prev), _ptr(Vs),
                                             _ptr(bs), _ptr(ws), _stream(Vt)), "fold_mean_center")
     return Vs, bs
@@ -232,17 +279,11 @@ def linear(a, Wt_star, c_star=None, eps: float = 1e-5, mode: str = "rmsnorm", al
     in-kernel tanh prologue; or a caller-owned CUDA tensor.
     """
     torch = _torch()
-    _dev(a, "a")
-    _dev(Wt_star, "Wt_star")
-    if a.dim() != 2 or Wt_star.dim() != 2 or a.shape[1] != Wt_star.shape[1]:
-        raise FlashNormError(2, "linear", f"a{list(a.shape)} and Wt_star{list(Wt_star.shape)}: need a[M,K], "
-                                          "Wt_star[N,K]")
-    if a.dtype != Wt_star.dtype:
-        raise FlashNormError(3, "linear", f"a is {a.dtype} but Wt_star is {Wt_star.dtype}")
-    M, K = a.shape
-    N = Wt_star.shape[0]
+    M, K, N = _operands(a, Wt_star, "linear")
+    if mode not in MODES or path not in PATHS:
+        raise FlashNormError(5, "linear", f"mode {mode!r} / path {path!r}: mode in {list(MODES)}, path in {list(PATHS)}")
     c_star = _vec(c_star, "c_star", N)
-    z = out if out is not None else torch.empty((M, N), dtype=a.dtype, device=a.device)
+    z = _out(out, "out", (M, N), a.dtype, a.device)
     if isinstance(workspace, str):
         if workspace != "auto":
             raise FlashNormError(5, "linear", f"workspace must be 'auto', None or a CUDA tensor, got {workspace!r}")
@@ -269,14 +310,14 @@ def linear_workspace_bytes(M: int, K: int, N: int, mode: str = "rmsnorm", dtype=
 def fold_glu_weights(Wg_t, Wu_t, g=None, out=None):
     """Gate/up folds for a GLU FFN: returns Wgu_star [2F, K], gate/up
     interleaved in 128-row blocks (include/flashnorm.h).  Wg_t, Wu_t: [F, K]."""
-    torch = _torch()
-    _dev(Wg_t, "Wg_t")
-    _dev(Wu_t, "Wu_t")
-    if Wg_t.shape != Wu_t.shape or Wg_t.dim() != 2 or Wg_t.dtype != Wu_t.dtype:
+    _mat(Wg_t, "Wg_t")
+    _mat(Wu_t, "Wu_t")
+    _dtype_code(Wg_t)
+    if Wg_t.shape != Wu_t.shape or Wg_t.dtype != Wu_t.dtype or Wg_t.device != Wu_t.device:
         raise FlashNormError(2, "fold_glu_weights", f"Wg_t{list(Wg_t.shape)} / Wu_t{list(Wu_t.shape)}: need two [F, K]")
     F, K = Wg_t.shape
     g = _vec(g, "g", K)
-    W = out if out is not None else torch.empty((2 * F, K), dtype=Wg_t.dtype, device=Wg_t.device)
+    W = _out(out, "out", (2 * F, K), Wg_t.dtype, Wg_t.device)
     _check(lib().flashnorm_fold_glu_weights(_ptr(Wg_t), _ptr(Wu_t), F, K, _dtype_code(Wg_t), _ptr(g), _ptr(W),
                                             _stream(Wg_t)), "fold_glu_weights")
     return W
@@ -286,12 +327,12 @@ def glu_linear(a, Wgu_star, eps: float = 1e-5, act: str = "silu", out=None, s_ou
     """Gate||up GEMM with the GLU epilogue: returns (h [M, F], s [M]) with y = (h W_down) * s
     (Figs 3(b)/4(b), readings c24-c25)."""
     torch = _torch()
-    _dev(a, "a")
-    _dev(Wgu_star, "Wgu_star")
-    M, K = a.shape
-    F = Wgu_star.shape[0] // 2
-    h = out if out is not None else torch.empty((M, F), dtype=a.dtype, device=a.device)
-    s = s_out if s_out is not None else torch.empty(M, dtype=torch.float32, device=a.device)
+    M, K, N2 = _operands(a, Wgu_star, "glu_linear", "Wgu_star")
+    if N2 % 2 or act not in GLU_ACTS:
+        raise FlashNormError(2, "glu_linear", f"Wgu_star must be [2F, K] (got {N2} rows), act in {list(GLU_ACTS)}")
+    F = N2 // 2
+    h = _out(out, "out", (M, F), a.dtype, a.device)
+    s = _out(s_out, "s_out", (M,), torch.float32, a.device)
     _check(lib().flashnorm_glu_linear(_ptr(a), _ptr(Wgu_star), M, K, F, float(eps), GLU_ACTS[act], _dtype_code(a),
                                       _ptr(h), _ptr(s), _stream(a)), "glu_linear")
     return h, s
@@ -300,13 +341,10 @@ def glu_linear(a, Wgu_star, eps: float = 1e-5, act: str = "silu", out=None, s_ou
 def qk_norm_rope_linear(a, Wt_star, n_q: int, n_k: int, head_dim: int, g_q, g_k, positions, cos_tab, sin_tab,
                         eps_qk: float = 1e-6, qk_scale: float = 1.0, eps: float = 1e-5, out=None):
     """[Q | K | V] with per-head QK-norm fused into RoPE (Figs 6(b)+7(b))."""
-    torch = _torch()
-    for t, nm in ((a, "a"), (Wt_star, "Wt_star"), (g_q, "g_q"), (g_k, "g_k"), (positions, "positions"),
-                  (cos_tab, "cos_tab"), (sin_tab, "sin_tab")):
-        _dev(t, nm)
-    M, K = a.shape
-    N = Wt_star.shape[0]
-    z = out if out is not None else torch.empty((M, N), dtype=a.dtype, device=a.device)
+    M, K, N = _operands(a, Wt_star, "qk_norm_rope_linear")
+    g_q, g_k = _vec(g_q, "g_q", head_dim), _vec(g_k, "g_k", head_dim)
+    _rope_tables(positions, cos_tab, sin_tab, M, head_dim, "qk_norm_rope_linear")
+    z = _out(out, "out", (M, N), a.dtype, a.device)
     _check(lib().flashnorm_qk_norm_rope_linear(_ptr(a), _ptr(Wt_star), M, K, N, n_q, n_k, head_dim, _ptr(g_q),
                                                _ptr(g_k), float(eps_qk), _ptr(positions), _ptr(cos_tab),
                                                _ptr(sin_tab), float(qk_scale), float(eps), _dtype_code(a), _ptr(z),
@@ -317,12 +355,9 @@ def qk_norm_rope_linear(a, Wt_star, n_q: int, n_k: int, head_dim: int, g_q, g_k,
 def relu_ffn_up(a, Wt_star, eps: float = 1e-5, out=None, s_out=None):
     """Fig 2(b): h = relu(a W*_up) (unscaled), s = 1/RMSe(a); y = (h W_down) * s via linear_scaled."""
     torch = _torch()
-    _dev(a, "a")
-    _dev(Wt_star, "Wt_star")
-    M, K = a.shape
-    F = Wt_star.shape[0]
-    h = out if out is not None else torch.empty((M, F), dtype=a.dtype, device=a.device)
-    s = s_out if s_out is not None else torch.empty(M, dtype=torch.float32, device=a.device)
+    M, K, F = _operands(a, Wt_star, "relu_ffn_up")
+    h = _out(out, "out", (M, F), a.dtype, a.device)
+    s = _out(s_out, "s_out", (M,), torch.float32, a.device)
     _check(lib().flashnorm_relu_ffn_up(_ptr(a), _ptr(Wt_star), M, K, F, float(eps), _dtype_code(a), _ptr(h), _ptr(s),
                                        _stream(a)), "relu_ffn_up")
     return h, s
@@ -330,14 +365,10 @@ def relu_ffn_up(a, Wt_star, eps: float = 1e-5, out=None, s_out=None):
 
 def linear_scaled(a, Wt_star, row_scale, c_star=None, out=None):
     """z = (a W*) * row_scale[m] + c*: the down projection with the deferred FFN-output scale."""
-    torch = _torch()
-    _dev(a, "a")
-    _dev(Wt_star, "Wt_star")
-    _dev(row_scale, "row_scale")
-    M, K = a.shape
-    N = Wt_star.shape[0]
+    M, K, N = _operands(a, Wt_star, "linear_scaled")
+    row_scale = _vec(row_scale, "row_scale", M)
     c_star = _vec(c_star, "c_star", N)
-    z = out if out is not None else torch.empty((M, N), dtype=a.dtype, device=a.device)
+    z = _out(out, "out", (M, N), a.dtype, a.device)
     _check(lib().flashnorm_linear_scaled(_ptr(a), _ptr(Wt_star), _ptr(c_star), _ptr(row_scale), M, K, N,
                                          _dtype_code(a), _ptr(z), _stream(a)), "linear_scaled")
     return z
@@ -347,9 +378,10 @@ def fold_colsum(Wt_star, out=None):
     """u = 1^T W*: u[j] = sum_k W*t[j][k] (fp64 sum, one f32 rounding) — the correction vector of
     the deferred LayerNorm (NEXT-4, reading c29)."""
     torch = _torch()
-    _dev(Wt_star, "Wt_star")
+    _mat(Wt_star, "Wt_star")
+    _dtype_code(Wt_star)
     N, K = Wt_star.shape
-    u = out if out is not None else torch.empty(N, dtype=torch.float32, device=Wt_star.device)
+    u = _out(out, "out", (N,), torch.float32, Wt_star.device)
     _check(lib().flashnorm_fold_colsum(_ptr(Wt_star), N, K, _dtype_code(Wt_star), _ptr(u), _stream(Wt_star)),
            "fold_colsum")
     return u
@@ -359,14 +391,10 @@ def layernorm_linear(a, Wt_star, u, c_star=None, eps: float = 1e-5, out=None):
     """LayerNorm -> linear with the mean AND the normalization deferred past the contraction:
     z = (a W* - mu u) / sqrt(var + eps) + c*, mu / var reduced beside the contraction (PAPER.md:33,
     42-46; reading c29).  W*, c* from fold_weights(W, g, b, c); u from fold_colsum(W*)."""
-    torch = _torch()
-    _dev(a, "a")
-    _dev(Wt_star, "Wt_star")
-    M, K = a.shape
-    N = Wt_star.shape[0]
+    M, K, N = _operands(a, Wt_star, "layernorm_linear")
     u = _vec(u, "u", N)
     c_star = _vec(c_star, "c_star", N)
-    z = out if out is not None else torch.empty((M, N), dtype=a.dtype, device=a.device)
+    z = _out(out, "out", (M, N), a.dtype, a.device)
     _check(lib().flashnorm_layernorm_linear(_ptr(a), _ptr(Wt_star), _ptr(u), _ptr(c_star), M, K, N, float(eps),
                                             _dtype_code(a), _ptr(z), _stream(a)), "layernorm_linear")
     return z
@@ -376,10 +404,7 @@ def linear_gather(a, Wt_star, dsts, col0: int, c_star=None, eps: float = 1e-5, m
                   alpha: float = 0.5):
     """This rank's column shard written by the GEMM epilogue into every buffer of `dsts` (each an
     [M, ldz] bf16 tensor: local, or peer-mapped gathered outputs) at columns [col0, col0 + N)."""
-    _dev(a, "a")
-    _dev(Wt_star, "Wt_star")
-    M, K = a.shape
-    N = Wt_star.shape[0]
+    M, K, N = _operands(a, Wt_star, "linear_gather")
     c_star = _vec(c_star, "c_star", N)
     if not dsts:
         raise FlashNormError(5, "linear_gather", "dsts is empty")
@@ -416,15 +441,30 @@ def comm_destroy(comm: int) -> None:
     _check(lib().flashnorm_comm_destroy(ctypes.c_void_p(comm)), "comm_destroy")
 
 
-def allgather_columns(z_local, comm: int, nranks: int, out=None, workspace=None):
+def comm_count(comm: int) -> int:
+    """Number of ranks of a communicator from comm_init (ncclCommCount)."""
+    n = ctypes.c_int(0)
+    _check(lib().flashnorm_comm_count(ctypes.c_void_p(comm), ctypes.byref(n)), "comm_count")
+    return int(n.value)
+
+
+def allgather_columns(z_local, comm: int, nranks: Optional[int] = None, out=None, workspace=None):
     """z [M, P*N_local] from every rank's column shard z_local [M, N_local] (NCCL all-gather through the
-    C ABI, then the library's permute), on the current stream."""
-    torch = _torch()
-    _dev(z_local, "z_local")
+    C ABI, then the library's permute), on the current stream.  P is the communicator's rank count
+    (a given `nranks` must equal it); out / workspace are checked against it."""
+    _mat(z_local, "z_local")
+    _dtype_code(z_local)
+    P = comm_count(comm)
+    if nranks is not None and int(nranks) != P:
+        raise FlashNormError(5, "allgather_columns", f"nranks={nranks} but the communicator has {P} ranks")
     M, Nl = z_local.shape
-    z = out if out is not None else torch.empty((M, nranks * Nl), dtype=z_local.dtype, device=z_local.device)
+    z = _out(out, "out", (M, P * Nl), z_local.dtype, z_local.device)
     if workspace is None:
-        workspace = torch.empty((nranks, M, Nl), dtype=z_local.dtype, device=z_local.device)
+        workspace = _torch().empty((P, M, Nl), dtype=z_local.dtype, device=z_local.device)
+    else:
+        _dev(workspace, "workspace")
+        if workspace.numel() * workspace.element_size() < P * M * Nl * z_local.element_size():
+            raise FlashNormError(2, "allgather_columns", f"workspace must hold {P}*{M}*{Nl} elements")
     _check(lib().flashnorm_allgather_columns(_ptr(z_local), M, Nl, _dtype_code(z_local), _ptr(z), _ptr(workspace),
                                              ctypes.c_void_p(comm), _stream(z_local)), "allgather_columns")
     return z
@@ -437,20 +477,29 @@ def glu_ffn(a, Wgu_star, Wd_t, eps: float = 1e-5, act: str = "silu"):
     return linear_scaled(h, Wd_t, s)
 
 
+def _rope_tables(positions, cos_tab, sin_tab, M: int, head_dim: int, name: str):
+    """positions int32[M]; cos_tab / sin_tab float32[max_pos, head_dim // 2] (reading c26).  Positions
+    must lie in [0, max_pos): the kernels index the tables with them (checked here on the device
+    tensor, one small D2H read)."""
+    torch = _torch()
+    _dev(positions, "positions")
+    if positions.dtype != torch.int32 or positions.dim() != 1 or positions.shape[0] != M:
+        raise FlashNormError(3, name, f"positions must be int32[{M}], got {positions.dtype}{list(positions.shape)}")
+    _mat(cos_tab, "cos_tab", cols=head_dim // 2, dtype=torch.float32)
+    _mat(sin_tab, "sin_tab", rows=cos_tab.shape[0], cols=head_dim // 2, dtype=torch.float32)
+    if M > 0:
+        lo, hi = int(positions.min()), int(positions.max())
+        if lo < 0 or hi >= cos_tab.shape[0]:
+            raise FlashNormError(5, name, f"positions span [{lo}, {hi}] outside the {cos_tab.shape[0]}-row tables")
+
+
 def qkv_rope_linear(a, Wt_star, n_rope: int, head_dim: int, positions, cos_tab, sin_tab, qk_scale: float = 1.0,
                     eps: float = 1e-5, out=None):
     """[Q | K | V] = RoPE-fused FlashNorm projection (Fig 5(b)).
     positions: int32 [M]; cos_tab / sin_tab: float32 [max_pos, head_dim // 2]."""
-    torch = _torch()
-    _dev(a, "a")
-    _dev(Wt_star, "Wt_star")
-    for t, nm in ((positions, "positions"), (cos_tab, "cos_tab"), (sin_tab, "sin_tab")):
-        _dev(t, nm)
-    if positions.dtype != torch.int32 or cos_tab.dtype != torch.float32 or sin_tab.dtype != torch.float32:
-        raise FlashNormError(3, "qkv_rope_linear", "positions must be int32, cos_tab / sin_tab float32")
-    M, K = a.shape
-    N = Wt_star.shape[0]
-    z = out if out is not None else torch.empty((M, N), dtype=a.dtype, device=a.device)
+    M, K, N = _operands(a, Wt_star, "qkv_rope_linear")
+    _rope_tables(positions, cos_tab, sin_tab, M, head_dim, "qkv_rope_linear")
+    z = _out(out, "out", (M, N), a.dtype, a.device)
     _check(lib().flashnorm_qkv_rope_linear(_ptr(a), _ptr(Wt_star), M, K, N, n_rope, head_dim, _ptr(positions),
                                            _ptr(cos_tab), _ptr(sin_tab), float(qk_scale), float(eps),
                                            _dtype_code(a), _ptr(z), _stream(a)), "qkv_rope_linear")
@@ -464,8 +513,19 @@ def linear_from_host(a_host, Wt_star, c_star, a_dev, z_dev, z_host, eps: float =
     Enqueues H2D(a) -> flashnorm_linear -> D2H(z) on the current stream (no sync).
     """
     torch = _torch()
+    _mat(Wt_star, "Wt_star")
+    if a_host.is_cuda or z_host.is_cuda or a_host.dim() != 2 or not (a_host.is_contiguous() and z_host.is_contiguous()):
+        raise FlashNormError(2, "linear_from_host", "a_host / z_host must be contiguous 2-D host tensors")
     M, K = a_host.shape
     N = Wt_star.shape[0]
+    if K != Wt_star.shape[1] or a_host.dtype != Wt_star.dtype:
+        raise FlashNormError(2, "linear_from_host", f"a_host {a_host.dtype}{list(a_host.shape)} vs Wt_star "
+                                                    f"{Wt_star.dtype}{list(Wt_star.shape)}")
+    if tuple(z_host.shape) != (M, N) or z_host.dtype != a_host.dtype:
+        raise FlashNormError(2, "linear_from_host", f"z_host must be {a_host.dtype}[{M}, {N}]")
+    _out(a_dev, "a_dev", (M, K), a_host.dtype, Wt_star.device)
+    _out(z_dev, "z_dev", (M, N), a_host.dtype, Wt_star.device)
+    c_star = _vec(c_star, "c_star", N)
     st = stream if stream is not None else torch.cuda.current_stream(Wt_star.device)
     s = lib().flashnorm_linear_from_host(_ptr(a_host), _ptr(Wt_star), _ptr(c_star), M, K, N, float(eps),
                                          float(alpha), MODES[mode], _dtype_code(Wt_star), _ptr(a_dev), _ptr(z_dev),
@@ -476,11 +536,11 @@ def linear_from_host(a_host, Wt_star, c_star, a_dev, z_dev, z_host, eps: float =
 
 def baseline_norm(a, g=None, b=None, eps: float = 1e-5, mode: str = "rmsnorm", alpha: float = 0.5, out=None):
     """Unfused normalization y = RN(Norm(a) * g + b) (measurement-only, Fig 1(a))."""
-    torch = _torch()
-    _dev(a, "a")
+    _mat(a, "a")
+    _dtype_code(a)
     M, K = a.shape
     g, b = _vec(g, "g", K), _vec(b, "b", K)
-    y = out if out is not None else torch.empty_like(a)
+    y = _out(out, "out", (M, K), a.dtype, a.device)
     _check(lib().flashnorm_baseline_norm(_ptr(a), _ptr(g), _ptr(b), M, K, float(eps), MODES[mode], float(alpha),
                                          _dtype_code(a), _ptr(y), _stream(a)), "baseline_norm")
     return y
@@ -488,10 +548,12 @@ def baseline_norm(a, g=None, b=None, eps: float = 1e-5, mode: str = "rmsnorm", a
 
 def gather_columns(z_parts, out=None):
     """z_parts [P, M, N_local] (all-gathered column shards) -> z [M, P*N_local]."""
-    torch = _torch()
     _dev(z_parts, "z_parts")
+    _dtype_code(z_parts)
+    if z_parts.dim() != 3:
+        raise FlashNormError(2, "gather_columns", f"z_parts must be [P, M, N_local], got {list(z_parts.shape)}")
     P, M, Nl = z_parts.shape
-    z = out if out is not None else torch.empty((M, P * Nl), dtype=z_parts.dtype, device=z_parts.device)
+    z = _out(out, "out", (M, P * Nl), z_parts.dtype, z_parts.device)
     _check(lib().flashnorm_gather_columns(_ptr(z_parts), P, M, Nl, _dtype_code(z_parts), _ptr(z),
                                           _stream(z_parts)), "gather_columns")
     return z

@@ -18,6 +18,53 @@
 #include "../../include/flashnorm.h"
 #include "kernels.h"
 #include <algorithm>
+#include <atomic>
+
+namespace fn {
+
+// Per-device, thread-safe launch prerequisites (a process may drive several GPUs from several
+// threads): the SM count and the opt-in dynamic shared memory size are properties of the
+// (device, kernel) pair, so they are cached per device, not once per process.
+int device_sms() {
+  constexpr int MAXDEV = 64;
+  static std::atomic<int> cache[MAXDEV];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= MAXDEV) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+  }
+  int n = cache[dev].load(std::memory_order_relaxed);
+  if (n == 0) {
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+    cache[dev].store(n, std::memory_order_relaxed);
+  }
+  return n;
+}
+
+cudaError_t ensure_smem_attr(const void* fptr, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, int> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const auto key = std::make_pair(dev, fptr);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = done.find(key);
+    if (it != done.end() && it->second >= bytes) return cudaSuccess;
+  }
+  e = cudaFuncSetAttribute(fptr, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  int& v = done[key];
+  if (v < bytes) v = bytes;
+  return cudaSuccess;
+}
+
+}  // namespace fn
 
 namespace {
 
@@ -59,15 +106,14 @@ fn_status check_ptr16(const char* what, const void* p) {
   return FN_OK;
 }
 
-int num_sms() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
+int num_sms() { return fn::device_sms(); }
+
+bool debug_layernorm() {
+  static const bool on = [] {
+    const char* e = getenv("FN_DEBUG_LAYERNORM");
+    return e != nullptr && atoi(e) != 0;
+  }();
+  return on;
 }
 
 // ---------------------------------------------------------------- TMA descriptors
@@ -178,6 +224,17 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
   if (mode == FN_DYT && !std::isfinite(alpha)) return fail(FN_ERR_VALUE, "alpha = %g must be finite", (double)alpha);
   if (M == 0) return FN_OK;
   if (a == z) return fail(FN_ERR_VALUE, "z must not alias a");
+  if (mode == FN_LAYERNORM && debug_layernorm()) {
+    // the LayerNorm mode trusts a mean-centered input: verify it in debug runs
+    float ratio = 0.f;
+    cudaError_t e = fn::layernorm_center_check(a, M, K, dtype == FN_BF16 ? 0 : 1, stream, &ratio);
+    if (e != cudaSuccess) return cuda_fail(e, "layernorm center check");
+    ++g_launches;
+    if (!(ratio <= 1e-2f))
+      return fail(FN_ERR_VALUE, "FN_LAYERNORM input is not mean-centered: max |mean(a_m)|/rms(a_m) = %g > 1e-2 "
+                                "(fold the centering into the preceding layer with flashnorm_fold_mean_center)",
+                  (double)ratio);
+  }
   int km = kernel_mode(mode);
   if (workspace != nullptr) {
     if ((s = check_ptr16("workspace", workspace)) != FN_OK) return s;
@@ -590,19 +647,21 @@ fn_status flashnorm_glu_linear(const void* a, const void* Wgu_star, int64_t M, i
 }
 
 namespace {
-// copy streams + events of the end-to-end entry, one set per device (created once)
+// copy streams + events of the end-to-end entry, one set per (calling thread, device), created
+// on first use: concurrent callers on different host threads never share an event (an event
+// re-recorded by another thread between this call's record and wait would order the wrong work).
+// The set lives as long as the thread (not destroyed at thread exit: the CUDA context may already
+// be gone then).
 struct E2EPipe {
   cudaStream_t h2d = nullptr, d2h = nullptr;
   cudaEvent_t start = nullptr, done = nullptr;
   cudaEvent_t h[16] = {}, g[16] = {};
 };
-std::mutex g_e2e_mu;
-std::map<int, E2EPipe> g_e2e;
+thread_local std::map<int, E2EPipe> g_e2e;
 cudaError_t e2e_pipe(E2EPipe** out) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  std::lock_guard<std::mutex> lk(g_e2e_mu);
   auto it = g_e2e.find(dev);
   if (it == g_e2e.end()) {
     E2EPipe p;

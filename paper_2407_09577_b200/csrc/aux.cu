@@ -11,6 +11,8 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <cstring>
+
 namespace fn {
 
 template <typename T>
@@ -109,6 +111,50 @@ cudaError_t launch_gather_columns(const void* parts, int64_t P, int64_t M, int64
   gather_columns_kernel<<<(unsigned)blocks, 256, 0, stream>>>(static_cast<const uint4*>(parts), P, M, nl16,
                                                               static_cast<uint4*>(z));
   return cudaGetLastError();
+}
+
+// Debug check behind FN_DEBUG_LAYERNORM (include/flashnorm.h, FN_LAYERNORM): the LayerNorm mode
+// trusts that its input was mean-centered by a V* fold.  One CTA per row measures
+// |mean(a_m)| / rms(a_m) (fp32) and folds it into a device-wide maximum (non-negative floats
+// order like their bit patterns, so atomicMax on the bits is a float max).
+__device__ unsigned g_ln_center_max;
+
+template <typename T>
+__global__ void __launch_bounds__(256) layernorm_center_check_kernel(const T* __restrict__ a, int K) {
+  __shared__ float red[8];
+  const T* row = a + (size_t)blockIdx.x * K;
+  float s = 0.f, q = 0.f;
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    const float x = to_f(row[k]);
+    s += x;
+    q = fmaf(x, x, q);
+  }
+  s = block_sum(s, red);
+  q = block_sum(q, red);
+  if (threadIdx.x == 0) {
+    const float mean = s / (float)K, rms = sqrtf(q / (float)K);
+    const float ratio = rms > 0.f ? fabsf(mean) / rms : 0.f;
+    atomicMax(&g_ln_center_max, __float_as_uint(ratio));
+  }
+}
+
+cudaError_t layernorm_center_check(const void* a, int64_t M, int64_t K, int dtype, cudaStream_t stream,
+                                   float* max_ratio) {
+  void* dptr = nullptr;
+  cudaError_t e = cudaGetSymbolAddress(&dptr, g_ln_center_max);
+  if (e != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(dptr, 0, sizeof(unsigned), stream)) != cudaSuccess) return e;
+  if (dtype == 0)
+    layernorm_center_check_kernel<__nv_bfloat16><<<(unsigned)M, 256, 0, stream>>>(
+        static_cast<const __nv_bfloat16*>(a), (int)K);
+  else
+    layernorm_center_check_kernel<float><<<(unsigned)M, 256, 0, stream>>>(static_cast<const float*>(a), (int)K);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  unsigned bits = 0;
+  if ((e = cudaMemcpyAsync(&bits, dptr, sizeof(bits), cudaMemcpyDeviceToHost, stream)) != cudaSuccess) return e;
+  if ((e = cudaStreamSynchronize(stream)) != cudaSuccess) return e;
+  memcpy(max_ratio, &bits, sizeof(bits));
+  return cudaSuccess;
 }
 
 }  // namespace fn

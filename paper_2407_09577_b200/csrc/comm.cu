@@ -101,6 +101,15 @@ fn_status flashnorm_comm_destroy(void* comm) {
   return r == ncclSuccess ? FN_OK : nccl_fail("ncclCommDestroy", r);
 }
 
+fn_status flashnorm_comm_count(void* comm, int* nranks) {
+  if (comm == nullptr || nranks == nullptr) return fn::api_fail(FN_ERR_NULL, "comm=%p nranks=%p: NULL", comm,
+                                                                (void*)nranks);
+  const NcclApi& n = nccl();
+  if (!n.ok) return fn::api_fail(FN_ERR_NCCL, "%s", n.why);
+  const ncclResult_t r = n.commCount(static_cast<ncclComm_t>(comm), nranks);
+  return r == ncclSuccess ? FN_OK : nccl_fail("ncclCommCount", r);
+}
+
 int64_t flashnorm_allgather_workspace_bytes(int64_t P, int64_t M, int64_t N_local, fn_dtype dtype) {
   if (P < 1 || M < 0 || N_local < 1) return 0;
   return P * M * N_local * (dtype == FN_F32 ? 4 : 2);

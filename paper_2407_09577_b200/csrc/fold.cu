@@ -564,16 +564,10 @@ cudaError_t launch_fold_mean_center(const CUtensorMap& tm_v, const void* Vt, int
   double* mu = partial + nchunk * d_in;
   const unsigned rgrid = (unsigned)((d_in + 31) / 32 + 1);  // + the b_prev CTA
   constexpr size_t smem = 2 * fold::COLSUM_ROWS * fold::K2_TILE_BYTES;
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(k2_tiles_kernel<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k2_tiles_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k2_tiles_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k2_tiles_kernel<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  }
+  const int sms = device_sms();
+  for (const void* f : {(const void*)k2_tiles_kernel<0, false>, (const void*)k2_tiles_kernel<0, true>,
+                        (const void*)k2_tiles_kernel<1, false>, (const void*)k2_tiles_kernel<1, true>})
+    if (cudaError_t e = ensure_smem_attr(f, (int)smem); e != cudaSuccess) return e;
   const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)sms * 3);
   // pass 1 in plain stream order; the reduce and pass 2 with programmatic dependent launch
   // (griddepcontrol.wait before they read the previous pass's output) to hide launch gaps.

@@ -281,8 +281,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
             wait_a(stage);
             const uint4* row = reinterpret_cast<const uint4*>(sA + stage * A_STAGE + t * 128);
             if (kb == 0) a0 = bf16lo(row[t & 7].x);
+            // the last K block's columns >= K are TMA zero fill: they would add -a0 to S1 and
+            // a0^2 to S2, so only the cmax logical 8-column chunks inside K are summed
+            const int cmax = min(8, (p.K - kb * 64) >> 3);
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
+              if (c >= cmax) break;
               const uint4 v = row[c ^ (t & 7)];
               float d;
               d = bf16lo(v.x) - a0; s0 += d; q0 = fmaf(d, d, q0);
@@ -630,14 +634,9 @@ template <int MODE, int BN, bool TBL>
 static cudaError_t launch_gemm2_k(const CUtensorMap& ta, const CUtensorMap& tb_half, const GemmParams& p, int pairs,
                                   const void* sched, cudaStream_t stream) {
   using namespace gemm2;
-  static bool attr_set = false;
   const void* fptr = (const void*)flashnorm_gemm2_kernel<MODE, BN, TBL>;
   const int smem = smem_bytes(BN);
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(fptr, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  if (cudaError_t e = ensure_smem_attr(fptr, smem); e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * pairs);
   cfg.blockDim = dim3(THREADS);

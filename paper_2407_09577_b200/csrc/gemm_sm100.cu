@@ -159,8 +159,11 @@ __global__ void __launch_bounds__(gemm::THREADS, 1)
           if (ln) {
             // s0, s1: sum(a - a0);  s2, s3: sum((a - a0)^2)
             if (kb == 0) a0 = bf16lo(row[t & 7].x);
+            // columns >= K of the last K block are TMA zero fill: not summed (see gemm2_sm100.cu)
+            const int cmax = min(8, (p.K - kb * 64) >> 3);
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
+              if (c >= cmax) break;
               const uint4 v = row[c ^ (t & 7)];
               float d;
               d = bf16lo(v.x) - a0; s0 += d; s2 = fmaf(d, d, s2);
@@ -456,15 +459,10 @@ int gemm_smem_bytes() { return gemm::SMEM_BYTES; }
 cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int mode,
                         int num_sms, cudaStream_t stream) {
   using namespace gemm;
-  static bool attr_set[3] = {false, false, false};
   const void* fptr = mode == MODE_RMS ? (const void*)flashnorm_gemm_kernel<MODE_RMS>
                      : mode == MODE_DYT ? (const void*)flashnorm_gemm_kernel<MODE_DYT>
                                         : (const void*)flashnorm_gemm_kernel<MODE_NONE>;
-  if (!attr_set[mode]) {
-    cudaError_t e = cudaFuncSetAttribute(fptr, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    attr_set[mode] = true;
-  }
+  if (cudaError_t e = ensure_smem_attr(fptr, SMEM_BYTES); e != cudaSuccess) return e;
   const int grid = p.num_tiles < num_sms ? p.num_tiles : num_sms;
   void* args[] = {(void*)&ta, (void*)&tb, (void*)&p};
   return cudaLaunchKernel(fptr, dim3(grid), dim3(THREADS), args, SMEM_BYTES, stream);

@@ -227,12 +227,8 @@ static cudaError_t launch_gemv_regs(const __nv_bfloat16* a, const __nv_bfloat16*
   const void* fptr = mode == MODE_RMS ? (const void*)flashnorm_gemv_regs_kernel<MODE_RMS>
                      : mode == MODE_DYT ? (const void*)flashnorm_gemv_regs_kernel<MODE_DYT>
                                         : (const void*)flashnorm_gemv_regs_kernel<MODE_NONE>;
-  static size_t attr_set[3] = {0, 0, 0};
-  if (smem > 48 * 1024 && attr_set[mode] < smem) {
-    cudaError_t e = cudaFuncSetAttribute(fptr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr_set[mode] = smem;
-  }
+  if (smem > 48 * 1024)
+    if (cudaError_t e = ensure_smem_attr(fptr, (int)smem); e != cudaSuccess) return e;
   // one CTA per SM, but never fewer than ~8 output rows per CTA
   int grid = (N + 7) / 8;
   if (grid > num_sms) grid = num_sms;
@@ -561,13 +557,7 @@ cudaError_t launch_gemv(const __nv_bfloat16* a, const __nv_bfloat16* Wt, const f
   if (mode == MODE_RMS) fptr = hi ? (const void*)flashnorm_gemv_kernel<MODE_RMS, true> : (const void*)flashnorm_gemv_kernel<MODE_RMS, false>;
   else if (mode == MODE_DYT) fptr = hi ? (const void*)flashnorm_gemv_kernel<MODE_DYT, true> : (const void*)flashnorm_gemv_kernel<MODE_DYT, false>;
   else fptr = hi ? (const void*)flashnorm_gemv_kernel<MODE_NONE, true> : (const void*)flashnorm_gemv_kernel<MODE_NONE, false>;
-  static size_t attr_set[6] = {0, 0, 0, 0, 0, 0};
-  const int aslot = mode * 2 + (hi ? 1 : 0);
-  if (attr_set[aslot] < smem) {
-    cudaError_t e = cudaFuncSetAttribute(fptr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr_set[aslot] = smem;
-  }
+  if (cudaError_t e = ensure_smem_attr(fptr, (int)smem); e != cudaSuccess) return e;
   // one launch slot of the dynamic tile counter per call (64 slots, round robin): calls
   // in flight at the same time (PDL overlap, other streams) use distinct counters
   static std::atomic<unsigned> seq{0};

@@ -699,17 +699,13 @@ int dtc_stages(int R, int S) {
   return st;
 }
 size_t dtc_smem(int R, int S) { return dtc_smem_for(R, dtc_stages(R, S), S); }
-void dtc_set_attr(int mode, int R) {
-  static bool done[3][3] = {};
-  if (!done[mode][R]) {
-    // budget less 256 B of static shared memory headroom (debug/trace builds add some)
-    cudaFuncSetAttribute(dtc_fptr(mode, R), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dtc::SMEM_MAX - 256);
-    done[mode][R] = true;
-  }
+cudaError_t dtc_set_attr(int mode, int R) {
+  // budget less 256 B of static shared memory headroom (debug/trace builds add some)
+  return ensure_smem_attr(dtc_fptr(mode, R), (int)dtc::SMEM_MAX - 256);
 }
 // can `clusters` clusters of S CTAs (tile height R x 128) be resident at once?
 bool cluster_fits(int mode, int R, int S, int clusters) {
-  dtc_set_attr(mode, R);
+  if (dtc_set_attr(mode, R) != cudaSuccess) return false;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(clusters * S);
   cfg.blockDim = dim3(dtc::THREADS);
@@ -786,7 +782,7 @@ cudaError_t launch_gemv_tc(const CUtensorMap& tw, const CUtensorMap& ta, const f
                            const __nv_bfloat16* aptr) {
   using namespace dtc;
   const DtcPlan p = dtc_plan(mode, K, N, num_sms);
-  dtc_set_attr(mode, p.R);
+  if (cudaError_t e = dtc_set_attr(mode, p.R); e != cudaSuccess) return e;
   const void* fptr = dtc_fptr(mode, p.R);
   const int tiles = (N + p.R * ROWS - 1) / (p.R * ROWS);
   int S = p.S, use_cluster = p.cluster;

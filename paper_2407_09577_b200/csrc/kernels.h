@@ -7,6 +7,14 @@
 
 namespace fn {
 
+// per-device, thread-safe (api.cu): SM count of the current device; set the kernel's opt-in
+// dynamic shared memory on the current device once (cached per (device, kernel))
+int device_sms();
+cudaError_t ensure_smem_attr(const void* fptr, int bytes);
+// debug (FN_DEBUG_LAYERNORM): max over rows of |mean(a_m)| / rms(a_m); synchronizes `stream`
+cudaError_t layernorm_center_check(const void* a, int64_t M, int64_t K, int dtype, cudaStream_t stream,
+                                   float* max_ratio);
+
 enum KernelMode { MODE_RMS = 0, MODE_DYT = 1, MODE_NONE = 2 };
 
 // RoPE epilogue (NEXT-2, Fig 5(b), readings c26-c27): output columns [0, n) are

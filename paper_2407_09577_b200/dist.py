@@ -86,15 +86,20 @@ class ColumnParallelFlashNorm:
         dist.all_gather_into_tensor(flat, z_local.contiguous(), group=self.group)
         return self._permute(flat.view(self.world, M, Nl))  # [P][M][Nl] -> [M][P*Nl]
 
-    def forward_fused_gather(self, a, eps: float = 1e-5, mode: str = "rmsnorm", alpha: float = 0.5):
+    def forward_fused_gather(self, a, eps: float = 1e-5, mode: str = "rmsnorm", alpha: float = 0.5,
+                             copy: bool = False):
         """Gathered output with the all-gather FUSED into the GEMM epilogue (NEXT-3): every rank's
         epilogue stores its shard straight into every rank's gathered buffer over NVLink
         (flashnorm_linear_gather with the peers' symmetric-memory pointers), tile by tile while the
         next tiles compute; a device-side barrier then orders the peers' reads.  Replaces the
-        NCCL all-gather + permute of `forward(gather=True)`.  Needs CUDA + NCCL and
-        torch symmetric memory; the epilogue itself is tested on one GPU (several local
-        destinations, tests/test_gpu_parity.py), the multi-GPU pointer exchange is not (round 1
-        ran on one GPU)."""
+        NCCL all-gather + permute of `forward(gather=True)`.
+
+        Lifetime of the result: the gathered z lives in one of TWO persistent symmetric buffers
+        that alternate between calls (peers write into them over NVLink).  The returned tensor is
+        valid until the call after next; work that reads it on the current stream before that
+        call is ordered by the entry barrier.  Pass ``copy=True`` for an owned tensor.  Needs CUDA,
+        NCCL and torch symmetric memory; tests/test_gpu_dist.py runs it at world 1 and, on a box
+        with >= 2 GPUs, at world N (tests/test_gpu_multi.py)."""
         import torch
         import torch.distributed._symmetric_memory as symm_mem
         from . import linear_gather
@@ -102,13 +107,24 @@ class ColumnParallelFlashNorm:
         N = Nl * self.world
         key = (M, N, a.dtype, a.device)
         if getattr(self, "_symm_key", None) != key:
-            buf = symm_mem.empty((M, N), dtype=a.dtype, device=a.device)
-            hdl = symm_mem.rendezvous(buf, self.group if self.group is not None else torch.distributed.group.WORLD)
-            peers = [hdl.get_buffer(p, (M, N), a.dtype) for p in range(self.world)]
-            self._symm_key, self._symm_buf, self._symm_hdl, self._symm_peers = key, buf, hdl, peers
-        self._symm_hdl.barrier(channel=0)  # the peers finished reading the previous result
-        linear_gather(a, self.W, self._symm_peers, self.rank * Nl, c_star=self.c, eps=eps, mode=mode, alpha=alpha)
-        self._symm_hdl.barrier(channel=0)  # every shard has landed in every buffer
-        return self._symm_buf
+            grp = self.group if self.group is not None else torch.distributed.group.WORLD
+            bufs, hdls, peers = [], [], []
+            for _ in range(2):
+                buf = symm_mem.empty((M, N), dtype=a.dtype, device=a.device)
+                hdl = symm_mem.rendezvous(buf, grp)
+                bufs.append(buf)
+                hdls.append(hdl)
+                peers.append([hdl.get_buffer(p, (M, N), a.dtype) for p in range(self.world)])
+            self._symm_key, self._symm_bufs, self._symm_hdls, self._symm_peers = key, bufs, hdls, peers
+            self._symm_slot = 0
+        i = self._symm_slot
+        self._symm_slot ^= 1
+        hdl = self._symm_hdls[i]
+        hdl.barrier(channel=0)  # every rank finished the work it ordered before this call on slot i
+        linear_gather(a, self.W, self._symm_peers[i], self.rank * Nl, c_star=self.c, eps=eps, mode=mode,
+                      alpha=alpha)
+        hdl.barrier(channel=0)  # every shard has landed in every rank's buffer
+        out = self._symm_bufs[i]
+        return out.clone() if copy else out
 
     __call__ = forward

@@ -108,6 +108,8 @@ def main(tag):
             pass
     with open(os.path.join(PROF, f"{tag}_summary.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
+    if reps:
+        traffic["source"] = f"profiles/{tag}_summary.md (ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum)"
     with open(traffic_path, "w") as f:
         json.dump(traffic, f, indent=1)
     print("\n".join(lines))
