@@ -546,3 +546,33 @@ def test_linear_from_host_matches_device_path(M):
         fn.linear_from_host(a_host, Ws, cs, a_dev, z_dev, z_host)
         torch.cuda.current_stream().synchronize()
         assert np.array_equal(z_host.view(torch.int16).numpy().view(np.uint16), ref)
+
+
+_DEBUG_LN = r'''
+import sys
+sys.path.insert(0, sys.argv[1])
+import torch
+import paper_2407_09577_b200 as fn
+from synth import device as SD
+a = SD.activations(5, 64, 512, "cuda", torch.bfloat16)
+W = SD.layer(5, 256, 512, "cuda", torch.bfloat16)[0]
+ac = (a.float() - a.float().mean(1, keepdim=True)).to(torch.bfloat16)   # mean-centered rows
+fn.linear(ac, W, mode="layernorm")
+try:
+    fn.linear(a + 1.0, W, mode="layernorm")                             # |mean|/rms ~ 0.7
+    print("NOT_REJECTED")
+except fn.FlashNormError as e:
+    print("REJECTED" if "not mean-centered" in str(e) else "OTHER " + str(e))
+'''
+
+
+def test_layernorm_debug_check_rejects_uncentered_input():
+    """include/flashnorm.h FN_LAYERNORM: with FN_DEBUG_LAYERNORM=1 an input that was not
+    mean-centered upstream (PAPER.md:49) is reported as FN_ERR_VALUE; a centered one passes."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _DEBUG_LN, root], env=dict(os.environ, FN_DEBUG_LAYERNORM="1"),
+                       capture_output=True, text=True, timeout=300)
+    assert "REJECTED" in r.stdout and "NOT_REJECTED" not in r.stdout, r.stdout + r.stderr[-3000:]
