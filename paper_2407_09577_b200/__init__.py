@@ -482,6 +482,8 @@ def _rope_tables(positions, cos_tab, sin_tab, M: int, head_dim: int, name: str):
     must lie in [0, max_pos): the kernels index the tables with them (checked here on the device
     tensor, one small D2H read)."""
     torch = _torch()
+    if head_dim <= 0 or head_dim % 2:
+        raise FlashNormError(5, name, f"head_dim = {head_dim} must be positive and even (RoPE pairs)")
     _dev(positions, "positions")
     if positions.dtype != torch.int32 or positions.dim() != 1 or positions.shape[0] != M:
         raise FlashNormError(3, name, f"positions must be int32[{M}], got {positions.dtype}{list(positions.shape)}")
