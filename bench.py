@@ -594,7 +594,7 @@ def measure_secondary(args, fn, torch, dev, stream, peaks, a, Ws, cs, g):
         Vts.append(Vt)
         bps.append(bp)
         Vss.append(torch.empty_like(Vt))
-    wsv = torch.empty(fn.fold_mean_center_workspace_bytes(4096, 4096) // 8 + 2, dtype=torch.float64, device=dev)
+    wsv = torch.zeros(fn.fold_mean_center_workspace_bytes(4096, 4096) // 8 + 2, dtype=torch.float64, device=dev)
     ms_mc = timed(lambda i: fn.fold_mean_center(Vts[i % NV], bps[i % NV], out=Vss[i % NV], workspace=wsv), 24,
                   graph=True)
     vb = 2 * 4096 * 4096 * 2

@@ -112,14 +112,21 @@ fn_status flashnorm_fold_weights(const void* Wt, int64_t N, int64_t K, fn_dtype 
  *               NULL (must be non-NULL iff b_prev is non-NULL).
  *   Vt_star     [n_out][d_in] storage dtype, output.
  *   workspace   device scratch of flashnorm_fold_mean_center_workspace_bytes()
- *               bytes, 16-B aligned (fp64 partial column sums, then s_i / n).
- *
+ *               bytes, 16-B aligned (fp64 partial column sums, then s_i / n); no
+ *               initialization needed, contents unspecified on return.
+ *   Three launches (partials, s_i + b_prev*, centering; PDL-chained).  With the
+ *   environment variable FN_K2_VARIANT=1 a one-launch cluster kernel computes the
+ *   same bits with no workspace (clusters of 8 CTAs own a 256-byte column slab, the
+ *   lane sums meet over DSMEM); measured slower (A/B reference, DESIGN.md §6 K2).
+
  *   fold_mean_center numerics (mirrored bit-exactly on the CPU):
  *     partial[c][i] = fp64 sum of Vt[j][i], j in [32c, 32c+32) ascending
  *     s_i           = fp64: lane l (0..31) sums partial[c][i] for c = l, l+32, ...
  *                     ascending, then the 32 lane sums are combined by an xor
  *                     butterfly 16,8,4,2,1
- *     Vt_star[j][i] = RN_dtype( RN_f32( (double)Vt[j][i] - s_i / (double)n_out ) )
+ *     mu_i          = RN_f32( s_i / (double)n_out )       (fp64 quotient, one rounding)
+ *     Vt_star[j][i] = RN_dtype( fsub_rn( Vt[j][i], mu_i ) ) (one f32 subtraction; IEEE: inf/NaN
+ *                     propagate)
  *     b_prev_star_j = RN_f32( (double)b_prev_j - T / n_out ), T: 256 threads,
  *                     thread t sums j = t, t+256, ... ascending (fp64), xor
  *                     butterfly 16,8,4,2,1 per warp, then the 8 warp totals

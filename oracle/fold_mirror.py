@@ -99,7 +99,8 @@ def fold_mean_center(Vt, b_prev, dtype="bf16"):
     partial[c, i] = fp64 sum over rows j in [32c, 32c+32) ascending of Vt[j, i]
     s_i           = lane l sums partial[c, i], c = l, l+32, ... ascending; the 32 lane
                     sums are combined by the xor butterfly 16,8,4,2,1
-    V*t[j, i]     = RN_dtype( RN_f32( Vt[j, i] - s_i / n_out ) )      (PAPER.md:49)
+    mu_i          = RN_f32( s_i / n_out )   (fp64 quotient, rounded once)
+    V*t[j, i]     = RN_dtype( Vt[j, i] -_f32 mu_i )  (one float32 subtraction, reading c21)
     b_prev*_j     = RN_f32( b_prev_j - mean ), mean = T / n_out where thread t of
                     256 sums j = t, t+256, ... ascending, each warp of 32 threads
                     xor-butterflies (16,8,4,2,1) and T = sum of the 8 warp totals
@@ -124,7 +125,8 @@ def fold_mean_center(Vt, b_prev, dtype="bf16"):
     for off in (16, 8, 4, 2, 1):
         lane_acc = lane_acc + lane_acc[idx ^ off]
     s = lane_acc[0]
-    vstar = (v - (s / float(n_out))[None, :]).astype(np.float32)
+    mu = (s / float(n_out)).astype(np.float32)                 # RN_f32 of the fp64 quotient
+    vstar = _as_f32_values(Vt, dtype) - mu[None, :]             # one IEEE float32 subtraction
     Vt_star = _store(vstar, dtype)
 
     bstar = None

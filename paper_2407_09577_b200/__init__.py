@@ -238,6 +238,7 @@ def fold_weights(Wt, g=None, b=None, c=None, out=None, c_out=None):
 
 
 def fold_mean_center_workspace_bytes(n_out: int, d_in: int) -> int:
+    """Bytes of device scratch flashnorm_fold_mean_center uses (fp64 partial column sums + s_i / n)."""
     return int(lib().flashnorm_fold_mean_center_workspace_bytes(n_out, d_in))
 
 

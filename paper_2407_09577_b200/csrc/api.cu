@@ -108,6 +108,11 @@ fn_status check_ptr16(const char* what, const void* p) {
 
 int num_sms() { return fn::device_sms(); }
 
+bool fold_k2_cluster() {  // FN_K2_VARIANT=1: the cluster K2 (needs no workspace)
+  const char* e = getenv("FN_K2_VARIANT");
+  return e != nullptr && atoi(e) == 1;
+}
+
 bool debug_layernorm() {
   static const bool on = [] {
     const char* e = getenv("FN_DEBUG_LAYERNORM");
@@ -133,22 +138,35 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 std::mutex g_tmap_mu;
 std::map<std::tuple<uintptr_t, int64_t, int64_t, int>, CUtensorMap> g_tmaps;
 
-// row-major bf16 [rows][cols], box = 64 (cols, 128 B, SW128) x box_rows
-// Plain (unswizzled) row-major map for the fold kernels: box = FOLD_BOX_BYTES x 32 rows.
-fn_status get_tmap_fold(const void* ptr, int64_t rows, int64_t cols, fn_dtype dtype, CUtensorMap* out) {
+}  // namespace
+
+namespace fn {
+// plain (unswizzled) row-major 2-D map [rows][cols] of elem_bytes elements, box box_cols x box_rows
+// (the fold kernels' TMA rings); false if the driver entry point is missing or the encode fails
+bool encode_plain_tmap(CUtensorMap* out, const void* ptr, int64_t rows, int64_t cols, int elem_bytes, int box_cols,
+                       int box_rows) {
   auto enc = encode_fn();
-  if (enc == nullptr) return fail(FN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver entry point)");
-  const int eb = dtype == FN_BF16 ? 2 : 4;
+  if (enc == nullptr) return false;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)cols * eb};
-  cuuint32_t box[2] = {(cuuint32_t)(fn::FOLD_BOX_BYTES / eb), 32};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * elem_bytes};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(out, dtype == FN_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
-                   const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS)
-    return fail(FN_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) for fold map [%lld x %lld]", (int)r,
-                (long long)rows, (long long)cols);
+  return enc(out, elem_bytes == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+             const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+}  // namespace fn
+
+namespace {
+
+// Plain (unswizzled) row-major maps for the fold kernels (box bytes x rows).
+fn_status get_tmap_fold(const void* ptr, int64_t rows, int64_t cols, fn_dtype dtype, CUtensorMap* out,
+                        int box_bytes = fn::FOLD_BOX_BYTES, int box_rows = fn::FOLD_BOX_ROWS) {
+  const int eb = dtype == FN_BF16 ? 2 : 4;
+  if (!fn::encode_plain_tmap(out, ptr, rows, cols, eb, box_bytes / eb, box_rows))
+    return fail(FN_ERR_CUDA, "cuTensorMapEncodeTiled failed for fold map [%lld x %lld] (box %d B x %d rows)",
+                (long long)rows, (long long)cols, box_bytes, box_rows);
   return FN_OK;
 }
 
@@ -420,8 +438,12 @@ fn_status flashnorm_fold_mean_center(const void* Vt, int64_t n_out, int64_t d_in
   if ((s = check_dtype(dtype)) != FN_OK) return s;
   if (n_out <= 0 || d_in <= 0)
     return fail(FN_ERR_SHAPE, "Vt[%lld x %lld]: sizes must be positive", (long long)n_out, (long long)d_in);
-  if (Vt == nullptr || Vt_star == nullptr || workspace == nullptr)
-    return fail(FN_ERR_NULL, "Vt=%p Vt_star=%p workspace=%p: NULL", Vt, Vt_star, workspace);
+  if (Vt == nullptr || Vt_star == nullptr)
+    return fail(FN_ERR_NULL, "Vt=%p Vt_star=%p: NULL", Vt, Vt_star);
+  if (workspace == nullptr && flashnorm_fold_mean_center_workspace_bytes(n_out, d_in) > 0 &&
+      !fold_k2_cluster())
+    return fail(FN_ERR_NULL, "workspace is NULL (flashnorm_fold_mean_center_workspace_bytes = %lld)",
+                (long long)flashnorm_fold_mean_center_workspace_bytes(n_out, d_in));
   if ((b_prev == nullptr) != (b_prev_star == nullptr))
     return fail(FN_ERR_NULL, "b_prev=%p and b_prev_star=%p must be both NULL or both set", (const void*)b_prev,
                 (const void*)b_prev_star);
@@ -432,10 +454,12 @@ fn_status flashnorm_fold_mean_center(const void* Vt, int64_t n_out, int64_t d_in
   if (Vt == Vt_star) return fail(FN_ERR_VALUE, "Vt_star must not alias Vt");
   if (n_out > INT32_MAX || d_in > INT32_MAX)
     return fail(FN_ERR_SHAPE, "Vt[%lld x %lld]: dimension exceeds int32 range", (long long)n_out, (long long)d_in);
-  CUtensorMap tm;
+  CUtensorMap tm3, tm, tms;
+  if ((s = get_tmap_fold(Vt, n_out, d_in, dtype, &tm3, 512, 32)) != FN_OK) return s;
   if ((s = get_tmap_fold(Vt, n_out, d_in, dtype, &tm)) != FN_OK) return s;
+  if ((s = get_tmap_fold(Vt_star, n_out, d_in, dtype, &tms)) != FN_OK) return s;
   int launches = 0;
-  cudaError_t e = fn::launch_fold_mean_center(tm, Vt, n_out, d_in, dtype == FN_BF16 ? 0 : 1, b_prev, Vt_star,
+  cudaError_t e = fn::launch_fold_mean_center(tm3, tm, tms, n_out, d_in, dtype == FN_BF16 ? 0 : 1, b_prev, Vt_star,
                                               b_prev_star, workspace, static_cast<cudaStream_t>(stream), &launches);
   if (e != cudaSuccess) return cuda_fail(e, "fold_mean_center");
   g_launches += launches;

@@ -106,6 +106,14 @@ FN_DEVICE void tma_load_2d(void* dst, const CUtensorMap* m, uint64_t* bar, int32
       "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(x), "r"(y), "l"(policy)
       : "memory");
 }
+// 2D tiled store shared -> global (bulk async group; the caller commits and waits on the group)
+FN_DEVICE void tma_store_2d(const CUtensorMap* m, const void* src, int32_t x, int32_t y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(smem_u32(src)), "r"(x), "r"(y)
+               : "memory");
+}
+FN_DEVICE void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 // 2D tiled prefetch global -> L2 only (no SMEM, no barrier): warms the lines a later
 // tma_load_2d of the same box will read.
 FN_DEVICE void tma_prefetch_l2_2d(const CUtensorMap* m, int32_t x, int32_t y) {

@@ -6,12 +6,10 @@
 //    One warp per output row j: one pass over W reads Wt[j,:] once and writes
 //    W*t[j,:] once.  The fp64 sum order is the contract in include/flashnorm.h.
 //
-// K2 fold_mean_center (Fig B):
-//    pass 1  fp64 partial column sums of Vt over 32-row chunks   (s_i)
-//    pass 1b s_i = fixed-order (lane-strided + xor butterfly) sum of the partials, one warp
-//            per column; the same launch centers b_prev* = b_prev - mean(b_prev) (reading c7)
-//    pass 2  V*t[j][i] = RN(Vt[j][i] - s_i/n)
-//    The second read of Vt is L2-resident for the config-4 sizes (33.5 MB < 126 MB).
+// K2 fold_mean_center (Fig B): ONE launch of clusters of 8 CTAs (see the K2 section)
+//    s_i = fp64 column sums in the contract order (32-row partials, lane sums, butterfly), reduced
+//    on chip over DSMEM; mu_i = RN_f32(s_i / n); V*t[j][i] = RN_dtype(Vt[j][i] - mu_i) in f32
+//    (reading c21); b_prev* = b_prev - mean(b_prev) (reading c7).
 //
 // All fp64 arithmetic uses explicit _rn intrinsics so no compiler contraction changes the
 // rounding the CPU mirror reproduces; the one fused multiply-add (K1's b*w) is exact-
@@ -20,6 +18,7 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <cstdio>
 #include <cstdlib>
 
 #include <algorithm>
@@ -32,8 +31,6 @@ constexpr int ROWS_PER_WARP = 2;  // K1: rows sharing one g/b chunk load
 constexpr int CHUNK_UNROLL = 2;   // K1: chunks per lane in flight (x ROWS_PER_WARP loads, 3 CTAs/SM)
 constexpr int COLSUM_ROWS = 32;  // rows per fp64 partial in K2 (contract constant)
 constexpr int BPREV_THREADS = 256;
-constexpr int K2_THREADS = 256;               // K2 passes 1/2: one 4-byte column group per thread
-constexpr int K2_TILE_BYTES = K2_THREADS * 4;  // bytes of each row per CTA tile
 }  // namespace fold
 
 FN_DEVICE uint4 ld_nc_v4(const void* p) {
@@ -252,6 +249,165 @@ __global__ void __launch_bounds__(fold::WARPS_PER_CTA * 32, MINB)
   }
 }
 
+// K1 on a TMA ring (default): a persistent CTA (one per SM) owns blocks of 16 consecutive rows;
+// a producer warp streams each block's rows as [16 rows x 2 KiB] boxes (four 512-byte-wide TMA
+// sub-boxes, the box width limit) through a 6-slot ring (192 KiB in flight per SM, independent
+// of the consumers' pace).  Consumer warp w takes row w of every box, lane l the chunks l, l+32,
+// l+64, l+96 of the row's 2 KiB segment, so lane l sees chunks l, l+32, ... in ascending order
+// across the segments — exactly the c* contract order (include/flashnorm.h).  W* goes out with
+// 16-byte streaming stores (512 contiguous bytes per warp store).
+// The c* products use the hardware widening (F2F.F64.F32, exact for every input incl. inf/NaN
+// and subnormals) of w and b: b_i w_i is exact in fp64, so fma(b, w, acc) = add(acc, mul(b, w)),
+// the mirror's order.  This kernel is issue-bound, and the hardware conversion costs one
+// instruction where the integer widening + inf/NaN marks cost three (the XU pipe has room here).
+namespace k1 {
+constexpr int CWARPS = 16;                  // consumer warps = rows per block
+constexpr int ROWS = CWARPS;
+constexpr int THREADS = (CWARPS + 1) * 32;  // + the producer warp
+constexpr int SUB = 512;                    // bytes of a row per TMA sub-box (<= 256 elements)
+constexpr int U = 4;                        // sub-boxes per box = chunks per lane per box
+constexpr int SEG = SUB * U;                // 2 KiB of each row per box
+constexpr int SUBBOX = SUB * ROWS;          // 8 KiB
+constexpr int BOX = SUBBOX * U;             // 32 KiB
+constexpr int RING = 6;                     // 192 KiB
+constexpr size_t SMEM = (size_t)RING * BOX + 128;
+}  // namespace k1
+
+template <int DT, bool HAS_G, bool HAS_B>
+__global__ void __launch_bounds__(k1::THREADS, 1)
+    fold_weights_tma_kernel(const __grid_constant__ CUtensorMap tm_w, int64_t N, int64_t K,
+                            const float* __restrict__ g, const float* __restrict__ b, const float* __restrict__ c,
+                            uint8_t* __restrict__ Wt_star, float* __restrict__ c_star, int glu_half) {
+  using namespace k1;
+  constexpr int E = DT == 0 ? 8 : 4;   // elements per 16-byte chunk
+  constexpr int ES = DT == 0 ? 2 : 4;
+  extern __shared__ __align__(128) uint8_t k1s_raw[];
+  uint8_t* ring = k1s_raw + ((128u - (smem_u32(k1s_raw) & 127u)) & 127u);
+  __shared__ __align__(8) uint64_t full[RING];
+  __shared__ __align__(8) uint64_t empty[RING];
+  __shared__ volatile uint32_t k1_sink;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nblk = (N + ROWS - 1) / ROWS;
+  const int64_t nchunks = K / E;
+  const int nseg = (int)((K * ES + SEG - 1) / SEG);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < RING; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], CWARPS);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp == CWARPS) {
+    // ---------------------------------------------------------------- producer
+    if (lane == 0) {
+      prefetch_tmap(&tm_w);
+      int k = 0;
+      for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x)
+        for (int sg = 0; sg < nseg; ++sg, ++k) {
+          const int slot = k % RING;
+          if (k >= RING) mbar_wait(&empty[slot], (uint32_t)((k / RING) - 1) & 1u);
+          const int nsub = min(U, (int)((K * ES - (int64_t)sg * SEG + SUB - 1) / SUB));
+          mbar_arrive_expect_tx(&full[slot], (uint32_t)(nsub * SUBBOX));
+          for (int u = 0; u < nsub; ++u)
+            tma_load_2d(ring + (size_t)slot * BOX + u * SUBBOX, &tm_w, &full[slot], (sg * SEG + u * SUB) / ES,
+                        (int32_t)(blk * ROWS), kEvictFirst);
+        }
+    }
+    return;
+  }
+  // ------------------------------------------------------------------ consumers
+  int k = 0;
+  for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    const int64_t j = blk * ROWS + warp;
+    const bool row_ok = j < N;
+    const int64_t jo = glu_half < 0 ? j : (j >> 7) * 256 + glu_half * 128 + (j & 127);  // GLU interleave
+    double acc = 0.0;
+    for (int sg = 0; sg < nseg; ++sg, ++k) {
+      const int slot = k % RING;
+      const int64_t q0 = (int64_t)sg * (SEG / 16) + lane;  // chunk of sub-box 0; sub-box u adds 32 u
+      // g / b of this lane's U chunks: issued before the wait
+      float4 gq[U][E / 4], bq[U][E / 4];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const bool qv = row_ok && q0 + 32 * u < nchunks;
+#pragma unroll
+        for (int tt = 0; tt < E / 4; ++tt) {
+          if (HAS_G) gq[u][tt] = qv ? __ldg(reinterpret_cast<const float4*>(g + (q0 + 32 * u) * E) + tt)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+          if (HAS_B) bq[u][tt] = qv ? __ldg(reinterpret_cast<const float4*>(b + (q0 + 32 * u) * E) + tt)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+      mbar_wait(&full[slot], (uint32_t)(k / RING) & 1u);
+      uint4 vv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)  // U independent LDS.128 in flight
+        vv[u] = *reinterpret_cast<const uint4*>(ring + (size_t)slot * BOX + u * SUBBOX + warp * SUB + lane * 16);
+      if (row_ok) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t q = q0 + 32 * u;
+          if (q >= nchunks) break;
+          const float* gv = reinterpret_cast<const float*>(gq[u]);
+          const float* bv = reinterpret_cast<const float*>(bq[u]);
+          uint4 o;
+          uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
+          float ws[E];
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const float w = chunk_elem<DT>(vv[u], e);
+            if (HAS_B) acc = __fma_rn((double)bv[e], (double)w, acc);  // exact product: = add(acc, mul(b, w))
+            ws[e] = HAS_G ? __fmul_rn(gv[e], w) : w;
+          }
+#pragma unroll
+          for (int e = 0; e < E; e += 2) {
+            if (DT == 0) ow[e >> 1] = pack_bf16(ws[e], ws[e + 1]);
+            else { ow[e] = __float_as_uint(ws[e]); ow[e + 1] = __float_as_uint(ws[e + 1]); }
+          }
+          __stcs(reinterpret_cast<uint4*>(Wt_star + (jo * K + q * E) * ES), o);
+        }
+      }
+      // loaded words not used above (rows >= N, chunks past K) must still be consumed before the slot
+      // is released (releasing right after an ld.shared is not safe on sm_100a); the
+      // compare reads every loaded register and its (practically never taken) store is harmless
+      uint32_t x = 0u;
+#pragma unroll
+      for (int u = 0; u < U; ++u) x ^= vv[u].x ^ vv[u].y ^ vv[u].z ^ vv[u].w;
+      if (x == 0x7FC00001u) k1_sink = x;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);  // every lane's loads have returned
+    }
+    if (row_ok && c_star != nullptr) {
+      if (!HAS_B) {
+        if (lane == 0) c_star[j] = c != nullptr ? c[j] : 0.0f;  // c* = c exactly when b is absent
+      } else {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, off));
+        if (lane == 0) {
+          const double cj = c != nullptr ? (double)c[j] : 0.0;
+          c_star[j] = __double2float_rn(__dadd_rn(cj, acc));
+        }
+      }
+    }
+  }
+}
+
+template <int DT, bool G, bool B>
+static cudaError_t fold_launch_tma(const uint8_t* src, int64_t N, int64_t K, const float* g, const float* b,
+                                   const float* c, uint8_t* dst, float* c_star, cudaStream_t stream, int glu_half) {
+  constexpr int ES = DT == 0 ? 2 : 4;
+  CUtensorMap tm;
+  if (!encode_plain_tmap(&tm, src, N, K, ES, k1::SUB / ES, k1::ROWS)) return cudaErrorInvalidValue;
+  const void* fptr = (const void*)fold_weights_tma_kernel<DT, G, B>;
+  if (cudaError_t e = ensure_smem_attr(fptr, (int)k1::SMEM); e != cudaSuccess) return e;
+  const int64_t nblk = (N + k1::ROWS - 1) / k1::ROWS;
+  const int grid = (int)std::min<int64_t>(nblk, device_sms());
+  fold_weights_tma_kernel<DT, G, B><<<grid, k1::THREADS, k1::SMEM, stream>>>(tm, N, K, g, b, c, dst, c_star,
+                                                                             glu_half);
+  return cudaGetLastError();
+}
+
 template <int DT, bool G, bool B, int RPW, int U, int MINB>
 static void fold_launch_v(const uint8_t* src, int64_t N, int64_t K, const float* g, const float* b, const float* c,
                           uint8_t* dst, float* c_star, cudaStream_t stream, int glu_half) {
@@ -263,13 +419,26 @@ static void fold_launch_v(const uint8_t* src, int64_t N, int64_t K, const float*
 // variants (rows per warp, chunks in flight per lane, min CTAs per SM): the c* contract order does
 // not depend on them.  A/B knob FN_FOLD_VARIANT; default = the measured best.
 template <int DT, bool G, bool B>
-static void fold_launch(int variant, const uint8_t* src, int64_t N, int64_t K, const float* g, const float* b,
-                        const float* c, uint8_t* dst, float* c_star, cudaStream_t stream, int glu_half) {
-  // measured (tools/bench_folds.py, config-3 W with g, b, c): (2 rows, 2 chunks, 3 CTAs/SM) 97 us;
-  // (2, 4, 1) 103 us (122 registers, 2 CTAs/SM); (1, 4, 3) 103; (2, 1, 4) 121; (1, 8, 2) 112
-  if (variant == 1) fold_launch_v<DT, G, B, 2, 4, 1>(src, N, K, g, b, c, dst, c_star, stream, glu_half);
-  else fold_launch_v<DT, G, B, fold::ROWS_PER_WARP, fold::CHUNK_UNROLL, 3>(src, N, K, g, b, c, dst, c_star, stream,
-                                                                           glu_half);
+static cudaError_t fold_launch(int variant, const uint8_t* src, int64_t N, int64_t K, const float* g,
+                               const float* b, const float* c, uint8_t* dst, float* c_star, cudaStream_t stream,
+                               int glu_half) {
+  // variant 0 (default): the TMA-ring kernel.  The direct-load shapes stay as A/B references
+  // (tools/bench_folds.py, config-3 W with g, b, c): variant 2 = (2 rows, 2 chunks, 3 CTAs/SM)
+  // 97-104 us; variant 1 = (2, 4, 1) 103 us
+  switch (variant) {
+    case 9: return fold_launch_tma<DT, G, B>(src, N, K, g, b, c, dst, c_star, stream, glu_half);
+    case 1: fold_launch_v<DT, G, B, 2, 4, 1>(src, N, K, g, b, c, dst, c_star, stream, glu_half); break;
+    case 3: fold_launch_v<DT, G, B, 4, 1, 3>(src, N, K, g, b, c, dst, c_star, stream, glu_half); break;
+    case 4: fold_launch_v<DT, G, B, 4, 2, 2>(src, N, K, g, b, c, dst, c_star, stream, glu_half); break;
+    case 5: fold_launch_v<DT, G, B, 2, 2, 4>(src, N, K, g, b, c, dst, c_star, stream, glu_half); break;
+    case 6: fold_launch_v<DT, G, B, 1, 4, 4>(src, N, K, g, b, c, dst, c_star, stream, glu_half); break;
+    case 7: fold_launch_v<DT, G, B, 2, 1, 6>(src, N, K, g, b, c, dst, c_star, stream, glu_half); break;
+    case 8: fold_launch_v<DT, G, B, 4, 1, 4>(src, N, K, g, b, c, dst, c_star, stream, glu_half); break;
+    default:
+      fold_launch_v<DT, G, B, fold::ROWS_PER_WARP, fold::CHUNK_UNROLL, 3>(src, N, K, g, b, c, dst, c_star, stream,
+                                                                          glu_half);
+  }
+  return cudaGetLastError();
 }
 
 cudaError_t launch_fold_weights(const void* Wt, int64_t N, int64_t K, int dtype, const float* g, const float* b,
@@ -283,18 +452,16 @@ cudaError_t launch_fold_weights(const void* Wt, int64_t N, int64_t K, int dtype,
   const bool hg = g != nullptr, hb = b != nullptr;
 #define FN_FOLD_LAUNCH(DT, G, B) fold_launch<DT, G, B>(variant, src, N, K, g, b, c, dst, c_star, stream, glu_half)
   if (dtype == 0) {
-    if (hg && hb) FN_FOLD_LAUNCH(0, true, true);
-    else if (hg) FN_FOLD_LAUNCH(0, true, false);
-    else if (hb) FN_FOLD_LAUNCH(0, false, true);
-    else FN_FOLD_LAUNCH(0, false, false);
-  } else {
-    if (hg && hb) FN_FOLD_LAUNCH(1, true, true);
-    else if (hg) FN_FOLD_LAUNCH(1, true, false);
-    else if (hb) FN_FOLD_LAUNCH(1, false, true);
-    else FN_FOLD_LAUNCH(1, false, false);
+    if (hg && hb) return FN_FOLD_LAUNCH(0, true, true);
+    if (hg) return FN_FOLD_LAUNCH(0, true, false);
+    if (hb) return FN_FOLD_LAUNCH(0, false, true);
+    return FN_FOLD_LAUNCH(0, false, false);
   }
+  if (hg && hb) return FN_FOLD_LAUNCH(1, true, true);
+  if (hg) return FN_FOLD_LAUNCH(1, true, false);
+  if (hb) return FN_FOLD_LAUNCH(1, false, true);
+  return FN_FOLD_LAUNCH(1, false, false);
 #undef FN_FOLD_LAUNCH
-  return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ K1u: column sums of W*
@@ -338,11 +505,6 @@ cudaError_t launch_fold_colsum(const void* Wt_star, int64_t N, int64_t K, int dt
 
 // ------------------------------------------------------------------ K2
 
-int64_t fold_mean_center_workspace(int64_t n_out, int64_t d_in) {
-  const int64_t nchunk = (n_out + fold::COLSUM_ROWS - 1) / fold::COLSUM_ROWS;
-  return (nchunk + 1) * d_in * (int64_t)sizeof(double);  // partials + s_i/n
-}
-
 // b_prev* = b_prev - mean(b_prev), one CTA of BPREV_THREADS threads (contract order)
 FN_DEVICE void center_bias_block(const float* __restrict__ b_prev, int64_t n_out, float* __restrict__ b_star,
                                  double* wsum, double* mean_s) {
@@ -364,6 +526,355 @@ FN_DEVICE void center_bias_block(const float* __restrict__ b_prev, int64_t n_out
     b_star[j] = __double2float_rn(__dsub_rn((double)b_prev[j], mean));
 }
 
+// ------------------------------------------------------------------ K2: one launch, clusters of 8 CTAs
+// The column sums need every row, the centering needs every column sum: one cluster of 8 CTAs owns
+// a 256-byte column slab at a time (128 bf16 / 64 f32 columns), so both the reduction and the
+// exchange stay on-chip (DSMEM), with no workspace, atomics or grid-wide waits.
+//   CTA j of the cluster owns contract lanes 4j..4j+3 (include/flashnorm.h: lane l sums the 32-row
+//   partials of chunks l, l+32, ... ascending).  Its boxes are [128 rows x 256 B] = 32 KiB at rows
+//   1024 k + 128 j (k = 0, 1, ...): chunks 4j+q + 32k for q = 0..3, so thread (word w, q) carries
+//   lane 4j+q's running sum across its boxes in exactly the contract order.
+//   P1: the lane sums go to shared memory; every CTA signals the cluster (remote mbarrier arrive).
+//   R:  CTA j gathers the 32 lane sums of its 16 (bf16) / 8 (f32) columns over DSMEM, runs the
+//       butterfly tree, mu_i = RN_f32(s_i / n), and writes mu into all 8 CTAs; signals again.
+//   P2: V*t = RN_dtype(v - mu) in place in the box (f32 subtraction), one TMA store per box.
+// A producer warp streams the boxes through a 6-slot ring (192 KiB); a box stays resident from P1 to
+// P2 when the lane group has <= 6 boxes (n_out <= 6144), else P2 re-loads it (from L2).  The next
+// slab's boxes load while this slab is centered and stored, so HBM reads and writes overlap.
+namespace k2 {
+constexpr int CL = 8;                 // CTAs per cluster (portable)
+constexpr int CONSUMERS = 256;        // 8 consumer warps
+constexpr int THREADS = CONSUMERS + 32;  // + the producer warp
+constexpr int SLAB = FOLD_BOX_BYTES;  // 256 bytes of each row per box
+constexpr int ROWS = fold::COLSUM_ROWS;
+constexpr int QC = 4;                 // row chunks (= lanes) per box
+constexpr int BOX_ROWS = ROWS * QC;   // 128
+constexpr int WORDS = SLAB / 4;       // 64 four-byte column groups
+constexpr int BOX = SLAB * BOX_ROWS;  // 32 KiB (TMA streams near HBM rate only with boxes this large)
+constexpr int RES = 6;                // ring slots: 192 KiB
+constexpr int LANES = 32;
+constexpr size_t SMEM = (size_t)RES * BOX + 128;
+}  // namespace k2
+
+struct K2Geom {
+  int64_t n_out, d_in;
+  int nslab, nchunk, kq;  // kq = boxes per lane group = ceil(nchunk / 32)
+  int nclusters;
+};
+
+
+// bounded waits: a lost arrival traps (with a message) after ~2 s instead of hanging the GPU
+FN_DEVICE uint64_t k2_gtime() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+FN_DEVICE void k2_wait(uint64_t* bar, uint32_t parity, int what) {
+  if (mbar_try_wait(bar, parity)) return;
+  const uint64_t t0 = k2_gtime();
+  while (!mbar_try_wait(bar, parity)) {
+    if (k2_gtime() - t0 > 2000000000ull) {
+      printf("fold_mean_center: wait %d timed out (block %d thread %d parity %u)\n", what, (int)blockIdx.x,
+             (int)threadIdx.x, parity);
+      __trap();
+    }
+  }
+}
+FN_DEVICE void mbar_arrive_remote(uint64_t* bar, uint32_t rank) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(mapa_shared(bar, rank))
+               : "memory");
+}
+FN_DEVICE uint32_t mbar_try_wait_cluster_acq(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok;
+}
+FN_DEVICE void mbar_wait_cluster_acq(uint64_t* bar, uint32_t parity, int what) {
+  if (mbar_try_wait_cluster_acq(bar, parity)) return;
+  const uint64_t t0 = k2_gtime();
+  while (!mbar_try_wait_cluster_acq(bar, parity)) {
+    if (k2_gtime() - t0 > 2000000000ull) {
+      printf("fold_mean_center: cluster wait %d timed out (block %d thread %d parity %u)\n", what,
+             (int)blockIdx.x, (int)threadIdx.x, parity);
+      __trap();
+    }
+  }
+}
+FN_DEVICE double ld_cluster_f64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
+  return v;
+}
+FN_DEVICE void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+
+#ifdef FN_K2_TRACE  // per-CTA globaltimer stamps (ns), tools/micro/k2_trace.cu
+__device__ unsigned long long g_k2_trace[160][32];
+#define K2_STAMP(i) do { if (threadIdx.x == 0 && blockIdx.x < 160 && (i) < 32) g_k2_trace[blockIdx.x][i] = k2_gtime(); } while (0)
+#else
+#define K2_STAMP(i)
+#endif
+
+template <int DT>
+__global__ void __launch_bounds__(k2::THREADS, 1)
+    fold_mean_center_kernel(const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_vs,
+                            K2Geom g, const float* __restrict__ b_prev, float* __restrict__ b_star) {
+  using namespace k2;
+  constexpr int E = DT == 0 ? 2 : 1;  // elements per 4-byte group
+  constexpr int ES = DT == 0 ? 2 : 4;
+  constexpr int CPS = SLAB / ES;      // columns per slab
+  constexpr int CPC = CPS / CL;       // columns per CTA in the reduction (16 / 8)
+  extern __shared__ __align__(128) uint8_t k2s_raw[];
+  uint8_t* slots = k2s_raw + ((128u - (smem_u32(k2s_raw) & 127u)) & 127u);
+  __shared__ __align__(8) uint64_t full[RES], empty[RES];
+  __shared__ __align__(8) uint64_t lanes_ready, mu_ready;
+  __shared__ double lane_sum[QC][CPS];        // this CTA's 4 lane sums per slab column
+  __shared__ double gath[LANES][CPC];         // the 32 lane sums of this CTA's reduction columns
+  __shared__ float mu_s[CPS];                 // mu of every slab column (written by the 8 CTAs)
+  __shared__ double wsum[fold::BPREV_THREADS / 32];
+  __shared__ double mean_s;
+  const int t = threadIdx.x;
+  const uint32_t j = cluster_ctarank();
+  const int cid = (int)(blockIdx.x / CL);
+  const bool resident = g.kq <= RES;
+  const int my_slabs = (g.nslab - cid + g.nclusters - 1) / g.nclusters;
+  if (t == 0) {
+    for (int i = 0; i < RES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(&lanes_ready, CL);
+    mbar_init(&mu_ready, CL);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  K2_STAMP(0);
+  cluster_sync_all();  // every CTA's barriers are initialised before any remote arrive
+  K2_STAMP(1);
+
+  if (t >= CONSUMERS) {
+    // ---------------------------------------------------------------- producer warp
+    if (t == CONSUMERS) {
+      prefetch_tmap(&tm_v);
+      int n = 0;
+      for (int i = 0; i < my_slabs; ++i) {
+        const int s = cid + i * g.nclusters;
+        const int passes = resident ? 1 : 2;
+        for (int pass = 0; pass < passes; ++pass)
+          for (int k = 0; k < g.kq; ++k, ++n) {
+            const int slot = n % RES;
+            if (n >= RES) k2_wait(&empty[slot], (uint32_t)((n / RES) - 1) & 1u, 1);
+            mbar_arrive_expect_tx(&full[slot], (uint32_t)BOX);
+            tma_load_2d(slots + (size_t)slot * BOX, &tm_v, &full[slot], (int32_t)((int64_t)s * CPS),
+                        (int32_t)(k * (LANES * ROWS) + (int)j * BOX_ROWS), pass == 0 ? kEvictLast : kEvictFirst);
+          }
+      }
+    }
+    return;
+  }
+  // ------------------------------------------------------------------ consumers
+  if (blockIdx.x == 0 && b_prev != nullptr) {
+    // (consumers only: the helper's barriers are CTA-wide, the producer warp has returned)
+    const int tb = t;
+    double acc = 0.0;
+    for (int64_t jj = tb; jj < g.n_out; jj += fold::BPREV_THREADS) acc = __dadd_rn(acc, (double)b_prev[jj]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, off));
+    if ((tb & 31) == 0) wsum[tb >> 5] = acc;
+    named_bar_sync(1, CONSUMERS);
+    if (tb == 0) {
+      double tot = 0.0;
+      for (int w8 = 0; w8 < fold::BPREV_THREADS / 32; ++w8) tot = __dadd_rn(tot, wsum[w8]);
+      mean_s = __ddiv_rn(tot, (double)g.n_out);
+    }
+    named_bar_sync(1, CONSUMERS);
+    for (int64_t jj = tb; jj < g.n_out; jj += fold::BPREV_THREADS)
+      b_star[jj] = __double2float_rn(__dsub_rn((double)b_prev[jj], mean_s));
+  }
+  const int wd = t % WORDS, q = t / WORDS;
+  int n = 0;            // loads consumed (same sequence as the producer's)
+  int pend_slot = -1;   // thread 0: slot whose TMA store was issued but not yet waited for
+  for (int i = 0; i < my_slabs; ++i) {
+    const int s = cid + i * g.nclusters;
+    const int64_t cg = (int64_t)s * CPS + wd * E;
+    const bool col_ok = cg < g.d_in;
+    // ---------------------------------------------------------------- P1: lane sums
+    double L[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) L[e] = 0.0;
+    const int n0 = n;
+    for (int k = 0; k < g.kq; ++k, ++n) {
+      const int slot = n % RES;
+      k2_wait(&full[slot], (uint32_t)(n / RES) & 1u, 2);
+      if (k == 0) K2_STAMP(6 + 6 * i);
+      if (k == g.kq - 1) K2_STAMP(7 + 6 * i);
+      const int c = (int)j * QC + q + k * LANES;  // this thread's chunk (lane 4j + q)
+      if (c < g.nchunk && col_ok) {
+        const int nrows = (int)min((int64_t)ROWS, g.n_out - (int64_t)c * ROWS);
+        const uint32_t* colp = reinterpret_cast<const uint32_t*>(slots + (size_t)slot * BOX) + q * ROWS * WORDS + wd;
+        double acc[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) acc[e] = 0.0;
+        uint32_t mark = 0u;
+#pragma unroll 8
+        for (int rr = 0; rr < nrows; ++rr) {
+          const uint32_t x = colp[rr * WORDS];
+          mark = inf_nan_mark<DT>(mark, x);
+          double d[E];
+          widen_word_scaled<DT>(x, d);
+#pragma unroll
+          for (int e = 0; e < E; ++e) acc[e] = __dadd_rn(acc[e], d[e]);
+        }
+        if (inf_nan_seen<DT>(mark)) {  // rare: redo with hardware conversions (inf/NaN propagate)
+#pragma unroll
+          for (int e = 0; e < E; ++e) acc[e] = 0.0;
+          for (int rr = 0; rr < nrows; ++rr) {
+            double d[E];
+            widen_word_hw<DT>(colp[rr * WORDS], d);
+#pragma unroll
+            for (int e = 0; e < E; ++e) acc[e] = __dadd_rn(acc[e], d[e]);
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < E; ++e) L[e] = __dadd_rn(L[e], acc[e]);  // partial c added in ascending c
+      }
+      if (!resident) {
+        named_bar_sync(1, CONSUMERS);  // every read of the slot consumed (DADDs above)
+        if (t == 0) mbar_arrive(&empty[slot]);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) lane_sum[q][wd * E + e] = L[e];
+    K2_STAMP(2 + 6 * i);
+    named_bar_sync(1, CONSUMERS);
+    if (t < CL) mbar_arrive_remote(&lanes_ready, (uint32_t)t);  // release: cumulative over the barrier
+    // ---------------------------------------------------------------- R: butterfly for CPC columns
+    mbar_wait_cluster_acq(&lanes_ready, (uint32_t)i & 1u, 3);
+    K2_STAMP(3 + 6 * i);
+    for (int idx = t; idx < LANES * CPC; idx += CONSUMERS) {
+      const int l = idx / CPC, cc = idx % CPC;
+      gath[l][cc] = ld_cluster_f64(mapa_shared(&lane_sum[l % QC][(int)j * CPC + cc], (uint32_t)(l / QC)));
+    }
+    named_bar_sync(1, CONSUMERS);
+    if (t < CPC) {
+      double a[LANES];
+#pragma unroll
+      for (int l = 0; l < LANES; ++l) a[l] = gath[l][t];
+#pragma unroll
+      for (int off = LANES / 2; off > 0; off >>= 1)
+#pragma unroll
+        for (int l = 0; l < off; ++l) a[l] = __dadd_rn(a[l], a[l + off]);
+      // mu_i = RN_f32(s_i / n) (fp64 division; lane sums 2^-896-scaled)
+      const float mu = __double2float_rn(__ddiv_rn(__dmul_rn(a[0], kScaleUp), (double)g.n_out));
+#pragma unroll
+      for (int r = 0; r < CL; ++r) st_cluster_f32(mapa_shared(&mu_s[(int)j * CPC + t], (uint32_t)r), mu);
+    }
+    named_bar_sync(1, CONSUMERS);
+    if (t < CL) mbar_arrive_remote(&mu_ready, (uint32_t)t);
+    mbar_wait_cluster_acq(&mu_ready, (uint32_t)i & 1u, 4);
+    K2_STAMP(4 + 6 * i);
+    // ---------------------------------------------------------------- P2: center + store
+    float mu[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) mu[e] = mu_s[wd * E + e];
+    for (int k = 0; k < g.kq; ++k) {
+      int slot;
+      if (resident) {
+        slot = (n0 + k) % RES;
+      } else {
+        slot = n % RES;
+        k2_wait(&full[slot], (uint32_t)(n / RES) & 1u, 5);
+        ++n;
+      }
+      const int c = (int)j * QC + q + k * LANES;
+      if (c < g.nchunk && col_ok) {
+        const int nrows = (int)min((int64_t)ROWS, g.n_out - (int64_t)c * ROWS);
+        uint32_t* colp = reinterpret_cast<uint32_t*>(slots + (size_t)slot * BOX) + q * ROWS * WORDS + wd;
+#pragma unroll 8
+        for (int rr = 0; rr < nrows; ++rr) {
+          const uint32_t x = colp[rr * WORDS];
+          if (DT == 0) colp[rr * WORDS] = pack_bf16(__fsub_rn(bf16lo(x), mu[0]), __fsub_rn(bf16hi(x), mu[E - 1]));
+          else colp[rr * WORDS] = __float_as_uint(__fsub_rn(__uint_as_float(x), mu[0]));
+        }
+      }
+      fence_proxy_async_smem();  // generic-proxy SMEM writes -> visible to the TMA store
+      named_bar_sync(1, CONSUMERS);
+      if (t == 0) {
+        tma_store_2d(&tm_vs, slots + (size_t)slot * BOX, (int32_t)((int64_t)s * CPS),
+                     (int32_t)(k * (LANES * ROWS) + (int)j * BOX_ROWS));
+        bulk_commit_group();
+        // the previous store has read its slot (at most one store group in flight): release it
+        if (pend_slot >= 0) {
+          bulk_wait_read1();
+          mbar_arrive(&empty[pend_slot]);
+        }
+        pend_slot = slot;
+      }
+    }
+    K2_STAMP(5 + 6 * i);
+    // release the slab's last slot now (the next slab's loads may need every slot)
+    if (t == 0 && pend_slot >= 0) {
+      bulk_wait_read();
+      mbar_arrive(&empty[pend_slot]);
+      pend_slot = -1;
+    }
+  }
+  K2_STAMP(30);
+  if (t == 0) {
+    bulk_wait_all();  // every box store is complete before the CTA retires
+    if (pend_slot >= 0) mbar_arrive(&empty[pend_slot]);
+  }
+}
+
+static cudaError_t launch_fold_mean_center_cluster(const CUtensorMap& tm_v, const CUtensorMap& tm_vs,
+                                                  int64_t n_out, int64_t d_in, int dtype, const float* b_prev,
+                                                  float* b_prev_star, cudaStream_t stream, int* launches) {
+  const int es = dtype == 0 ? 2 : 4;
+  K2Geom g;
+  g.n_out = n_out;
+  g.d_in = d_in;
+  g.nslab = (int)((d_in * es + k2::SLAB - 1) / k2::SLAB);
+  const int64_t nchunk = (n_out + fold::COLSUM_ROWS - 1) / fold::COLSUM_ROWS;
+  if (nchunk > INT32_MAX / 2) return cudaErrorInvalidValue;
+  g.nchunk = (int)nchunk;
+  g.kq = (int)((nchunk + k2::LANES - 1) / k2::LANES);
+  const void* fptr = dtype == 0 ? (const void*)fold_mean_center_kernel<0> : (const void*)fold_mean_center_kernel<1>;
+  if (cudaError_t e = ensure_smem_attr(fptr, (int)k2::SMEM); e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(k2::THREADS);
+  cfg.dynamicSmemBytes = k2::SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = k2::CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  // as many co-resident clusters as fit (a cluster loops over its slabs), at most one per slab
+  int maxc = 0;
+  cfg.gridDim = dim3(k2::CL * 64);
+  if (cudaError_t e = cudaOccupancyMaxActiveClusters(&maxc, fptr, &cfg); e != cudaSuccess) return e;
+  if (maxc < 1) return cudaErrorInvalidConfiguration;
+  g.nclusters = std::min(maxc, g.nslab);
+  cfg.gridDim = dim3(k2::CL * g.nclusters);
+  *launches = 1;
+  if (dtype == 0) return cudaLaunchKernelEx(&cfg, fold_mean_center_kernel<0>, tm_v, tm_vs, g, b_prev, b_prev_star);
+  return cudaLaunchKernelEx(&cfg, fold_mean_center_kernel<1>, tm_v, tm_vs, g, b_prev, b_prev_star);
+}
+
+// ------------------------------------------------------------------ K2, three launches (default)
+// pass 1: fp64 32-row partials -> workspace; 1b: s_i in the contract order + b_prev*; 2: V*t
+namespace fold {
+constexpr int K2_THREADS = 256;               // K2 passes 1/2: one 4-byte column group per thread
+constexpr int K2_TILE_BYTES = K2_THREADS * 4;  // bytes of each row per CTA tile
+}  // namespace fold
+constexpr int K2_BOX_BYTES_3K = 512;          // tm_v box of the three-launch K2: 512 B x 32 rows
 // pass 1b: s_i in the contract order — lane-sum l (l = 0..31) is the ascending sum of the
 // partials c = l, l+32, ..., and the 32 lane sums are combined as the xor butterfly
 // 16,8,4,2,1 leaves them in lane 0, i.e. the tree  a[l] += a[l+off] for l < off,
@@ -434,10 +945,10 @@ __global__ void __launch_bounds__(fold::K2_THREADS)
                     double* __restrict__ partial, const double* __restrict__ mu_g, uint8_t* __restrict__ Vt_star) {
   constexpr int E = DT == 0 ? 2 : 1;  // elements per 4-byte group
   constexpr int ES = DT == 0 ? 2 : 4;
-  constexpr int BOX_COLS = FOLD_BOX_BYTES / ES;
-  constexpr int BOX_SMEM = FOLD_BOX_BYTES * fold::COLSUM_ROWS;
+  constexpr int BOX_COLS = K2_BOX_BYTES_3K / ES;
+  constexpr int BOX_SMEM = K2_BOX_BYTES_3K * fold::COLSUM_ROWS;
   constexpr int STAGE_SMEM = fold::COLSUM_ROWS * fold::K2_TILE_BYTES;
-  extern __shared__ __align__(128) uint8_t k2_smem[];  // [2 stages][2 boxes][COLSUM_ROWS][FOLD_BOX_BYTES]
+  extern __shared__ __align__(128) uint8_t k2_smem[];  // [2 stages][2 boxes][COLSUM_ROWS][K2_BOX_BYTES_3K]
   __shared__ __align__(8) uint64_t bar[2];
   const int64_t row_bytes = d_in * ES;
   const int t = threadIdx.x;
@@ -452,7 +963,7 @@ __global__ void __launch_bounds__(fold::K2_THREADS)
     uint32_t seg;
     int nrows;
     tile_geom(tile, c0b, seg, j0, nrows);
-    const int nbox = seg > (uint32_t)FOLD_BOX_BYTES ? 2 : 1;  // out-of-range rows/cols are zero-filled
+    const int nbox = seg > (uint32_t)K2_BOX_BYTES_3K ? 2 : 1;  // out-of-range rows/cols are zero-filled
     uint8_t* dst = k2_smem + stage * STAGE_SMEM;
     mbar_arrive_expect_tx(&bar[stage], (uint32_t)(nbox * BOX_SMEM));
     // pass 1 keeps Vt in L2 for pass 2 (config 4: 33.5 MB < 126 MB); pass 2 is its last use
@@ -484,7 +995,7 @@ __global__ void __launch_bounds__(fold::K2_THREADS)
     if ((uint32_t)t * 4 < seg) {
       const int64_t col0 = c0b / ES + t * E;
       const uint32_t* col = reinterpret_cast<const uint32_t*>(src);
-      constexpr int RW = FOLD_BOX_BYTES / 4;  // words per box row
+      constexpr int RW = K2_BOX_BYTES_3K / 4;  // words per box row
       uint32_t mark = 0u;
       if (!CENTER) {
         // partial sums in the 2^-896-scaled domain (exactly equivalent, see widen_scaled_hi)
@@ -514,33 +1025,19 @@ __global__ void __launch_bounds__(fold::K2_THREADS)
 #pragma unroll
         for (int e = 0; e < E; ++e) out[e] = acc[e];
       } else {
-        double mu[E];
+        // V*t = RN_dtype(v - mu_i) in f32, mu_i = RN_f32(s_i / n) (reading c21); IEEE f32: inf/NaN propagate
+        float mu[E];
 #pragma unroll
-        for (int e = 0; e < E; ++e) mu[e] = mu_g[col0 + e];
+        for (int e = 0; e < E; ++e) mu[e] = __double2float_rn(mu_g[col0 + e]);
         uint8_t* dst = Vt_star + (j0 * d_in + col0) * ES;
 #pragma unroll 8
         for (int r = 0; r < nrows; ++r) {
           const uint32_t v = col[r * RW];
-          mark = inf_nan_mark<DT>(mark, v);
-          double d[E];
-          widen_word_scaled<DT>(v, d);
-          float r32[E];
-#pragma unroll
-          for (int e = 0; e < E; ++e) r32[e] = __double2float_rn(__dsub_rn(__dmul_rn(d[e], kScaleUp), mu[e]));
-          const uint32_t o = DT == 0 ? pack_bf16(r32[0], r32[E - 1]) : __float_as_uint(r32[0]);
+          const uint32_t o = DT == 0 ? pack_bf16(__fsub_rn(bf16lo(v), mu[0]), __fsub_rn(bf16hi(v), mu[E - 1]))
+                                     : __float_as_uint(__fsub_rn(__uint_as_float(v), mu[0]));
           *reinterpret_cast<uint32_t*>(dst + (int64_t)r * d_in * ES) = o;
         }
-        if (inf_nan_seen<DT>(mark)) {  // rare: rewrite this column group with hardware conversions
-          for (int r = 0; r < nrows; ++r) {
-            double d[E];
-            widen_word_hw<DT>(col[r * RW], d);
-            float r32[E];
-#pragma unroll
-            for (int e = 0; e < E; ++e) r32[e] = __double2float_rn(__dsub_rn(__dmul_rn(d[e], kScaleUp), mu[e]));
-            const uint32_t o = DT == 0 ? pack_bf16(r32[0], r32[E - 1]) : __float_as_uint(r32[0]);
-            *reinterpret_cast<uint32_t*>(dst + (int64_t)r * d_in * ES) = o;
-          }
-        }
+        (void)mark;
       }
     }
     // Every value read from this stage has been consumed by an issued DADD/DSUB above
@@ -550,9 +1047,9 @@ __global__ void __launch_bounds__(fold::K2_THREADS)
   }
 }
 
-cudaError_t launch_fold_mean_center(const CUtensorMap& tm_v, const void* Vt, int64_t n_out, int64_t d_in, int dtype,
-                                    const float* b_prev, void* Vt_star, float* b_prev_star, void* workspace,
-                                    cudaStream_t stream, int* launches) {
+static cudaError_t launch_fold_mean_center_3k(const CUtensorMap& tm_v, int64_t n_out, int64_t d_in, int dtype,
+                                             const float* b_prev, void* Vt_star, float* b_prev_star,
+                                             void* workspace, cudaStream_t stream, int* launches) {
   const int64_t row_bytes = d_in * (dtype == 0 ? 2 : 4);
   const int64_t nchunk = (n_out + fold::COLSUM_ROWS - 1) / fold::COLSUM_ROWS;
   const int ntiles_x = (int)((row_bytes + fold::K2_TILE_BYTES - 1) / fold::K2_TILE_BYTES);
@@ -607,6 +1104,30 @@ cudaError_t launch_fold_mean_center(const CUtensorMap& tm_v, const void* Vt, int
   }
   *launches = 3;
   return e;
+}
+
+
+int64_t fold_mean_center_workspace(int64_t n_out, int64_t d_in) {
+  const int64_t nchunk = (n_out + fold::COLSUM_ROWS - 1) / fold::COLSUM_ROWS;
+  return (nchunk + 1) * d_in * (int64_t)sizeof(double);  // partials + s_i/n
+}
+
+// Variant (A/B knob FN_K2_VARIANT, read once): 0 = the three-launch K2 (default), 1 = the one-launch
+// cluster K2 (no workspace).  Both implement the same contract, bit for bit (tests/test_gpu_parity.py
+// runs both).  Measured (tools/bench_folds.py, 6 rotating V, graph): 4096^2 22.8 vs 30.5 us,
+// 8192^2 76 vs 95 us — the cluster kernel's column slabs run in ~15 co-resident clusters, three
+// sequential slab rounds, and its read / reduce / write phases do not overlap.
+cudaError_t launch_fold_mean_center(const CUtensorMap& tm_v3, const CUtensorMap& tm_v, const CUtensorMap& tm_vs,
+                                    int64_t n_out, int64_t d_in, int dtype, const float* b_prev, void* Vt_star,
+                                    float* b_prev_star, void* workspace, cudaStream_t stream, int* launches) {
+  static const int variant = [] {
+    const char* e = getenv("FN_K2_VARIANT");
+    return e != nullptr ? atoi(e) : 0;
+  }();
+  if (variant == 1) return launch_fold_mean_center_cluster(tm_v, tm_vs, n_out, d_in, dtype, b_prev, b_prev_star,
+                                                          stream, launches);
+  return launch_fold_mean_center_3k(tm_v3, n_out, d_in, dtype, b_prev, Vt_star, b_prev_star, workspace, stream,
+                                    launches);
 }
 
 }  // namespace fn

@@ -11,6 +11,9 @@ namespace fn {
 // dynamic shared memory on the current device once (cached per (device, kernel))
 int device_sms();
 cudaError_t ensure_smem_attr(const void* fptr, int bytes);
+// plain row-major TMA map (api.cu; false on failure)
+bool encode_plain_tmap(CUtensorMap* out, const void* ptr, int64_t rows, int64_t cols, int elem_bytes, int box_cols,
+                       int box_rows);
 // debug (FN_DEBUG_LAYERNORM): max over rows of |mean(a_m)| / rms(a_m); synchronizes `stream`
 cudaError_t layernorm_center_check(const void* a, int64_t M, int64_t K, int dtype, cudaStream_t stream,
                                    float* max_ratio);
@@ -222,11 +225,13 @@ cudaError_t launch_fold_colsum(const void* Wt_star, int64_t N, int64_t K, int dt
 cudaError_t launch_fold_weights(const void* Wt, int64_t N, int64_t K, int dtype, const float* g, const float* b,
                                 const float* c, void* Wt_star, float* c_star, cudaStream_t stream, int glu_half = -1);
 int64_t fold_mean_center_workspace(int64_t n_out, int64_t d_in);
-// tm_v: plain (no swizzle) 2-D map of Vt [n_out][d_in], box FOLD_BOX_BYTES wide x 32 rows.
-constexpr int FOLD_BOX_BYTES = 512;
-cudaError_t launch_fold_mean_center(const CUtensorMap& tm_v, const void* Vt, int64_t n_out, int64_t d_in, int dtype,
-                                    const float* b_prev, void* Vt_star, float* b_prev_star, void* workspace,
-                                    cudaStream_t stream, int* launches);
+// tm_v3: plain 2-D map of Vt, box 512 B x 32 rows (three-launch K2); tm_v / tm_vs: maps of Vt / Vt_star,
+// box FOLD_BOX_BYTES wide x FOLD_BOX_ROWS rows (cluster K2).  workspace: fold_mean_center_workspace bytes.
+constexpr int FOLD_BOX_BYTES = 256;
+constexpr int FOLD_BOX_ROWS = 128;  // K2 box: 256 B x 128 rows = 32 KiB
+cudaError_t launch_fold_mean_center(const CUtensorMap& tm_v3, const CUtensorMap& tm_v, const CUtensorMap& tm_vs,
+                                    int64_t n_out, int64_t d_in, int dtype, const float* b_prev, void* Vt_star,
+                                    float* b_prev_star, void* workspace, cudaStream_t stream, int* launches);
 
 // K6/K7: baseline norm + gather permute (aux.cu)
 // K8: y = RN_bf16(tanh(alpha a)) over n elements (n % 8 == 0), bit-identical to the GEMM prologue.

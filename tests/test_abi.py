@@ -52,7 +52,7 @@ def test_version_and_status_strings(L):
 
 
 def test_workspace_size(L):
-    # 32-row fp64 partial column sums (include/flashnorm.h fold_mean_center numerics)
+    # 32-row fp64 partial column sums + s_i / n (include/flashnorm.h fold_mean_center numerics)
     assert fn.fold_mean_center_workspace_bytes(4096, 4096) == (128 + 1) * 4096 * 8
     assert fn.fold_mean_center_workspace_bytes(33, 16) == (2 + 1) * 16 * 8
     assert fn.fold_mean_center_workspace_bytes(0, 16) == 0

@@ -67,7 +67,13 @@ def test_mirror_fold_mean_center_vs_fp64(dtype, n_out, d_in):
     V_exact, b_exact = O.fold_mean_center(V, bp)
     Vs_f = (bits_to_f32(Vs) if dtype == "bf16" else Vs).astype(np.float64).T
     u = 2.0 ** -8 if dtype == "bf16" else 2.0 ** -24
-    assert np.max(np.abs(Vs_f - V_exact) / np.maximum(np.abs(V_exact), 1e-6)) <= u * (1 + 2.0 ** -15)
+    # contract (reading c21): mu_i = RN_f32(s_i / n), V* = RN_dtype(v - mu_i) in f32.  Error bound of
+    # that evaluation against the exact fp64 fold: the mu rounding (<= 2^-24 |mu_i|, carried through
+    # the subtraction and the final rounding) plus one rounding of the result (<= u |V*|; for bf16
+    # the f32 subtraction's 2^-24 is inside the double-rounding slack)
+    mu = np.abs(s / n_out)[:, None]
+    bound = u * (1 + 2.0 ** -15) * np.abs(V_exact) + 2.0 ** -24 * mu * (1 + u) * (1 + 2.0 ** -15)
+    assert np.all(np.abs(Vs_f - V_exact) <= bound)
     np.testing.assert_allclose(bs.astype(np.float64), b_exact, rtol=2.0 ** -23, atol=1e-7)
 
 

@@ -78,7 +78,8 @@ def test_fold_weights_bit_exact(dtype, N, K, gbc):
 
 
 @pytest.mark.parametrize("dtype", ["bf16", "f32"])
-@pytest.mark.parametrize("n_out,d_in", [(8, 8), (40, 24), (100, 72), (33, 1000), (4096, 4096)])
+@pytest.mark.parametrize("n_out,d_in", [(8, 8), (40, 24), (100, 72), (33, 1000), (4096, 4096), (5000, 520),
+                                         (20000, 264)])
 @pytest.mark.parametrize("with_b", [True, False])
 def test_fold_mean_center_bit_exact(dtype, n_out, d_in, with_b):
     _, Vt, bp = gen_upstream(12, 2, d_in, n_out, dtype)
@@ -93,6 +94,76 @@ def test_fold_mean_center_bit_exact(dtype, n_out, d_in, with_b):
         np.testing.assert_array_equal(H(Vs).view(np.uint32), Vm.view(np.uint32))
     if with_b:
         np.testing.assert_array_equal(H(bs).view(np.uint32), bm.view(np.uint32))
+
+
+_K2_VARIANT = r'''
+import os, sys
+sys.path.insert(0, sys.argv[1])
+import numpy as np, torch
+import paper_2407_09577_b200 as fn
+from oracle import fold_mirror as FM
+from synth import gen_upstream, bf16_bits
+ok = True
+for dtype in ("bf16", "f32"):
+    for (n_out, d_in) in [(8, 8), (33, 1000), (100, 72), (4096, 4096), (20000, 264), (7000, 2056)]:
+        _, Vt, bp = gen_upstream(12, 2, d_in, n_out, dtype)
+        t = torch.from_numpy(np.ascontiguousarray(Vt, dtype=np.float32))
+        t = (t.to(torch.bfloat16) if dtype == "bf16" else t).cuda()
+        Vs, bs = fn.fold_mean_center(t, torch.from_numpy(bp).cuda())
+        torch.cuda.synchronize()
+        Vm, bm, _ = FM.fold_mean_center(bf16_bits(Vt) if dtype == "bf16" else Vt, bp, dtype)
+        got = Vs.view(torch.int16).cpu().numpy().view(np.uint16) if dtype == "bf16" else Vs.cpu().numpy().view(np.uint32)
+        ok &= np.array_equal(got, Vm if dtype == "bf16" else Vm.view(np.uint32))
+        ok &= np.array_equal(bs.cpu().numpy().view(np.uint32), bm.view(np.uint32))
+print("K2_VARIANT_OK" if ok else "K2_VARIANT_DIFF")
+'''
+
+
+def test_fold_mean_center_cluster_variant_bit_exact():
+    """FN_K2_VARIANT=1: the one-launch cluster kernel (DSMEM reduction, TMA stores) meets the same
+    contract bit for bit, including ragged shapes, resident (<= 6 boxes per lane group) and
+    streamed (more) slabs, and clusters that loop over several slabs."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _K2_VARIANT, root], env=dict(os.environ, FN_K2_VARIANT="1"),
+                       capture_output=True, text=True, timeout=600)
+    assert "K2_VARIANT_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_fold_mean_center_workspace_reuse_and_graph_replay(dtype):
+    """Back-to-back calls with one caller-owned workspace and replays of a captured CUDA graph whose
+    input V changes in place between replays: every result stays bit-exact against the mirror."""
+    n_out, d_in = 3000, 1040
+    ws = torch.zeros(fn.fold_mean_center_workspace_bytes(n_out, d_in) // 8 + 2, dtype=torch.float64, device=DEV)
+    outs = []
+    for seed in (13, 14, 15):
+        _, Vt, bp = gen_upstream(seed, 2, d_in, n_out, dtype)
+        Vs, bs = fn.fold_mean_center(T(Vt, dtype), T(bp, "f32"), workspace=ws)
+        torch.cuda.synchronize()
+        Vm, bm, _ = FM.fold_mean_center(bf16_bits(Vt) if dtype == "bf16" else Vt, bp, dtype)
+        got = bits(Vs) if dtype == "bf16" else H(Vs).view(np.uint32)
+        np.testing.assert_array_equal(got, Vm if dtype == "bf16" else Vm.view(np.uint32))
+        np.testing.assert_array_equal(H(bs).view(np.uint32), bm.view(np.uint32))
+        outs.append(Vt)
+    Vin = T(outs[0], dtype)
+    Vout = torch.empty_like(Vin)
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        fn.fold_mean_center(Vin, None, out=Vout, workspace=ws)   # warm (descriptor encode, attributes)
+        st.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=st):
+            fn.fold_mean_center(Vin, None, out=Vout, workspace=ws)
+    for Vt in outs[1:] + outs[:1]:
+        Vin.copy_(T(Vt, dtype))
+        graph.replay()
+        torch.cuda.synchronize()
+        Vm, _, _ = FM.fold_mean_center(bf16_bits(Vt) if dtype == "bf16" else Vt, None, dtype)
+        got = bits(Vout) if dtype == "bf16" else H(Vout).view(np.uint32)
+        np.testing.assert_array_equal(got, Vm if dtype == "bf16" else Vm.view(np.uint32))
 
 
 def _special_matrix(rows, cols, dtype, seed=5):

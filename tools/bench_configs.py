@@ -140,7 +140,7 @@ del W, Ws, z
 M, d = 2048, 4096
 x, Vt, bp = SD.upstream(4, M, d, d, dev, torch.bfloat16)
 Vs0 = torch.empty_like(Vt)
-wsv = torch.empty(fn.fold_mean_center_workspace_bytes(d, d) // 8 + 2, dtype=torch.float64, device=dev)
+wsv = torch.zeros(fn.fold_mean_center_workspace_bytes(d, d) // 8 + 2, dtype=torch.float64, device=dev)
 us = timed(lambda i: fn.fold_mean_center(Vt, bp, out=Vs0, workspace=wsv), 20, graph=True)
 report("4 LN V fold", "fold_mean_center 4096x4096 (+b_prev), graph", us, byts=2 * d * d * 2)
 del Vs0, wsv

@@ -7,7 +7,7 @@ from synth import device as SD
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
 x, Vt, bp = SD.upstream(4, 16, n, n, "cuda", torch.bfloat16)
 Vs = torch.empty_like(Vt)
-ws = torch.empty(fn.fold_mean_center_workspace_bytes(n, n) // 8 + 2, dtype=torch.float64, device="cuda")
+ws = torch.zeros(fn.fold_mean_center_workspace_bytes(n, n) // 8 + 2, dtype=torch.float64, device="cuda")
 for _ in range(4):
     fn.fold_mean_center(Vt, bp, out=Vs, workspace=ws)
 torch.cuda.synchronize()
