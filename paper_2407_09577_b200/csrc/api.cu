@@ -197,6 +197,36 @@ fn_status get_tmap(const void* ptr, int64_t rows, int64_t cols, int box_rows, CU
   return FN_OK;
 }
 
+// 3-D view of a row-major bf16 [rows][cols] matrix (cols % 64 == 0) as {64, rows, cols / 64} with strides
+// {cols * 2, 128} bytes: one box {64, box_rows, 2} is two consecutive SW128 [box_rows x 64] tiles of
+// k blocks kb, kb + 1 (the decode kernel's 32 KiB stage); cached like get_tmap
+fn_status get_tmap_kpair(const void* ptr, int64_t rows, int64_t cols, int box_rows, CUtensorMap* out) {
+  const auto key = std::make_tuple(reinterpret_cast<uintptr_t>(ptr), rows, cols, 100000 + box_rows);
+  std::lock_guard<std::mutex> lk(g_tmap_mu);
+  auto it = g_tmaps.find(key);
+  if (it != g_tmaps.end()) {
+    *out = it->second;
+    return FN_OK;
+  }
+  auto enc = encode_fn();
+  if (enc == nullptr) return fail(FN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (driver entry point)");
+  CUtensorMap m;
+  cuuint64_t dims[3] = {64, (cuuint64_t)rows, (cuuint64_t)(cols / 64)};
+  cuuint64_t strides[2] = {(cuuint64_t)cols * 2, 128};
+  cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 2};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(FN_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) for the k-pair view of [%lld x %lld] box %d", (int)r,
+                (long long)rows, (long long)cols, box_rows);
+  if (g_tmaps.size() > 4096) g_tmaps.clear();
+  g_tmaps.emplace(key, m);
+  *out = m;
+  return FN_OK;
+}
+
 int kernel_mode(fn_mode m) {
   switch (m) {
     case FN_RMSNORM:
@@ -290,8 +320,14 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
   const bool use_gemv = path == FN_PATH_GEMV || path == FN_PATH_GEMV_MMA || (path == FN_PATH_AUTO && gemv_ok);
   if (use_gemv && path != FN_PATH_GEMV_MMA && tc_ok) {
     CUtensorMap tw, ta;
-    if ((s = get_tmap(Wt_star, N, K, fn::gemv_tc_tile_rows(km, (int)K, (int)N, num_sms()), &tw)) != FN_OK) return s;
-    if ((s = get_tmap(a, M, K, 16, &ta)) != FN_OK) return s;
+    const int trows = std::min(fn::gemv_tc_tile_rows(km, (int)K, (int)N, num_sms()), 256);  // TMA box rows
+    if (fn::gemv_tc_kblocks(km, (int)K, (int)N, num_sms()) == 2) {
+      if ((s = get_tmap_kpair(Wt_star, N, K, trows, &tw)) != FN_OK) return s;
+      if ((s = get_tmap_kpair(a, M, K, 16, &ta)) != FN_OK) return s;
+    } else {
+      if ((s = get_tmap(Wt_star, N, K, trows, &tw)) != FN_OK) return s;
+      if ((s = get_tmap(a, M, K, 16, &ta)) != FN_OK) return s;
+    }
     cudaError_t e = fn::launch_gemv_tc(tw, ta, c_star, static_cast<__nv_bfloat16*>(z), (int)M, (int)K, (int)N, eps,
                                        alpha, km, num_sms(), stream, ex.row_scale, ex.rope,
                                        static_cast<const __nv_bfloat16*>(Wt_star), static_cast<const __nv_bfloat16*>(a));

@@ -47,16 +47,20 @@ constexpr int TOK = 16;                 // token rows (MMA N; rows >= M are TMA 
 constexpr int BK = 64;                  // k per stage (one SW128 atom row of bf16)
 constexpr int T_STAGE = TOK * BK * 2;   // 2 KiB
 constexpr int THREADS = 192;
-constexpr int TMEM_COLS = 32;           // D of MMA j in columns [16j, 16j+16), j < R <= 2
+constexpr int TMEM_COLS = 32;           // D of MMA j in columns [16j, 16j+16), j < R <= 2 (R = 4: 64)
+constexpr int BOX_ROWS_MAX = 256;       // TMA box rows (R = 4 tiles load two boxes per stage)
 constexpr int MAX_S = 8;                // K splits per tile (portable cluster size)
 constexpr int MAX_CTAS = 160;           // tiles * S <= #SMs (148)
 constexpr int SLOTS = 4;                // global-mode partial buffers, round robin over launches
 constexpr size_t SMEM_MAX = 232448;     // opt-in dynamic SMEM per CTA (ring sizes stay below it)
 // tile = R x 128 W* rows (R MMAs per k step sharing the token operand)
-template <int R> struct Cfg {
-  static constexpr int W_STAGE = R * ROWS * BK * 2;                  // 16 / 32 KiB
-  static constexpr int STAGES = R == 1 ? 12 : 6;                     // default: ~204-216 KiB ring
-  static size_t smem(int stages) { return 1024 + (size_t)stages * (W_STAGE + T_STAGE) + 1024; }
+// stage = KB consecutive 64-wide k blocks (KB = 2: one 3-D TMA box of 32 KiB for a 128-row tile —
+// TMA streams near the HBM rate only with boxes this large, tools/micro/stream_bw.cu)
+template <int R, int KB = 1> struct Cfg {
+  static constexpr int W_STAGE = R * ROWS * BK * 2 * KB;             // 16 / 32 KiB
+  static constexpr int TK_STAGE = T_STAGE * KB;                      // token bytes per stage
+  static constexpr int STAGES = (R * KB) == 1 ? 12 : 6;              // default: ~204-216 KiB ring
+  static size_t smem(int stages) { return 1024 + (size_t)stages * (W_STAGE + TK_STAGE) + 1024; }
 };
 }  // namespace dtc
 
@@ -105,8 +109,8 @@ __device__ long long g_tc_epi[2][8];
 #define TC_STAGE(w, i)
 #endif
 
-template <int MODE, int R>
-__global__ void __launch_bounds__(dtc::THREADS, 2)  // <= 168 registers: two CTAs may share an SM
+template <int MODE, int R, int KB>
+__global__ void __launch_bounds__(dtc::THREADS, R == 4 ? 1 : 2)  // R < 4: <= 168 registers (two CTAs may share an SM)
     flashnorm_gemv_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_a,
                              const float* __restrict__ cstar, __nv_bfloat16* __restrict__ z, int M, int K, int N,
                              float eps, float alpha, int S, int slot, int use_cluster,
@@ -114,7 +118,9 @@ __global__ void __launch_bounds__(dtc::THREADS, 2)  // <= 168 registers: two CTA
                              int stages, int flags, const __nv_bfloat16* __restrict__ wptr,
                              const __nv_bfloat16* __restrict__ aptr) {
   using namespace dtc;
-  constexpr int W_STAGE = Cfg<R>::W_STAGE;
+  constexpr int W_STAGE = Cfg<R, KB>::W_STAGE;
+  constexpr int T_STAGE = Cfg<R, KB>::TK_STAGE;  // shadows dtc::T_STAGE: KB token boxes per stage
+  constexpr int KSUB = ROWS * BK * 2;             // bytes of one 128-row x 64-k W* sub-block
   const int STAGES = stages;  // ring depth (runtime: the host sizes it for 1 or 2 CTAs per SM)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -139,13 +145,41 @@ __global__ void __launch_bounds__(dtc::THREADS, 2)  // <= 168 registers: two CTA
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
-  const int rank = (int)(blockIdx.x % (unsigned)S);  // == %cluster_ctarank in cluster mode
+  const int rank = (int)(blockIdx.x % (unsigned)S);  // K-split rank within the tile
+  // cluster mode: use_cluster = CTAs per cluster = T tiles x S splits; the tile's leader (rank 0) has
+  // cluster rank `lead` (clusters are consecutive blockIdx.x ranges, tiles consecutive inside them)
+  const uint32_t lead = use_cluster ? (uint32_t)((int)(blockIdx.x % (unsigned)use_cluster) - rank) : 0u;
   const int tile = (int)(blockIdx.x / (unsigned)S);
   const int n0 = tile * R * ROWS;
-  const int nkb = (K + BK - 1) / BK;
+  constexpr int TCOLS = R * TOK > TMEM_COLS ? R * TOK : TMEM_COLS;  // TMEM columns (power of two >= 32)
+  constexpr int NBOX = R * ROWS > BOX_ROWS_MAX ? R * ROWS / BOX_ROWS_MAX : 1;  // TMA boxes per W* stage
+  const int nkb = (K + BK * KB - 1) / (BK * KB);  // stages of KB k blocks
   const int kb0 = (int)(((long long)rank * nkb) / S);
   const int kb1 = (int)(((long long)(rank + 1) * nkb) / S);
   const int my_kb = kb1 - kb0;  // >= 1 (S <= nkb)
+  // stage i of this CTA: KB = 1 -> 2-D box at k = i * 64; KB = 2 -> 3-D box {64, rows, 2} at k block 2 i
+  auto load_w = [&](void* dst, uint64_t* bar, int i) {
+    if (KB == 1) {
+#pragma unroll
+      for (int b = 0; b < NBOX; ++b)
+        tma_load_2d(static_cast<uint8_t*>(dst) + b * (W_STAGE / NBOX), &tmap_w, bar, i * BK,
+                    n0 + b * (R * ROWS / NBOX), kEvictFirst);
+    } else {
+      tma_load_3d(dst, &tmap_w, bar, 0, n0, i * KB, kEvictFirst);
+    }
+  };
+  auto load_t = [&](void* dst, uint64_t* bar, int i) {
+    if (KB == 1) tma_load_2d(dst, &tmap_a, bar, i * BK, 0, kEvictLast);
+    else tma_load_3d(dst, &tmap_a, bar, 0, 0, i * KB, kEvictLast);
+  };
+  auto prefetch_w = [&](int i, int nrow0) {
+    if (KB == 1) {
+#pragma unroll
+      for (int b = 0; b < NBOX; ++b) tma_prefetch_l2_2d(&tmap_w, i * BK, nrow0 + b * (R * ROWS / NBOX));
+    } else {
+      tma_prefetch_l2_3d(&tmap_w, 0, nrow0, i * KB);
+    }
+  };
 
   pdl_launch_dependents();  // the next call's CTAs may queue for free SMs right away
 #ifdef FN_GEMV_TC_TRACE
@@ -171,7 +205,7 @@ __global__ void __launch_bounds__(dtc::THREADS, 2)  // <= 168 registers: two CTA
       mbar_arrive_expect_tx(recv_bar, (uint32_t)((S - 1) * RECV_STRIDE * 4));
   }
   if (warp == 1) {
-    tmem_alloc(tmem_holder, TMEM_COLS);
+    tmem_alloc(tmem_holder, TCOLS);
     tmem_relinquish();
   }
   tc_fence_before();
@@ -188,13 +222,13 @@ __global__ void __launch_bounds__(dtc::THREADS, 2)  // <= 168 registers: two CTA
       // W* is constant: its first `pre` stages stream before the dependency wait
       for (int i = 0; i < pre; ++i) {
         mbar_arrive_expect_tx(&full[i], W_STAGE + T_STAGE);
-        tma_load_2d(sW + i * W_STAGE, &tmap_w, &full[i], (kb0 + i) * BK, n0, kEvictFirst);
+        load_w(sW + i * W_STAGE, &full[i], kb0 + i);
       }
       // ... and the rest of this CTA's W* slice is pulled into L2 (up to l2pf boxes), so the
       // HBM stream keeps going while this call waits for the previous one; the ring refills
       // after the wait then hit L2
       for (int i = pre; i < my_kb && i < pre + l2pf; ++i)
-        tma_prefetch_l2_2d(&tmap_w, (kb0 + i) * BK, n0);  // the box is the whole R x 128-row tile
+        prefetch_w(kb0 + i, n0);  // the box is the whole R x 128-row tile
       if (flags & 2) {
         // ... and the whole slice of the CTA half a grid away: CTAs start in blockIdx order as
         // the previous call's CTAs leave, so the upper half typically starts late; its W* is
@@ -202,12 +236,12 @@ __global__ void __launch_bounds__(dtc::THREADS, 2)  // <= 168 registers: two CTA
         const int pb = (int)((blockIdx.x + gridDim.x / 2) % gridDim.x);
         const int prank = pb % S, pn0 = (pb / S) * R * ROWS;
         const int pk0 = (int)(((long long)prank * nkb) / S), pk1 = (int)(((long long)(prank + 1) * nkb) / S);
-        for (int i = pk0; i < pk1; ++i) tma_prefetch_l2_2d(&tmap_w, i * BK, pn0);
+        for (int i = pk0; i < pk1; ++i) prefetch_w(i, pn0);
       }
       pdl_wait_prior_grid();  // tokens may be the previous kernel's output
       TC_TRACE(1);
       for (int i = 0; i < pre; ++i)
-        tma_load_2d(sT + i * T_STAGE, &tmap_a, &full[i], (kb0 + i) * BK, 0, kEvictLast);
+        load_t(sT + i * T_STAGE, &full[i], kb0 + i);
       int stage = pre == STAGES ? 0 : pre;
       uint32_t phase = pre == STAGES ? 1u : 0u;
       for (int i = 0; i < pre; ++i) TC_STAGE(1, i);
@@ -215,8 +249,8 @@ __global__ void __launch_bounds__(dtc::THREADS, 2)  // <= 168 registers: two CTA
         mbar_wait(&empty[stage], phase ^ 1);
         TC_STAGE(1, i);
         mbar_arrive_expect_tx(&full[stage], W_STAGE + T_STAGE);
-        tma_load_2d(sW + stage * W_STAGE, &tmap_w, &full[stage], (kb0 + i) * BK, n0, kEvictFirst);
-        tma_load_2d(sT + stage * T_STAGE, &tmap_a, &full[stage], (kb0 + i) * BK, 0, kEvictLast);
+        load_w(sW + stage * W_STAGE, &full[stage], kb0 + i);
+        load_t(sT + stage * T_STAGE, &full[stage], kb0 + i);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
@@ -236,13 +270,16 @@ __global__ void __launch_bounds__(dtc::THREADS, 2)  // <= 168 registers: two CTA
         if (i == my_kb - 1) TC_TRACE(7);
 #endif
         tc_fence_after();
-        const uint64_t bdesc = make_sw128_desc(smem_u32(sT + stage * T_STAGE));
 #pragma unroll
-        for (int j = 0; j < R; ++j) {  // rows [128j, 128j+128) of the tile: 16 KiB into the box
-          const uint64_t adesc = make_sw128_desc(smem_u32(sW + stage * W_STAGE + j * ROWS * BK * 2));
+        for (int kk = 0; kk < KB; ++kk) {  // the stage's k blocks: [kb][rows][64] / [kb][16][64] in SMEM
+          const uint64_t bdesc = make_sw128_desc(smem_u32(sT + stage * T_STAGE + kk * dtc::T_STAGE));
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)
-            umma_bf16(tmem_base + j * TOK, adesc + 2 * k, bdesc + 2 * k, idesc, (i | k) != 0);
+          for (int j = 0; j < R; ++j) {  // rows [128j, 128j+128) of the tile: 16 KiB into the box
+            const uint64_t adesc = make_sw128_desc(smem_u32(sW + stage * W_STAGE + (kk * R + j) * KSUB));
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              umma_bf16(tmem_base + j * TOK, adesc + 2 * k, bdesc + 2 * k, idesc, (i | kk | k) != 0);
+          }
         }
         umma_commit(&empty[stage]);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -260,16 +297,19 @@ __global__ void __launch_bounds__(dtc::THREADS, 2)  // <= 168 registers: two CTA
       uint32_t phase = 0;
       for (int i = 0; i < my_kb; ++i) {
         mbar_wait_warp(&full[stage], phase);
-        uint4* p = reinterpret_cast<uint4*>(sT + stage * T_STAGE) + t;
-        uint4 v = *p;
-        uint32_t* w = reinterpret_cast<uint32_t*>(&v);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          __nv_bfloat162 x = *reinterpret_cast<__nv_bfloat162*>(&w[e]);
-          x = __hmul2(x, alpha2);
-          w[e] = tanh_approx_bf16x2(*reinterpret_cast<uint32_t*>(&x));
+        for (int kk = 0; kk < KB; ++kk) {
+          uint4* p = reinterpret_cast<uint4*>(sT + stage * T_STAGE + kk * dtc::T_STAGE) + t;
+          uint4 v = *p;
+          uint32_t* w = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            __nv_bfloat162 x = *reinterpret_cast<__nv_bfloat162*>(&w[e]);
+            x = __hmul2(x, alpha2);
+            w[e] = tanh_approx_bf16x2(*reinterpret_cast<uint32_t*>(&x));
+          }
+          *p = v;
         }
-        *p = v;
         fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
         named_bar_sync(2, 128);
         if (t == 0) mbar_arrive(&ready[stage]);
@@ -293,11 +333,12 @@ __global__ void __launch_bounds__(dtc::THREADS, 2)  // <= 168 registers: two CTA
         }
       };
       const int pre = my_kb < STAGES ? my_kb : STAGES;
-      if (flags & 4) pf(n0, kb0 + pre, kb1);
+      const int nkb64 = (K + BK - 1) / BK;  // pf() works in 64-wide k blocks
+      if (flags & 4) pf(n0, (kb0 + pre) * KB, min(kb1 * KB, nkb64));
       if (flags & 8) {
         const int pb = (int)((blockIdx.x + gridDim.x / 2) % gridDim.x);
         const int prank = pb % S, pn0 = (pb / S) * R * ROWS;
-        pf(pn0, (int)(((long long)prank * nkb) / S), (int)(((long long)(prank + 1) * nkb) / S));
+        pf(pn0, (int)(((long long)prank * nkb) / S) * KB, min((int)(((long long)(prank + 1) * nkb) / S) * KB, nkb64));
       }
     }
     if (MODE == MODE_RMS) {
@@ -307,8 +348,8 @@ __global__ void __launch_bounds__(dtc::THREADS, 2)  // <= 168 registers: two CTA
       // ring at ~400 cycles per stage (tools/micro/gemv_tc_trace.cu, per-stage clocks)
       pdl_wait_prior_grid();  // tokens may be the previous kernel's output
       const int t = (int)threadIdx.x - 64;  // 0..127
-      const int k0 = kb0 * BK;
-      const int nch = (min(kb1 * BK, K) - k0) / 8;  // 16-byte chunks (K % 8 == 0)
+      const int k0 = kb0 * BK * KB;
+      const int nch = (min(kb1 * BK * KB, K) - k0) / 8;  // 16-byte chunks (K % 8 == 0)
       constexpr int CPT = 2;                        // chunks per thread per token per round
       float sm[TOK];
 #pragma unroll
@@ -418,8 +459,8 @@ __global__ void __launch_bounds__(dtc::THREADS, 2)  // <= 168 registers: two CTA
         if (warp == 2) {
           cluster_wait();  // the leader's recv barrier is initialised (arrive at kernel start)
           if (lane == 0) {
-            dsmem_bulk_copy(mapa_shared(recv + (rank - 1) * RECV_STRIDE, 0u), part, RECV_STRIDE * 4,
-                            mapa_shared(recv_bar, 0u));
+            dsmem_bulk_copy(mapa_shared(recv + (rank - 1) * RECV_STRIDE, lead), part, RECV_STRIDE * 4,
+                            mapa_shared(recv_bar, lead));
             bulk_commit_group();
             bulk_wait_read();  // the source (this CTA's SMEM) stays valid until read
           }
@@ -465,7 +506,7 @@ __global__ void __launch_bounds__(dtc::THREADS, 2)  // <= 168 registers: two CTA
         for (int r = 1; r < S; ++r) {  // fixed rank order
 #pragma unroll
           for (int j = 0; j < R; ++j) {
-            const uint32_t src = mapa_shared(part + (j * ROWS + row) * TOK, (uint32_t)r);
+            const uint32_t src = mapa_shared(part + (j * ROWS + row) * TOK, lead + (uint32_t)r);
 #pragma unroll
             for (int m4 = 0; m4 < TOK / 4; ++m4) {
               const float4 p = ld_cluster_v4(src + m4 * 16);
@@ -473,7 +514,7 @@ __global__ void __launch_bounds__(dtc::THREADS, 2)  // <= 168 registers: two CTA
             }
           }
           if (MODE == MODE_RMS) {
-            const uint32_t ss = mapa_shared(part + R * ROWS * TOK, (uint32_t)r);
+            const uint32_t ss = mapa_shared(part + R * ROWS * TOK, lead + (uint32_t)r);
 #pragma unroll
             for (int m4 = 0; m4 < TOK / 4; ++m4) {
               const float4 p = ld_cluster_v4(ss + m4 * 16);
@@ -601,7 +642,7 @@ __global__ void __launch_bounds__(dtc::THREADS, 2)  // <= 168 registers: two CTA
             }
             continue;
           }
-        } else if (R == 2 && MODE == MODE_RMS && rope.pos != nullptr && rope.g_q == nullptr &&
+        } else if (R >= 2 && MODE == MODE_RMS && rope.pos != nullptr && rope.g_q == nullptr &&
                    n0 + j * ROWS < rope.n) {
           float pv[TOK];
 #pragma unroll
@@ -646,7 +687,7 @@ __global__ void __launch_bounds__(dtc::THREADS, 2)  // <= 168 registers: two CTA
   TC_EPI(5);
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, TMEM_COLS);
+    tmem_dealloc(tmem_base, TCOLS);
   }
   TC_EPI(6);
 #ifdef FN_GEMV_TC_TRACE
@@ -662,16 +703,18 @@ __global__ void __launch_bounds__(dtc::THREADS, 2)  // <= 168 registers: two CTA
 // ------------------------------------------------------------------ host side
 
 namespace {
-template <int MODE, int R>
+template <int MODE, int R, int KB>
 const void* dtc_kernel() {
-  return (const void*)flashnorm_gemv_tc_kernel<MODE, R>;
+  return (const void*)flashnorm_gemv_tc_kernel<MODE, R, KB>;
 }
-const void* dtc_fptr(int mode, int R) {
-  if (R == 1)
-    return mode == MODE_RMS ? dtc_kernel<MODE_RMS, 1>() : mode == MODE_DYT ? dtc_kernel<MODE_DYT, 1>()
-                                                                           : dtc_kernel<MODE_NONE, 1>();
-  return mode == MODE_RMS ? dtc_kernel<MODE_RMS, 2>() : mode == MODE_DYT ? dtc_kernel<MODE_DYT, 2>()
-                                                                         : dtc_kernel<MODE_NONE, 2>();
+template <int R, int KB>
+const void* dtc_fptr_rk(int mode) {
+  return mode == MODE_RMS ? dtc_kernel<MODE_RMS, R, KB>() : mode == MODE_DYT ? dtc_kernel<MODE_DYT, R, KB>()
+                                                                             : dtc_kernel<MODE_NONE, R, KB>();
+}
+const void* dtc_fptr(int mode, int R, int KB) {
+  if (R == 1) return KB == 2 ? dtc_fptr_rk<1, 2>(mode) : dtc_fptr_rk<1, 1>(mode);
+  return R == 2 ? dtc_fptr_rk<2, 1>(mode) : dtc_fptr_rk<4, 1>(mode);
 }
 int env_int(const char* name, int dflt) {
   const char* e = getenv(name);
@@ -680,48 +723,53 @@ int env_int(const char* name, int dflt) {
 // A/B knobs (defaults = the measured best): FN_DECODE_STAGES ring depth cap, FN_DECODE_PUSH
 // push-mode cluster reduction, FN_DECODE_PF2 partner-slice L2 prefetch
 int dtc_flags() {
+  // LSU prefetch of the whole own slice (FN_DECODE_LSUPF=1) measured 25 % below the HBM rate on long
+  // streams (N = 18432: 5.05 vs 6.78 TB/s) and no better on config 2 than a bounded TMA prefetch
+  // (FN_DECODE_L2PF stages beyond the ring): off by default
   static const int f = (env_int("FN_DECODE_PUSH", 1) ? 1 : 0) | (env_int("FN_DECODE_PF2", 0) ? 2 : 0) |
-                       (env_int("FN_DECODE_LSUPF", 1) & 7) << 2;  // bit 2 of LSUPF: evict_normal hint
+                       (env_int("FN_DECODE_LSUPF", 0) & 7) << 2;  // bit 2 of LSUPF: evict_normal hint
   return f;
 }
 size_t dtc_recv_bytes(int R, int S) {
   return (dtc_flags() & 1) && S > 1 ? (size_t)(S - 1) * (R * dtc::ROWS * dtc::TOK + dtc::TOK) * 4 : 0;
 }
-size_t dtc_smem_for(int R, int stages, int S) {
-  const size_t ring = R == 1 ? dtc::Cfg<1>::smem(stages) : dtc::Cfg<2>::smem(stages);
+size_t dtc_smem_for(int R, int KB, int stages, int S) {
+  const size_t ring = R == 1 ? (KB == 2 ? dtc::Cfg<1, 2>::smem(stages) : dtc::Cfg<1, 1>::smem(stages))
+                             : R == 2 ? dtc::Cfg<2, 1>::smem(stages) : dtc::Cfg<4, 1>::smem(stages);
   return ring + dtc_recv_bytes(R, S);
 }
 // deepest ring (<= the default depth) that fits the SMEM budget beside the receive slots
-int dtc_stages(int R, int S) {
+int dtc_stages(int R, int KB, int S) {
   static const int cap = env_int("FN_DECODE_STAGES", 0);
-  int st = cap >= 2 ? cap : (R == 1 ? dtc::Cfg<1>::STAGES : dtc::Cfg<2>::STAGES);
-  while (st > 2 && dtc_smem_for(R, st, S) > dtc::SMEM_MAX - 256) --st;
+  int st = cap >= 2 ? cap : ((R * KB) == 1 ? dtc::Cfg<1, 1>::STAGES : dtc::Cfg<2, 1>::STAGES);
+  while (st > 2 && dtc_smem_for(R, KB, st, S) > dtc::SMEM_MAX - 256) --st;
   return st;
 }
-size_t dtc_smem(int R, int S) { return dtc_smem_for(R, dtc_stages(R, S), S); }
-cudaError_t dtc_set_attr(int mode, int R) {
+size_t dtc_smem(int R, int KB, int S) { return dtc_smem_for(R, KB, dtc_stages(R, KB, S), S); }
+cudaError_t dtc_set_attr(int mode, int R, int KB) {
   // budget less 256 B of static shared memory headroom (debug/trace builds add some)
-  return ensure_smem_attr(dtc_fptr(mode, R), (int)dtc::SMEM_MAX - 256);
+  return ensure_smem_attr(dtc_fptr(mode, R, KB), (int)dtc::SMEM_MAX - 256);
 }
-// can `clusters` clusters of S CTAs (tile height R x 128) be resident at once?
-bool cluster_fits(int mode, int R, int S, int clusters) {
-  if (dtc_set_attr(mode, R) != cudaSuccess) return false;
+// can `clusters` clusters of C CTAs each (tile height R x 128, K split S) be resident at once?
+bool cluster_fits(int mode, int R, int KB, int S, int C, int clusters) {
+  if (dtc_set_attr(mode, R, KB) != cudaSuccess) return false;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(clusters * S);
+  cfg.gridDim = dim3(clusters * C);
   cfg.blockDim = dim3(dtc::THREADS);
-  cfg.dynamicSmemBytes = dtc_smem(R, S);
+  cfg.dynamicSmemBytes = dtc_smem(R, KB, S);
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = S;
+  at[0].val.clusterDim.x = C;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
   int n = 0;
-  return cudaOccupancyMaxActiveClusters(&n, dtc_fptr(mode, R), &cfg) == cudaSuccess && n >= clusters;
+  return cudaOccupancyMaxActiveClusters(&n, dtc_fptr(mode, R, KB), &cfg) == cudaSuccess && n >= clusters;
 }
 struct DtcPlan {
-  int R, S, cluster;
+  int R, S, cluster, T;  // cluster: CTAs per cluster (T tiles x S splits), 0 = global-memory reduction
+  int KB;                // 64-wide k blocks per ring stage (2: one 32 KiB 3-D TMA box, R = 1, K % 64 == 0)
 };
 // Tile height (R x 128 rows) and K split S, with the S CTAs of a tile in one co-resident
 // cluster (DSMEM reduction).  R = 1 whenever its tiles fit the SMs; R = 2 extends the kernel
@@ -741,29 +789,42 @@ DtcPlan dtc_plan(int mode, int K, int N, int num_sms) {
   }
   const int nkb = (K + BK - 1) / BK;
   const int cap = std::min(num_sms, MAX_CTAS);
-  DtcPlan best{1, 1, 0};
+  static const int s_env = [] {
+    const char* e = getenv("FN_DECODE_SMAX");  // A/B knob: cap on the K split
+    return e != nullptr ? atoi(e) : MAX_S;
+  }();
+  static const int t_env = env_int("FN_DECODE_TMAX", 4);          // A/B knob: cap on tiles per cluster
+  static const int force_global = env_int("FN_DECODE_GLOBAL", 0);  // A/B knob: global-memory split-K reduction
+  // A/B knob: k blocks per stage.  2 = 32 KiB 3-D boxes (6-stage ring): config 2 9.79 vs 9.70 us for
+  // 16 KiB boxes with the bounded prefetch, long streams equal; default 1
+  static const int kb_env = env_int("FN_DECODE_KB", 1);
+  DtcPlan best{1, 1, 0, 1, 1};
   int best_ctas = -1;
-  for (int R = 1; R <= 2; ++R) {
+  for (int R = 1; R <= 4; R *= 2) {
     const int tiles = (N + R * ROWS - 1) / (R * ROWS);
     if (tiles > cap) continue;
-    if (R == 2 && best_ctas > 0) break;  // R = 2 only when R = 1 does not fit
-    static const int s_env = [] {
-      const char* e = getenv("FN_DECODE_SMAX");  // A/B knob: cap on the K split
-      return e != nullptr ? atoi(e) : MAX_S;
-    }();
-    const int smax = std::max(1, std::min(std::min(cap / tiles, std::min(MAX_S, s_env)), nkb));
-    int fit = 1;
-    static const int force_global = env_int("FN_DECODE_GLOBAL", 0);  // A/B knob: global-memory split-K reduction
-    for (int c = smax; c > 1 && !force_global; --c)
-      if (cluster_fits(mode, R, c, tiles)) { fit = c; break; }
-    DtcPlan p{R, fit, fit > 1 ? 1 : 0};
-    if (fit == 1 && smax > 1) p = DtcPlan{R, smax, 0};  // no cluster fits: global-memory reduction
+    if (R > 1 && best_ctas > 0) break;  // taller tiles only when shorter ones do not fit the SMs
+    const int KB = (R == 1 && K % BK == 0 && kb_env == 2) ? 2 : 1;
+    const int nst = (nkb + KB - 1) / KB;  // ring stages of the whole K
+    // R = 4 (N up to 512 x #SMs) runs unsplit: the split-K partial buffers hold R <= 2 tiles
+    const int smax = R == 4 ? 1 : std::max(1, std::min(std::min(cap / tiles, std::min(MAX_S, s_env)), nst));
+    // the most CTAs (tiles x S <= #SMs) whose clusters of T tiles x S splits are all co-resident;
+    // T > 1 packs several tiles' split groups into one cluster, which lets S = 3 fit where
+    // clusters of 3 do not (GPC shapes: 45 clusters of 3, but 24 of 6 on this part)
+    DtcPlan p{R, 1, 0, 1, KB};
+    for (int S = smax; S > 1 && !force_global && p.S == 1; --S)
+      for (int T = 1; T <= t_env && T * S <= MAX_S; T *= 2) {
+        if (tiles % T) break;
+        if (cluster_fits(mode, R, KB, S, T * S, tiles / T)) { p = DtcPlan{R, S, T * S, T, KB}; break; }
+      }
+    if (p.S == 1 && smax > 1) p = DtcPlan{R, smax, 0, 1, KB};  // no cluster fits: global-memory reduction
     const int ctas = tiles * p.S;
     if (ctas > best_ctas) { best = p; best_ctas = ctas; }
   }
   if (env_int("FN_DECODE_VERBOSE", 0))
-    fprintf(stderr, "[flashnorm] decode plan K=%d N=%d: R=%d S=%d cluster=%d stages=%d smem=%zu\n", K, N, best.R,
-            best.S, best.cluster, dtc_stages(best.R, best.S), dtc_smem(best.R, best.S));
+    fprintf(stderr, "[flashnorm] decode plan K=%d N=%d: R=%d KB=%d S=%d T=%d cluster=%d stages=%d smem=%zu\n", K, N,
+            best.R, best.KB, best.S, best.T, best.cluster, dtc_stages(best.R, best.KB, best.S),
+            dtc_smem(best.R, best.KB, best.S));
   std::lock_guard<std::mutex> lk(mu);
   cache.emplace(key, best);
   return best;
@@ -773,7 +834,7 @@ DtcPlan dtc_plan(int mode, int K, int N, int num_sms) {
 int gemv_tc_split(int K, int N, int num_sms) { return dtc_plan(MODE_RMS, K, N, num_sms).S; }
 
 bool gemv_tc_supported(int M, int N, int num_sms) {
-  return M >= 1 && M <= dtc::TOK && (N + 2 * dtc::ROWS - 1) / (2 * dtc::ROWS) <= std::min(num_sms, dtc::MAX_CTAS);
+  return M >= 1 && M <= dtc::TOK && (N + 4 * dtc::ROWS - 1) / (4 * dtc::ROWS) <= std::min(num_sms, dtc::MAX_CTAS);
 }
 
 cudaError_t launch_gemv_tc(const CUtensorMap& tw, const CUtensorMap& ta, const float* cstar, __nv_bfloat16* z,
@@ -782,32 +843,33 @@ cudaError_t launch_gemv_tc(const CUtensorMap& tw, const CUtensorMap& ta, const f
                            const __nv_bfloat16* aptr) {
   using namespace dtc;
   const DtcPlan p = dtc_plan(mode, K, N, num_sms);
-  if (cudaError_t e = dtc_set_attr(mode, p.R); e != cudaSuccess) return e;
-  const void* fptr = dtc_fptr(mode, p.R);
+  if (cudaError_t e = dtc_set_attr(mode, p.R, p.KB); e != cudaSuccess) return e;
+  const void* fptr = dtc_fptr(mode, p.R, p.KB);
   const int tiles = (N + p.R * ROWS - 1) / (p.R * ROWS);
-  int S = p.S, use_cluster = p.cluster;
+  int S = p.S, use_cluster = p.cluster;  // CTAs per cluster (0: none)
   // global-mode partial-buffer slot: launches in flight together use different slots
   static std::atomic<unsigned> seq{0};
   int slot = (int)(seq.fetch_add(1u) % SLOTS);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(tiles * S);
   cfg.blockDim = dim3(THREADS);
-  cfg.dynamicSmemBytes = dtc_smem(p.R, S);
+  cfg.dynamicSmemBytes = dtc_smem(p.R, p.KB, S);
   cfg.stream = stream;
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   at[1].id = cudaLaunchAttributeClusterDimension;
-  at[1].val.clusterDim.x = use_cluster ? S : 1;
+  at[1].val.clusterDim.x = use_cluster ? use_cluster : 1;
   at[1].val.clusterDim.y = 1;
   at[1].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 2;
   static const int l2pf = [] {
-    const char* e = getenv("FN_DECODE_L2PF");  // A/B knob: W* boxes per CTA prefetched to L2 pre-wait
-    return e != nullptr ? atoi(e) : 0;  // measured: TMA prefetches queue behind/ahead of the ring loads
+    const char* e = getenv("FN_DECODE_L2PF");  // A/B knob: W* stages per CTA prefetched to L2 pre-wait
+    // measured on config 2 (graph, 8 rotating W*): 0 / 4 / 8 / 12 stages -> 10.6 / 10.1 / 9.71 / 9.70 us
+    return e != nullptr ? atoi(e) : 12;
   }();
-  int stages = dtc_stages(p.R, S);
+  int stages = dtc_stages(p.R, p.KB, S);
   int flags = dtc_flags();
   void* args[] = {(void*)&tw, (void*)&ta, (void*)&cstar, (void*)&z, (void*)&M, (void*)&K, (void*)&N,
                   (void*)&eps, (void*)&alpha, (void*)&S, (void*)&slot, (void*)&use_cluster, (void*)&row_scale,
@@ -817,5 +879,6 @@ cudaError_t launch_gemv_tc(const CUtensorMap& tw, const CUtensorMap& ta, const f
 }
 
 int gemv_tc_tile_rows(int mode, int K, int N, int num_sms) { return dtc_plan(mode, K, N, num_sms).R * dtc::ROWS; }
+int gemv_tc_kblocks(int mode, int K, int N, int num_sms) { return dtc_plan(mode, K, N, num_sms).KB; }
 
 }  // namespace fn

@@ -204,6 +204,9 @@ bool gemv_supported(int M, int K);  // decode kernel handles this (M, K)
 bool gemv_tc_supported(int M, int N, int num_sms);
 int gemv_tc_split(int K, int N, int num_sms);      // K splits per tile
 int gemv_tc_tile_rows(int mode, int K, int N, int num_sms);  // W* rows per tile (128 or 256; the TMA box)
+// 64-wide k blocks per decode ring stage: 1 -> 2-D maps (box 64 x rows); 2 -> 3-D maps
+// {64, rows, K/64} with strides {row, 128 B}, box {64, rows, 2} (W*) / {64, 16, 2} (tokens)
+int gemv_tc_kblocks(int mode, int K, int N, int num_sms);
 cudaError_t launch_gemv_tc(const CUtensorMap& tw, const CUtensorMap& ta, const float* cstar, __nv_bfloat16* z,
                            int M, int K, int N, float eps, float alpha, int mode, int num_sms, cudaStream_t stream,
                            const float* row_scale = nullptr,

@@ -347,12 +347,13 @@ def test_gemm_eps_placement_detectable():
 # ============================================================ linear: bf16 decode GEMV
 
 @pytest.mark.parametrize("M", [1, 5, 16])
-@pytest.mark.parametrize("K,N", [(4096, 6144), (1000, 24), (8192, 136), (64, 8), (4160, 20000), (2048, 4104), (512, 40000)])
+@pytest.mark.parametrize("K,N", [(4096, 6144), (1000, 24), (8192, 136), (64, 8), (4160, 20000), (2048, 4104), (512, 40000),
+                                 (520, 75776)])
 @pytest.mark.parametrize("mode", ["rmsnorm", "dyt", "none"])
 @pytest.mark.parametrize("path", ["gemv", "gemv_mma"])
 def test_gemv_parity(M, K, N, mode, path):
-    """gemv: tcgen05 split-K decode kernel (clusters of up to 8 CTAs; N=20000 has more 128-row
-    tiles than SMs and falls back to mma.sync); gemv_mma: the mma.sync decode kernel."""
+    """gemv: tcgen05 split-K decode kernel (clusters of up to 8 CTAs; N=20000 has more 128-row tiles
+    than SMs and runs 256-row tiles, N=40000 512-row tiles); gemv_mma: the mma.sync decode kernel."""
     if path == "gemv_mma" and M * K * 2 > 150 * 1024:
         path = "auto"
     a, Wt, g, b, c, ref = _layer_and_ref(6, M, K, N, "bf16", mode)
@@ -474,6 +475,18 @@ def test_config2_decode_full(M):
     """Llama-3-8B decode: RMSNorm + QKV 4096 -> 6144, all outputs vs oracle."""
     a, Wt, g, b, c, Ws, cs = _full_size(M, 4096, 6144, 31)
     z = H(fn.linear(a, Ws, cs, eps=1e-5))
+    ref = _oracle_rows(H(a), Wt, H(g), None, None, 1e-5, "rmsnorm")
+    assert O.rowwise_rel_err(z, ref) <= TOL_BF16
+
+
+@pytest.mark.parametrize("M", [1, 16])
+def test_decode_wide_n_70b_gate_up(M):
+    """Decode through the tcgen05 kernel for N > 256 x #SMs: the Llama-3-70B gate||up shape (K = 8192,
+    N = 57344 = 112 tiles of 512 rows), every output against the fp64 oracle."""
+    a, Wt, g, b, c, Ws, cs = _full_size(M, 8192, 57344, 34)
+    n0 = fn.launch_count()
+    z = H(fn.linear(a, Ws, cs, eps=1e-5, path="gemv"))
+    assert fn.launch_count() - n0 == 1
     ref = _oracle_rows(H(a), Wt, H(g), None, None, 1e-5, "rmsnorm")
     assert O.rowwise_rel_err(z, ref) <= TOL_BF16
 
