@@ -49,6 +49,9 @@ constexpr int T_STAGE = TOK * BK * 2;   // 2 KiB
 constexpr int THREADS = 192;
 constexpr int TMEM_COLS = 32;           // D of MMA j in columns [16j, 16j+16), j < R <= 2 (R = 4: 64)
 constexpr int BOX_ROWS_MAX = 256;       // TMA box rows (R = 4 tiles load two boxes per stage)
+constexpr int TOK_GS = 8;               // resident tokens: stages per readiness group
+constexpr int TOK_GROUPS = 8;           // resident tokens: at most 64 stages (128 KiB) ...
+constexpr int TOK_MAX_BYTES = 64 * 1024;  // ... but the host keeps it <= 64 KiB
 constexpr int MAX_S = 8;                // K splits per tile (portable cluster size)
 constexpr int MAX_CTAS = 160;           // tiles * S <= #SMs (148)
 constexpr int SLOTS = 4;                // global-mode partial buffers, round robin over launches
@@ -109,6 +112,9 @@ __device__ long long g_tc_epi[2][8];
 #define TC_STAGE(w, i)
 #endif
 
+// resident-token slice size (stages) is carried in bits 8..15 of `flags`
+FN_DEVICE int nkb_host_tokmax(int flags) { return (flags >> 8) & 0xFF; }
+
 template <int MODE, int R, int KB>
 __global__ void __launch_bounds__(dtc::THREADS, R == 4 ? 1 : 2)  // R < 4: <= 168 registers (two CTAs may share an SM)
     flashnorm_gemv_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_a,
@@ -124,14 +130,21 @@ __global__ void __launch_bounds__(dtc::THREADS, R == 4 ? 1 : 2)  // R < 4: <= 16
   const int STAGES = stages;  // ring depth (runtime: the host sizes it for 1 or 2 CTAs per SM)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  // resident tokens (flags & 32, R = KB = 1): this CTA's whole token slice [my_kb][16 x 64] SW128 is staged
+  // ONCE after the dependency wait by warps 2-5 (DyT: tanh applied then, once per element) and the ring
+  // carries W* only; tokmax = the host's bound on my_kb (its size)
+  const bool tokres = (flags & 32) != 0;
+  const int tokmax = tokres ? (nkb_host_tokmax(flags)) : 0;
   uint8_t* sW = smem;                                  // [STAGES][R*128 x 64] SW128
-  uint8_t* sT = sW + STAGES * W_STAGE;                 // [STAGES][16 x 64]    SW128
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sT + STAGES * T_STAGE);
+  uint8_t* sT = sW + STAGES * W_STAGE;                 // [STAGES][16 x 64] SW128, or [tokmax][16 x 64] resident
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sT + (tokres ? tokmax * dtc::T_STAGE : STAGES * T_STAGE));
   uint64_t* full = bars;               // [STAGES] W* + tokens landed
   uint64_t* empty = bars + STAGES;     // [STAGES] stage consumed
   uint64_t* ready = bars + 2 * STAGES; // [STAGES] DyT: tokens transformed
   uint64_t* tfull = bars + 3 * STAGES; // accumulator complete
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tfull + 1);
+  uint64_t* tokready = tfull + 1;      // [TOK_GROUPS] resident tokens: group g of TOK_GS stages transformed
+  uint64_t* tokland = tokready + dtc::TOK_GROUPS;  // [TOK_GROUPS] resident tokens: group g landed (TMA)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tokland + dtc::TOK_GROUPS);
   float* ssq_own = reinterpret_cast<float*>(tmem_holder + 4);  // [16] this CTA's partial ssq per token
   float* ssq_red = ssq_own + TOK;                              // [4 warps][16]
   int* last_flag = reinterpret_cast<int*>(ssq_red + 4 * TOK);
@@ -141,7 +154,7 @@ __global__ void __launch_bounds__(dtc::THREADS, R == 4 ? 1 : 2)  // R < 4: <= 16
   // push mode: the leader's receive slots, one per peer rank, beside the ring (a peer may finish
   // before the leader's ring is drained): [S-1][R*128*16 + 16] fp32
   constexpr int RECV_STRIDE = R * ROWS * TOK + TOK;
-  float* recv = reinterpret_cast<float*>(sT + STAGES * T_STAGE + 1024);
+  float* recv = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 1024);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -199,6 +212,10 @@ __global__ void __launch_bounds__(dtc::THREADS, R == 4 ? 1 : 2)  // R < 4: <= 16
       mbar_init(&ready[s], 1);
     }
     mbar_init(tfull, 1);
+    for (int g = 0; g < TOK_GROUPS; ++g) {
+      mbar_init(&tokready[g], 1);
+      mbar_init(&tokland[g], 1);
+    }
     mbar_init(recv_bar, 1);  // push mode: the leader's expect_tx + each peer's bulk copy (complete_tx)
     fence_mbar_init();
     if (S > 1 && use_cluster && (flags & 1) && rank == 0)
@@ -220,8 +237,9 @@ __global__ void __launch_bounds__(dtc::THREADS, R == 4 ? 1 : 2)  // R < 4: <= 16
     if (elect_one()) {
       const int pre = my_kb < STAGES ? my_kb : STAGES;
       // W* is constant: its first `pre` stages stream before the dependency wait
+      const uint32_t stage_tx = W_STAGE + (tokres ? 0 : T_STAGE);
       for (int i = 0; i < pre; ++i) {
-        mbar_arrive_expect_tx(&full[i], W_STAGE + T_STAGE);
+        mbar_arrive_expect_tx(&full[i], stage_tx);
         load_w(sW + i * W_STAGE, &full[i], kb0 + i);
       }
       // ... and the rest of this CTA's W* slice is pulled into L2 (up to l2pf boxes), so the
@@ -240,17 +258,26 @@ __global__ void __launch_bounds__(dtc::THREADS, R == 4 ? 1 : 2)  // R < 4: <= 16
       }
       pdl_wait_prior_grid();  // tokens may be the previous kernel's output
       TC_TRACE(1);
-      for (int i = 0; i < pre; ++i)
-        load_t(sT + i * T_STAGE, &full[i], kb0 + i);
+      if (!tokres) {
+        for (int i = 0; i < pre; ++i) load_t(sT + i * T_STAGE, &full[i], kb0 + i);
+      } else {
+        // the whole token slice at once, one barrier per group of TOK_GS stages (ahead of every
+        // post-wait W* load in the TMA queue)
+        for (int g = 0; g * TOK_GS < my_kb; ++g) {
+          const int i0 = g * TOK_GS, i1 = min(my_kb, i0 + TOK_GS);
+          mbar_arrive_expect_tx(&tokland[g], (uint32_t)((i1 - i0) * dtc::T_STAGE));
+          for (int i = i0; i < i1; ++i) load_t(sT + i * dtc::T_STAGE, &tokland[g], kb0 + i);
+        }
+      }
       int stage = pre == STAGES ? 0 : pre;
       uint32_t phase = pre == STAGES ? 1u : 0u;
       for (int i = 0; i < pre; ++i) TC_STAGE(1, i);
       for (int i = pre; i < my_kb; ++i) {
         mbar_wait(&empty[stage], phase ^ 1);
         TC_STAGE(1, i);
-        mbar_arrive_expect_tx(&full[stage], W_STAGE + T_STAGE);
+        mbar_arrive_expect_tx(&full[stage], stage_tx);
         load_w(sW + stage * W_STAGE, &full[stage], kb0 + i);
-        load_t(sT + stage * T_STAGE, &full[stage], kb0 + i);
+        if (!tokres) load_t(sT + stage * T_STAGE, &full[stage], kb0 + i);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
@@ -261,8 +288,14 @@ __global__ void __launch_bounds__(dtc::THREADS, R == 4 ? 1 : 2)  // R < 4: <= 16
       int stage = 0;
       uint32_t phase = 0;
       for (int i = 0; i < my_kb; ++i) {
-        if (MODE == MODE_DYT) mbar_wait(&ready[stage], phase);
-        else mbar_wait(&full[stage], phase);
+        if (tokres) {
+          if (i % TOK_GS == 0) mbar_wait(MODE == MODE_DYT ? &tokready[i / TOK_GS] : &tokland[i / TOK_GS], 0);
+          mbar_wait(&full[stage], phase);
+        } else if (MODE == MODE_DYT) {
+          mbar_wait(&ready[stage], phase);
+        } else {
+          mbar_wait(&full[stage], phase);
+        }
 #ifdef FN_GEMV_TC_TRACE
         TC_STAGE(0, i);
         if (i == 0) TC_TRACE(5);
@@ -272,7 +305,8 @@ __global__ void __launch_bounds__(dtc::THREADS, R == 4 ? 1 : 2)  // R < 4: <= 16
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < KB; ++kk) {  // the stage's k blocks: [kb][rows][64] / [kb][16][64] in SMEM
-          const uint64_t bdesc = make_sw128_desc(smem_u32(sT + stage * T_STAGE + kk * dtc::T_STAGE));
+          const uint64_t bdesc =
+              make_sw128_desc(smem_u32(tokres ? sT + i * dtc::T_STAGE : sT + stage * T_STAGE + kk * dtc::T_STAGE));
 #pragma unroll
           for (int j = 0; j < R; ++j) {  // rows [128j, 128j+128) of the tile: 16 KiB into the box
             const uint64_t adesc = make_sw128_desc(smem_u32(sW + stage * W_STAGE + (kk * R + j) * KSUB));
@@ -288,7 +322,33 @@ __global__ void __launch_bounds__(dtc::THREADS, R == 4 ? 1 : 2)  // R < 4: <= 16
     }
   } else {
     // ------------------------------------------------------------ side warp (warp 2), then epilogue
-    if (MODE == MODE_DYT) {
+    if (tokres) {
+      if (MODE == MODE_DYT) {
+        // the token slice landed once (TMA, per group): tanh(alpha a) in place, once per element, exactly
+        // as the in-ring transform (RN_bf16(tanh(RN_bf16(alpha) a))); rows >= M are zero fill
+        const int t = (int)threadIdx.x - 64;  // 0..127
+        const __nv_bfloat162 alpha2 = __floats2bfloat162_rn(alpha, alpha);
+        for (int g = 0; g * TOK_GS < my_kb; ++g) {
+          const int i0 = g * TOK_GS, i1 = min(my_kb, i0 + TOK_GS);
+          mbar_wait_warp(&tokland[g], 0);
+          for (int i = i0; i < i1; ++i) {
+            uint4* p = reinterpret_cast<uint4*>(sT + i * dtc::T_STAGE) + t;
+            uint4 v = *p;
+            uint32_t* w = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              __nv_bfloat162 x = *reinterpret_cast<__nv_bfloat162*>(&w[e]);
+              x = __hmul2(x, alpha2);
+              w[e] = tanh_approx_bf16x2(*reinterpret_cast<uint32_t*>(&x));
+            }
+            *p = v;
+          }
+          fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
+          named_bar_sync(2, 128);
+          if (t == 0) mbar_arrive(&tokready[g]);
+        }
+      }
+    } else if (MODE == MODE_DYT) {
       // tanh(alpha a) in place on each token stage before its MMA: warps 2-5, one 16-byte
       // chunk per thread (2 KiB per stage), so the transform keeps ahead of the W* stream
       const __nv_bfloat162 alpha2 = __floats2bfloat162_rn(alpha, alpha);
@@ -733,30 +793,33 @@ int dtc_flags() {
 size_t dtc_recv_bytes(int R, int S) {
   return (dtc_flags() & 1) && S > 1 ? (size_t)(S - 1) * (R * dtc::ROWS * dtc::TOK + dtc::TOK) * 4 : 0;
 }
-size_t dtc_smem_for(int R, int KB, int stages, int S) {
-  const size_t ring = R == 1 ? (KB == 2 ? dtc::Cfg<1, 2>::smem(stages) : dtc::Cfg<1, 1>::smem(stages))
-                             : R == 2 ? dtc::Cfg<2, 1>::smem(stages) : dtc::Cfg<4, 1>::smem(stages);
+// tok: resident-token stages (0 = tokens ride the ring)
+size_t dtc_smem_for(int R, int KB, int stages, int S, int tok) {
+  size_t ring;
+  if (tok > 0) ring = 1024 + (size_t)stages * dtc::Cfg<1, 1>::W_STAGE + (size_t)tok * dtc::T_STAGE + 1024;
+  else ring = R == 1 ? (KB == 2 ? dtc::Cfg<1, 2>::smem(stages) : dtc::Cfg<1, 1>::smem(stages))
+                     : R == 2 ? dtc::Cfg<2, 1>::smem(stages) : dtc::Cfg<4, 1>::smem(stages);
   return ring + dtc_recv_bytes(R, S);
 }
 // deepest ring (<= the default depth) that fits the SMEM budget beside the receive slots
-int dtc_stages(int R, int KB, int S) {
+int dtc_stages(int R, int KB, int S, int tok) {
   static const int cap = env_int("FN_DECODE_STAGES", 0);
-  int st = cap >= 2 ? cap : ((R * KB) == 1 ? dtc::Cfg<1, 1>::STAGES : dtc::Cfg<2, 1>::STAGES);
-  while (st > 2 && dtc_smem_for(R, KB, st, S) > dtc::SMEM_MAX - 256) --st;
+  int st = cap >= 2 ? cap : (tok > 0 ? 13 : ((R * KB) == 1 ? dtc::Cfg<1, 1>::STAGES : dtc::Cfg<2, 1>::STAGES));
+  while (st > 2 && dtc_smem_for(R, KB, st, S, tok) > dtc::SMEM_MAX - 256) --st;
   return st;
 }
-size_t dtc_smem(int R, int KB, int S) { return dtc_smem_for(R, KB, dtc_stages(R, KB, S), S); }
+size_t dtc_smem(int R, int KB, int S, int tok) { return dtc_smem_for(R, KB, dtc_stages(R, KB, S, tok), S, tok); }
 cudaError_t dtc_set_attr(int mode, int R, int KB) {
   // budget less 256 B of static shared memory headroom (debug/trace builds add some)
   return ensure_smem_attr(dtc_fptr(mode, R, KB), (int)dtc::SMEM_MAX - 256);
 }
 // can `clusters` clusters of C CTAs each (tile height R x 128, K split S) be resident at once?
-bool cluster_fits(int mode, int R, int KB, int S, int C, int clusters) {
+bool cluster_fits(int mode, int R, int KB, int S, int C, int clusters, int tok) {
   if (dtc_set_attr(mode, R, KB) != cudaSuccess) return false;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(clusters * C);
   cfg.blockDim = dim3(dtc::THREADS);
-  cfg.dynamicSmemBytes = dtc_smem(R, KB, S);
+  cfg.dynamicSmemBytes = dtc_smem(R, KB, S, tok);
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = C;
@@ -770,6 +833,7 @@ bool cluster_fits(int mode, int R, int KB, int S, int C, int clusters) {
 struct DtcPlan {
   int R, S, cluster, T;  // cluster: CTAs per cluster (T tiles x S splits), 0 = global-memory reduction
   int KB;                // 64-wide k blocks per ring stage (2: one 32 KiB 3-D TMA box, R = 1, K % 64 == 0)
+  int tok;               // resident-token stages per CTA (0: tokens ride the ring)
 };
 // Tile height (R x 128 rows) and K split S, with the S CTAs of a tile in one co-resident
 // cluster (DSMEM reduction).  R = 1 whenever its tiles fit the SMs; R = 2 extends the kernel
@@ -798,7 +862,8 @@ DtcPlan dtc_plan(int mode, int K, int N, int num_sms) {
   // A/B knob: k blocks per stage.  2 = 32 KiB 3-D boxes (6-stage ring): config 2 9.79 vs 9.70 us for
   // 16 KiB boxes with the bounded prefetch, long streams equal; default 1
   static const int kb_env = env_int("FN_DECODE_KB", 1);
-  DtcPlan best{1, 1, 0, 1, 1};
+  static const int tokres_env = env_int("FN_DECODE_TOKRES", 1);  // A/B knob: resident token slice
+  DtcPlan best{1, 1, 0, 1, 1, 0};
   int best_ctas = -1;
   for (int R = 1; R <= 4; R *= 2) {
     const int tiles = (N + R * ROWS - 1) / (R * ROWS);
@@ -811,20 +876,31 @@ DtcPlan dtc_plan(int mode, int K, int N, int num_sms) {
     // the most CTAs (tiles x S <= #SMs) whose clusters of T tiles x S splits are all co-resident;
     // T > 1 packs several tiles' split groups into one cluster, which lets S = 3 fit where
     // clusters of 3 do not (GPC shapes: 45 clusters of 3, but 24 of 6 on this part)
-    DtcPlan p{R, 1, 0, 1, KB};
+    // tokens resident when the per-CTA slice (ceil(stages / S) x 2 KiB) stays small
+    auto tok_for = [&](int S) {
+      const int tm = (nst + S - 1) / S;
+      // measured (config 2): DyT 11.1 -> ~10 us (the transform leaves the per-stage path); RMS / none
+      // slower with the shallower W* ring (9 vs 12 stages), so only DyT keeps its tokens resident
+      return (tokres_env && mode == MODE_DYT && R == 1 && KB == 1 && tm * T_STAGE <= TOK_MAX_BYTES &&
+              tm <= TOK_GS * TOK_GROUPS) ? tm : 0;
+    };
+    DtcPlan p{R, 1, 0, 1, KB, tok_for(1)};
     for (int S = smax; S > 1 && !force_global && p.S == 1; --S)
       for (int T = 1; T <= t_env && T * S <= MAX_S; T *= 2) {
         if (tiles % T) break;
-        if (cluster_fits(mode, R, KB, S, T * S, tiles / T)) { p = DtcPlan{R, S, T * S, T, KB}; break; }
+        if (cluster_fits(mode, R, KB, S, T * S, tiles / T, tok_for(S))) {
+          p = DtcPlan{R, S, T * S, T, KB, tok_for(S)};
+          break;
+        }
       }
-    if (p.S == 1 && smax > 1) p = DtcPlan{R, smax, 0, 1, KB};  // no cluster fits: global-memory reduction
+    if (p.S == 1 && smax > 1) p = DtcPlan{R, smax, 0, 1, KB, tok_for(smax)};  // global-memory reduction
     const int ctas = tiles * p.S;
     if (ctas > best_ctas) { best = p; best_ctas = ctas; }
   }
   if (env_int("FN_DECODE_VERBOSE", 0))
-    fprintf(stderr, "[flashnorm] decode plan K=%d N=%d: R=%d KB=%d S=%d T=%d cluster=%d stages=%d smem=%zu\n", K, N,
-            best.R, best.KB, best.S, best.T, best.cluster, dtc_stages(best.R, best.KB, best.S),
-            dtc_smem(best.R, best.KB, best.S));
+    fprintf(stderr, "[flashnorm] decode plan K=%d N=%d: R=%d KB=%d S=%d T=%d cluster=%d tok=%d stages=%d smem=%zu\n",
+            K, N, best.R, best.KB, best.S, best.T, best.cluster, best.tok, dtc_stages(best.R, best.KB, best.S, best.tok),
+            dtc_smem(best.R, best.KB, best.S, best.tok));
   std::lock_guard<std::mutex> lk(mu);
   cache.emplace(key, best);
   return best;
@@ -853,7 +929,7 @@ cudaError_t launch_gemv_tc(const CUtensorMap& tw, const CUtensorMap& ta, const f
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(tiles * S);
   cfg.blockDim = dim3(THREADS);
-  cfg.dynamicSmemBytes = dtc_smem(p.R, p.KB, S);
+  cfg.dynamicSmemBytes = dtc_smem(p.R, p.KB, S, p.tok);
   cfg.stream = stream;
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -869,8 +945,8 @@ cudaError_t launch_gemv_tc(const CUtensorMap& tw, const CUtensorMap& ta, const f
     // measured on config 2 (graph, 8 rotating W*): 0 / 4 / 8 / 12 stages -> 10.6 / 10.1 / 9.71 / 9.70 us
     return e != nullptr ? atoi(e) : 12;
   }();
-  int stages = dtc_stages(p.R, p.KB, S);
-  int flags = dtc_flags();
+  int stages = dtc_stages(p.R, p.KB, S, p.tok);
+  int flags = dtc_flags() | (p.tok > 0 ? 32 | (p.tok << 8) : 0);
   void* args[] = {(void*)&tw, (void*)&ta, (void*)&cstar, (void*)&z, (void*)&M, (void*)&K, (void*)&N,
                   (void*)&eps, (void*)&alpha, (void*)&S, (void*)&slot, (void*)&use_cluster, (void*)&row_scale,
                   (void*)&rope, (void*)&l2pf, (void*)&stages, (void*)&flags, (void*)&wptr,
