@@ -391,17 +391,21 @@ def measure_multi_gpu(args, fn, torch, dev, stream, a, Ws, cs, z, ws, rank, barr
     except Exception as e:  # reported, never fatal for the metric line
         out["nccl_gather"] = {"error": repr(e)[:300]}
         zg = None
-    try:
-        for _ in range(2):
-            zf = layer.forward_fused_gather(a, eps=1e-5)
-        barrier_sync()
-        ms_f = max_over_ranks(_events_ms(torch, stream, lambda i: layer.forward_fused_gather(a, eps=1e-5), steps))
-        zf = layer.forward_fused_gather(a, eps=1e-5, copy=True)
-        barrier_sync()
-        same = bool(zg is not None and torch.equal(zf.view(torch.int16), zg.view(torch.int16)))
-        out["fused_gather"] = {"ms": ms_f, "bit_exact_vs_nccl": same}
-    except Exception as e:
-        out["fused_gather"] = {"error": repr(e)[:300]}
+    for key, mc in (("fused_gather", "auto"), ("fused_gather_peer_stores", False)):
+        try:
+            for _ in range(2):
+                layer.forward_fused_gather(a, eps=1e-5, multicast=mc)
+            barrier_sync()
+            ms_f = max_over_ranks(_events_ms(torch, stream,
+                                             lambda i: layer.forward_fused_gather(a, eps=1e-5, multicast=mc), steps))
+            zf = layer.forward_fused_gather(a, eps=1e-5, copy=True, multicast=mc)
+            barrier_sync()
+            same = bool(zg is not None and torch.equal(zf.view(torch.int16), zg.view(torch.int16)))
+            out[key] = {"ms": ms_f, "bit_exact_vs_nccl": same, "stores": layer.last_gather}
+        except Exception as e:
+            out[key] = {"error": repr(e)[:300]}
+        if key == "fused_gather" and out[key].get("stores") != "multicast":
+            break  # no NVLS mapping: "auto" already measured the peer stores
     return out
 
 

@@ -338,6 +338,18 @@ fn_status flashnorm_linear_gather(const void* a, const void* Wt_star, const floa
                                   int64_t N, float eps, float alpha, fn_mode mode, fn_dtype dtype,
                                   void* const* z_dsts, int ndst, int64_t ldz, int64_t col0, void* stream);
 
+/* flashnorm_linear_gather_multicast — the same fused gather through ONE NVLink-SHARP (NVLS) multicast
+ * address: z_mc is the multicast mapping of a buffer bound on every rank (cuMulticastCreate /
+ * cuMulticastBindMem, e.g. torch symmetric memory's multicast_ptr); the epilogue stores each 16-byte
+ * segment of this rank's shard with multimem.st, and the NVSwitch writes it into every rank's
+ * [M][ldz] buffer — each rank sends its shard once (M x N x 2 bytes) instead of P - 1 times.
+ * Same arithmetic and bits as flashnorm_linear_gather.  z_mc must be a multicast address (a plain
+ * pointer faults); ordering of the peers' readers is the caller's (a barrier after the stream).
+ * ldz, col0 as flashnorm_linear_gather; bf16 only. */
+fn_status flashnorm_linear_gather_multicast(const void* a, const void* Wt_star, const float* c_star, int64_t M,
+                                            int64_t K, int64_t N, float eps, float alpha, fn_mode mode,
+                                            fn_dtype dtype, void* z_mc, int64_t ldz, int64_t col0, void* stream);
+
 /* --------------------------------------------------------------------------
  * Opt-in multi-GPU plumbing.  W* is column-sharded, the
  * activations replicated: every rank computes its shard z_local [M][N_local]

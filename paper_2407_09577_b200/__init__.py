@@ -23,7 +23,8 @@ __all__ = [
     "FlashNormError", "lib", "lib_path", "fold_weights", "fold_mean_center", "fold_mean_center_workspace_bytes",
     "linear", "linear_from_host", "baseline_norm", "gather_columns", "launch_count", "reset_launch_count",
     "version", "linear_workspace_bytes", "fold_glu_weights", "glu_linear", "linear_scaled", "glu_ffn", "qkv_rope_linear", "relu_ffn_up", "qk_norm_rope_linear",
-    "fold_colsum", "layernorm_linear", "linear_gather", "comm_unique_id", "comm_init", "comm_destroy",
+    "fold_colsum", "layernorm_linear", "linear_gather", "linear_gather_multicast", "comm_unique_id", "comm_init",
+    "comm_destroy",
     "allgather_columns", "comm_count",
     "MODES", "GLU_ACTS", "PATHS", "EXPORTS",
 ]
@@ -41,7 +42,7 @@ EXPORTS = [
     "flashnorm_fold_weights", "flashnorm_fold_mean_center_workspace_bytes", "flashnorm_fold_mean_center",
     "flashnorm_linear", "flashnorm_linear_ex", "flashnorm_linear_workspace_bytes", "flashnorm_linear_ws",
     "flashnorm_linear_from_host", "flashnorm_fold_glu_weights", "flashnorm_glu_linear", "flashnorm_linear_scaled",
-    "flashnorm_fold_colsum", "flashnorm_layernorm_linear", "flashnorm_linear_gather",
+    "flashnorm_fold_colsum", "flashnorm_layernorm_linear", "flashnorm_linear_gather", "flashnorm_linear_gather_multicast",
     "flashnorm_comm_unique_id", "flashnorm_comm_init", "flashnorm_comm_destroy", "flashnorm_comm_count",
     "flashnorm_allgather_workspace_bytes", "flashnorm_allgather_columns",
     "flashnorm_qkv_rope_linear", "flashnorm_relu_ffn_up", "flashnorm_qk_norm_rope_linear", "flashnorm_baseline_norm",
@@ -97,6 +98,8 @@ def lib() -> ctypes.CDLL:
         "flashnorm_linear_gather": [_vp, _vp, _vp, _i64, _i64, _i64, _f32, _f32, _int, _int, _vp, _int, _i64, _i64,
                                     _vp],
         "flashnorm_layernorm_linear": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _f32, _int, _vp, _vp],
+        "flashnorm_linear_gather_multicast": [_vp, _vp, _vp, _i64, _i64, _i64, _f32, _f32, _int, _int, _vp, _i64,
+                                              _i64, _vp],
         "flashnorm_linear_from_host": [_vp, _vp, _vp, _i64, _i64, _i64, _f32, _f32, _int, _int, _vp, _vp, _vp,
                                        _vp],
         "flashnorm_baseline_norm": [_vp, _vp, _vp, _i64, _i64, _f32, _int, _f32, _int, _vp, _vp],
@@ -419,6 +422,18 @@ def linear_gather(a, Wt_star, dsts, col0: int, c_star=None, eps: float = 1e-5, m
     _check(lib().flashnorm_linear_gather(_ptr(a), _ptr(Wt_star), _ptr(c_star), M, K, N, float(eps), float(alpha),
                                          MODES[mode], _dtype_code(a), ptrs, len(dsts), ldz, int(col0), _stream(a)),
            "linear_gather")
+
+
+def linear_gather_multicast(a, Wt_star, z_mc: int, ldz: int, col0: int, c_star=None, eps: float = 1e-5,
+                            mode: str = "rmsnorm", alpha: float = 0.5):
+    """This rank's column shard stored by the GEMM epilogue through an NVLS multicast address `z_mc`
+    (an integer device address, e.g. torch symmetric memory's multicast_ptr): the NVSwitch writes it
+    into every rank's [M, ldz] buffer at columns [col0, col0 + N) (include/flashnorm.h)."""
+    M, K, N = _operands(a, Wt_star, "linear_gather_multicast")
+    c_star = _vec(c_star, "c_star", N)
+    _check(lib().flashnorm_linear_gather_multicast(_ptr(a), _ptr(Wt_star), _ptr(c_star), M, K, N, float(eps),
+                                                   float(alpha), MODES[mode], _dtype_code(a), ctypes.c_void_p(z_mc),
+                                                   int(ldz), int(col0), _stream(a)), "linear_gather_multicast")
 
 
 def comm_unique_id() -> bytes:

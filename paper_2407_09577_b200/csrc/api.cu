@@ -245,6 +245,7 @@ struct LinearExtras {
   const float* ln_u = nullptr;      // exact deferred LayerNorm (rmsnorm mode): u = 1^T W* [N]
   int ndst = 0, ldz = 0, col0 = 0;  // fused column gather: z shard -> ndst [M x ldz] buffers at col0
   void* const* zdst = nullptr;
+  int mc = 0;                       // zdst[0] is an NVLS multicast address (multimem.st)
 };
 
 fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, int64_t M, int64_t K, int64_t N,
@@ -416,6 +417,7 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
   p.rope = ex.rope;
   p.ln_u = ex.ln_u;
   p.ndst = ex.ndst;
+  p.mc = ex.mc;
   p.ldz = ex.ldz;
   p.col0 = ex.col0;
   for (int d = 0; d < fn::MAX_GATHER_DST; ++d)
@@ -587,6 +589,31 @@ fn_status flashnorm_linear_gather(const void* a, const void* Wt_star, const floa
   ex.zdst = z_dsts;
   // z (the plain output) is unused on this path: pass the first destination for the checks
   return linear_impl(a, Wt_star, c_star, M, K, N, eps, alpha, mode, dtype, z_dsts[0], FN_PATH_GEMM, nullptr, 0,
+                     static_cast<cudaStream_t>(stream), ex);
+}
+
+fn_status flashnorm_linear_gather_multicast(const void* a, const void* Wt_star, const float* c_star, int64_t M,
+                                            int64_t K, int64_t N, float eps, float alpha, fn_mode mode,
+                                            fn_dtype dtype, void* z_mc, int64_t ldz, int64_t col0, void* stream) {
+  if (dtype != FN_BF16) return fail(FN_ERR_UNSUPPORTED, "flashnorm_linear_gather_multicast is bf16-only");
+  if (z_mc == nullptr) return fail(FN_ERR_NULL, "z_mc is NULL");
+  if (col0 < 0 || ldz < col0 + N || ldz > INT32_MAX)
+    return fail(FN_ERR_SHAPE, "shard columns [%lld, %lld) do not fit rows of ldz = %lld", (long long)col0,
+                (long long)(col0 + N), (long long)ldz);
+  if (ldz % 8 != 0 || col0 % 8 != 0)
+    return fail(FN_ERR_ALIGN, "ldz = %lld and col0 = %lld must be multiples of 8 (16-byte rows)", (long long)ldz,
+                (long long)col0);
+  fn_status s;
+  if ((s = check_ptr16("z_mc", z_mc)) != FN_OK) return s;
+  if (z_mc == a) return fail(FN_ERR_VALUE, "z_mc aliases a");
+  void* dsts[1] = {z_mc};
+  LinearExtras ex;
+  ex.ndst = 1;
+  ex.ldz = (int)ldz;
+  ex.col0 = (int)col0;
+  ex.zdst = dsts;
+  ex.mc = 1;
+  return linear_impl(a, Wt_star, c_star, M, K, N, eps, alpha, mode, dtype, z_mc, FN_PATH_GEMM, nullptr, 0,
                      static_cast<cudaStream_t>(stream), ex);
 }
 

@@ -128,6 +128,13 @@ FN_DEVICE void tma_store_2d(const CUtensorMap* m, const void* src, int32_t x, in
                "r"(smem_u32(src)), "r"(x), "r"(y)
                : "memory");
 }
+// 16-byte store through an NVLS multicast address (NVSwitch replicates it to every bound GPU)
+FN_DEVICE void multimem_st_v4(void* mc_addr, uint4 v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(mc_addr),
+               "f"(__uint_as_float(v.x)), "f"(__uint_as_float(v.y)), "f"(__uint_as_float(v.z)),
+               "f"(__uint_as_float(v.w))
+               : "memory");
+}
 FN_DEVICE void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 // 2D tiled prefetch global -> L2 only (no SMEM, no barrier): warms the lines a later
 // tma_load_2d of the same box will read.

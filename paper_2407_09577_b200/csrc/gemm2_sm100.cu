@@ -564,8 +564,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
               uint4* dst = reinterpret_cast<uint4*>(p.zdst[d] + off);
 #pragma unroll
               for (int q = 0; q < 4; ++q)
-                if (n_base + j * 32 + q * 8 < p.N)
-                  dst[q] = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+                if (n_base + j * 32 + q * 8 < p.N) {
+                  const uint4 v4 = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+                  if (p.mc) multimem_st_v4(dst + q, v4);  // NVLS: one store, every rank's buffer
+                  else dst[q] = v4;
+                }
             }
           }
         }

@@ -63,6 +63,10 @@ struct GemmParams {
   // buffers, e.g. every rank's gathered z), at columns [col0, col0 + N); ndst = 0 -> z [M x N]
   int ndst, ldz, col0;
   __nv_bfloat16* zdst[8];
+  // mc = 1 (ndst == 1): zdst[0] is an NVLS multicast address; the epilogue stores with multimem.st,
+  // so the switch replicates each 16-byte segment to every rank's buffer (one NVLink write per
+  // rank instead of P - 1)
+  int mc;
   int bn;  // pair kernel tile width (256 or 224, gemm2_pick_bn); num_n_blocks = ceil(N / bn)
   int rms_local;  // pair kernel, RMS: A completes on each CTA's own barrier (see gemm2_sm100.cu)
   int tile_rot;   // pair kernel wave order: 0 plain grid stride, 1 rotated (pair_tile_rotation), 2 matched table

@@ -87,12 +87,18 @@ class ColumnParallelFlashNorm:
         return self._permute(flat.view(self.world, M, Nl))  # [P][M][Nl] -> [M][P*Nl]
 
     def forward_fused_gather(self, a, eps: float = 1e-5, mode: str = "rmsnorm", alpha: float = 0.5,
-                             copy: bool = False):
+                             copy: bool = False, multicast="auto"):
         """Gathered output with the all-gather FUSED into the GEMM epilogue (NEXT-3): every rank's
         epilogue stores its shard straight into every rank's gathered buffer over NVLink
         (flashnorm_linear_gather with the peers' symmetric-memory pointers), tile by tile while the
         next tiles compute; a device-side barrier then orders the peers' reads.  Replaces the
         NCCL all-gather + permute of `forward(gather=True)`.
+
+        NVLS: when the symmetric buffer has a multicast mapping (torch symmetric memory's
+        ``multicast_ptr`` is non-zero: NVSwitch with NVLink SHARP) and ``multicast`` is "auto" or True,
+        the epilogue stores through it with multimem.st (flashnorm_linear_gather_multicast): each rank
+        sends its shard once and the switch replicates it to every rank, instead of P - 1 peer stores.
+        ``multicast=True`` without a multicast mapping raises; False forces the peer stores.
 
         Lifetime of the result: the gathered z lives in one of TWO persistent symmetric buffers
         that alternate between calls (peers write into them over NVLink).  The returned tensor is
@@ -120,9 +126,19 @@ class ColumnParallelFlashNorm:
         i = self._symm_slot
         self._symm_slot ^= 1
         hdl = self._symm_hdls[i]
+        mc_ptr = int(getattr(hdl, "multicast_ptr", 0) or 0)
+        if multicast is True and not mc_ptr:
+            raise RuntimeError("forward_fused_gather(multicast=True): no NVLS multicast mapping on this group")
         hdl.barrier(channel=0)  # every rank finished the work it ordered before this call on slot i
-        linear_gather(a, self.W, self._symm_peers[i], self.rank * Nl, c_star=self.c, eps=eps, mode=mode,
-                      alpha=alpha)
+        if mc_ptr and multicast in ("auto", True):
+            from . import linear_gather_multicast
+            linear_gather_multicast(a, self.W, mc_ptr, N, self.rank * Nl, c_star=self.c, eps=eps, mode=mode,
+                                    alpha=alpha)
+            self.last_gather = "multicast"
+        else:
+            linear_gather(a, self.W, self._symm_peers[i], self.rank * Nl, c_star=self.c, eps=eps, mode=mode,
+                          alpha=alpha)
+            self.last_gather = "peer stores"
         hdl.barrier(channel=0)  # every shard has landed in every rank's buffer
         out = self._symm_bufs[i]
         return out.clone() if copy else out

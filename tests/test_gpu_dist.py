@@ -36,6 +36,12 @@ for _ in range(3):
     out = layer.forward_fused_gather(a, eps=1e-5)
     torch.cuda.synchronize()
     assert torch.equal(out.view(torch.int16), ref.view(torch.int16)), "fused gather differs"
+try:
+    layer.forward_fused_gather(a, eps=1e-5, multicast=True)
+    assert layer.last_gather == "multicast"
+    print("MULTICAST_AVAILABLE")
+except RuntimeError as e:
+    assert "no NVLS multicast mapping" in str(e)
 g2 = layer(a, gather=True)
 assert torch.equal(g2.view(torch.int16), ref.view(torch.int16))
 dist.destroy_process_group()

@@ -63,10 +63,13 @@ for (M, K, N) in [(300, 512, 1024 * world), (16, 4096, 768 * world), (4096, 4096
     layer = ColumnParallelFlashNorm(Wl.contiguous(), cl.contiguous(), world=world, rank=rank)
     zt = layer(a, gather=True)
     ok &= torch.equal(zt.view(torch.int16), full.view(torch.int16))
-    for _ in range(3):
-        zf = layer.forward_fused_gather(a, eps=1e-5)
-        torch.cuda.synchronize()
-        ok &= torch.equal(zf.view(torch.int16), full.view(torch.int16))
+    for mc in ("auto", False):  # NVLS multimem.st when the group has a multicast mapping, and peer stores
+        for _ in range(3):
+            zf = layer.forward_fused_gather(a, eps=1e-5, multicast=mc)
+            torch.cuda.synchronize()
+            ok &= torch.equal(zf.view(torch.int16), full.view(torch.int16))
+        if rank == 0:
+            print("fused gather", mc, "->", layer.last_gather)
     del a, W, Ws, full, zl, parts, cat, zc, zt, layer
 okt = torch.tensor([1 if ok else 0], device=dev)
 dist.all_reduce(okt, op=dist.ReduceOp.MIN)

@@ -660,3 +660,18 @@ def test_layernorm_debug_check_rejects_uncentered_input():
     r = subprocess.run([sys.executable, "-c", _DEBUG_LN, root], env=dict(os.environ, FN_DEBUG_LAYERNORM="1"),
                        capture_output=True, text=True, timeout=300)
     assert "REJECTED" in r.stdout and "NOT_REJECTED" not in r.stdout, r.stdout + r.stderr[-3000:]
+
+
+def test_linear_gather_multicast_validation():
+    """flashnorm_linear_gather_multicast rejects bad arguments before any launch (the store path
+    itself needs an NVLS multicast mapping: tests/test_gpu_multi.py on a multi-GPU NVSwitch node)."""
+    M, K, N = 64, 256, 256
+    a = T(gen_activations(63, M, K, "normal", "bf16"))
+    Wt, g, _, _ = gen_layer(63, N, K, "bf16")
+    Ws, cs = fn.fold_weights(T(Wt), T(g, "f32"))
+    with pytest.raises(fn.FlashNormError, match="FN_ERR_NULL"):
+        fn.linear_gather_multicast(a, Ws, 0, N, 0, c_star=cs)
+    with pytest.raises(fn.FlashNormError, match="FN_ERR_SHAPE"):
+        fn.linear_gather_multicast(a, Ws, 1 << 40, N - 8, 0, c_star=cs)
+    with pytest.raises(fn.FlashNormError, match="FN_ERR_ALIGN"):
+        fn.linear_gather_multicast(a, Ws, (1 << 40) + 8, N, 0, c_star=cs)
