@@ -182,21 +182,30 @@ fn_status flashnorm_linear_ex(const void* a, const void* Wt_star, const float* c
                               int64_t M, int64_t K, int64_t N, float eps, float alpha,
                               fn_mode mode, fn_dtype dtype, void* z, fn_path path, void* stream);
 
-/* flashnorm_linear_ws — flashnorm_linear_ex with caller-owned device scratch.
- * For mode == FN_DYT on a bf16 GEMM path (M > 16 or an explicit GEMM path) a
- * workspace of flashnorm_linear_workspace_bytes() = M*K*2 bytes lets the
- * library compute RN_bf16(tanh(alpha a)) ONCE per element (kernel K8, an
- * HBM-bound pre-pass; DyT is named at PAPER.md:5 and its bias at PAPER.md:25,
- * the elementwise formula is reading c10) and then run the GEMM in mode FN_NONE
- * on it, instead of recomputing tanh in the A-tile prologue of every N tile
- * (MUFU tanh: ~16 values/clk/SM on sm_100a, the same rate at which the tensor
- * core consumes A at BN = 256, DESIGN.md §6 K8).  z is bit-identical to the
- * prologue path.  Two kernel launches instead of one.
- *   workspace        16-B aligned device scratch, or NULL (then workspace_bytes
- *                    must be 0 and the call is exactly flashnorm_linear_ex);
- *                    must not alias a, Wt_star or z.  Contents on return are
- *                    unspecified; ownership stays with the caller.
- *   workspace_bytes  its size; FN_ERR_VALUE if a DyT GEMM needs more.
+/* flashnorm_linear_ws — flashnorm_linear_ex with caller-owned device scratch, used for two things:
+ *  (1) mode == FN_DYT on a bf16 GEMM path (M > 16 or an explicit GEMM path): the library computes
+ *      RN_bf16(tanh(alpha a)) ONCE per element (kernel K8, an HBM-bound pre-pass; DyT is named at
+ *      PAPER.md:5 and its bias at PAPER.md:25, the elementwise formula is reading c10) and then runs
+ *      the GEMM in mode FN_NONE on it, instead of recomputing tanh in the A-tile prologue of every N
+ *      tile (MUFU tanh: ~16 values/clk/SM on sm_100a, the rate at which the tensor core consumes A at
+ *      BN = 256, DESIGN.md §6 K8).  z is bit-identical to the prologue path.  Two launches.
+ *  (2) the stream-K tail of the CTA-pair GEMM (plain epilogue): when the pair-tile count T is not
+ *      a multiple of the 74 CTA pairs and T < 4 x 74, the last (T mod 74) + 74 tiles are split
+ *      into equal K ranges, and a tile split over two pairs is finished by the pair holding its
+ *      last k block, which adds the other's fp32 partial in a fixed order
+ *      (deterministic, but not bit-identical to the unsplit tile).  Which kernels use it is the
+ *      environment variable FN_GEMM2_SK, read at every call: 0 (default) none, 1 the mode-none
+ *      kernel (FN_NONE, DyT after its pre-pass), 2 also rmsnorm / layernorm — it measured no
+ *      faster on config 4; flashnorm_linear_workspace_bytes follows the policy.
+ *  Layout: [4 KiB stream-K flags][stream-K fp32 partials][DyT buffer of M*K*2].  The FIRST 4 KiB
+ *  MUST BE ZERO before a call (zero-fill the buffer once); every call leaves them zero, so one
+ *  workspace serves any sequence of calls on one stream (and CUDA graph replays).  The rest is
+ *  scratch, contents unspecified on return.
+ *   workspace        16-B aligned device scratch, or NULL (then workspace_bytes must be 0 and the
+ *                    call is exactly flashnorm_linear_ex); must not alias a, Wt_star or z;
+ *                    ownership stays with the caller.
+ *   workspace_bytes  its size; a DyT GEMM that needs more returns FN_ERR_VALUE; a workspace too
+ *                    small for the stream-K scratch runs whole tiles.
  * Other modes / paths ignore the workspace.
  * flashnorm_linear_workspace_bytes returns the size a call with the same
  * arguments would use (0 = none needed). */

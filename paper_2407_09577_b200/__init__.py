@@ -292,7 +292,7 @@ def linear(a, Wt_star, c_star=None, eps: float = 1e-5, mode: str = "rmsnorm", al
         if workspace != "auto":
             raise FlashNormError(5, "linear", f"workspace must be 'auto', None or a CUDA tensor, got {workspace!r}")
         nb = linear_workspace_bytes(M, K, N, mode, a.dtype, path)
-        workspace = torch.empty(nb, dtype=torch.uint8, device=a.device) if nb > 0 else None
+        workspace = _auto_workspace(nb, a.device) if nb > 0 else None
     ws_bytes = 0
     if workspace is not None:
         _dev(workspace, "workspace")
@@ -302,6 +302,22 @@ def linear(a, Wt_star, c_star=None, eps: float = 1e-5, mode: str = "rmsnorm", al
                                    _stream(a))
     _check(st, "linear")
     return z
+
+
+_WS_CACHE = {}
+
+
+def _auto_workspace(nbytes: int, device):
+    """The library-facing scratch of linear(workspace="auto"): one zero-filled buffer per (device,
+    stream), grown on demand and reused — its first 4 KiB (stream-K flags) must be zero before a
+    call and every call leaves them zero (include/flashnorm.h flashnorm_linear_ws)."""
+    torch = _torch()
+    key = (device.index, torch.cuda.current_stream(device).cuda_stream)
+    buf = _WS_CACHE.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
+        _WS_CACHE[key] = buf
+    return buf
 
 
 def linear_workspace_bytes(M: int, K: int, N: int, mode: str = "rmsnorm", dtype=None, path: str = "auto") -> int:

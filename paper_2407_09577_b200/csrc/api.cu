@@ -227,6 +227,35 @@ fn_status get_tmap_kpair(const void* ptr, int64_t rows, int64_t cols, int box_ro
   return FN_OK;
 }
 
+int stg_enabled() {
+  static const int on = [] {
+    const char* e = getenv("FN_GEMM2_STG");  // A/B knob: 256-bit epilogue stores (1 = on)
+    return e != nullptr ? atoi(e) : 1;
+  }();
+  return on;
+}
+
+// stream-K tail policy, read at every call (A/B knob FN_GEMM2_SK): 0 (default) off, 1 the
+// mode-none kernel only (DyT pre-pass, plain GEMM), 2 also the RMS / LayerNorm-retrofit kernel.
+// Measured on config 4: mode none within +-2% (constant data +2.5%, random data
+// -1.5%, CUDA graphs), RMS -4..-7%: the partial traffic, the finisher fixups and the ssq group's
+// per-item reductions cost as much as the 13% shorter MMA span saves.
+bool sk_allowed(int kernel_mode) {
+  const char* e = getenv("FN_GEMM2_SK");
+  const int pol = e != nullptr ? atoi(e) : 0;
+  return kernel_mode == fn::MODE_NONE ? pol >= 1 : (kernel_mode == fn::MODE_RMS && pol >= 2);
+}
+
+// stream-K scratch of a pair-kernel launch (0: the shape does not use it); `ws_off`: its offset in
+// the caller's workspace (after the DyT pre-pass buffer, 256-B aligned)
+// the stream-K flags live in the first 4 KiB of a linear workspace, always (zero between calls)
+constexpr int64_t kSkFlagBytes = 4096;
+int64_t sk_scratch(int64_t M, int64_t K, int64_t N, int bn, int* sk_tiles, int* sk_dp_waves) {
+  const int mb = (int)((M + 255) / 256), nb = (int)((N + bn - 1) / bn);
+  return fn::gemm2_sk_plan(mb * nb, (int)((K + 63) / 64), num_sms(), sk_tiles, sk_dp_waves);
+}
+int64_t align256(int64_t x) { return (x + 255) / 256 * 256; }
+
 int kernel_mode(fn_mode m) {
   switch (m) {
     case FN_RMSNORM:
@@ -344,27 +373,47 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
     ++g_launches;
     return FN_OK;
   }
-  // DyT with a workspace: K8 computes tanh(alpha a) once per element (dyt.cu explains why the
-  // in-SMEM prologue is MUFU-bound), then the GEMM runs in mode NONE on it — bit-identical z.
+  // Workspace layout (include/flashnorm.h flashnorm_linear_ws): [4 KiB stream-K flags][stream-K fp32
+  // partials][DyT pre-pass buffer].  DyT with a workspace: K8 computes tanh(alpha a) once per element
+  // (dyt.cu explains why the in-SMEM prologue is MUFU-bound), then the GEMM runs in mode NONE on it —
+  // bit-identical z.
   int launches = 1;
-  if (km == fn::MODE_DYT && workspace != nullptr) {
-    if (workspace_bytes < M * K * 2)
-      return fail(FN_ERR_VALUE, "workspace_bytes = %lld < M*K*2 = %lld", (long long)workspace_bytes,
-                  (long long)(M * K * 2));
-    cudaError_t e = fn::launch_dyt_prepass(static_cast<const __nv_bfloat16*>(a), static_cast<__nv_bfloat16*>(workspace),
-                                           M * K, alpha, num_sms(), stream);
-    if (e != cudaSuccess) return cuda_fail(e, "dyt_prepass");
-    a = workspace;
-    km = fn::MODE_NONE;
-    launches = 2;
-  }
+  const bool prepass = km == fn::MODE_DYT && workspace != nullptr;
+  const int km_gemm = prepass ? fn::MODE_NONE : km;
   // CTA-pair (cta_group::2, 256x256 tiles) kernel when M > 128; the 1-CTA kernel for M <= 128
   // and FN_PATH_GEMM1.
   const bool pair = M > 128 && (path != FN_PATH_GEMM1);
   // 224-wide pair tiles when they even out the last wave (plain / LayerNorm / scaled / gather
   // epilogues; GLU, RoPE and QK-norm keep their 256-column tile algebra, DyT its prologue)
-  const bool allow_224 = km != fn::MODE_DYT && ex.glu_act < 0 && ex.rope.pos == nullptr;
+  const bool allow_224 = km_gemm != fn::MODE_DYT && ex.glu_act < 0 && ex.rope.pos == nullptr;
   const int bn = pair ? fn::gemm2_pick_bn((int)M, (int)N, num_sms(), allow_224) : 256;
+  // stream-K tail (pair kernel, plain RMS / LayerNorm-retrofit / none epilogues) when the caller's
+  // workspace holds its scratch (flashnorm_linear_workspace_bytes counts it)
+  int sk_tiles = 0, sk_waves = 0;
+  int64_t sk_bytes = 0;
+  if (pair && sk_allowed(km_gemm) && workspace != nullptr &&
+      (km_gemm == fn::MODE_NONE || (km_gemm == fn::MODE_RMS && ex.ln_u == nullptr)) && ex.glu_act < 0 &&
+      ex.rope.pos == nullptr && ex.ndst == 0)
+    sk_bytes = sk_scratch(M, K, N, bn, &sk_tiles, &sk_waves);
+  const int64_t dyt_off = (workspace != nullptr) ? align256(kSkFlagBytes + sk_bytes) : 0;
+  if (workspace != nullptr && (sk_bytes > 0 || prepass) &&
+      workspace_bytes < dyt_off + (prepass ? M * K * 2 : 0)) {
+    sk_tiles = 0;  // too small for the stream-K scratch: whole tiles only
+    sk_bytes = 0;
+  }
+  if (prepass) {
+    const int64_t off = align256(kSkFlagBytes + sk_bytes);
+    if (workspace_bytes < off + M * K * 2)
+      return fail(FN_ERR_VALUE, "workspace_bytes = %lld < %lld (flashnorm_linear_workspace_bytes)",
+                  (long long)workspace_bytes, (long long)(off + M * K * 2));
+    void* ybuf = static_cast<uint8_t*>(workspace) + off;
+    cudaError_t e = fn::launch_dyt_prepass(static_cast<const __nv_bfloat16*>(a), static_cast<__nv_bfloat16*>(ybuf),
+                                           M * K, alpha, num_sms(), stream);
+    if (e != cudaSuccess) return cuda_fail(e, "dyt_prepass");
+    a = ybuf;
+    km = fn::MODE_NONE;
+    launches = 2;
+  }
   CUtensorMap ta, tb;
   if ((s = get_tmap(a, M, K, 128, &ta)) != FN_OK) return s;
   if ((s = get_tmap(Wt_star, N, K, pair ? bn / 2 : 256, &tb)) != FN_OK) return s;
@@ -418,10 +467,15 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
   p.ln_u = ex.ln_u;
   p.ndst = ex.ndst;
   p.mc = ex.mc;
+  p.stg = stg_enabled();
   p.ldz = ex.ldz;
   p.col0 = ex.col0;
   for (int d = 0; d < fn::MAX_GATHER_DST; ++d)
     p.zdst[d] = d < ex.ndst ? static_cast<__nv_bfloat16*>(ex.zdst[d]) : nullptr;
+  p.sk_tiles = sk_bytes > 0 ? sk_tiles : 0;
+  p.sk_dp_waves = sk_waves;
+  p.sk_flag = sk_bytes > 0 ? static_cast<unsigned*>(workspace) : nullptr;
+  p.sk_part = sk_bytes > 0 ? reinterpret_cast<float*>(static_cast<uint8_t*>(workspace) + kSkFlagBytes) : nullptr;
   cudaError_t e = pair ? fn::launch_gemm2(ta, tb, p, km, num_sms(), stream)
                        : fn::launch_gemm(ta, tb, p, km, num_sms(), stream);
   if (e != cudaSuccess) return cuda_fail(e, pair ? "gemm2_sm100" : "gemm_sm100");
@@ -520,11 +574,21 @@ fn_status flashnorm_linear_ex(const void* a, const void* Wt_star, const float* c
 
 int64_t flashnorm_linear_workspace_bytes(int64_t M, int64_t K, int64_t N, fn_mode mode, fn_dtype dtype,
                                          fn_path path) {
-  if (mode != FN_DYT || dtype != FN_BF16 || M <= 0 || K <= 0 || N <= 0) return 0;
+  if (dtype != FN_BF16 || M <= 0 || K <= 0 || N <= 0) return 0;
   if (path == FN_PATH_GEMV || path == FN_PATH_GEMV_MMA || path == FN_PATH_SIMT) return 0;
   const bool gemv_ok = fn::gemv_tc_supported((int)M, (int)N, num_sms()) || fn::gemv_supported((int)M, (int)K);
   if (path == FN_PATH_AUTO && gemv_ok) return 0;  // decode: tanh is computed once per CTA anyway
-  return M * K * 2;
+  // the pair kernel's stream-K scratch (same decision as linear_impl; DyT runs it in mode none)
+  int64_t sk = 0;
+  const bool pair = M > 128 && path != FN_PATH_GEMM1;
+  const int km = (mode == FN_RMSNORM || mode == FN_LAYERNORM) ? fn::MODE_RMS : fn::MODE_NONE;  // DyT: pre-pass + none
+  if (pair && sk_allowed(km)) {
+    const int bn = fn::gemm2_pick_bn((int)M, (int)N, num_sms(), true);
+    int skt = 0, skw = 0;
+    sk = sk_scratch(M, K, N, bn, &skt, &skw);
+  }
+  if (sk == 0 && mode != FN_DYT) return 0;
+  return align256(kSkFlagBytes + sk) + (mode == FN_DYT ? M * K * 2 : 0);
 }
 
 fn_status flashnorm_linear_ws(const void* a, const void* Wt_star, const float* c_star, int64_t M, int64_t K,

@@ -55,13 +55,38 @@ constexpr int BAR_BYTES = 1024;
 constexpr int SSQ_SLOTS = 16;          // per-CTA cache of reduced row ssq, by M block
 static_assert(SSQ_SLOTS == PAIR_SSQ_SLOTS, "the host schedule mirrors this cache");
 constexpr int SMEM_BYTES = 1024 + STAGES * (A_STAGE + B_STAGE) + BAR_BYTES + (4 + SSQ_SLOTS) * BM * 4 + 32 +
-                             (2 + SSQ_SLOTS) * BM * 4;  // + LayerNorm mean buffers
+                             (2 + SSQ_SLOTS) * BM * 4 +  // + LayerNorm mean buffers
+                             4 * 256 * 4;                // + the tile's c* per epilogue warp
 // the pair tile width is a template parameter: 256 (default) or 224 (picked by the host when it
 // evens out the last wave of tiles over the CTA pairs, gemm2_pick_bn); TMEM stays 2 x 256 columns
 constexpr int smem_bytes(int bn) { return SMEM_BYTES - STAGES * (B_STAGE - (bn / 2) * BK * 2); }
 }  // namespace gemm2
 
-template <int MODE, int BN_ = gemm2::BN, bool TBL = true>
+FN_DEVICE unsigned sk_ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+FN_DEVICE void sk_st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+FN_DEVICE uint64_t sk_gtime() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+#ifdef FN_SK_TRACE  // tools/micro/sk_trace.cu: per-CTA globaltimer stamps (ns) of the first 4 items
+__device__ unsigned long long g_sk_trace[160][4][6];
+#define SK_STAMP(li, e) do { if (lane == 0 && (li) < 4 && blockIdx.x < 160) g_sk_trace[blockIdx.x][li][e] = sk_gtime(); } while (0)
+__device__ unsigned long long g_sk_chunk[160][4][4][8][2];  // [cta][item][epilogue warp][chunk][tmem ready, stored]
+#define SK_CSTAMP(li, j, e) do { if (lane == 0 && (li) < 4 && blockIdx.x < 160 && (j) < 8) g_sk_chunk[blockIdx.x][li][ew][j][e] = sk_gtime(); } while (0)
+#else
+#define SK_STAMP(li, e)
+#define SK_CSTAMP(li, j, e)
+#endif
+
+template <int MODE, int BN_ = gemm2::BN, bool TBL = true, bool SK = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
     flashnorm_gemm2_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                            GemmParams p,
@@ -94,6 +119,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
   const uint8_t* sig_src = sig_dst + 16;                                      // 16 B: its (unused) source
   float* mu_buf = reinterpret_cast<float*>(sig_dst + 32);  // [2][BM] LayerNorm (ln_u): row means
   float* mu_cache = mu_buf + 2 * BM;                       // [SSQ_SLOTS][BM]
+  float* cst_smem = mu_cache + SSQ_SLOTS * BM;             // [4 warps][256] the tile's c*
   const bool ln = MODE == MODE_RMS && p.ln_u != nullptr;   // exact deferred LayerNorm (reading c29)
   // RMS with LOCAL A completion (p.rms_local): each CTA's A half lands on its own `afull`, the
   // ssq group reads it there while the MMA runs (release `empty` = MMA commit + ssq group), and
@@ -145,6 +171,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
     }
     return next_pair_tile(j, cluster, nclusters, rot, num_tiles);
   };
+  // every role walks the same item sequence: whole tiles (k blocks [0, nkb)) or, with the
+  // stream-K tail (SK), the pair's whole-tile waves and then its stream-K items (kernels.h)
+  auto next_item = [&](int& j, PairItem& it) -> bool {
+    if constexpr (SK) {
+      if (j < p.sk_dp_waves) {
+        it = PairItem{cluster + j * nclusters, 0, nkb, 0, -1};
+        ++j;
+        return true;
+      }
+      if (!sk_item(p, cluster, nclusters, j - p.sk_dp_waves, it)) return false;
+      ++j;
+      return true;
+    } else {
+      const int t = next_tile(j);
+      if (t < 0) return false;
+      it = PairItem{t, 0, nkb, 0, -1};
+      return true;
+    }
+  };
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer (both CTAs)
@@ -152,11 +197,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
       const uint32_t full0 = mapa_shared(&full[0], 0);  // leader's barrier array
       int stage = 0;
       uint32_t phase = 0;
-      for (int jw = 0, tile = next_tile(jw); tile >= 0;
-         tile = next_tile(jw)) {
+      PairItem it;
+      for (int jw = 0; next_item(jw, it);) {
         int m_blk, n_blk;
-        tile_coords(tile, p, m_blk, n_blk);
-        for (int kb = 0; kb < nkb; ++kb) {
+        tile_coords(it.tile, p, m_blk, n_blk);
+        for (int kb = it.kb0; kb < it.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           const uint32_t fb = full0 + stage * 8;
           if (MODE == MODE_DYT || la) {
@@ -185,33 +230,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      for (int jw = 0, tile = next_tile(jw); tile >= 0;
-         tile = next_tile(jw), ++local) {
+      PairItem it;
+      for (int jw = 0; next_item(jw, it); ++local) {
         const int as = local & 1;
         const uint32_t aphase = (local >> 1) & 1;
         int m_blk, n_blk_unused;
-        tile_coords(tile, p, m_blk, n_blk_unused);
+        tile_coords(it.tile, p, m_blk, n_blk_unused);
         const int slot = m_blk % SSQ_SLOTS;
         bool cached = false;
+        if (it.kb0 == 0 && it.kb1 == nkb) {  // partial K ranges (stream-K) neither use nor fill the ssq cache
 #pragma unroll
-        for (int i = 0; i < SSQ_SLOTS; ++i)
-          if (i == slot) { cached = tag[i] == m_blk; tag[i] = m_blk; }
+          for (int i = 0; i < SSQ_SLOTS; ++i)
+            if (i == slot) { cached = tag[i] == m_blk; tag[i] = m_blk; }
+        }
         uint64_t* release = (MODE == MODE_RMS && !cached && !la) ? mma_done : empty;
         mbar_wait(&tempty[as], aphase ^ 1);
+        SK_STAMP(local, 0);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + as * BN;
-        for (int kb = 0; kb < nkb; ++kb) {
+        for (int kb = it.kb0; kb < it.kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           if (MODE == MODE_DYT || la) mbar_wait(&ready[stage], phase);  // both CTAs' A ready (DyT: transformed)
           tc_fence_after();
           const uint64_t adesc = make_sw128_desc(smem_u32(sA + stage * A_STAGE));
           const uint64_t bdesc = make_sw128_desc(smem_u32(sB + stage * B_STAGE));
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) umma_bf16_pair(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+          for (int k = 0; k < BK / 16; ++k)
+            umma_bf16_pair(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb != it.kb0 || k != 0) ? 1u : 0u);
           umma_commit_pair_mc(&release[stage], 0x3);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
         umma_commit_pair_mc(&tfull[as], 0x3);
+        SK_STAMP(local, 1);
       }
     }
   } else if (warp == 3) {
@@ -221,9 +271,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
       const uint32_t sig0 = mapa_shared(sig_dst, 0);  // 16-byte landing slot in the leader
       int stage = 0;
       uint32_t phase = 0;
-      for (int jw = 0, tile = next_tile(jw); tile >= 0;
-         tile = next_tile(jw)) {
-        for (int kb = 0; kb < nkb; ++kb) {
+      PairItem it;
+      for (int jw = 0; next_item(jw, it);) {
+        for (int kb = it.kb0; kb < it.kb1; ++kb) {
           mbar_wait(&afull[stage], phase);
           if (leader) mbar_arrive_expect_tx(&ready[stage], 16);  // + the peer's 16-byte signal
           else dsmem_signal16(sig0, sig_src, ready0 + stage * 8);
@@ -247,15 +297,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
       };
       int stage = 0;
       int local = 0;
-      for (int jw = 0, tile = next_tile(jw); tile >= 0;
-         tile = next_tile(jw), ++local) {
+      PairItem it;
+      for (int jw = 0; next_item(jw, it); ++local) {
         int m_blk, n_blk_unused;
-        tile_coords(tile, p, m_blk, n_blk_unused);
+        tile_coords(it.tile, p, m_blk, n_blk_unused);
         const int slot = m_blk % SSQ_SLOTS;
         bool cached = false;
+        if (it.kb0 == 0 && it.kb1 == nkb) {  // mirrors the MMA thread: partial K ranges bypass the cache
 #pragma unroll
-        for (int i = 0; i < SSQ_SLOTS; ++i)
-          if (i == slot) { cached = tag[i] == m_blk; tag[i] = m_blk; }
+          for (int i = 0; i < SSQ_SLOTS; ++i)
+            if (i == slot) { cached = tag[i] == m_blk; tag[i] = m_blk; }
+        }
+        const int nk_it = it.kb1 - it.kb0;
         float ssq, mu = 0.f;
         if (cached) {
           // this CTA already reduced these 128 rows for an earlier N tile: the ring
@@ -309,8 +362,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
           ssq_cache[slot * BM + t] = ssq;
           mu_cache[slot * BM + t] = mu;
         } else {
+          // (a stream-K item: the partial ssq of its k blocks; the finisher adds the contributor's)
           float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-          for (int kb = 0; kb < nkb; ++kb) {
+          for (int kb = 0; kb < nk_it; ++kb) {
             wait_a(stage);
             const uint4* row = reinterpret_cast<const uint4*>(sA + stage * A_STAGE + t * 128);
 #pragma unroll
@@ -332,7 +386,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
             if (++stage == STAGES) stage = 0;
           }
           ssq = (s0 + s1) + (s2 + s3);
-          ssq_cache[slot * BM + t] = ssq;
+          if (it.kb0 == 0 && it.kb1 == nkb) ssq_cache[slot * BM + t] = ssq;
         }
         const int as = local & 1;
         const uint32_t aphase = (local >> 1) & 1;
@@ -352,9 +406,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
       const uint32_t sig0 = mapa_shared(sig_dst, 0);  // 16-byte landing slot in the leader
       int stage = 0;
       uint32_t phase = 0;
-      for (int jw = 0, tile = next_tile(jw); tile >= 0;
-         tile = next_tile(jw)) {
-        for (int kb = 0; kb < nkb; ++kb) {
+      PairItem it;
+      for (int jw = 0; next_item(jw, it);) {
+        for (int kb = it.kb0; kb < it.kb1; ++kb) {
           mbar_wait_warp(&afull[stage], phase);
           uint4* row = reinterpret_cast<uint4*>(sA + stage * A_STAGE + t * 128);
           uint4 v[8];
@@ -388,26 +442,108 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
     const uint32_t tempty0 = mapa_shared(&tempty[0], 0);
     int local = 0;
     const float invK = 1.0f / static_cast<float>(p.K);
-    for (int jw = 0, tile = next_tile(jw); tile >= 0;
-         tile = next_tile(jw), ++local) {
+    PairItem it;
+    for (int jw = 0; next_item(jw, it); ++local) {
       int m_blk, n_blk;
-      tile_coords(tile, p, m_blk, n_blk);
+      tile_coords(it.tile, p, m_blk, n_blk);
       const int as = local & 1;
       const uint32_t aphase = (local >> 1) & 1;
-      float r = 1.0f, mu = 0.f;
+      const int rl = ew * 32 + lane;  // this thread's row within the CTA's 128
+      if (ew == 0) SK_STAMP(local, 2);
+      float r = 1.0f, mu = 0.f, ssq = 0.f, ssq_part = 0.f;
+      // stream-K (kernels.h): the partial of the other pair's k range lives in sk_part
+      float* skp = nullptr;
+      float* sks = nullptr;
+      unsigned* skf = nullptr;
+      if (SK && it.fix != 0) {
+        // [32-column chunk j][float4 q][row]: a warp's 32 rows of one float4 are 512 contiguous bytes
+        skp = p.sk_part + ((size_t)it.sk * 2 + rank) * (BM * 256) + (size_t)rl * 4;
+        sks = p.sk_part + (size_t)p.sk_tiles * 2 * BM * 256 + ((size_t)it.sk * 2 + rank) * BM + rl;
+        skf = p.sk_flag + it.sk * 2 + rank;
+      }
+      const bool fin = SK && (it.fix == 1 || it.fix == 3);
+      if (fin) {  // finisher: wait for the contributor's partial (acquire), before this item's ssq
+        if (ew == 0 && lane == 0) {
+          const uint64_t t0 = sk_gtime();
+          while (sk_ld_acquire(skf) == 0u) {
+            __nanosleep(64);
+            if (sk_gtime() - t0 > 2000000000ull) __trap();  // a lost partial: fail loudly, never hang
+          }
+        }
+        named_bar_sync(2, 128);
+        if (ew == 0) SK_STAMP(local, 3);
+        if (MODE == MODE_RMS) ssq_part = __ldcg(sks);
+        // fix 3: the partial into the OTHER accumulator buffer while this item's MMA still runs:
+        // the finisher is its pair's last item, so that buffer is drained (this warp group's
+        // previous epilogue) and never written again; the chunk loop then reads both from TMEM
+        const uint32_t pbuf = tmem_base + ((ew * 32u) << 16) + (as ^ 1) * BN;
+#pragma unroll 1
+        for (int j = 0; j < (it.fix == 3 ? BN / 32 : 0); ++j) {
+          const float4* src = reinterpret_cast<const float4*>(skp) + j * 8 * BM;
+          uint32_t pv[32];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float4 c4 = __ldcg(src + q * BM);
+            pv[4 * q] = __float_as_uint(c4.x); pv[4 * q + 1] = __float_as_uint(c4.y);
+            pv[4 * q + 2] = __float_as_uint(c4.z); pv[4 * q + 3] = __float_as_uint(c4.w);
+          }
+          tmem_st_32x32b_x32(pbuf + j * 32, pv);
+        }
+        tmem_wait_st();
+      }
       if (MODE == MODE_RMS) {
         mbar_wait_warp(&sfull[as], aphase);
-        const float ssq = ssq_buf[as * BM + ew * 32 + lane];
-        if (ln) mu = mu_buf[as * BM + ew * 32 + lane];
-        epi_fence[ew * 32 + lane] = ssq + mu;  // consumes both loads before the buffer is released
+        ssq = ssq_buf[as * BM + rl];
+        if (ln) mu = mu_buf[as * BM + rl];
+        epi_fence[rl] = ssq + mu;  // consumes both loads before the buffer is released
         named_bar_sync(2, 128);
         if (ew == 0 && lane == 0) mbar_arrive(&sempty[as]);
-        r = rsqrtf(fmaf(ssq, invK, p.eps));
+        if (fin) ssq = ssq_part + ssq;  // fixed order: earlier k blocks first
+      }
+      if (MODE == MODE_RMS) r = rsqrtf(fmaf(ssq, invK, p.eps));
+      // the tile's c* slice to this warp's SMEM while the accumulator is still being produced (its
+      // L2 round trip off the per-chunk chain below)
+      float* cst_w = cst_smem + ew * 256;
+      if (p.cstar != nullptr) {
+        __syncwarp();  // the previous tile's reads of cst_w are done
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int cc = n_blk * BN + lane * 8 + h * 4;
+          float4 cv = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (cc < p.N) cv = __ldg(reinterpret_cast<const float4*>(p.cstar + cc));
+          reinterpret_cast<float4*>(cst_w)[lane * 2 + h] = cv;
+        }
+        __syncwarp();
       }
       mbar_wait_warp(&tfull[as], aphase);
+      if (ew == 0) SK_STAMP(local, 4);
       tc_fence_after();
-      const int row = m_blk * 2 * BM + rank * BM + ew * 32 + lane;
+      const int row = m_blk * 2 * BM + rank * BM + rl;
       const uint32_t taddr = tmem_base + ((ew * 32u) << 16) + as * BN;
+      if (SK && it.fix == 2) {
+        // contributor: the fp32 accumulator (and the partial ssq) to sk_part, then release the flag
+#pragma unroll 1
+        for (int j = 0; j < BN / 32; ++j) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(taddr + j * 32, v);
+          tmem_wait_ld();
+          float4* dst = reinterpret_cast<float4*>(skp) + j * 8 * BM;
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            __stcg(dst + q * BM, make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                                        __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3])));
+        }
+        if (MODE == MODE_RMS) __stcg(sks, ssq);
+        tc_fence_before();
+        named_bar_sync(2, 128);  // all 128 rows stored; TMEM reads of this buffer completed
+        if (ew == 0 && lane == 0) {
+          mbar_arrive_cluster(tempty0 + as * 8);
+          __threadfence();
+          sk_st_release(skf, 1u);
+        }
+        if (ew == 0) SK_STAMP(local, 5);
+        continue;
+      }
       if (MODE == MODE_RMS && p.glu_act >= 0 && p.glu_act != RELU_FFN) {
         // GLU epilogue: TMEM columns [0,128) = gate block n_blk, [128,256) = up block n_blk
         const int F = p.N / 2;
@@ -449,15 +585,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
       for (int j = 0; j < BN / 32; ++j) {
         if (n_base + j * 32 >= p.N) break;  // warp-uniform
         uint32_t v[32];
-        tmem_ld_32x32b_x32(taddr + j * 32, v);
-        tmem_wait_ld();
-        float cb[32];
-        if (p.cstar != nullptr) {
-          const float4* c4 = reinterpret_cast<const float4*>(p.cstar + n_base + j * 32);
+        if (SK && it.fix == 1) {  // + the contributor's partial (earlier k blocks) from L2
+          const float4* src = reinterpret_cast<const float4*>(skp) + j * 8 * BM;
+          float4 pc[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) pc[q] = __ldcg(src + q * BM);  // in flight with the TMEM load
+          tmem_ld_32x32b_x32(taddr + j * 32, v);
+          tmem_wait_ld();
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
-            float4 cv = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (n_base + j * 32 + q * 4 < p.N) cv = __ldg(c4 + q);
+            v[4 * q] = __float_as_uint(pc[q].x + __uint_as_float(v[4 * q]));
+            v[4 * q + 1] = __float_as_uint(pc[q].y + __uint_as_float(v[4 * q + 1]));
+            v[4 * q + 2] = __float_as_uint(pc[q].z + __uint_as_float(v[4 * q + 2]));
+            v[4 * q + 3] = __float_as_uint(pc[q].w + __uint_as_float(v[4 * q + 3]));
+          }
+        } else if (SK && it.fix == 3) {  // + the partial staged in the other TMEM buffer
+          uint32_t pv[32];
+          tmem_ld_32x32b_x32(taddr + j * 32, v);
+          tmem_ld_32x32b_x32(taddr + ((as ^ 1) - as) * BN + j * 32, pv);
+          tmem_wait_ld();
+#pragma unroll
+          for (int q = 0; q < 32; ++q) v[q] = __float_as_uint(__uint_as_float(pv[q]) + __uint_as_float(v[q]));
+        } else {
+          tmem_ld_32x32b_x32(taddr + j * 32, v);
+          tmem_wait_ld();
+        }
+        SK_CSTAMP(local, j, 0);
+        float cb[32];
+        if (p.cstar != nullptr) {
+          const float4* c4 = reinterpret_cast<const float4*>(cst_w + j * 32);  // zero past N
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float4 cv = c4[q];
             cb[4 * q + 0] = cv.x; cb[4 * q + 1] = cv.y; cb[4 * q + 2] = cv.z; cb[4 * q + 3] = cv.w;
           }
         } else {
@@ -548,13 +707,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
             packed[q] = pack_bf16(fmaf(__uint_as_float(v[2 * q]), r, cb[2 * q]),
                                   fmaf(__uint_as_float(v[2 * q + 1]), r, cb[2 * q + 1]));
         }
+#ifdef FN_SK_TRACE
+        if (p.stg == 2) {  // trace experiment: no output stores
+          if (packed[0] == 0x12345678u && packed[15] == 0x9abcdef0u) p.z[0] = __float2bfloat16(1.f);
+        } else
+#endif
         if (row < p.M) {
           if (p.ndst == 0) {
             uint4* dst = reinterpret_cast<uint4*>(zrow + j * 32);
+            if (p.stg == 1 && n_base + j * 32 + 32 <= p.N && (reinterpret_cast<uintptr_t>(dst) & 31) == 0) {
+              // two full 32-byte sectors per lane (256-bit stores)
+              st_global_v8(dst, make_uint4(packed[0], packed[1], packed[2], packed[3]),
+                           make_uint4(packed[4], packed[5], packed[6], packed[7]));
+              st_global_v8(dst + 2, make_uint4(packed[8], packed[9], packed[10], packed[11]),
+                           make_uint4(packed[12], packed[13], packed[14], packed[15]));
+            } else {
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-              if (n_base + j * 32 + q * 8 < p.N)
-                dst[q] = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+              for (int q = 0; q < 4; ++q)
+                if (n_base + j * 32 + q * 8 < p.N)
+                  dst[q] = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+            }
           } else {
             // fused gather: the same 64-byte row segment to every destination (st.global to a
             // peer-mapped address is an NVLink store), overlapped with the next tile's mainloop
@@ -572,10 +744,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
             }
           }
         }
+        SK_CSTAMP(local, j, 1);
       }
       tc_fence_before();
       named_bar_sync(2, 128);  // all 4 warps' TMEM loads of this buffer completed
-      if (ew == 0 && lane == 0) mbar_arrive_cluster(tempty0 + as * 8);  // one arrival per CTA, at the leader
+      if (ew == 0 && lane == 0) {
+        mbar_arrive_cluster(tempty0 + as * 8);  // one arrival per CTA, at the leader
+        if (fin) *skf = 0u;                     // consumed: zero for the next call
+      }
+      if (ew == 0) SK_STAMP(local, 5);
     }
   }
 
@@ -589,6 +766,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
 }
 
 int gemm2_smem_bytes() { return gemm2::SMEM_BYTES; }
+
+// stream-K tail plan (kernels.h GemmParams::sk_*): with C pairs and T tiles, T % C != 0 and at
+// least one whole wave, the last (T % C) + C tiles are split into equal K ranges (U / C >= nkb
+// k blocks per pair: every split tile has one contributor and one finisher); sk_dp_waves whole
+// waves go first.  Returns the scratch bytes (0: no stream-K).
+int64_t gemm2_sk_plan(int num_tiles, int nkb, int num_sms, int* sk_tiles, int* sk_dp_waves) {
+  *sk_tiles = 0;
+  *sk_dp_waves = 0;
+  const int C = num_sms / 2;
+  if (C <= 0 || num_tiles < C || num_tiles % C == 0 || nkb < 2) return 0;
+  const int waves = num_tiles / C;  // whole waves
+  if (waves > 3) return 0;          // the ragged last wave costs < 1/4 of the run: not worth the fixup
+  *sk_tiles = num_tiles % C + C;
+  *sk_dp_waves = waves - 1;
+  return (int64_t)(*sk_tiles) * 2 * gemm2::BM * (256 + 1) * 4 + (int64_t)(*sk_tiles) * 2 * 4 + 64;
+}
 
 // Pair tile width for an M x N problem: the one with the shorter makespan, counted as
 // ceil(tiles / pairs) rounds of bn columns (the last N block counted whole), 224 discounted by
@@ -633,11 +826,11 @@ static const PairSchedule* pair_schedule(const GemmParams& p, int pairs) {
   return it->second.get();
 }
 
-template <int MODE, int BN, bool TBL>
+template <int MODE, int BN, bool TBL, bool SK = false>
 static cudaError_t launch_gemm2_k(const CUtensorMap& ta, const CUtensorMap& tb_half, const GemmParams& p, int pairs,
                                   const void* sched, cudaStream_t stream) {
   using namespace gemm2;
-  const void* fptr = (const void*)flashnorm_gemm2_kernel<MODE, BN, TBL>;
+  const void* fptr = (const void*)flashnorm_gemm2_kernel<MODE, BN, TBL, SK>;
   const int smem = smem_bytes(BN);
   if (cudaError_t e = ensure_smem_attr(fptr, smem); e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -656,6 +849,12 @@ static cudaError_t launch_gemm2_t(const CUtensorMap& ta, const CUtensorMap& tb_h
                                   int num_sms, cudaStream_t stream) {
   int pairs = num_sms / 2;
   if (p.num_tiles < pairs) pairs = p.num_tiles;
+  if (p.sk_tiles > 0) {  // stream-K tail: whole-tile waves in grid-stride order, then the K-split items
+    static const PairScheduleNone none_sk = {0};
+    if constexpr (MODE == MODE_RMS || MODE == MODE_NONE)
+      return launch_gemm2_k<MODE, BN, false, true>(ta, tb_half, p, pairs, &none_sk, stream);
+    return cudaErrorInvalidValue;
+  }
   // one wave or less: the order cannot matter, and the table-free instance skips the 16 KiB
   // parameter upload (measured ~0.4 us per call on small shapes)
   const PairSchedule* sched = p.num_tiles > pairs ? pair_schedule(p, pairs) : nullptr;

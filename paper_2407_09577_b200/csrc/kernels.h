@@ -67,10 +67,49 @@ struct GemmParams {
   // so the switch replicates each 16-byte segment to every rank's buffer (one NVLink write per
   // rank instead of P - 1)
   int mc;
+  int stg;  // pair kernel epilogue: 1 = 32-byte (256-bit) row-segment stores, 0 = 16-byte (A/B knob)
   int bn;  // pair kernel tile width (256 or 224, gemm2_pick_bn); num_n_blocks = ceil(N / bn)
   int rms_local;  // pair kernel, RMS: A completes on each CTA's own barrier (see gemm2_sm100.cu)
   int tile_rot;   // pair kernel wave order: 0 plain grid stride, 1 rotated (pair_tile_rotation), 2 matched table
+  // stream-K tail (pair kernel, sk_tiles > 0): the first sk_dp_waves waves are whole tiles
+  // (cluster + w * C), the last sk_tiles tiles are cut into K ranges of U / C k blocks per pair
+  // (U = sk_tiles x num_k_blocks); a tile split over two pairs is finished by the pair holding
+  // its last k block, which adds the other pair's fp32 partial (sk_part, flag sk_flag) in a
+  // fixed order before the usual epilogue.  sk_part: [sk_tiles][2 CTAs][128 rows][256] fp32 +
+  // [sk_tiles][2][128] partial ssq; sk_flag: [sk_tiles][2] (zero between calls).
+  int sk_tiles, sk_dp_waves;
+  float* sk_part;
+  unsigned* sk_flag;
 };
+
+// one unit of a pair's work: tile `tile`, k blocks [kb0, kb1); fix 0 = whole tile (or a stream-K
+// tile this pair owns entirely), 1 = stream-K finisher (adds the contributor's partial, read from
+// L2 in its epilogue), 3 = a finisher that is its pair's LAST item (the partial is staged into the
+// idle TMEM accumulator buffer while its MMA runs), 2 = stream-K contributor (writes its partial,
+// no output); sk >= 0: index of the stream-K tile
+struct PairItem {
+  int tile, kb0, kb1, fix, sk;
+};
+// the pair's stream-K items over its K range [u0, u1) = tiles a..c: the contributor part (head of
+// tile c) first — it never waits, so every partial gets written — then the finisher part (tail of
+// tile a, which waits for the partial of the pair before), then the whole tiles c-1 .. a+1, whose
+// MMA hides the finisher's epilogue (a finisher last would leave its partial reads as the tail).
+// s = 0, 1, 2...; false when done.
+__host__ __device__ inline bool sk_item(const GemmParams& p, int cluster, int C, int s, PairItem& it) {
+  const long long nkb = p.num_k_blocks;
+  const long long U = (long long)p.sk_tiles * nkb;
+  const long long u0 = (long long)cluster * U / C, u1 = (long long)(cluster + 1) * U / C;
+  if (u1 <= u0) return false;
+  const long long a = u0 / nkb, c = (u1 - 1) / nkb;
+  if (s > c - a) return false;
+  const long long tt = s == 0 ? c : (s == 1 ? a : c - (s - 1));
+  it.kb0 = (int)((u0 > tt * nkb ? u0 : tt * nkb) - tt * nkb);
+  it.kb1 = (int)((u1 < (tt + 1) * nkb ? u1 : (tt + 1) * nkb) - tt * nkb);
+  it.fix = it.kb1 < nkb ? 2 : (it.kb0 > 0 ? (s == c - a ? 3 : 1) : 0);
+  it.sk = (int)tt;
+  it.tile = p.sk_dp_waves * C + (int)tt;
+  return true;
+}
 constexpr int MAX_GATHER_DST = 8;
 enum GluAct { GLU_SILU = 0, GLU_RELU = 1, GLU_BILINEAR = 2 };
 // Fig 2(b) (ReLU FFN, not gated): z = RN(relu(acc)) unscaled, s_out = r — the scale is deferred
@@ -193,6 +232,8 @@ inline bool build_pair_schedule(const GemmParams& p, int C, PairSchedule& s) {
 // K3: tcgen05 prefill GEMM (gemm_sm100.cu)
 int gemm_smem_bytes();
 int gemm2_pick_bn(int M, int N, int num_sms, bool allow_224);
+// stream-K tail plan of the pair kernel (gemm2_sm100.cu): scratch bytes, 0 = none
+int64_t gemm2_sk_plan(int num_tiles, int nkb, int num_sms, int* sk_tiles, int* sk_dp_waves);
 cudaError_t launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int mode, int num_sms,
                         cudaStream_t stream);
 

@@ -93,7 +93,7 @@ def test_linear_ws_validation_codes(L):
     assert f(*args, P(0x4000), 300 * 64 * 2 - 16, None) == 5          # too small for the DyT pre-pass
     assert f(*args[:11], 9, P(0x4000), 0, None) == 5                  # unknown path
     wb = L.flashnorm_linear_workspace_bytes
-    assert wb(300, 64, 64, 2, 0, 0) == 300 * 64 * 2                   # DyT GEMM: M*K*2
+    assert wb(300, 64, 64, 2, 0, 0) == 4096 + 300 * 64 * 2            # DyT GEMM: 4 KiB flags + M*K*2
     assert wb(8, 64, 64, 2, 0, 0) == 0                                # DyT decode: none
     assert wb(300, 64, 64, 0, 0, 0) == 0                              # rmsnorm: none
     assert wb(300, 64, 64, 2, 1, 0) == 0                              # f32: none

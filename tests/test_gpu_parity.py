@@ -8,6 +8,7 @@
   permutation, column-shard concatenation)
 """
 import math
+import os
 
 import numpy as np
 import pytest
@@ -296,9 +297,11 @@ def test_dyt_prologue_and_prepass(M, K, N, path):
     a, Wt, g, b, c, ref = _layer_and_ref(3, M, K, N, "bf16", "dyt")
     Ws, cs = fn.fold_weights(T(Wt), T(g, "f32"), T(b, "f32"), T(c, "f32"))
     ad = T(a)
-    assert fn.linear_workspace_bytes(M, K, N, "dyt", torch.bfloat16, path) == M * K * 2
+    nb = fn.linear_workspace_bytes(M, K, N, "dyt", torch.bfloat16, path)
+    assert nb >= 4096 + M * K * 2
     z_pro = fn.linear(ad, Ws, cs, mode="dyt", alpha=0.5, path=path, workspace=None)
-    ws = torch.full((M * K * 2 + 64,), 0x7F, dtype=torch.uint8, device=DEV)   # poisoned, oversized
+    ws = torch.full((nb + 64,), 0x7F, dtype=torch.uint8, device=DEV)   # poisoned past the 4 KiB of flags, oversized
+    ws[:4096] = 0
     n0 = fn.launch_count()
     z_pre = fn.linear(ad, Ws, cs, mode="dyt", alpha=0.5, path=path, workspace=ws)
     assert fn.launch_count() - n0 == 2
@@ -311,11 +314,22 @@ def test_linear_workspace_rules():
     M, K, N = 256, 128, 256
     a = SD.activations(9, M, K, DEV, torch.bfloat16)
     Wt = SD.layer(9, N, K, DEV, torch.bfloat16)[0]
-    assert fn.linear_workspace_bytes(M, K, N, "rmsnorm", torch.bfloat16) == 0
+    assert fn.linear_workspace_bytes(M, K, N, "rmsnorm", torch.bfloat16) == 0      # 2 pair tiles: no stream-K
     assert fn.linear_workspace_bytes(8, K, N, "dyt", torch.bfloat16) == 0          # decode GEMV
-    assert fn.linear_workspace_bytes(8, K, N, "dyt", torch.bfloat16, "gemm1") == 8 * K * 2
+    assert fn.linear_workspace_bytes(8, K, N, "dyt", torch.bfloat16, "gemm1") == 4096 + 8 * K * 2
     assert fn.linear_workspace_bytes(M, K, N, "dyt", torch.float32) == 0
-    small = torch.empty(M * K * 2 - 16, dtype=torch.uint8, device=DEV)
+    # stream-K policy (FN_GEMM2_SK, read per call): off by default (measured no faster), 1 = the
+    # mode-none kernel, 2 = also RMS; config 4 (128 pair tiles on 74 pairs) then needs its scratch
+    assert fn.linear_workspace_bytes(2048, 4096, 4096, "none", torch.bfloat16) == 0
+    os.environ["FN_GEMM2_SK"] = "1"
+    try:
+        assert fn.linear_workspace_bytes(2048, 4096, 4096, "none", torch.bfloat16) > 0
+        assert fn.linear_workspace_bytes(2048, 4096, 4096, "rmsnorm", torch.bfloat16) == 0
+        os.environ["FN_GEMM2_SK"] = "2"
+        assert fn.linear_workspace_bytes(2048, 4096, 4096, "rmsnorm", torch.bfloat16) > 0
+    finally:
+        del os.environ["FN_GEMM2_SK"]
+    small = torch.empty(4096 + M * K * 2 - 16, dtype=torch.uint8, device=DEV)
     with pytest.raises(fn.FlashNormError, match="workspace_bytes"):
         fn.linear(a, Wt, mode="dyt", workspace=small)
     z = torch.empty(M, N, dtype=torch.bfloat16, device=DEV)
@@ -675,3 +689,59 @@ def test_linear_gather_multicast_validation():
         fn.linear_gather_multicast(a, Ws, 1 << 40, N - 8, 0, c_star=cs)
     with pytest.raises(fn.FlashNormError, match="FN_ERR_ALIGN"):
         fn.linear_gather_multicast(a, Ws, (1 << 40) + 8, N, 0, c_star=cs)
+
+
+# ============================================================ stream-K tail of the pair kernel
+
+@pytest.mark.parametrize("M,K,N,mode", [(2048, 4096, 4096, "rmsnorm"), (2048, 4096, 4096, "none"),
+                                        (2048, 4096, 4096, "layernorm"), (2048, 4096, 4096, "dyt"),
+                                        (4096, 1024, 2816, "rmsnorm"), (2304, 520, 4104, "rmsnorm"),
+                                        (2048, 192, 4096, "rmsnorm")])
+def test_stream_k_tail_parity_and_determinism(M, K, N, mode, monkeypatch):
+    """Shapes whose pair-tile count is not a multiple of the 74 CTA pairs (config 4: 128 tiles) run
+    the stream-K tail when a workspace is given: every 256-row M block against the fp64 oracle, and
+    repeated calls (flags reset, partial order fixed) bit-identical; the no-workspace (whole-tile)
+    result agrees within the tolerance.  FN_GEMM2_SK=2 (read per call) extends the tail to the RMS
+    kernel, which the default policy keeps whole-tile."""
+    monkeypatch.setenv("FN_GEMM2_SK", "2")
+    a, Wt, g, b, c, ref = _layer_and_ref(81, M, K, N, "bf16", mode)
+    Ws, cs = fn.fold_weights(T(Wt), T(g, "f32"), T(b, "f32"), T(c, "f32"))
+    at = T(a)
+    nb = fn.linear_workspace_bytes(M, K, N, mode, torch.bfloat16)
+    assert nb > 0
+    ws = torch.zeros(nb, dtype=torch.uint8, device=DEV)
+    z0 = fn.linear(at, Ws, cs, eps=1e-5, mode=mode, alpha=0.5, workspace=ws)
+    for _ in range(3):
+        assert torch.equal(fn.linear(at, Ws, cs, eps=1e-5, mode=mode, alpha=0.5, workspace=ws), z0)
+    assert not ws[:4096].any(), "stream-K flags not left zero"
+    assert O.rowwise_rel_err(H(z0), ref) <= TOL_BF16
+    z_whole = fn.linear(at, Ws, cs, eps=1e-5, mode=mode, alpha=0.5, workspace=None if mode != "dyt" else "auto")
+    assert O.rowwise_rel_err(H(z_whole), ref) <= TOL_BF16
+
+
+def test_stream_k_tail_graph_replay(monkeypatch):
+    """The stream-K flags end every call at zero, so a captured CUDA graph replays correctly with a
+    changing input."""
+    monkeypatch.setenv("FN_GEMM2_SK", "2")
+    M, K, N = 2048, 1024, 4096
+    a0 = gen_activations(82, M, K, "normal", "bf16")
+    a1 = gen_activations(83, M, K, "normal", "bf16")
+    Wt, g, _, _ = gen_layer(82, N, K, "bf16")
+    Ws, _ = fn.fold_weights(T(Wt), T(g, "f32"))
+    nb = fn.linear_workspace_bytes(M, K, N, "rmsnorm", torch.bfloat16)
+    ws = torch.zeros(nb, dtype=torch.uint8, device=DEV)
+    ain = T(a0)
+    z = torch.empty((M, N), dtype=torch.bfloat16, device=DEV)
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        fn.linear(ain, Ws, None, out=z, workspace=ws)
+        st.synchronize()
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr, stream=st):
+            fn.linear(ain, Ws, None, out=z, workspace=ws)
+    for a in (a1, a0, a1):
+        ain.copy_(T(a))
+        gr.replay()
+        torch.cuda.synchronize()
+        ref = O.norm_linear(a, Wt.T, g, None, None, 1e-5, "rmsnorm")
+        assert O.rowwise_rel_err(H(z), ref) <= TOL_BF16
