@@ -512,7 +512,8 @@ def glu_ffn(a, Wgu_star, Wd_t, eps: float = 1e-5, act: str = "silu"):
 def _rope_tables(positions, cos_tab, sin_tab, M: int, head_dim: int, name: str):
     """positions int32[M]; cos_tab / sin_tab float32[max_pos, head_dim // 2] (reading c26).  Positions
     must lie in [0, max_pos): the kernels index the tables with them (checked here on the device
-    tensor, one small D2H read)."""
+    tensor with one small D2H read — skipped while the stream is being captured into a CUDA graph,
+    where a sync is illegal; the caller then owns the range)."""
     torch = _torch()
     if head_dim <= 0 or head_dim % 2:
         raise FlashNormError(5, name, f"head_dim = {head_dim} must be positive and even (RoPE pairs)")
@@ -521,8 +522,8 @@ def _rope_tables(positions, cos_tab, sin_tab, M: int, head_dim: int, name: str):
         raise FlashNormError(3, name, f"positions must be int32[{M}], got {positions.dtype}{list(positions.shape)}")
     _mat(cos_tab, "cos_tab", cols=head_dim // 2, dtype=torch.float32)
     _mat(sin_tab, "sin_tab", rows=cos_tab.shape[0], cols=head_dim // 2, dtype=torch.float32)
-    if M > 0:
-        lo, hi = int(positions.min()), int(positions.max())
+    if M > 0 and not torch.cuda.is_current_stream_capturing():
+        lo, hi = (int(v) for v in torch.aminmax(positions))
         if lo < 0 or hi >= cos_tab.shape[0]:
             raise FlashNormError(5, name, f"positions span [{lo}, {hi}] outside the {cos_tab.shape[0]}-row tables")
 

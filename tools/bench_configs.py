@@ -146,16 +146,21 @@ report("4 LN V fold", "fold_mean_center 4096x4096 (+b_prev), graph", us, byts=2 
 del Vs0, wsv
 Vs, bs = fn.fold_mean_center(Vt, bp)
 astar = torch.empty(M, d, dtype=torch.bfloat16, device=dev)
-us = timed(lambda i: fn.linear(x, Vs, bs, mode="none", out=astar), 20)
-report("4 upstream x V* + b*", "linear none M=2048 K=4096 N=4096", us, flops=2 * M * d * d)
+# config-4 GEMMs run ~45 us: CUDA graphs of back-to-back calls (the Python wrapper's per-call cost
+# is of the same order, so eager timing would measure the host)
+us = timed(lambda i: fn.linear(x, Vs, bs, mode="none", out=astar), 20, graph=True)
+report("4 upstream x V* + b*", "linear none M=2048 K=4096 N=4096 (graph)", us, flops=2 * M * d * d)
 for Nout in (4096, 16384):
     W, g, b, c = SD.layer(5, Nout, d, dev, torch.bfloat16, with_b=True, with_c=True)
     Ws, cs = fn.fold_weights(W, g, b, c)
+    u = fn.fold_colsum(Ws)
     z = torch.empty(M, Nout, dtype=torch.bfloat16, device=dev)
-    for mode in ("layernorm", "dyt"):
-        us = timed(lambda i: fn.linear(astar, Ws, cs, mode=mode, out=z), 20)
-        report(f"4 M=2048 K=4096 N={Nout}", f"linear {mode}", us, flops=2 * M * d * Nout)
-    del W, Ws, z
+    for mode in ("layernorm", "rmsnorm", "dyt"):
+        us = timed(lambda i: fn.linear(astar, Ws, cs, mode=mode, out=z), 20, graph=True)
+        report(f"4 M=2048 K=4096 N={Nout}", f"linear {mode} (graph)", us, flops=2 * M * d * Nout)
+    us = timed(lambda i: fn.layernorm_linear(x, Ws, u, cs, eps=1e-5, out=z), 20, graph=True)
+    report(f"4 M=2048 K=4096 N={Nout}", "layernorm_linear (exact LN, no V fold; graph)", us, flops=2 * M * d * Nout)
+    del W, Ws, z, u
 
 # ---------------- config 5: Llama-3-70B FFN shapes, one rank's shard for P = 1, 2, 4, 8
 M, K, Nfull = 8192, 8192, 57344

@@ -45,7 +45,7 @@ def main():
     _, Vt, bp = SD.upstream(1, 8, K, 72, dev, bf)
     run("fold_mean_center", lambda: fn.fold_mean_center(Vt, bp))
     u = fn.fold_colsum(Ws)
-    ws = torch.empty(M * K * 2, dtype=torch.uint8, device=dev)
+    ws = torch.zeros(fn.linear_workspace_bytes(M, K, N, "dyt", torch.bfloat16), dtype=torch.uint8, device=dev)
     for path in ("gemm", "gemm1"):
         for mode in ("rmsnorm", "none", "dyt"):
             run(f"linear {mode} {path}", lambda: fn.linear(a, Ws, cs, mode=mode, path=path))
