@@ -30,6 +30,31 @@ FN_DEVICE bool elect_one() {
 // bf16x2 word -> two floats (exact)
 FN_DEVICE float bf16lo(uint32_t w) { return __uint_as_float(w << 16); }
 FN_DEVICE float bf16hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+// packed fp32 pairs {lo, hi} (sm_100 FADD2 / FFMA2): each lane is the IEEE RN scalar op, so a
+// pair of scalar accumulators becomes one register pair with the same numbers, half the issues
+FN_DEVICE uint64_t f2_pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+FN_DEVICE uint64_t f2_bf16x2(uint32_t w) { return f2_pack(bf16lo(w), bf16hi(w)); }
+FN_DEVICE uint64_t f2_add(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+FN_DEVICE uint64_t f2_sub(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+FN_DEVICE uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+FN_DEVICE float f2_lo(uint64_t a) { return __uint_as_float(static_cast<uint32_t>(a)); }
+FN_DEVICE float f2_hi(uint64_t a) { return __uint_as_float(static_cast<uint32_t>(a >> 32)); }
 // two floats -> bf16x2 word, round-to-nearest-even (lo in the low half)
 FN_DEVICE uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);

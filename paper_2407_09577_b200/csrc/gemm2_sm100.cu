@@ -329,63 +329,66 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
           // LayerNorm: sum(a - a0) and sum((a - a0)^2) with the shift a0 = a[m][0] (logical chunk 0
           // of stage kb = 0), so var = S2/K - (S1/K)^2 does not cancel for rows with a large mean;
           // ssq := K var (the epilogue's rsqrt(ssq/K + eps) is then LayerNorm's 1/sqrt(var + eps))
-          float s0 = 0.f, s1 = 0.f, q0 = 0.f, q1 = 0.f, a0 = 0.f;
+          // (s0, s1) and (q0, q1) as packed pairs {lo, hi}: lo elements -> s0 / q0, hi -> s1 / q1
+          uint64_t S = 0, Q = 0, A0 = 0;
+          float a0 = 0.f;
           for (int kb = 0; kb < nkb; ++kb) {
             wait_a(stage);
             const uint4* row = reinterpret_cast<const uint4*>(sA + stage * A_STAGE + t * 128);
-            if (kb == 0) a0 = bf16lo(row[t & 7].x);
+            if (kb == 0) {
+              a0 = bf16lo(row[t & 7].x);
+              A0 = f2_pack(a0, a0);
+            }
             // the last K block's columns >= K are TMA zero fill: they would add -a0 to S1 and
             // a0^2 to S2, so only the cmax logical 8-column chunks inside K are summed
             const int cmax = min(8, (p.K - kb * 64) >> 3);
+            // all 8 loads in flight first (a guarded load per chunk serialised LDS -> use), then
+            // the chunks inside K; the masked tail chunks are TMA zero fill, read but not summed
+            uint4 v8[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) v8[c] = row[c ^ (t & 7)];
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
-              if (c >= cmax) break;
-              const uint4 v = row[c ^ (t & 7)];
-              float d;
-              d = bf16lo(v.x) - a0; s0 += d; q0 = fmaf(d, d, q0);
-              d = bf16hi(v.x) - a0; s1 += d; q1 = fmaf(d, d, q1);
-              d = bf16lo(v.y) - a0; s0 += d; q0 = fmaf(d, d, q0);
-              d = bf16hi(v.y) - a0; s1 += d; q1 = fmaf(d, d, q1);
-              d = bf16lo(v.z) - a0; s0 += d; q0 = fmaf(d, d, q0);
-              d = bf16hi(v.z) - a0; s1 += d; q1 = fmaf(d, d, q1);
-              d = bf16lo(v.w) - a0; s0 += d; q0 = fmaf(d, d, q0);
-              d = bf16hi(v.w) - a0; s1 += d; q1 = fmaf(d, d, q1);
+              if (cmax < 8 && c >= cmax) break;
+              const uint4 v = v8[c];
+              uint64_t D;
+              D = f2_sub(f2_bf16x2(v.x), A0); S = f2_add(S, D); Q = f2_fma(D, D, Q);
+              D = f2_sub(f2_bf16x2(v.y), A0); S = f2_add(S, D); Q = f2_fma(D, D, Q);
+              D = f2_sub(f2_bf16x2(v.z), A0); S = f2_add(S, D); Q = f2_fma(D, D, Q);
+              D = f2_sub(f2_bf16x2(v.w), A0); S = f2_add(S, D); Q = f2_fma(D, D, Q);
             }
-            ssq_fence[t] = (s0 + s1) + (q0 + q1);  // issues only after every LDS above returned
+            ssq_fence[t] = (f2_lo(S) + f2_hi(S)) + (f2_lo(Q) + f2_hi(Q));  // issues only after every LDS above returned
             named_bar_sync(1, 128);
             if (t == 0) mbar_arrive(&empty[stage]);
             if (++stage == STAGES) stage = 0;
           }
-          const float S1 = s0 + s1, S2 = q0 + q1, invK = 1.0f / (float)p.K;
+          const float S1 = f2_lo(S) + f2_hi(S), S2 = f2_lo(Q) + f2_hi(Q), invK = 1.0f / (float)p.K;
           ssq = fmaxf(S2 - S1 * (S1 * invK), 0.0f);
           mu = fmaf(S1, invK, a0);
           ssq_cache[slot * BM + t] = ssq;
           mu_cache[slot * BM + t] = mu;
         } else {
           // (a stream-K item: the partial ssq of its k blocks; the finisher adds the contributor's)
-          float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+          // packed pairs: P01 = (s0, s1) <- lo / hi of words x and z, P23 = (s2, s3) <- y and w
+          uint64_t P01 = 0, P23 = 0;
           for (int kb = 0; kb < nk_it; ++kb) {
             wait_a(stage);
             const uint4* row = reinterpret_cast<const uint4*>(sA + stage * A_STAGE + t * 128);
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
               const uint4 v = row[c ^ (t & 7)];
-              float x;
-              x = bf16lo(v.x); s0 = fmaf(x, x, s0);
-              x = bf16hi(v.x); s1 = fmaf(x, x, s1);
-              x = bf16lo(v.y); s2 = fmaf(x, x, s2);
-              x = bf16hi(v.y); s3 = fmaf(x, x, s3);
-              x = bf16lo(v.z); s0 = fmaf(x, x, s0);
-              x = bf16hi(v.z); s1 = fmaf(x, x, s1);
-              x = bf16lo(v.w); s2 = fmaf(x, x, s2);
-              x = bf16hi(v.w); s3 = fmaf(x, x, s3);
+              uint64_t X;
+              X = f2_bf16x2(v.x); P01 = f2_fma(X, X, P01);
+              X = f2_bf16x2(v.y); P23 = f2_fma(X, X, P23);
+              X = f2_bf16x2(v.z); P01 = f2_fma(X, X, P01);
+              X = f2_bf16x2(v.w); P23 = f2_fma(X, X, P23);
             }
-            ssq_fence[t] = (s0 + s1) + (s2 + s3);  // issues only after every LDS above returned
+            ssq_fence[t] = (f2_lo(P01) + f2_hi(P01)) + (f2_lo(P23) + f2_hi(P23));  // issues only after every LDS above returned
             named_bar_sync(1, 128);                 // drains the 128 stores
             if (t == 0) mbar_arrive(&empty[stage]);
             if (++stage == STAGES) stage = 0;
           }
-          ssq = (s0 + s1) + (s2 + s3);
+          ssq = (f2_lo(P01) + f2_hi(P01)) + (f2_lo(P23) + f2_hi(P23));
           if (it.kb0 == 0 && it.kb1 == nkb) ssq_cache[slot * BM + t] = ssq;
         }
         const int as = local & 1;

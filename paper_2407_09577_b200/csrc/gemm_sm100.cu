@@ -151,31 +151,36 @@ __global__ void __launch_bounds__(gemm::THREADS, 1)
       uint32_t phase = 0;
       int local = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+        // packed pairs (sm_100 FADD2 / FFMA2, common.cuh): A01 = (s0, s1), A23 = (s2, s3)
+        uint64_t A01 = 0, A23 = 0, A0 = 0;
         float a0 = 0.f;  // LayerNorm: shift a[m][0] (see gemm2_sm100.cu)
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait_warp(&full[stage], phase);
           const uint4* row = reinterpret_cast<const uint4*>(sA + stage * A_STAGE + t * 128);
           if (ln) {
             // s0, s1: sum(a - a0);  s2, s3: sum((a - a0)^2)
-            if (kb == 0) a0 = bf16lo(row[t & 7].x);
+            if (kb == 0) {
+              a0 = bf16lo(row[t & 7].x);
+              A0 = f2_pack(a0, a0);
+            }
             // columns >= K of the last K block are TMA zero fill: not summed (see gemm2_sm100.cu)
             const int cmax = min(8, (p.K - kb * 64) >> 3);
+            // all 8 loads in flight first (a guarded load per chunk serialised LDS -> use), then
+            // the chunks inside K; the masked tail chunks are TMA zero fill, read but not summed
+            uint4 v8[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) v8[c] = row[c ^ (t & 7)];
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
-              if (c >= cmax) break;
-              const uint4 v = row[c ^ (t & 7)];
-              float d;
-              d = bf16lo(v.x) - a0; s0 += d; s2 = fmaf(d, d, s2);
-              d = bf16hi(v.x) - a0; s1 += d; s3 = fmaf(d, d, s3);
-              d = bf16lo(v.y) - a0; s0 += d; s2 = fmaf(d, d, s2);
-              d = bf16hi(v.y) - a0; s1 += d; s3 = fmaf(d, d, s3);
-              d = bf16lo(v.z) - a0; s0 += d; s2 = fmaf(d, d, s2);
-              d = bf16hi(v.z) - a0; s1 += d; s3 = fmaf(d, d, s3);
-              d = bf16lo(v.w) - a0; s0 += d; s2 = fmaf(d, d, s2);
-              d = bf16hi(v.w) - a0; s1 += d; s3 = fmaf(d, d, s3);
+              if (cmax < 8 && c >= cmax) break;
+              const uint4 v = v8[c];
+              uint64_t D;
+              D = f2_sub(f2_bf16x2(v.x), A0); A01 = f2_add(A01, D); A23 = f2_fma(D, D, A23);
+              D = f2_sub(f2_bf16x2(v.y), A0); A01 = f2_add(A01, D); A23 = f2_fma(D, D, A23);
+              D = f2_sub(f2_bf16x2(v.z), A0); A01 = f2_add(A01, D); A23 = f2_fma(D, D, A23);
+              D = f2_sub(f2_bf16x2(v.w), A0); A01 = f2_add(A01, D); A23 = f2_fma(D, D, A23);
             }
-            ssq_fence[t] = (s0 + s1) + (s2 + s3);
+            ssq_fence[t] = (f2_lo(A01) + f2_hi(A01)) + (f2_lo(A23) + f2_hi(A23));
             named_bar_sync(1, 128);
             if (t == 0) mbar_arrive(&empty[stage]);
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -184,15 +189,11 @@ __global__ void __launch_bounds__(gemm::THREADS, 1)
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
             const uint4 v = row[c ^ (t & 7)];  // swizzled order: conflict-free, sum is order-free
-            float x;
-            x = bf16lo(v.x); s0 = fmaf(x, x, s0);
-            x = bf16hi(v.x); s1 = fmaf(x, x, s1);
-            x = bf16lo(v.y); s2 = fmaf(x, x, s2);
-            x = bf16hi(v.y); s3 = fmaf(x, x, s3);
-            x = bf16lo(v.z); s0 = fmaf(x, x, s0);
-            x = bf16hi(v.z); s1 = fmaf(x, x, s1);
-            x = bf16lo(v.w); s2 = fmaf(x, x, s2);
-            x = bf16hi(v.w); s3 = fmaf(x, x, s3);
+            uint64_t X;
+            X = f2_bf16x2(v.x); A01 = f2_fma(X, X, A01);
+            X = f2_bf16x2(v.y); A23 = f2_fma(X, X, A23);
+            X = f2_bf16x2(v.z); A01 = f2_fma(X, X, A01);
+            X = f2_bf16x2(v.w); A23 = f2_fma(X, X, A23);
           }
           // WAR hazard on the A stage: LDS results can still be in flight when a later
           // barrier/arrive issues (neither waits on the LDS scoreboard; under full
@@ -203,7 +204,7 @@ __global__ void __launch_bounds__(gemm::THREADS, 1)
           // only then does the group release the stage (2nd arrival on `empty`,
           // next to the MMA commit).  The MMA itself never waits for this group:
           // the RMS runs beside the contraction, not in front of it (Fig 8(c)).
-          ssq_fence[t] = (s0 + s1) + (s2 + s3);
+          ssq_fence[t] = (f2_lo(A01) + f2_hi(A01)) + (f2_lo(A23) + f2_hi(A23));
           named_bar_sync(1, 128);
           if (t == 0) mbar_arrive(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -211,6 +212,7 @@ __global__ void __launch_bounds__(gemm::THREADS, 1)
         const int as = local & 1;
         const uint32_t aphase = (local >> 1) & 1;
         mbar_wait_warp(&sempty[as], aphase ^ 1);
+        const float s0 = f2_lo(A01), s1 = f2_hi(A01), s2 = f2_lo(A23), s3 = f2_hi(A23);
         if (ln) {
           const float S1 = s0 + s1, S2 = s2 + s3, invK = 1.0f / (float)p.K;
           ssq_buf[as * BM + t] = fmaxf(S2 - S1 * (S1 * invK), 0.0f);  // K var

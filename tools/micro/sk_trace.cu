@@ -15,6 +15,9 @@ int main(int argc, char** argv) {
   cudaMemset(w, 0x3c, (size_t)N * K * 2);
   const int64_t wb = flashnorm_linear_workspace_bytes(M, K, N, FN_NONE, FN_BF16, FN_PATH_AUTO);
   cudaMalloc(&ws, wb + 16);
+  float* u;
+  cudaMalloc(&u, N * sizeof(float));
+  cudaMemset(u, 0, N * sizeof(float));
   cudaMemset(ws, 0, wb + 16);
   printf("workspace %lld\n", (long long)wb);
   const int ncalls = (argc > 2 && argv[2][0] == 'x') ? 7 : 6;  // an odd count leaves the whole-tile call's trace
@@ -23,8 +26,11 @@ int main(int argc, char** argv) {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    fn_status st = flashnorm_linear_ws(a, w, nullptr, M, K, N, 0.f, 0.f, argc > 1 && argv[1][0] == 'r' ? FN_RMSNORM : FN_NONE, FN_BF16, z,
-                                       FN_PATH_AUTO, it % 2 ? ws : nullptr, it % 2 ? wb : 0, nullptr);
+    fn_status st = argc > 1 && argv[1][0] == 'l'
+                       ? flashnorm_layernorm_linear(a, w, u, nullptr, M, K, N, 1e-5f, FN_BF16, z, nullptr)
+                       : flashnorm_linear_ws(a, w, nullptr, M, K, N, 0.f, 0.f,
+                                             argc > 1 && argv[1][0] == 'r' ? FN_RMSNORM : FN_NONE, FN_BF16, z,
+                                             FN_PATH_AUTO, it % 2 ? ws : nullptr, it % 2 ? wb : 0, nullptr);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
@@ -69,6 +75,10 @@ int main(int argc, char** argv) {
   }
   for (int mode = 0; mode < 2; ++mode) {  // back-to-back launches (GPU-bound: ~40 us kernels)
     auto call = [&] {
+      if (argc > 1 && argv[1][0] == 'l') {
+        flashnorm_layernorm_linear(a, w, u, nullptr, M, K, N, 1e-5f, FN_BF16, z, nullptr);
+        return;
+      }
       flashnorm_linear_ws(a, w, nullptr, M, K, N, 0.f, 0.f, argc > 1 && argv[1][0] == 'r' ? FN_RMSNORM : FN_NONE,
                           FN_BF16, z, FN_PATH_AUTO, mode ? ws : nullptr, mode ? wb : 0, nullptr);
     };
