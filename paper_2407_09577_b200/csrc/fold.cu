@@ -422,9 +422,10 @@ template <int DT, bool G, bool B>
 static cudaError_t fold_launch(int variant, const uint8_t* src, int64_t N, int64_t K, const float* g,
                                const float* b, const float* c, uint8_t* dst, float* c_star, cudaStream_t stream,
                                int glu_half) {
-  // variant 0 (default): the TMA-ring kernel.  The direct-load shapes stay as A/B references
-  // (tools/bench_folds.py, config-3 W with g, b, c): variant 2 = (2 rows, 2 chunks, 3 CTAs/SM)
-  // 97-104 us; variant 1 = (2, 4, 1) 103 us
+  // default (variant 0): direct 16-byte loads, (2 rows per warp, 2 chunks in flight per lane, 3
+  // CTAs/SM), 97-104 us on the config-3 W with g, b, c (tools/bench_folds.py); variant 9 = the
+  // TMA-ring kernel (fold_weights_tma_kernel, 32 KiB boxes through a 192 KiB ring) measured no
+  // faster; variants 1, 3-8 = other (rows, chunks, CTAs/SM) shapes, e.g. 1 = (2, 4, 1) 103 us
   switch (variant) {
     case 9: return fold_launch_tma<DT, G, B>(src, N, K, g, b, c, dst, c_star, stream, glu_half);
     case 1: fold_launch_v<DT, G, B, 2, 4, 1>(src, N, K, g, b, c, dst, c_star, stream, glu_half); break;
