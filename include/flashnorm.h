@@ -114,10 +114,14 @@ fn_status flashnorm_fold_weights(const void* Wt, int64_t N, int64_t K, fn_dtype 
  *   workspace   device scratch of flashnorm_fold_mean_center_workspace_bytes()
  *               bytes, 16-B aligned (fp64 partial column sums, then s_i / n); no
  *               initialization needed, contents unspecified on return.
- *   Three launches (partials, s_i + b_prev*, centering; PDL-chained).  With the
- *   environment variable FN_K2_VARIANT=1 a one-launch cluster kernel computes the
+ *   One cooperative launch when V fits the SMs' shared memory (ceil(n_out/64) x
+ *   ceil(row_bytes/512) tiles of 32 KiB, at most 7 per SM: the 4096 x 4096 bf16 V of
+ *   config 4 does): every CTA holds its tiles from the HBM read to the V* store, with
+ *   two grid-wide barriers (partials -> s_i -> centering).  Otherwise three launches
+ *   (partials, s_i + b_prev*, centering; PDL-chained).  FN_K2_VARIANT=3 forces the
+ *   three launches; FN_K2_VARIANT=1 a one-launch cluster kernel that computes the
  *   same bits with no workspace (clusters of 8 CTAs own a 256-byte column slab, the
- *   lane sums meet over DSMEM); measured slower (A/B reference, DESIGN.md §6 K2).
+ *   lane sums meet over DSMEM); both measured slower (A/B references, DESIGN.md §6 K2).
 
  *   fold_mean_center numerics (mirrored bit-exactly on the CPU):
  *     partial[c][i] = fp64 sum of Vt[j][i], j in [32c, 32c+32) ascending

@@ -551,7 +551,7 @@ fn_status flashnorm_fold_mean_center(const void* Vt, int64_t n_out, int64_t d_in
   if ((s = get_tmap_fold(Vt, n_out, d_in, dtype, &tm)) != FN_OK) return s;
   if ((s = get_tmap_fold(Vt_star, n_out, d_in, dtype, &tms)) != FN_OK) return s;
   int launches = 0;
-  cudaError_t e = fn::launch_fold_mean_center(tm3, tm, tms, n_out, d_in, dtype == FN_BF16 ? 0 : 1, b_prev, Vt_star,
+  cudaError_t e = fn::launch_fold_mean_center(tm3, tm, tms, Vt, n_out, d_in, dtype == FN_BF16 ? 0 : 1, b_prev, Vt_star,
                                               b_prev_star, workspace, static_cast<cudaStream_t>(stream), &launches);
   if (e != cudaSuccess) return cuda_fail(e, "fold_mean_center");
   g_launches += launches;

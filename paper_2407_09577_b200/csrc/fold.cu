@@ -16,6 +16,7 @@
 // equivalent because the product is exact.  bf16/f32 -> fp64 widening is done with integer
 // ops in a 2^-896-scaled domain (widen_scaled_hi), not on the quarter-rate conversion unit.
 #include "common.cuh"
+#include <cooperative_groups.h>
 #include "kernels.h"
 
 #include <cstdio>
@@ -24,6 +25,7 @@
 #include <algorithm>
 
 namespace fn {
+namespace cg = cooperative_groups;
 
 namespace fold {
 constexpr int WARPS_PER_CTA = 8;  // K1
@@ -1108,6 +1110,284 @@ static cudaError_t launch_fold_mean_center_3k(const CUtensorMap& tm_v, int64_t n
 }
 
 
+// ------------------------------------------------------------------ K2, one persistent launch (default when it fits)
+// One CTA per SM, all co-resident (cooperative launch), V read from HBM exactly once and V* written
+// once: every CTA TMA-loads ALL of its [32 rows x 512 B] tiles into shared memory at entry (up to 14
+// tiles = 224 KiB in flight per SM — the whole 4096^2 bf16 V of config 4 fits in 148 SMs' SMEM), so
+// the read phase streams at full HBM rate from the first cycle.  Then
+//   P1  thread (word, tile) sums its tile's 32 rows in fp64 (the 32-row partial of the contract)
+//       -> workspace partial[c][i];                                      grid.sync()
+//   R   warp per column i, lane l = contract lane l: sums partial[c][i], c = l, l+32, ... ascending,
+//       xor butterfly 16..1 with shuffles (exactly the contract tree), mu_i = RN_f32(s_i / n) ->
+//       workspace;                                                       grid.sync()
+//   P2  v* = RN_dtype(v -_f32 mu_i) in place in the resident tiles, one TMA store per tile.
+// Same contract and bits as the three-launch K2 (include/flashnorm.h); b_prev* by the last CTA.
+namespace k2p {
+constexpr int THREADS = 512;
+constexpr int GROUPS = THREADS / 128;    // tile groups of 128 threads (one 4-byte column word each)
+constexpr int TW = 512;                  // bytes of each row per tile (= the three-launch box)
+constexpr int ROWS = 32;                 // fold::COLSUM_ROWS (rows per partial)
+constexpr int RES_BYTES = 14 * TW * ROWS;  // 224 KiB of resident tiles per CTA
+constexpr size_t SMEM = (size_t)RES_BYTES + 128;
+}  // namespace k2p
+
+// R phase of the persistent K2 (contract order, see the comment inside)
+FN_DEVICE void k2p_column_means(const double* __restrict__ partial, float* __restrict__ mu_g, int64_t n_out,
+                                int64_t d_in, int nchunk, int b, int G) {
+  constexpr int THREADS = k2p::THREADS;
+  const int t = threadIdx.x;
+  // A warp owns 8 columns; thread (k = lane & 7, q = lane >> 3) holds contract lanes l = 8q + u, u = 0..7,
+  // of column 8cb + k: each loads partial[32m + 8q + u][i] (8 consecutive columns = 64 B per row
+  // segment, all loads of a round in flight), adds them in ascending m (a missing partial adds +0.0:
+  // exact, a lane sum starts at +0.0 and is never -0.0); the butterfly's offsets 16 and 8 pair lanes
+  // of threads lane^16 / lane^8 (shuffles), offsets 4, 2, 1 pair values inside the thread — the
+  // contract tree a[l] += a[l + off], bit for bit (fp addition commutes).
+  {
+    const int lane = t & 31, k = lane & 7, q = lane >> 3;
+    // warp-major across CTAs: column blocks spread over every SM (per-SM load concurrency)
+    const int64_t gw = (int64_t)(t >> 5) * G + b, nw = (int64_t)G * (THREADS / 32);
+    for (int64_t cb = gw; cb * 8 < d_in; cb += nw) {
+      const int64_t i = cb * 8 + k;
+      const bool ok = i < d_in;
+      double a[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] = 0.0;
+      for (int m0 = 0; m0 < nchunk; m0 += 32) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int c = m0 + 8 * q + u;
+          v[u] = (ok && c < nchunk) ? __ldcg(partial + (int64_t)c * d_in + i) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a[u] = __dadd_rn(a[u], v[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] = __dadd_rn(a[u], __shfl_xor_sync(0xffffffffu, a[u], 16));
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] = __dadd_rn(a[u], __shfl_xor_sync(0xffffffffu, a[u], 8));
+#pragma unroll
+      for (int off = 4; off > 0; off >>= 1)
+#pragma unroll
+        for (int u = 0; u < off; ++u) a[u] = __dadd_rn(a[u], a[u + off]);
+      if (q == 0 && ok) mu_g[i] = __double2float_rn(__ddiv_rn(__dmul_rn(a[0], kScaleUp), (double)n_out));
+    }
+  }
+}
+
+// b_prev* = b_prev - mean(b_prev) in the contract order (first 256 threads; reading c7)
+FN_DEVICE void k2p_center_bias(const float* __restrict__ b_prev, int64_t n_out, float* __restrict__ b_star,
+                               double* wsum, double* mean_s) {
+  const int t = threadIdx.x;
+  if (t < fold::BPREV_THREADS) {
+    double acc = 0.0;
+    for (int64_t jj = t; jj < n_out; jj += fold::BPREV_THREADS) acc = __dadd_rn(acc, (double)b_prev[jj]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, off));
+    if ((t & 31) == 0) wsum[t >> 5] = acc;
+  }
+  __syncthreads();
+  if (t == 0) {
+    double tot = 0.0;
+    for (int w8 = 0; w8 < fold::BPREV_THREADS / 32; ++w8) tot = __dadd_rn(tot, wsum[w8]);
+    *mean_s = __ddiv_rn(tot, (double)n_out);
+  }
+  __syncthreads();
+  for (int64_t jj = t; jj < n_out; jj += blockDim.x)
+    b_star[jj] = __double2float_rn(__dsub_rn((double)b_prev[jj], *mean_s));
+}
+
+template <int DT, int TR>
+__global__ void __launch_bounds__(k2p::THREADS, 1)
+    fold_mean_center_persist_kernel(const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_vs,
+                                    int64_t n_out, int64_t d_in, int nchunk, int ntx, int ntiles, int order,
+                                    double* __restrict__ partial, float* __restrict__ mu_g,
+                                    const float* __restrict__ b_prev, float* __restrict__ b_star) {
+  using namespace k2p;
+  constexpr int E = DT == 0 ? 2 : 1;  // elements per 4-byte word
+  constexpr int ES = DT == 0 ? 2 : 4;
+  constexpr int TCOLS = TW / ES;      // columns per tile
+  constexpr int RW = TW / 4;          // words per tile row
+  constexpr int TILE = TW * TR;       // tile: TR rows (TR / 32 partial chunks) x 512 B
+  constexpr int HALVES = TR / ROWS;
+  extern __shared__ __align__(128) uint8_t k2p_raw[];
+  uint8_t* tiles = k2p_raw + ((128u - (smem_u32(k2p_raw) & 127u)) & 127u);
+  __shared__ __align__(8) uint64_t full[RES_BYTES / (TW * ROWS)];
+  __shared__ double wsum[fold::BPREV_THREADS / 32];
+  __shared__ double mean_s;
+  const int t = threadIdx.x;
+  const int G = (int)gridDim.x;
+  const int b = (int)blockIdx.x;
+  const int t0 = (int)((int64_t)ntiles * b / G), t1 = (int)((int64_t)ntiles * (b + 1) / G);
+  const int nt = t1 - t0;  // <= MAXT (host-checked)
+  // tile index -> (band c of TR rows, column tile x): order 1 = band-major (a CTA reads whole bands:
+  // contiguous DRAM rows), order 0 = column-tile-major
+  const int nband = (nchunk + HALVES - 1) / HALVES;
+  auto tile_cx = [&](int ti, int& c, int& x) {
+    if (order) {
+      c = ti / ntx;
+      x = ti - c * ntx;
+    } else {
+      x = ti / nband;
+      c = ti - x * nband;
+    }
+  };
+  K2_STAMP(0);
+  if (t == 0) {
+    for (int j = 0; j < nt; ++j) mbar_init(&full[j], 1);
+    fence_mbar_init();
+    prefetch_tmap(&tm_v);
+    prefetch_tmap(&tm_vs);
+    for (int j = 0; j < nt; ++j) {
+      int c, x;
+      tile_cx(t0 + j, c, x);
+      mbar_arrive_expect_tx(&full[j], (uint32_t)TILE);
+      tma_load_2d(tiles + (size_t)j * TILE, &tm_v, &full[j], x * TCOLS, c * TR, kEvictFirst);
+    }
+  }
+  __syncthreads();
+  K2_STAMP(1);
+  cg::grid_group grid = cg::this_grid();
+  const int w = t & 127, grp = t >> 7;
+  // ---------------------------------------------------------------- P1: 32-row fp64 partials
+  for (int it = grp; it < nt * HALVES; it += GROUPS) {
+    const int j = it / HALVES, h = it - j * HALVES;
+    int cb, x;
+    tile_cx(t0 + j, cb, x);
+    const int c = cb * HALVES + h;  // the 32-row partial chunk
+    mbar_wait(&full[j], 0u);
+    if (it == 0) K2_STAMP(2);
+    const int64_t col0 = (int64_t)x * TCOLS + w * E;
+    if (col0 < d_in && c < nchunk) {
+      const int nrows = (int)min((int64_t)ROWS, n_out - (int64_t)c * ROWS);
+      const uint32_t* col = reinterpret_cast<const uint32_t*>(tiles + (size_t)j * TILE) + h * ROWS * RW + w;
+      double acc[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc[e] = 0.0;
+      uint32_t mark = 0u;
+#pragma unroll 8
+      for (int r = 0; r < nrows; ++r) {
+        const uint32_t v = col[r * RW];
+        mark = inf_nan_mark<DT>(mark, v);
+        double d[E];
+        widen_word_scaled<DT>(v, d);
+#pragma unroll
+        for (int e = 0; e < E; ++e) acc[e] = __dadd_rn(acc[e], d[e]);
+      }
+      if (inf_nan_seen<DT>(mark)) {  // rare: redo with hardware conversions (inf/NaN propagate)
+#pragma unroll
+        for (int e = 0; e < E; ++e) acc[e] = 0.0;
+        for (int r = 0; r < nrows; ++r) {
+          double d[E];
+          widen_word_hw<DT>(col[r * RW], d);
+#pragma unroll
+          for (int e = 0; e < E; ++e) acc[e] = __dadd_rn(acc[e], d[e]);
+        }
+      }
+      double* out = partial + (int64_t)c * d_in + col0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) out[e] = acc[e];
+    }
+  }
+  K2_STAMP(3);
+  grid.sync();
+  K2_STAMP(4);
+  // ---------------------------------------------------------------- R: warp per column, lane = contract lane
+  k2p_column_means(partial, mu_g, n_out, d_in, nchunk, b, G);
+  K2_STAMP(5);
+  grid.sync();
+  K2_STAMP(6);
+  // ---------------------------------------------------------------- P2: center in place, TMA store
+  for (int j = grp; j < nt; j += GROUPS) {
+    int c, x;
+    tile_cx(t0 + j, c, x);
+    const int64_t col0 = (int64_t)x * TCOLS + w * E;
+    if (col0 < d_in) {
+      float mu[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) mu[e] = __ldcg(mu_g + col0 + e);
+      uint32_t* col = reinterpret_cast<uint32_t*>(tiles + (size_t)j * TILE) + w;
+#pragma unroll 8
+      for (int r = 0; r < TR; ++r) {  // rows past n_out are zero fill: the TMA store clips them
+        const uint32_t v = col[r * RW];
+        col[r * RW] = DT == 0 ? pack_bf16(__fsub_rn(bf16lo(v), mu[0]), __fsub_rn(bf16hi(v), mu[E - 1]))
+                              : __float_as_uint(__fsub_rn(__uint_as_float(v), mu[0]));
+      }
+    }
+    fence_proxy_async_smem();  // generic-proxy SMEM writes -> visible to the TMA store
+    named_bar_sync(1 + grp, 128);
+    if (w == 0) {
+      tma_store_2d(&tm_vs, tiles + (size_t)j * TILE, x * TCOLS, c * TR);
+      bulk_commit_group();
+    }
+  }
+  K2_STAMP(7);
+  if (b == G - 1 && b_prev != nullptr) k2p_center_bias(b_prev, n_out, b_star, wsum, &mean_s);
+  if (w == 0) bulk_wait_read();  // the tiles stay valid until their stores have read them
+  K2_STAMP(8);
+}
+
+// grid for the persistent K2 (0 = does not fit: a CTA would need more resident tiles than fit)
+static int k2p_grid(int64_t n_out, int64_t d_in, int dtype, int tr, int* ntx_out, int* nchunk_out, int* ntiles_out) {
+  const int64_t row_bytes = d_in * (dtype == 0 ? 2 : 4);
+  const int64_t nchunk = (n_out + k2p::ROWS - 1) / k2p::ROWS;
+  const int64_t nband = (n_out + tr - 1) / tr;
+  const int64_t ntx = (row_bytes + k2p::TW - 1) / k2p::TW;
+  const int64_t ntiles = nband * ntx;
+  const int64_t sms = device_sms();
+  const int64_t maxt = k2p::RES_BYTES / (k2p::TW * tr);
+  if (ntiles > maxt * sms || ntiles > INT32_MAX) return 0;
+  *ntx_out = (int)ntx;
+  *nchunk_out = (int)nchunk;
+  *ntiles_out = (int)ntiles;
+  return (int)std::min<int64_t>(sms, ntiles);
+}
+
+static int k2p_tile_rows() {
+  static const int tr = [] {
+    const char* e = getenv("FN_K2P_TR");  // A/B knob: rows per resident tile (32 or 64)
+    const int v = e != nullptr ? atoi(e) : 64;
+    return v == 32 ? 32 : 64;
+  }();
+  return tr;
+}
+
+static cudaError_t launch_fold_mean_center_persist(const void* Vt, void* Vt_star, int grid, int tr, int ntx,
+                                                   int nchunk, int ntiles, int64_t n_out, int64_t d_in, int dtype,
+                                                   const float* b_prev, float* b_prev_star, void* workspace,
+                                                   cudaStream_t stream, int* launches) {
+  const int es = dtype == 0 ? 2 : 4;
+  CUtensorMap tm_v, tm_vs;
+  if (!encode_plain_tmap(&tm_v, Vt, n_out, d_in, es, k2p::TW / es, tr) ||
+      !encode_plain_tmap(&tm_vs, Vt_star, n_out, d_in, es, k2p::TW / es, tr))
+    return cudaErrorInvalidValue;
+  const void* fptr = dtype == 0 ? (tr == 64 ? (const void*)fold_mean_center_persist_kernel<0, 64>
+                                            : (const void*)fold_mean_center_persist_kernel<0, 32>)
+                                : (tr == 64 ? (const void*)fold_mean_center_persist_kernel<1, 64>
+                                            : (const void*)fold_mean_center_persist_kernel<1, 32>);
+  if (cudaError_t e = ensure_smem_attr(fptr, (int)k2p::SMEM); e != cudaSuccess) return e;
+  double* partial = static_cast<double*>(workspace);
+  float* mu = reinterpret_cast<float*>(partial + (int64_t)nchunk * d_in);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(k2p::THREADS);
+  cfg.dynamicSmemBytes = k2p::SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident: grid.sync() is legal
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  *launches = 1;
+  static const int order = [] {
+    const char* e = getenv("FN_K2P_ORDER");  // A/B knob: tile order, 1 = band-major, 0 = column-tile-major
+    return e != nullptr ? atoi(e) : 1;
+  }();
+  void* args[] = {(void*)&tm_v, (void*)&tm_vs, (void*)&n_out, (void*)&d_in, (void*)&nchunk, (void*)&ntx,
+                  (void*)&ntiles, (void*)&order, (void*)&partial, (void*)&mu, (void*)&b_prev, (void*)&b_prev_star};
+  return cudaLaunchKernelExC(&cfg, fptr, args);
+}
+
 int64_t fold_mean_center_workspace(int64_t n_out, int64_t d_in) {
   const int64_t nchunk = (n_out + fold::COLSUM_ROWS - 1) / fold::COLSUM_ROWS;
   return (nchunk + 1) * d_in * (int64_t)sizeof(double);  // partials + s_i/n
@@ -1119,14 +1399,21 @@ int64_t fold_mean_center_workspace(int64_t n_out, int64_t d_in) {
 // 8192^2 76 vs 95 us — the cluster kernel's column slabs run in ~15 co-resident clusters, three
 // sequential slab rounds, and its read / reduce / write phases do not overlap.
 cudaError_t launch_fold_mean_center(const CUtensorMap& tm_v3, const CUtensorMap& tm_v, const CUtensorMap& tm_vs,
-                                    int64_t n_out, int64_t d_in, int dtype, const float* b_prev, void* Vt_star,
-                                    float* b_prev_star, void* workspace, cudaStream_t stream, int* launches) {
+                                    const void* Vt, int64_t n_out, int64_t d_in, int dtype, const float* b_prev,
+                                    void* Vt_star, float* b_prev_star, void* workspace, cudaStream_t stream,
+                                    int* launches) {
   static const int variant = [] {
     const char* e = getenv("FN_K2_VARIANT");
     return e != nullptr ? atoi(e) : 0;
   }();
   if (variant == 1) return launch_fold_mean_center_cluster(tm_v, tm_vs, n_out, d_in, dtype, b_prev, b_prev_star,
                                                           stream, launches);
+  int ntx = 0, nchunk = 0, ntiles = 0;
+  const int tr = k2p_tile_rows();
+  const int pgrid = variant == 3 ? 0 : k2p_grid(n_out, d_in, dtype, tr, &ntx, &nchunk, &ntiles);
+  if (pgrid > 0)
+    return launch_fold_mean_center_persist(Vt, Vt_star, pgrid, tr, ntx, nchunk, ntiles, n_out, d_in, dtype, b_prev,
+                                           b_prev_star, workspace, stream, launches);
   return launch_fold_mean_center_3k(tm_v3, n_out, d_in, dtype, b_prev, Vt_star, b_prev_star, workspace, stream,
                                     launches);
 }

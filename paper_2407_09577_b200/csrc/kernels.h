@@ -277,9 +277,11 @@ int64_t fold_mean_center_workspace(int64_t n_out, int64_t d_in);
 // box FOLD_BOX_BYTES wide x FOLD_BOX_ROWS rows (cluster K2).  workspace: fold_mean_center_workspace bytes.
 constexpr int FOLD_BOX_BYTES = 256;
 constexpr int FOLD_BOX_ROWS = 128;  // K2 box: 256 B x 128 rows = 32 KiB
+// Vt: the input again (the one-launch persistent K2 encodes its own maps of Vt / Vt_star)
 cudaError_t launch_fold_mean_center(const CUtensorMap& tm_v3, const CUtensorMap& tm_v, const CUtensorMap& tm_vs,
-                                    int64_t n_out, int64_t d_in, int dtype, const float* b_prev, void* Vt_star,
-                                    float* b_prev_star, void* workspace, cudaStream_t stream, int* launches);
+                                    const void* Vt, int64_t n_out, int64_t d_in, int dtype, const float* b_prev,
+                                    void* Vt_star, float* b_prev_star, void* workspace, cudaStream_t stream,
+                                    int* launches);
 
 // K6/K7: baseline norm + gather permute (aux.cu)
 // K8: y = RN_bf16(tanh(alpha a)) over n elements (n % 8 == 0), bit-identical to the GEMM prologue.

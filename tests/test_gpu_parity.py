@@ -80,7 +80,7 @@ def test_fold_weights_bit_exact(dtype, N, K, gbc):
 
 @pytest.mark.parametrize("dtype", ["bf16", "f32"])
 @pytest.mark.parametrize("n_out,d_in", [(8, 8), (40, 24), (100, 72), (33, 1000), (4096, 4096), (5000, 520),
-                                         (20000, 264)])
+                                         (20000, 264), (66304, 256), (6144, 4096)])
 @pytest.mark.parametrize("with_b", [True, False])
 def test_fold_mean_center_bit_exact(dtype, n_out, d_in, with_b):
     _, Vt, bp = gen_upstream(12, 2, d_in, n_out, dtype)
@@ -120,15 +120,18 @@ print("K2_VARIANT_OK" if ok else "K2_VARIANT_DIFF")
 '''
 
 
-def test_fold_mean_center_cluster_variant_bit_exact():
+@pytest.mark.parametrize("variant", ["1", "3"])
+def test_fold_mean_center_cluster_variant_bit_exact(variant):
     """FN_K2_VARIANT=1: the one-launch cluster kernel (DSMEM reduction, TMA stores) meets the same
     contract bit for bit, including ragged shapes, resident (<= 6 boxes per lane group) and
-    streamed (more) slabs, and clusters that loop over several slabs."""
+    streamed (more) slabs, and clusters that loop over several slabs.  FN_K2_VARIANT=3: the
+    three-launch kernels (the default's fallback when V does not fit the persistent kernel's
+    resident tiles) on the same shapes."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-c", _K2_VARIANT, root], env=dict(os.environ, FN_K2_VARIANT="1"),
+    r = subprocess.run([sys.executable, "-c", _K2_VARIANT, root], env=dict(os.environ, FN_K2_VARIANT=variant),
                        capture_output=True, text=True, timeout=600)
     assert "K2_VARIANT_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
 

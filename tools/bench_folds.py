@@ -74,3 +74,20 @@ for (N, K) in ((28672, 4096), (6144, 4096), (4096, 14336)):
     print(f"fold_weights {N}x{K} bf16 (g,b,c) ({nbuf} rotating): {us:.1f} us  {byts / us / 1e3:.0f} GB/s  "
           f"({byts / us / 1e3 / HBM:.2f} of HBM)", flush=True)
     del Ls, Ws
+
+# ceilings at the same sizes: a plain device copy (torch copy_, read + write bytes) over rotating
+# buffers, the same graph timing — what any two-stream (read + write) kernel of this size can reach
+for nbytes in (2 * 4096 * 4096, 2 * 8192 * 8192, 2 * 28672 * 4096):
+    nbuf = max(2, -(-3 * 126 * 2 ** 20 // (2 * nbytes)))
+    srcs = [torch.empty(nbytes // 2, dtype=torch.bfloat16, device=dev).normal_() for _ in range(nbuf)]
+    dsts = [torch.empty_like(s) for s in srcs]
+    it = [0]
+
+    def f():
+        i = it[0] % nbuf
+        it[0] += 1
+        dsts[i].copy_(srcs[i])
+    us = graph_time(f, reps=4 * nbuf)
+    print(f"copy ceiling {nbytes / 1e6:.1f} MB -> {nbytes / 1e6:.1f} MB ({nbuf} rotating): {us:.1f} us  "
+          f"{2 * nbytes / us / 1e3:.0f} GB/s  ({2 * nbytes / us / 1e3 / HBM:.2f} of HBM)", flush=True)
+    del srcs, dsts

@@ -1,0 +1,4 @@
+#!/bin/bash
+mkdir -p gpurun_out
+python -c "from paper_2407_09577_b200 import build; build.build()" > gpurun_out/build_r02l.log 2>&1 || { tail -30 gpurun_out/build_r02l.log; exit 1; }
+for rep in 1 2; do for v in 0 21 22 23 24; do FN_FOLD_VARIANT=$v timeout 120 python tools/ab_fold.py 2>&1; done; done | tee gpurun_out/ab_fold_r02l.txt
