@@ -122,7 +122,17 @@ def lib() -> ctypes.CDLL:
     for name in ("flashnorm_status_string", "flashnorm_last_error", "flashnorm_version"):
         getattr(L, name).restype = ctypes.c_char_p
     _LIB = L
+    global _FAST_LINEAR_WS
+    try:  # the CPython fast-call shim (csrc/pyfast.c), bound to THIS library's function
+        from . import _pyfast
+        _pyfast.bind(ctypes.cast(L.flashnorm_linear_ws, ctypes.c_void_p).value)
+        _FAST_LINEAR_WS = _pyfast.linear_ws
+    except ImportError:
+        _FAST_LINEAR_WS = L.flashnorm_linear_ws
     return L
+
+
+_FAST_LINEAR_WS = None
 
 
 def _check(status: int, name: str):
@@ -213,9 +223,18 @@ def _ptr(t):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
 
-def _stream(t):
+def _raw_stream(device) -> int:
+    """The current CUDA stream of `device` as an integer handle (torch's raw accessor: ~0.1 us
+    against ~2 us for torch.cuda.current_stream(), which builds a Stream object)."""
     torch = _torch()
-    return ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+    get = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if get is not None:
+        return get(device.index if device.index is not None else torch.cuda.current_device())
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _stream(t):
+    return ctypes.c_void_p(_raw_stream(t.device))
 
 
 # ------------------------------------------------------------------ public API
@@ -287,32 +306,44 @@ def linear(a, Wt_star, c_star=None, eps: float = 1e-5, mode: str = "rmsnorm", al
     if mode not in MODES or path not in PATHS:
         raise FlashNormError(5, "linear", f"mode {mode!r} / path {path!r}: mode in {list(MODES)}, path in {list(PATHS)}")
     c_star = _vec(c_star, "c_star", N)
-    z = _out(out, "out", (M, N), a.dtype, a.device)
+    dev = a.device
+    z = _out(out, "out", (M, N), a.dtype, dev)
+    stream = _raw_stream(dev)
     if isinstance(workspace, str):
         if workspace != "auto":
             raise FlashNormError(5, "linear", f"workspace must be 'auto', None or a CUDA tensor, got {workspace!r}")
-        nb = linear_workspace_bytes(M, K, N, mode, a.dtype, path)
-        workspace = _auto_workspace(nb, a.device) if nb > 0 else None
+        key = (M, K, N, mode, a.dtype, path)
+        nb = _WSB_CACHE.get(key)
+        if nb is None:
+            nb = _WSB_CACHE[key] = linear_workspace_bytes(M, K, N, mode, a.dtype, path)
+        workspace = _auto_workspace(nb, dev, stream) if nb > 0 else None
     ws_bytes = 0
     if workspace is not None:
         _dev(workspace, "workspace")
         ws_bytes = workspace.numel() * workspace.element_size()
-    st = lib().flashnorm_linear_ws(_ptr(a), _ptr(Wt_star), _ptr(c_star), M, K, N, float(eps), float(alpha),
-                                   MODES[mode], _dtype_code(a), _ptr(z), PATHS[path], _ptr(workspace), ws_bytes,
-                                   _stream(a))
-    _check(st, "linear")
+    # raw integer pointers (ctypes converts them for the c_void_p argtypes): the decode path is
+    # host-bound when launched eagerly, so this wrapper keeps its per-call work small
+    if _FAST_LINEAR_WS is None:
+        lib()
+    st = _FAST_LINEAR_WS(a.data_ptr(), Wt_star.data_ptr(), None if c_star is None else c_star.data_ptr(),
+                                   M, K, N, eps, alpha, MODES[mode], _DT_F32 if a.dtype == torch.float32 else _DT_BF16,
+                                   z.data_ptr(), PATHS[path], None if workspace is None else workspace.data_ptr(),
+                                   ws_bytes, stream)
+    if st:
+        _check(st, "linear")
     return z
 
 
+_WSB_CACHE = {}  # (M, K, N, mode, dtype, path) -> flashnorm_linear_workspace_bytes
 _WS_CACHE = {}
 
 
-def _auto_workspace(nbytes: int, device):
+def _auto_workspace(nbytes: int, device, stream=None):
     """The library-facing scratch of linear(workspace="auto"): one zero-filled buffer per (device,
     stream), grown on demand and reused — its first 4 KiB (stream-K flags) must be zero before a
     call and every call leaves them zero (include/flashnorm.h flashnorm_linear_ws)."""
     torch = _torch()
-    key = (device.index, torch.cuda.current_stream(device).cuda_stream)
+    key = (device.index, _raw_stream(device) if stream is None else stream)
     buf = _WS_CACHE.get(key)
     if buf is None or buf.numel() < nbytes:
         buf = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)

@@ -62,7 +62,35 @@ def _compile(src: str, verbose: bool) -> str:
     return obj
 
 
+def _pyfast_path() -> str:
+    import sysconfig
+    return os.path.join(HERE, "_pyfast" + (sysconfig.get_config_var("EXT_SUFFIX") or ".so"))
+
+
+def build_pyfast() -> str:
+    """The CPython fast-call shim (csrc/pyfast.c, plain C, no CUDA): argument marshalling for the
+    per-token entry, bound at run time to the ctypes-loaded library's function."""
+    import sysconfig
+    out = _pyfast_path()
+    src = os.path.join(CSRC, "pyfast.c")
+    if os.path.exists(out) and os.path.getmtime(out) >= os.path.getmtime(src):
+        return out
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        raise RuntimeError("gcc not found (needed for the _pyfast shim)")
+    tmp = out + ".tmp"
+    cmd = [cc, "-O2", "-shared", "-fPIC", "-I", sysconfig.get_paths()["include"], src, "-o", tmp]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"_pyfast build failed:\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    os.replace(tmp, out)
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    if force and os.path.exists(_pyfast_path()):
+        os.remove(_pyfast_path())
+    build_pyfast()
     if not force and not needs_build():
         return LIB
     os.makedirs(BUILD, exist_ok=True)

@@ -424,9 +424,13 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
   p.num_m_blocks = (int)(pair ? (M + 255) / 256 : (M + 127) / 128);
   p.num_n_blocks = (int)((N + bn - 1) / bn);
   p.bn = bn;
+  // RMS / exact-LayerNorm side group reads each CTA's A stage after its OWN TMA barrier (afull), the
+  // ordering the memory model states directly; FN_GEMM2_RMS_LOCAL=0 restores the older order (after
+  // the leader's multicast MMA commit), ~1 % faster but ordered only through the MMA's own reads
+  // (tools/ab_local.sh, profiles/r02q_ab_local.txt)
   static const int rms_local = [] {
-    const char* e = getenv("FN_GEMM2_RMS_LOCAL");  // A/B knob (DESIGN.md §12 item 1)
-    return e != nullptr ? atoi(e) : 0;
+    const char* e = getenv("FN_GEMM2_RMS_LOCAL");
+    return e != nullptr ? atoi(e) : 1;
   }();
   p.rms_local = rms_local;
   static const int tile_rot = [] {

@@ -99,6 +99,22 @@ def test_linear_ws_validation_codes(L):
     assert wb(300, 64, 64, 2, 1, 0) == 0                              # f32: none
 
 
+def test_pyfast_shim_is_bound_and_returns_the_c_status(L):
+    """linear() calls flashnorm_linear_ws through the CPython fast-call shim (csrc/pyfast.c) bound
+    to this library's function: the same status codes as the ctypes call, same thread-local error."""
+    import importlib
+    fast = importlib.import_module("paper_2407_09577_b200._pyfast")
+    assert fn._FAST_LINEAR_WS is fast.linear_ws
+    args = (0x1000, 0x2000, None, 300, 64, 64, 1e-5, 0.5, 2, 0, 0x3000, 0)
+    assert fast.linear_ws(*args, None, 16, None) == 1                 # bytes without a pointer
+    assert b"workspace" in L.flashnorm_last_error()
+    assert fast.linear_ws(*args, 0x4008, 300 * 64 * 2, None) == 4     # misaligned workspace
+    assert fast.linear_ws(*args[:11], 9, 0x4000, 0, None) == 5        # unknown path
+    assert fast.linear_ws(None, None, None, 1, 64, 64, 1e-5, 0.5, 0, 0, None, 0, None, 0, None) == 1
+    with pytest.raises(TypeError):
+        fast.linear_ws(*args)
+
+
 def test_glu_validation_codes(L):
     gl = L.flashnorm_glu_linear
     assert gl(P(0x1000), P(0x2000), 4, 64, 100, 1e-5, 0, 0, P(0x3000), P(0x4000), None) == 2   # F % 128
