@@ -12,5 +12,5 @@ echo "== configs"; timeout 900 python tools/bench_configs.py > gpurun_out/config
 echo "== ncu launches"; timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --secondary-iters 5 > /dev/null 2>&1; echo "ncu_launch_exit=$?"
 echo "== ncu full gemm"; timeout 900 ncu --set full --clock-control none --import-source on -k regex:flashnorm_gemm2?_kernel -s 3 -c 1 -o gpurun_out/prof_gemm_$TAG -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --secondary-iters 5 > gpurun_out/ncu_gemm_$TAG.log 2>&1; echo "ncu_gemm_exit=$?"
 echo "== ncu full gemv"; timeout 900 ncu --set full --clock-control none --import-source on -k regex:flashnorm_gemv_tc_kernel -s 8 -c 1 -o gpurun_out/prof_gemv_$TAG -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --secondary-iters 5 > gpurun_out/ncu_gemv_$TAG.log 2>&1; echo "ncu_gemv_exit=$?"
-echo "== ncu full folds/dyt"; timeout 600 ncu --set full --clock-control none --import-source on -k regex:"fold_weights_kernel|k2_tiles_kernel|colsum_reduce_kernel|dyt_prepass" -c 6 -o gpurun_out/prof_aux_$TAG -f python tools/prof_folds.py > gpurun_out/ncu_aux_$TAG.log 2>&1; echo "ncu_aux_exit=$?"
+echo "== ncu full folds/dyt"; timeout 600 ncu --set full --clock-control none --import-source on -k regex:"fold_weights_kernel|fold_mean_center_persist|k2_tiles_kernel|colsum_reduce_kernel|dyt_prepass" -c 6 -o gpurun_out/prof_aux_$TAG -f python tools/prof_folds.py > gpurun_out/ncu_aux_$TAG.log 2>&1; echo "ncu_aux_exit=$?"
 ls -la gpurun_out
