@@ -140,7 +140,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], la ? 2 : 1);  // RMS: ssq group (la: + MMA commit);  NONE/DyT: MMA commit
+      // RMS: ssq group (la: MMA commit + one arrival per side-group warp);  NONE/DyT: MMA commit
+      mbar_init(&empty[s], la ? 1 + 4 : 1);
       mbar_init(&mma_done[s], 1);
       mbar_init(&afull[s], 1);
       mbar_init(&ready[s], 1);
@@ -317,7 +318,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
           if (la) {
             for (int kb = 0; kb < nkb; ++kb) {
               wait_a(stage);
-              if (t == 0) mbar_arrive(&empty[stage]);
+              if ((t & 31) == 0) mbar_arrive(&empty[stage]);
               if (++stage == STAGES) stage = 0;
             }
           } else {
@@ -330,7 +331,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
           // of stage kb = 0), so var = S2/K - (S1/K)^2 does not cancel for rows with a large mean;
           // ssq := K var (the epilogue's rsqrt(ssq/K + eps) is then LayerNorm's 1/sqrt(var + eps))
           // (s0, s1) and (q0, q1) as packed pairs {lo, hi}: lo elements -> s0 / q0, hi -> s1 / q1
-          uint64_t S = 0, Q = 0, A0 = 0;
+          uint64_t S = 0, Q = 0, Sb = 0, Qb = 0, A0 = 0;  // two chains each (words x,y / z,w)
           float a0 = 0.f;
           for (int kb = 0; kb < nkb; ++kb) {
             wait_a(stage);
@@ -354,15 +355,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
               uint64_t D;
               D = f2_sub(f2_bf16x2(v.x), A0); S = f2_add(S, D); Q = f2_fma(D, D, Q);
               D = f2_sub(f2_bf16x2(v.y), A0); S = f2_add(S, D); Q = f2_fma(D, D, Q);
-              D = f2_sub(f2_bf16x2(v.z), A0); S = f2_add(S, D); Q = f2_fma(D, D, Q);
-              D = f2_sub(f2_bf16x2(v.w), A0); S = f2_add(S, D); Q = f2_fma(D, D, Q);
+              D = f2_sub(f2_bf16x2(v.z), A0); Sb = f2_add(Sb, D); Qb = f2_fma(D, D, Qb);
+              D = f2_sub(f2_bf16x2(v.w), A0); Sb = f2_add(Sb, D); Qb = f2_fma(D, D, Qb);
             }
-            ssq_fence[t] = (f2_lo(S) + f2_hi(S)) + (f2_lo(Q) + f2_hi(Q));  // issues only after every LDS above returned
-            named_bar_sync(1, 128);
-            if (t == 0) mbar_arrive(&empty[stage]);
+            // the fence store issues only after every LDS above returned; with la each warp then
+            // releases the stage on its own (no 128-thread barrier per stage)
+            ssq_fence[t] = (f2_lo(S) + f2_hi(S)) + (f2_lo(Q) + f2_hi(Q)) + (f2_lo(Sb) + f2_lo(Qb));
+            if (la) {
+              __syncwarp();
+              if ((t & 31) == 0) mbar_arrive(&empty[stage]);
+            } else {
+              named_bar_sync(1, 128);
+              if (t == 0) mbar_arrive(&empty[stage]);
+            }
             if (++stage == STAGES) stage = 0;
           }
-          const float S1 = f2_lo(S) + f2_hi(S), S2 = f2_lo(Q) + f2_hi(Q), invK = 1.0f / (float)p.K;
+          const float S1 = (f2_lo(S) + f2_hi(S)) + (f2_lo(Sb) + f2_hi(Sb));
+          const float S2 = (f2_lo(Q) + f2_hi(Q)) + (f2_lo(Qb) + f2_hi(Qb)), invK = 1.0f / (float)p.K;
           ssq = fmaxf(S2 - S1 * (S1 * invK), 0.0f);
           mu = fmaf(S1, invK, a0);
           ssq_cache[slot * BM + t] = ssq;
@@ -384,8 +393,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
               X = f2_bf16x2(v.w); P23 = f2_fma(X, X, P23);
             }
             ssq_fence[t] = (f2_lo(P01) + f2_hi(P01)) + (f2_lo(P23) + f2_hi(P23));  // issues only after every LDS above returned
-            named_bar_sync(1, 128);                 // drains the 128 stores
-            if (t == 0) mbar_arrive(&empty[stage]);
+            if (la) {  // each warp releases the stage on its own
+              __syncwarp();
+              if ((t & 31) == 0) mbar_arrive(&empty[stage]);
+            } else {
+              named_bar_sync(1, 128);  // drains the 128 stores
+              if (t == 0) mbar_arrive(&empty[stage]);
+            }
             if (++stage == STAGES) stage = 0;
           }
           ssq = (f2_lo(P01) + f2_hi(P01)) + (f2_lo(P23) + f2_hi(P23));
