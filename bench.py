@@ -582,8 +582,11 @@ def measure_secondary(args, fn, torch, dev, stream, peaks, a, Ws, cs, g):
         "fold_colsum_us": ms_cs * 1e3, "fold_colsum_GB/s": N * K * 2 / (ms_cs * 1e-3) / 1e9}
     del a4, W4, W4s, z4, u3, u4
 
-    # folds (offline, once per weight load): config-3 W (235 MB in + 235 MB out)
+    # folds (offline, once per weight load): config-3 W (235 MB in + 235 MB out); like the decode
+    # section, let the SM clock recover from the GEMMs' power cap first
     Wf, gf, bf_, cf = SD.layer(5, N, K, dev, torch.bfloat16, with_b=True, with_c=True)
+    torch.cuda.synchronize(dev)
+    time.sleep(1.0)
     Wo = torch.empty_like(Wf)
     co = torch.empty(N, dtype=torch.float32, device=dev)
     ms_fold = timed(lambda i: fn.fold_weights(Wf, gf, bf_, cf, out=Wo, c_out=co), 10)
