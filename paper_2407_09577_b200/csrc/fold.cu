@@ -1255,7 +1255,7 @@ __global__ void __launch_bounds__(k2p::THREADS, 1)
     int cb, x;
     tile_cx(t0 + j, cb, x);
     const int c = cb * HALVES + h;  // the 32-row partial chunk
-    mbar_wait(&full[j], 0u);
+    k2_wait(&full[j], 0u, 7);  // bounded: a lost TMA completion traps instead of hanging the GPU
     if (it == 0) K2_STAMP(2);
     const int64_t col0 = (int64_t)x * TCOLS + w * E;
     if (col0 < d_in && c < nchunk) {
@@ -1411,9 +1411,14 @@ cudaError_t launch_fold_mean_center(const CUtensorMap& tm_v3, const CUtensorMap&
   int ntx = 0, nchunk = 0, ntiles = 0;
   const int tr = k2p_tile_rows();
   const int pgrid = variant == 3 ? 0 : k2p_grid(n_out, d_in, dtype, tr, &ntx, &nchunk, &ntiles);
-  if (pgrid > 0)
-    return launch_fold_mean_center_persist(Vt, Vt_star, pgrid, tr, ntx, nchunk, ntiles, n_out, d_in, dtype, b_prev,
-                                           b_prev_star, workspace, stream, launches);
+  if (pgrid > 0) {
+    const cudaError_t e = launch_fold_mean_center_persist(Vt, Vt_star, pgrid, tr, ntx, nchunk, ntiles, n_out, d_in,
+                                                          dtype, b_prev, b_prev_star, workspace, stream, launches);
+    // a cooperative launch the device refuses (e.g. too few co-resident CTAs under MPS limits) falls
+    // back to the three launches, which need no co-residency; any other error is reported
+    if (e != cudaErrorCooperativeLaunchTooLarge && e != cudaErrorNotSupported) return e;
+    (void)cudaGetLastError();
+  }
   return launch_fold_mean_center_3k(tm_v3, n_out, d_in, dtype, b_prev, Vt_star, b_prev_star, workspace, stream,
                                     launches);
 }
