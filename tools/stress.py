@@ -27,4 +27,16 @@ for (M, K, N) in [(4096, 512, 28672), (256, 512, 28672), (4096, 1024, 28672), (4
         ok = nd == 0 and (ref is None or err < 1e-2)
         bad += not ok
         print(f"{'OK ' if ok else 'BAD'} M={M} K={K} N={N} {mode}: nondeterministic reps {nd}/10, err {err:.2e}", flush=True)
+    # exact deferred LayerNorm (per-warp stage release of the side group, 3 packed ops per 2 elements)
+    u = fn.fold_colsum(Ws)
+    z0 = fn.layernorm_linear(a, Ws, u, cs, eps=1e-5)
+    nd = sum(int(not torch.equal(fn.layernorm_linear(a, Ws, u, cs, eps=1e-5), z0))
+             for _ in range(int(os.environ.get("REPS", "10"))))
+    mu = af.mean(1, keepdim=True)
+    ref = ((af - mu) @ Ws.float().T) * torch.rsqrt(((af - mu) ** 2).mean(1, keepdim=True) + 1e-5) + cs
+    err = float(((z0.float() - ref).abs() / ref.abs().amax(1, keepdim=True)).max())
+    ok = nd == 0 and err < 1e-2
+    bad += not ok
+    print(f"{'OK ' if ok else 'BAD'} M={M} K={K} N={N} layernorm_linear: nondeterministic reps {nd}, err {err:.2e}",
+          flush=True)
 print("STRESS", "PASS" if bad == 0 else f"FAIL ({bad})")
