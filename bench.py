@@ -322,6 +322,17 @@ def run_ours(args, ws, rank, local):
     barrier_sync()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1))
     e2e_value = flops_rank * ws * e2e_steps / (e2e_ms * 1e-3) / 1e12
+    # the link this path is bound by: a bare pinned D2H copy of the same z (PCIe), same stream
+    for _ in range(2):
+        z_host.copy_(z, non_blocking=True)
+    torch.cuda.synchronize(dev)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        z_host.copy_(z, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    d2h_gbs = M * Nl * 2 * e2e_steps / (e0.elapsed_time(e1) * 1e-3) / 1e9
+    e2e_link_ms = (M * Nl * 2) / (d2h_gbs * 1e9) * 1e3  # the D2H alone, per step
 
     clocks.stop()
     if rank != 0:
@@ -346,7 +357,10 @@ def run_ours(args, ws, rank, local):
                      "peak_source": f"{peaks_src} bf16_tflops (burst, cuBLAS)"},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "TFLOP/s", "h2d_bytes_per_step": M * K * 2,
-                "d2h_bytes_per_step": M * Nl * 2, "steps": e2e_steps},
+                "d2h_bytes_per_step": M * Nl * 2, "steps": e2e_steps,
+                "ms_per_step": e2e_ms / e2e_steps, "d2h_link_GB/s": d2h_gbs,
+                "frac_of_d2h_link_bound": e2e_link_ms / (e2e_ms / e2e_steps),
+                "note": "bound by the PCIe D2H of z: d2h_link_GB/s is a bare pinned copy of the same z"},
         "gpu_launches": launches,
         "clocks": clocks.summary(),
     }
