@@ -1,6 +1,8 @@
 """paper_2407_09577_b200 — B200-native FlashNorm (arXiv 2407.09577) hot path.
 
-Thin ctypes binding over ``libflashnorm.so`` (the C ABI in include/flashnorm.h).
+Thin ctypes binding over ``libflashnorm.so`` (the C ABI in include/flashnorm.h); the
+per-token entry (``linear`` → ``flashnorm_linear_ws``) goes through ``_pyfast``, a CPython
+fast-call shim (csrc/pyfast.c) bound to the same library function.
 The names follow the ABI:
 
 * :func:`fold_weights`      — W* = diag(g) W, c* = c + b W
