@@ -198,9 +198,10 @@ fn_status flashnorm_linear_ex(const void* a, const void* Wt_star, const float* c
  *      into equal K ranges, and a tile split over two pairs is finished by the pair holding its
  *      last k block, which adds the other's fp32 partial in a fixed order
  *      (deterministic, but not bit-identical to the unsplit tile).  Which kernels use it is the
- *      environment variable FN_GEMM2_SK, read at every call: 0 (default) none, 1 the mode-none
- *      kernel (FN_NONE, DyT after its pre-pass), 2 also rmsnorm / layernorm — it measured no
- *      faster on config 4; flashnorm_linear_workspace_bytes follows the policy.
+ *      environment variable FN_GEMM2_SK, read at every call: 0 none, 1 the mode-none kernel
+ *      (FN_NONE, DyT after its pre-pass), 2 also rmsnorm / layernorm; unset (default): the
+ *      mode-none kernel when K >= 8192 (+2.7 % on the FFN down projection, no gain at K = 4096,
+ *      DESIGN.md §6); flashnorm_linear_workspace_bytes follows the policy.
  *  Layout: [4 KiB stream-K flags][stream-K fp32 partials][DyT buffer of M*K*2].  The FIRST 4 KiB
  *  MUST BE ZERO before a call (zero-fill the buffer once); every call leaves them zero, so one
  *  workspace serves any sequence of calls on one stream (and CUDA graph replays).  The rest is
@@ -259,6 +260,13 @@ fn_status flashnorm_glu_linear(const void* a, const void* Wgu_star, int64_t M, i
                                fn_glu_act act, fn_dtype dtype, void* h, float* s, void* stream);
 fn_status flashnorm_linear_scaled(const void* a, const void* Wt_star, const float* c_star, const float* row_scale,
                                   int64_t M, int64_t K, int64_t N, fn_dtype dtype, void* z, void* stream);
+/* flashnorm_linear_scaled_ws — flashnorm_linear_scaled with the caller's workspace, exactly as
+ *   flashnorm_linear_ws treats it for FN_NONE (size: flashnorm_linear_workspace_bytes(M, K, N,
+ *   FN_NONE, ...); first 4 KiB zero before the call, left zero): lets the stream-K tail run on
+ *   the down projection (K = F, usually >= 8192).  NULL workspace = flashnorm_linear_scaled. */
+fn_status flashnorm_linear_scaled_ws(const void* a, const void* Wt_star, const float* c_star, const float* row_scale,
+                                     int64_t M, int64_t K, int64_t N, fn_dtype dtype, void* z, void* workspace,
+                                     int64_t workspace_bytes, void* stream);
 
 /* --------------------------------------------------------------------------
  * flashnorm_qkv_rope_linear — the Q/K/V projection with RoPE (NEXT-2, PAPER.md:80-94,

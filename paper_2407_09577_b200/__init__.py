@@ -44,6 +44,7 @@ EXPORTS = [
     "flashnorm_fold_weights", "flashnorm_fold_mean_center_workspace_bytes", "flashnorm_fold_mean_center",
     "flashnorm_linear", "flashnorm_linear_ex", "flashnorm_linear_workspace_bytes", "flashnorm_linear_ws",
     "flashnorm_linear_from_host", "flashnorm_fold_glu_weights", "flashnorm_glu_linear", "flashnorm_linear_scaled",
+    "flashnorm_linear_scaled_ws",
     "flashnorm_fold_colsum", "flashnorm_layernorm_linear", "flashnorm_linear_gather", "flashnorm_linear_gather_multicast",
     "flashnorm_comm_unique_id", "flashnorm_comm_init", "flashnorm_comm_destroy", "flashnorm_comm_count",
     "flashnorm_allgather_workspace_bytes", "flashnorm_allgather_columns",
@@ -90,6 +91,7 @@ def lib() -> ctypes.CDLL:
                                           _vp, _f32, _f32, _int, _vp, _vp],
         "flashnorm_relu_ffn_up": [_vp, _vp, _i64, _i64, _i64, _f32, _int, _vp, _vp, _vp],
         "flashnorm_linear_scaled": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _vp, _vp],
+        "flashnorm_linear_scaled_ws": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _vp, _vp, _i64, _vp],
         "flashnorm_fold_colsum": [_vp, _i64, _i64, _int, _vp, _vp],
         "flashnorm_comm_unique_id": [_vp],
         "flashnorm_comm_init": [_vp, _int, _int, ctypes.POINTER(ctypes.c_void_p)],
@@ -416,14 +418,26 @@ def relu_ffn_up(a, Wt_star, eps: float = 1e-5, out=None, s_out=None):
     return h, s
 
 
-def linear_scaled(a, Wt_star, row_scale, c_star=None, out=None):
-    """z = (a W*) * row_scale[m] + c*: the down projection with the deferred FFN-output scale."""
+def linear_scaled(a, Wt_star, row_scale, c_star=None, out=None, workspace="auto"):
+    """z = (a W*) * row_scale[m] + c*: the down projection with the deferred FFN-output scale.
+    workspace: "auto" (the stream-K scratch flashnorm_linear_workspace_bytes asks for, if any),
+    None, or a caller-owned CUDA tensor (flashnorm_linear_scaled_ws)."""
     M, K, N = _operands(a, Wt_star, "linear_scaled")
     row_scale = _vec(row_scale, "row_scale", M)
     c_star = _vec(c_star, "c_star", N)
     z = _out(out, "out", (M, N), a.dtype, a.device)
-    _check(lib().flashnorm_linear_scaled(_ptr(a), _ptr(Wt_star), _ptr(c_star), _ptr(row_scale), M, K, N,
-                                         _dtype_code(a), _ptr(z), _stream(a)), "linear_scaled")
+    if isinstance(workspace, str):
+        if workspace != "auto":
+            raise FlashNormError(5, "linear_scaled", f"workspace must be 'auto', None or a CUDA tensor, got {workspace!r}")
+        nb = linear_workspace_bytes(M, K, N, "none", a.dtype, "auto")
+        workspace = _auto_workspace(nb, a.device) if nb > 0 else None
+    ws_bytes = 0
+    if workspace is not None:
+        _dev(workspace, "workspace")
+        ws_bytes = workspace.numel() * workspace.element_size()
+    _check(lib().flashnorm_linear_scaled_ws(_ptr(a), _ptr(Wt_star), _ptr(c_star), _ptr(row_scale), M, K, N,
+                                            _dtype_code(a), _ptr(z), _ptr(workspace), ws_bytes, _stream(a)),
+           "linear_scaled")
     return z
 
 

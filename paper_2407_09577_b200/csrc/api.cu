@@ -240,9 +240,13 @@ int stg_enabled() {
 // Measured on config 4: mode none within +-2% (constant data +2.5%, random data
 // -1.5%, CUDA graphs), RMS -4..-7%: the partial traffic, the finisher fixups and the ssq group's
 // per-item reductions cost as much as the 13% shorter MMA span saves.
-bool sk_allowed(int kernel_mode) {
+// Default (no FN_GEMM2_SK in the environment): the mode-none kernel at K >= 8192, where the fixup is
+// amortized over a long K — the FFN down projection 4096 x 14336 -> 4096 runs +2.7 % with it
+// (profiles/r03g_ab_sk_ffn_down.txt); RMS never by default.
+bool sk_allowed(int kernel_mode, int64_t K) {
   const char* e = getenv("FN_GEMM2_SK");
-  const int pol = e != nullptr ? atoi(e) : 0;
+  if (e == nullptr) return kernel_mode == fn::MODE_NONE && K >= 8192;
+  const int pol = atoi(e);
   return kernel_mode == fn::MODE_NONE ? pol >= 1 : (kernel_mode == fn::MODE_RMS && pol >= 2);
 }
 
@@ -391,7 +395,7 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
   // workspace holds its scratch (flashnorm_linear_workspace_bytes counts it)
   int sk_tiles = 0, sk_waves = 0;
   int64_t sk_bytes = 0;
-  if (pair && sk_allowed(km_gemm) && workspace != nullptr &&
+  if (pair && sk_allowed(km_gemm, K) && workspace != nullptr &&
       (km_gemm == fn::MODE_NONE || (km_gemm == fn::MODE_RMS && ex.ln_u == nullptr)) && ex.glu_act < 0 &&
       ex.rope.pos == nullptr && ex.ndst == 0)
     sk_bytes = sk_scratch(M, K, N, bn, &sk_tiles, &sk_waves);
@@ -586,7 +590,7 @@ int64_t flashnorm_linear_workspace_bytes(int64_t M, int64_t K, int64_t N, fn_mod
   int64_t sk = 0;
   const bool pair = M > 128 && path != FN_PATH_GEMM1;
   const int km = (mode == FN_RMSNORM || mode == FN_LAYERNORM) ? fn::MODE_RMS : fn::MODE_NONE;  // DyT: pre-pass + none
-  if (pair && sk_allowed(km)) {
+  if (pair && sk_allowed(km, K)) {
     const int bn = fn::gemm2_pick_bn((int)M, (int)N, num_sms(), true);
     int skt = 0, skw = 0;
     sk = sk_scratch(M, K, N, bn, &skt, &skw);
@@ -695,6 +699,19 @@ fn_status flashnorm_linear_scaled(const void* a, const void* Wt_star, const floa
   ex.row_scale = row_scale;
   return linear_impl(a, Wt_star, c_star, M, K, N, 0.0f, 0.0f, FN_NONE, dtype, z, FN_PATH_AUTO, nullptr, 0,
                      static_cast<cudaStream_t>(stream), ex);
+}
+
+fn_status flashnorm_linear_scaled_ws(const void* a, const void* Wt_star, const float* c_star, const float* row_scale,
+                                     int64_t M, int64_t K, int64_t N, fn_dtype dtype, void* z, void* workspace,
+                                     int64_t workspace_bytes, void* stream) {
+  if (dtype != FN_BF16) return fail(FN_ERR_UNSUPPORTED, "flashnorm_linear_scaled is bf16-only");
+  if (row_scale == nullptr && M > 0) return fail(FN_ERR_NULL, "row_scale is NULL");
+  fn_status s;
+  if ((s = check_ptr16("row_scale", row_scale)) != FN_OK) return s;
+  LinearExtras ex;
+  ex.row_scale = row_scale;
+  return linear_impl(a, Wt_star, c_star, M, K, N, 0.0f, 0.0f, FN_NONE, dtype, z, FN_PATH_AUTO, workspace,
+                     workspace_bytes, static_cast<cudaStream_t>(stream), ex);
 }
 
 fn_status flashnorm_qkv_rope_linear(const void* a, const void* Wt_star, int64_t M, int64_t K, int64_t N,

@@ -122,6 +122,27 @@ def test_linear_scaled_parity(M, K, N):
     assert O.rowwise_rel_err(H(z), ref) <= TOL_BF16
 
 
+@pytest.mark.parametrize("M,K,N", [(2304, 8192, 2560), (4096, 14336, 4096)])
+def test_linear_scaled_stream_k_tail(M, K, N):
+    """K >= 8192: the down projection runs the stream-K tail by default (workspace "auto"): rows of
+    every 256-row M block against the fp64 oracle, deterministic across launches, and within
+    tolerance of the whole-tile kernel (workspace=None)."""
+    a = SD.activations(17, M, K, DEV, torch.bfloat16)
+    Wt, _, _, c = SD.layer(17, N, K, DEV, torch.bfloat16, with_c=True)
+    s = torch.linspace(0.25, 4.0, M, device=DEV, dtype=torch.float32)
+    assert fn.linear_workspace_bytes(M, K, N, "none", torch.bfloat16) > 4096  # stream-K scratch planned
+    z = fn.linear_scaled(a, Wt, s, c_star=c)
+    z2 = fn.linear_scaled(a, Wt, s, c_star=c)
+    zw = fn.linear_scaled(a, Wt, s, c_star=c, workspace=None)
+    torch.cuda.synchronize()
+    assert torch.equal(z, z2)
+    rows = np.unique(np.concatenate([np.arange(0, M, 256), np.arange(255, M, 256), [M - 1]]))
+    ah = H(a)[rows]
+    ref = O.linear(ah, H(Wt).T) * H(s)[rows][:, None] + H(c)[None, :]
+    assert O.rowwise_rel_err(H(z)[rows], ref) <= TOL_BF16
+    assert O.rowwise_rel_err(H(z), H(zw).astype(np.float64)) <= 1e-2
+
+
 def test_glu_config3_ffn_full_size_sampled():
     """Llama-3-8B FFN at config 3: M = K = 4096, F = 14336 (gate||up = 28672) — sampled rows"""
     M, K, F = 4096, 4096, 14336
