@@ -706,6 +706,8 @@ fn_status flashnorm_linear_scaled_ws(const void* a, const void* Wt_star, const f
                                      int64_t workspace_bytes, void* stream) {
   if (dtype != FN_BF16) return fail(FN_ERR_UNSUPPORTED, "flashnorm_linear_scaled is bf16-only");
   if (row_scale == nullptr && M > 0) return fail(FN_ERR_NULL, "row_scale is NULL");
+  if (workspace == nullptr && workspace_bytes != 0)
+    return fail(FN_ERR_NULL, "workspace is NULL but workspace_bytes = %lld", (long long)workspace_bytes);
   fn_status s;
   if ((s = check_ptr16("row_scale", row_scale)) != FN_OK) return s;
   LinearExtras ex;

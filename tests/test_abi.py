@@ -115,6 +115,20 @@ def test_pyfast_shim_is_bound_and_returns_the_c_status(L):
         fast.linear_ws(*args)
 
 
+def test_linear_scaled_ws_validation_codes(L):
+    f = L.flashnorm_linear_scaled_ws
+    args = (P(0x1000), P(0x2000), None, P(0x5000), 300, 64, 64, 0, P(0x3000))
+    assert f(*args[:3], None, *args[4:], None, 0, None) == 1          # row_scale NULL
+    assert f(*args[:3], P(0x5008), *args[4:], None, 0, None) == 4     # misaligned row_scale
+    assert f(*args, None, 16, None) == 1                              # bytes without a pointer
+    assert f(*args, P(0x4008), 4096, None) == 4                       # misaligned workspace
+    assert f(*args, P(0x3000), 4096, None) == 5                       # aliases z
+    assert f(*args[:7], 1, *args[8:], None, 0, None) == 6             # f32: bf16-only entry
+    wb = L.flashnorm_linear_workspace_bytes
+    assert wb(4096, 14336, 4096, 3, 0, 0) > 4096                      # mode none, K >= 8192: stream-K scratch
+    assert wb(2048, 4096, 4096, 3, 0, 0) == 0                         # K = 4096: whole tiles
+
+
 def test_glu_validation_codes(L):
     gl = L.flashnorm_glu_linear
     assert gl(P(0x1000), P(0x2000), 4, 64, 100, 1e-5, 0, 0, P(0x3000), P(0x4000), None) == 2   # F % 128
