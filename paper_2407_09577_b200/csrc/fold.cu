@@ -1152,15 +1152,21 @@ FN_DEVICE void k2p_column_means(const double* __restrict__ partial, float* __res
       double a[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) a[u] = 0.0;
-      for (int m0 = 0; m0 < nchunk; m0 += 32) {
-        double v[8];
+      // rounds of 32 chunks, 4 rounds' loads (32 per thread) issued before any of them is added:
+      // one L2 round trip per 4 rounds instead of one per round (config 4: 128 chunks = 4 rounds)
+      for (int m0 = 0; m0 < nchunk; m0 += 4 * 32) {
+        double v[4][8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int c = m0 + 8 * q + u;
-          v[u] = (ok && c < nchunk) ? __ldcg(partial + (int64_t)c * d_in + i) : 0.0;
-        }
+        for (int m = 0; m < 4; ++m)
 #pragma unroll
-        for (int u = 0; u < 8; ++u) a[u] = __dadd_rn(a[u], v[u]);
+          for (int u = 0; u < 8; ++u) {
+            const int c = m0 + 32 * m + 8 * q + u;
+            v[m][u] = (ok && c < nchunk) ? __ldcg(partial + (int64_t)c * d_in + i) : 0.0;
+          }
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+#pragma unroll
+          for (int u = 0; u < 8; ++u) a[u] = __dadd_rn(a[u], v[m][u]);  // ascending chunk per lane
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) a[u] = __dadd_rn(a[u], __shfl_xor_sync(0xffffffffu, a[u], 16));
