@@ -7,8 +7,12 @@
 #include <cstdio>
 #include <cuda_runtime.h>
 #include "flashnorm.h"
+#include <cuda.h>
 
 __global__ void __cluster_dims__(2, 1, 1) empty_k() {}
+__global__ void empty_big(const __grid_constant__ CUtensorMap m0, const __grid_constant__ CUtensorMap m1, const float* p0,
+                          void* p1, int a, int b, int c, float d, float e, int f, int g, int h, const float* p2,
+                          int4 r0, int4 r1, int4 r2, int i, int j, int k, const void* p3, const void* p4) {}
 
 int main() {
   const int K = 4096, N = 6144, M = 1, R = 4000;
@@ -49,5 +53,29 @@ int main() {
   cudaStreamSynchronize(st);
   printf("bare cudaLaunchKernelEx (cluster 2 + PDL, empty kernel): %.2f us/call host\n",
          std::chrono::duration<double, std::micro>(t1 - t0).count() / R);
+  // the decode kernel's launch shape: runtime cluster of 2, PDL, 226 KiB dynamic SMEM, ~400 B of params
+  cudaFuncSetAttribute(empty_big, cudaFuncAttributeMaxDynamicSharedMemorySize, 231488);
+  cudaLaunchAttribute at2[2];
+  at2[0] = at[0];
+  at2[1].id = cudaLaunchAttributeClusterDimension;
+  at2[1].val.clusterDim.x = 2;
+  at2[1].val.clusterDim.y = 1;
+  at2[1].val.clusterDim.z = 1;
+  cfg.attrs = at2;
+  cfg.numAttrs = 2;
+  cfg.dynamicSmemBytes = 231488;
+  CUtensorMap m{};
+  const float* fp = nullptr;
+  void* vp = nullptr;
+  int4 r{};
+  for (int i = 0; i < 50; ++i) cudaLaunchKernelEx(&cfg, empty_big, m, m, fp, vp, 1, 2, 3, 1.f, 1.f, 1, 1, 1, fp, r, r, r, 1, 1, 1, (const void*)vp, (const void*)vp);
+  cudaStreamSynchronize(st);
+  t0 = std::chrono::steady_clock::now();
+  for (int i = 0; i < R; ++i)
+    cudaLaunchKernelEx(&cfg, empty_big, m, m, fp, vp, 1, 2, 3, 1.f, 1.f, 1, 1, 1, fp, r, r, r, 1, 1, 1, (const void*)vp, (const void*)vp);
+  t1 = std::chrono::steady_clock::now();
+  cudaStreamSynchronize(st);
+  printf("bare launch, decode shape (runtime cluster 2 + PDL + 226 KiB dyn SMEM + ~400 B params): %.2f us/call host (%s)\n",
+         std::chrono::duration<double, std::micro>(t1 - t0).count() / R, cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
