@@ -22,7 +22,7 @@ ROOT = os.path.dirname(HERE)
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libflashnorm.so")
 SOURCES = ["api.cu", "fold.cu", "gemm_sm100.cu", "gemm2_sm100.cu", "gemv.cu", "simt_f32.cu", "aux.cu", "dyt.cu", "gemv_tc.cu",
-           "comm.cu"]
+           "comm.cu", "gemv_wide.cu"]
 HEADERS = ["common.cuh", "kernels.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",

@@ -348,6 +348,21 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
                       fn::gemv_supported((int)M, (int)K);
   const bool gemv_ok = tc_ok || mma_ok;
   if (path == FN_PATH_SIMT) return fail(FN_ERR_UNSUPPORTED, "SIMT path is f32-only");
+  // batched decode, 17 <= M <= 128 (K4w): the swap-AB tcgen05 kernel with the tokens as the MMA N
+  const bool wide_ok = (path == FN_PATH_AUTO || path == FN_PATH_GEMV) && !gemv_ok && ex.glu_act < 0 &&
+                       ex.ln_u == nullptr && ex.ndst == 0 && ex.row_scale == nullptr && ex.rope.pos == nullptr &&
+                       (km == fn::MODE_RMS || km == fn::MODE_NONE) &&
+                       fn::gemv_wide_supported(km, (int)M, (int)K, (int)N, num_sms());
+  if (wide_ok) {
+    CUtensorMap tw, ta;
+    if ((s = get_tmap(Wt_star, N, K, 128, &tw)) != FN_OK) return s;
+    if ((s = get_tmap(a, M, K, fn::gemv_wide_tokens((int)M), &ta)) != FN_OK) return s;
+    cudaError_t e = fn::launch_gemv_wide(tw, ta, c_star, static_cast<__nv_bfloat16*>(z), (int)M, (int)K, (int)N, eps,
+                                         km, num_sms(), stream, static_cast<const __nv_bfloat16*>(a));
+    if (e != cudaSuccess) return cuda_fail(e, "gemv_wide");
+    ++g_launches;
+    return FN_OK;
+  }
   if ((path == FN_PATH_GEMV && !gemv_ok) || (path == FN_PATH_GEMV_MMA && !mma_ok))
     return fail(FN_ERR_UNSUPPORTED, "decode path needs M <= 16 and M*K*2 <= ~192 KiB (M=%lld K=%lld)",
                 (long long)M, (long long)K);

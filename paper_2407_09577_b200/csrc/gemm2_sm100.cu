@@ -140,8 +140,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      // RMS: ssq group (la: MMA commit + one arrival per side-group warp);  NONE/DyT: MMA commit
-      mbar_init(&empty[s], la ? 1 + 4 : 1);
+      // RMS: ssq group (la: + MMA commit);  NONE/DyT: MMA commit
+      mbar_init(&empty[s], la ? 2 : 1);
       mbar_init(&mma_done[s], 1);
       mbar_init(&afull[s], 1);
       mbar_init(&ready[s], 1);
@@ -318,7 +318,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
           if (la) {
             for (int kb = 0; kb < nkb; ++kb) {
               wait_a(stage);
-              if ((t & 31) == 0) mbar_arrive(&empty[stage]);
+              if (t == 0) mbar_arrive(&empty[stage]);
               if (++stage == STAGES) stage = 0;
             }
           } else {
@@ -358,16 +358,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
               D = f2_sub(f2_bf16x2(v.z), A0); Sb = f2_add(Sb, D); Qb = f2_fma(D, D, Qb);
               D = f2_sub(f2_bf16x2(v.w), A0); Sb = f2_add(Sb, D); Qb = f2_fma(D, D, Qb);
             }
-            // the fence store issues only after every LDS above returned; with la each warp then
-            // releases the stage on its own (no 128-thread barrier per stage)
+            // the fence store issues only after every LDS above returned; the 128-thread barrier
+            // drains it before the release (a per-warp release after __syncwarp raced in the batched
+            // decode kernel's analogous ssq reads)
             ssq_fence[t] = (f2_lo(S) + f2_hi(S)) + (f2_lo(Q) + f2_hi(Q)) + (f2_lo(Sb) + f2_lo(Qb));
-            if (la) {
-              __syncwarp();
-              if ((t & 31) == 0) mbar_arrive(&empty[stage]);
-            } else {
-              named_bar_sync(1, 128);
-              if (t == 0) mbar_arrive(&empty[stage]);
-            }
+            named_bar_sync(1, 128);
+            if (t == 0) mbar_arrive(&empty[stage]);
             if (++stage == STAGES) stage = 0;
           }
           const float S1 = (f2_lo(S) + f2_hi(S)) + (f2_lo(Sb) + f2_hi(Sb));
@@ -393,13 +389,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::THREADS, 1)
               X = f2_bf16x2(v.w); P23 = f2_fma(X, X, P23);
             }
             ssq_fence[t] = (f2_lo(P01) + f2_hi(P01)) + (f2_lo(P23) + f2_hi(P23));  // issues only after every LDS above returned
-            if (la) {  // each warp releases the stage on its own
-              __syncwarp();
-              if ((t & 31) == 0) mbar_arrive(&empty[stage]);
-            } else {
-              named_bar_sync(1, 128);  // drains the 128 stores
-              if (t == 0) mbar_arrive(&empty[stage]);
-            }
+            named_bar_sync(1, 128);                 // drains the 128 stores
+            if (t == 0) mbar_arrive(&empty[stage]);
             if (++stage == STAGES) stage = 0;
           }
           ssq = (f2_lo(P01) + f2_hi(P01)) + (f2_lo(P23) + f2_hi(P23));

@@ -72,15 +72,6 @@ __device__ float4 g_dtc_part[dtc::SLOTS][dtc::MAX_CTAS][2 * dtc::ROWS * dtc::TOK
 __device__ float4 g_dtc_ssq[dtc::SLOTS][dtc::MAX_CTAS][dtc::TOK / 4];
 __device__ unsigned g_dtc_cnt[dtc::SLOTS][dtc::MAX_CTAS];
 
-FN_DEVICE void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t (&r)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr)
-      : "memory");
-}
 FN_DEVICE float4 ld_cluster_v4(uint32_t cluster_addr) {
   float4 v;
   asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"

@@ -389,6 +389,23 @@ def test_gemv_repeated_launches_bit_identical(M, K, N, mode):
         assert torch.equal(fn.linear(a, Wt, mode=mode, path="gemv"), z0)
 
 
+@pytest.mark.parametrize("M,K,N", [(17, 4096, 6144), (32, 4096, 6144), (48, 512, 1000), (64, 4096, 6144),
+                                   (100, 1024, 2048), (128, 4096, 6144), (24, 8192, 1536)])
+@pytest.mark.parametrize("mode", ["rmsnorm", "none", "layernorm"])
+def test_batched_decode_parity(M, K, N, mode):
+    """17 <= M <= 128 (K4w, gemv_wide.cu): swap-AB tcgen05 with the tokens as the MMA N, split-K over a
+    cluster with the peers' partials pushed to the leader — every output against the fp64 oracle,
+    repeated launches bit-identical."""
+    a, Wt, g, b, c, ref = _layer_and_ref(21, M, K, N, "bf16", mode)
+    Ws, cs = fn.fold_weights(T(Wt, "bf16"), T(g, "f32"), T(b, "f32"), T(c, "f32"))
+    at = T(a, "bf16")
+    z = fn.linear(at, Ws, cs, mode=mode, eps=1e-5)
+    z2 = fn.linear(at, Ws, cs, mode=mode, eps=1e-5)
+    torch.cuda.synchronize()
+    assert torch.equal(z, z2)
+    assert O.rowwise_rel_err(z.float().cpu().numpy(), ref) <= TOL_BF16
+
+
 def test_decode_and_prefill_paths_agree():
     a, Wt, g, b, c, ref = _layer_and_ref(7, 16, 4096, 1024, "bf16", "rmsnorm")
     z1 = _run(a, Wt, g, b, c, "bf16", "rmsnorm", path="gemv")
