@@ -520,6 +520,15 @@ def measure_secondary(args, fn, torch, dev, stream, peaks, a, Ws, cs, g):
         dec[f"M{Mdec}"] = {"us": ms * 1e3, "GB/s": gbs, "frac_hbm": gbs / hbm, "bytes": byts,
                            "eager_us": ms_eager * 1e3, "eager_GB/s": gbs_e, "eager_frac_hbm": gbs_e / hbm,
                            "unfused_us": ms_u * 1e3, "fusion_gain": ms_u / ms}
+    # batched decode (17..128 tokens, K4w): the same W* stream with more tokens per call
+    for Mdec in (32, 64):
+        ad = SD.activations(7, Mdec, DECODE_K, dev, torch.bfloat16)
+        zd = torch.empty((Mdec, DECODE_N), dtype=torch.bfloat16, device=dev)
+        ms = timed(lambda i: fn.linear(ad, Wd[i % NB], None, eps=1e-5, out=zd), args.secondary_iters, graph=True)
+        byts = DECODE_K * DECODE_N * 2 + Mdec * DECODE_K * 2 + Mdec * DECODE_N * 2
+        dec[f"M{Mdec}"] = {"us": ms * 1e3, "GB/s": byts / (ms * 1e-3) / 1e9,
+                           "frac_hbm": byts / (ms * 1e-3) / 1e9 / hbm, "bytes": byts,
+                           "kernel": "flashnorm_gemv_wide_kernel (batched decode, tokens as the MMA N)"}
     out["decode"] = {"workload": "llama3-8b decode: RMSNorm + QKV 4096->6144 (BASELINE config 2)",
                      "unit": "GB/s", "peak_hbm_gbs": hbm, "l2": f"{NB} rotating W* buffers ({NB * 50.3:.0f} MB >= 3x L2)",
                      "timing": "us/frac_hbm: CUDA graph of back-to-back calls (PDL-chained launches); "
