@@ -349,16 +349,30 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
   const bool gemv_ok = tc_ok || mma_ok;
   if (path == FN_PATH_SIMT) return fail(FN_ERR_UNSUPPORTED, "SIMT path is f32-only");
   // batched decode, 17 <= M <= 128 (K4w): the swap-AB tcgen05 kernel with the tokens as the MMA N
+  // DyT takes its tanh pre-pass (K8) into the caller's workspace, then runs in mode none
+  const int64_t dyt_ws_off = align256(kSkFlagBytes);
+  const bool wide_dyt = km == fn::MODE_DYT && workspace != nullptr && workspace_bytes >= dyt_ws_off + M * K * 2;
+  const int km_wide = wide_dyt ? fn::MODE_NONE : km;
   const bool wide_ok = (path == FN_PATH_AUTO || path == FN_PATH_GEMV) && !gemv_ok && ex.glu_act < 0 &&
-                       ex.ln_u == nullptr && ex.ndst == 0 && ex.row_scale == nullptr && ex.rope.pos == nullptr &&
-                       (km == fn::MODE_RMS || km == fn::MODE_NONE) &&
-                       fn::gemv_wide_supported(km, (int)M, (int)K, (int)N, num_sms());
+                       ex.ln_u == nullptr && ex.ndst == 0 && ex.rope.pos == nullptr &&
+                       (ex.row_scale == nullptr || km_wide == fn::MODE_NONE) &&
+                       (km_wide == fn::MODE_RMS || km_wide == fn::MODE_NONE) &&
+                       fn::gemv_wide_supported(km_wide, (int)M, (int)K, (int)N, num_sms());
   if (wide_ok) {
+    if (wide_dyt) {
+      void* ybuf = static_cast<uint8_t*>(workspace) + dyt_ws_off;
+      cudaError_t e = fn::launch_dyt_prepass(static_cast<const __nv_bfloat16*>(a), static_cast<__nv_bfloat16*>(ybuf),
+                                             M * K, alpha, num_sms(), stream);
+      if (e != cudaSuccess) return cuda_fail(e, "dyt_prepass");
+      ++g_launches;
+      a = ybuf;
+      km = fn::MODE_NONE;
+    }
     CUtensorMap tw, ta;
     if ((s = get_tmap(Wt_star, N, K, 128, &tw)) != FN_OK) return s;
     if ((s = get_tmap(a, M, K, fn::gemv_wide_tokens((int)M), &ta)) != FN_OK) return s;
     cudaError_t e = fn::launch_gemv_wide(tw, ta, c_star, static_cast<__nv_bfloat16*>(z), (int)M, (int)K, (int)N, eps,
-                                         km, num_sms(), stream, static_cast<const __nv_bfloat16*>(a));
+                                         km, num_sms(), stream, static_cast<const __nv_bfloat16*>(a), ex.row_scale);
     if (e != cudaSuccess) return cuda_fail(e, "gemv_wide");
     ++g_launches;
     return FN_OK;

@@ -17,8 +17,8 @@
 // summed in fixed rank order (deterministic).  Per CTA (192 threads): warp 0 TMA producer (W* 16 KiB
 // + tokens T x 128 B per stage), warp 1 TMEM allocator + MMA issuer, warps 2-5 the per-token
 // partial ssq (RMS, from global after the dependency wait, off the ring) and then the epilogue, 16
-// tokens at a time.  Modes: rmsnorm / layernorm (pre-centered input) and none; DyT, RoPE, GLU and
-// row-scale calls keep their other kernels.  W* streams before the PDL dependency wait (a constant
+// tokens at a time.  Modes: rmsnorm / layernorm (pre-centered input) and none (optionally with a
+// per-row output scale); DyT runs as the K8 tanh pre-pass + none; RoPE and GLU keep their kernels.  W* streams before the PDL dependency wait (a constant
 // operand, as in K4: include/flashnorm.h states the precondition); tokens are loaded after it.
 #include "common.cuh"
 #include "kernels.h"
@@ -45,7 +45,8 @@ template <int MODE, int T>
 __global__ void __launch_bounds__(dw::THREADS, 1)
     flashnorm_gemv_wide_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_a,
                                const float* __restrict__ cstar, __nv_bfloat16* __restrict__ z, int M, int K, int N,
-                               float eps, int S, int stages, int l2pf, const __nv_bfloat16* __restrict__ aptr) {
+                               float eps, int S, int stages, int l2pf, const __nv_bfloat16* __restrict__ aptr,
+                               const float* __restrict__ row_scale) {
   using namespace dw;
   constexpr int T_STAGE = T * BK * 2;      // token bytes per stage
   constexpr int RECV = ROWS * T + T;       // floats per peer slot: partial D + partial ssq
@@ -250,8 +251,13 @@ __global__ void __launch_bounds__(dw::THREADS, 1)
 #pragma unroll
           for (int m = 0; m < 16; ++m) {
             const int tok = c * 16 + m;
-            const float rr = MODE == MODE_RMS ? rsqrtf(fmaf(ssq[m], invK, eps)) : 1.0f;
-            if (tok < M) z[(size_t)tok * N + n] = __float2bfloat16_rn(fmaf(acc[m], rr, cb));
+            if (tok < M) {
+              // rmsnorm / layernorm: the deferred 1/RMS; none: 1 or the given per-row scale (the
+              // down projection of a GLU / ReLU FFN, flashnorm_linear_scaled)
+              const float rr = MODE == MODE_RMS ? rsqrtf(fmaf(ssq[m], invK, eps))
+                                                : (row_scale != nullptr ? __ldg(row_scale + tok) : 1.0f);
+              z[(size_t)tok * N + n] = __float2bfloat16_rn(fmaf(acc[m], rr, cb));
+            }
           }
         }
       }
@@ -349,7 +355,7 @@ bool gemv_wide_supported(int mode, int M, int K, int N, int num_sms) {
 
 cudaError_t launch_gemv_wide(const CUtensorMap& tw, const CUtensorMap& ta, const float* cstar, __nv_bfloat16* z,
                              int M, int K, int N, float eps, int mode, int num_sms, cudaStream_t stream,
-                             const __nv_bfloat16* aptr) {
+                             const __nv_bfloat16* aptr, const float* row_scale) {
   const DwPlan p = dw_plan(mode, M, K, N, num_sms);
   if (p.S <= 0) return cudaErrorInvalidConfiguration;
   const void* fptr = dw_fptr(mode, p.T);
@@ -373,7 +379,7 @@ cudaError_t launch_gemv_wide(const CUtensorMap& tw, const CUtensorMap& ta, const
   const int l2pf = 12;  // W* stages per CTA prefetched to L2 before the dependency wait (as K4)
   int S = p.S, stages = p.stages;
   void* args[] = {(void*)&tw, (void*)&ta, (void*)&cstar, (void*)&z, (void*)&M, (void*)&K, (void*)&N,
-                  (void*)&eps, (void*)&S, (void*)&stages, (void*)&l2pf, (void*)&aptr};
+                  (void*)&eps, (void*)&S, (void*)&stages, (void*)&l2pf, (void*)&aptr, (void*)&row_scale};
   return cudaLaunchKernelExC(&cfg, fptr, args);
 }
 

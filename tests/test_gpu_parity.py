@@ -391,7 +391,7 @@ def test_gemv_repeated_launches_bit_identical(M, K, N, mode):
 
 @pytest.mark.parametrize("M,K,N", [(17, 4096, 6144), (32, 4096, 6144), (48, 512, 1000), (64, 4096, 6144),
                                    (100, 1024, 2048), (128, 4096, 6144), (24, 8192, 1536)])
-@pytest.mark.parametrize("mode", ["rmsnorm", "none", "layernorm"])
+@pytest.mark.parametrize("mode", ["rmsnorm", "none", "layernorm", "dyt"])
 def test_batched_decode_parity(M, K, N, mode):
     """17 <= M <= 128 (K4w, gemv_wide.cu): swap-AB tcgen05 with the tokens as the MMA N, split-K over a
     cluster with the peers' partials pushed to the leader — every output against the fp64 oracle,
@@ -403,6 +403,20 @@ def test_batched_decode_parity(M, K, N, mode):
     z2 = fn.linear(at, Ws, cs, mode=mode, eps=1e-5)
     torch.cuda.synchronize()
     assert torch.equal(z, z2)
+    assert O.rowwise_rel_err(z.float().cpu().numpy(), ref) <= TOL_BF16
+
+
+@pytest.mark.parametrize("M", [17, 48, 128])
+def test_batched_decode_linear_scaled(M):
+    """The GLU / ReLU FFN down projection at 17..128 tokens (K4w, mode none with the per-row scale)
+    against the oracle, and against the GEMM kernel (path='gemm1') within tolerance."""
+    K, N = 2048, 4096
+    a = gen_activations(22, M, K, "normal", "bf16")
+    Wt, _, _, c = gen_layer(22, N, K, "bf16", with_c=True)
+    s = np.linspace(0.25, 4.0, M).astype(np.float32)
+    z = fn.linear_scaled(T(a, "bf16"), T(Wt, "bf16"), T(s, "f32"), c_star=T(c, "f32"))
+    torch.cuda.synchronize()
+    ref = O.linear(a, Wt.T) * s[:, None] + c[None, :]
     assert O.rowwise_rel_err(z.float().cpu().numpy(), ref) <= TOL_BF16
 
 
