@@ -66,10 +66,13 @@ typedef enum {
 typedef enum { FN_BF16 = 0, FN_F32 = 1 } fn_dtype;
 
 typedef enum {
-    FN_PATH_AUTO = 0,    /* M <= 16: decode kernel, else tcgen05 GEMM                       */
+    FN_PATH_AUTO = 0,    /* M <= 16: decode kernel; 17 <= M <= 128 (rmsnorm / layernorm /
+                            none, DyT with a workspace): the batched-decode kernel when its
+                            cluster plan fits; else tcgen05 GEMM                              */
     FN_PATH_GEMM = 1,    /* force the tcgen05/TMEM/TMA kernel (bf16 only)                   */
     FN_PATH_GEMV = 2,    /* force the decode kernel (bf16, M <= 16): the tcgen05 split-K
-                            kernel when ceil(N/128) <= #SMs, else the mma.sync kernel       */
+                            kernel when ceil(N/128) <= #SMs, else the mma.sync kernel;
+                            17 <= M <= 128: the batched-decode kernel where supported        */
     FN_PATH_SIMT = 3,    /* the fp32 FFMA kernel (the only path for FN_F32)                 */
     FN_PATH_GEMM1 = 4,   /* force the 1-CTA tcgen05 kernel (FN_PATH_GEMM picks the CTA-pair
                             cta_group::2 kernel when M > 128)                               */
@@ -158,14 +161,15 @@ fn_status flashnorm_fold_mean_center(const void* Vt, int64_t n_out, int64_t d_in
  *   eps     >= 0 and finite (ignored for dyt/none);  alpha finite (dyt only).
  *   M == 0 is a no-op returning FN_OK.  A row with ssq == 0 and eps == 0 yields
  *   IEEE inf/NaN in that row (documented; not reported per row).
- *   bf16: tcgen05 GEMM (prefill) or decode GEMV, chosen by M (FN_PATH_AUTO);
+ *   bf16: tcgen05 GEMM (prefill), batched decode (17..128 tokens) or decode GEMV (<= 16),
+ *         chosen by M (FN_PATH_AUTO);
  *   f32:  FFMA SIMT kernel (no TF32).
  *   FN_LAYERNORM trusts that `a` was mean-centered upstream: release builds do
  *   not check it.  With the environment variable FN_DEBUG_LAYERNORM=1 the call first
  *   measures max_m |mean(a_m)| / rms(a_m) on the device (one extra kernel and a stream
  *   synchronization) and returns FN_ERR_VALUE, naming the value, if it exceeds 1e-2.
  *
- *   Programmatic dependent launch (decode path, M <= 16): the decode kernels are launched
+ *   Programmatic dependent launch (decode paths, M <= 128): the decode kernels are launched
  *   with programmatic stream serialization and start streaming Wt_star (and c_star) into
  *   shared memory BEFORE waiting for the preceding kernel on `stream`; `a` is read only
  *   after that wait and `z` written only after it.  Precondition: Wt_star and c_star are not
