@@ -354,7 +354,8 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
   const bool wide_dyt = km == fn::MODE_DYT && workspace != nullptr && workspace_bytes >= dyt_ws_off + M * K * 2;
   const int km_wide = wide_dyt ? fn::MODE_NONE : km;
   const bool wide_ok = (path == FN_PATH_AUTO || path == FN_PATH_GEMV) && !gemv_ok && ex.glu_act < 0 &&
-                       ex.ln_u == nullptr && ex.ndst == 0 && ex.rope.pos == nullptr &&
+                       ex.ln_u == nullptr && ex.ndst == 0 &&
+                       (ex.rope.pos == nullptr || (km_wide == fn::MODE_RMS && ex.rope.g_q == nullptr)) &&
                        (ex.row_scale == nullptr || km_wide == fn::MODE_NONE) &&
                        (km_wide == fn::MODE_RMS || km_wide == fn::MODE_NONE) &&
                        fn::gemv_wide_supported(km_wide, (int)M, (int)K, (int)N, num_sms());
@@ -372,7 +373,8 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
     if ((s = get_tmap(Wt_star, N, K, 128, &tw)) != FN_OK) return s;
     if ((s = get_tmap(a, M, K, fn::gemv_wide_tokens((int)M), &ta)) != FN_OK) return s;
     cudaError_t e = fn::launch_gemv_wide(tw, ta, c_star, static_cast<__nv_bfloat16*>(z), (int)M, (int)K, (int)N, eps,
-                                         km, num_sms(), stream, static_cast<const __nv_bfloat16*>(a), ex.row_scale);
+                                         km, num_sms(), stream, static_cast<const __nv_bfloat16*>(a), ex.row_scale,
+                                         ex.rope);
     if (e != cudaSuccess) return cuda_fail(e, "gemv_wide");
     ++g_launches;
     return FN_OK;

@@ -18,7 +18,8 @@
 // + tokens T x 128 B per stage), warp 1 TMEM allocator + MMA issuer, warps 2-5 the per-token
 // partial ssq (RMS, from global after the dependency wait, off the ring) and then the epilogue, 16
 // tokens at a time.  Modes: rmsnorm / layernorm (pre-centered input) and none (optionally with a
-// per-row output scale); DyT runs as the K8 tanh pre-pass + none; RoPE and GLU keep their kernels.  W* streams before the PDL dependency wait (a constant
+// per-row output scale), RoPE on the Q/K columns (rmsnorm, NEXT-2); DyT runs as the K8 tanh pre-pass
+// + none; QK-norm and GLU keep their kernels.  W* streams before the PDL dependency wait (a constant
 // operand, as in K4: include/flashnorm.h states the precondition); tokens are loaded after it.
 #include "common.cuh"
 #include "kernels.h"
@@ -46,7 +47,7 @@ __global__ void __launch_bounds__(dw::THREADS, 1)
     flashnorm_gemv_wide_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_a,
                                const float* __restrict__ cstar, __nv_bfloat16* __restrict__ z, int M, int K, int N,
                                float eps, int S, int stages, int l2pf, const __nv_bfloat16* __restrict__ aptr,
-                               const float* __restrict__ row_scale) {
+                               const float* __restrict__ row_scale, const RopeParams rope) {
   using namespace dw;
   constexpr int T_STAGE = T * BK * 2;      // token bytes per stage
   constexpr int RECV = ROWS * T + T;       // floats per peer slot: partial D + partial ssq
@@ -247,7 +248,19 @@ __global__ void __launch_bounds__(dw::THREADS, 1)
 #pragma unroll
             for (int m = 0; m < 16; ++m) ssq[m] += sl[ROWS * T + c * 16 + m];
         }
+        // RoPE on the Q/K columns [0, rope.n) (NEXT-2, Fig 5(b), as K4): the pair partner of W* row n
+        // is row n ^ 1, held by lane ^ 1; cos/sin scaled once per token by r * qk
+        const bool rope_row = MODE == MODE_RMS && rope.pos != nullptr && n0 < rope.n;  // warp-uniform per tile
+        float pv[16];
+        if (rope_row) {
+#pragma unroll
+          for (int m = 0; m < 16; ++m) pv[m] = __shfl_xor_sync(0xffffffffu, acc[m], 1);
+        }
         if (n < N) {
+          const bool rot = rope_row && n < rope.n;
+          const int hh = rope.h >> 1;
+          const int ri = rot ? (n % rope.h) >> 1 : 0;
+          const float sgn = (n & 1) ? 1.0f : -1.0f;  // y0 = x0 c - x1 s, y1 = x1 c + x0 s
 #pragma unroll
           for (int m = 0; m < 16; ++m) {
             const int tok = c * 16 + m;
@@ -256,7 +269,15 @@ __global__ void __launch_bounds__(dw::THREADS, 1)
               // down projection of a GLU / ReLU FFN, flashnorm_linear_scaled)
               const float rr = MODE == MODE_RMS ? rsqrtf(fmaf(ssq[m], invK, eps))
                                                 : (row_scale != nullptr ? __ldg(row_scale + tok) : 1.0f);
-              z[(size_t)tok * N + n] = __float2bfloat16_rn(fmaf(acc[m], rr, cb));
+              if (rot) {
+                const int pos = __ldg(rope.pos + tok);
+                const float rq = rr * rope.qk;
+                const float cc = __ldg(rope.cos_tab + (size_t)pos * hh + ri) * rq;
+                const float sn = __ldg(rope.sin_tab + (size_t)pos * hh + ri) * rq;
+                z[(size_t)tok * N + n] = __float2bfloat16_rn(fmaf(acc[m], cc, sgn * pv[m] * sn));
+              } else {
+                z[(size_t)tok * N + n] = __float2bfloat16_rn(fmaf(acc[m], rr, cb));
+              }
             }
           }
         }
@@ -355,7 +376,7 @@ bool gemv_wide_supported(int mode, int M, int K, int N, int num_sms) {
 
 cudaError_t launch_gemv_wide(const CUtensorMap& tw, const CUtensorMap& ta, const float* cstar, __nv_bfloat16* z,
                              int M, int K, int N, float eps, int mode, int num_sms, cudaStream_t stream,
-                             const __nv_bfloat16* aptr, const float* row_scale) {
+                             const __nv_bfloat16* aptr, const float* row_scale, RopeParams rope) {
   const DwPlan p = dw_plan(mode, M, K, N, num_sms);
   if (p.S <= 0) return cudaErrorInvalidConfiguration;
   const void* fptr = dw_fptr(mode, p.T);
@@ -379,7 +400,8 @@ cudaError_t launch_gemv_wide(const CUtensorMap& tw, const CUtensorMap& ta, const
   const int l2pf = 12;  // W* stages per CTA prefetched to L2 before the dependency wait (as K4)
   int S = p.S, stages = p.stages;
   void* args[] = {(void*)&tw, (void*)&ta, (void*)&cstar, (void*)&z, (void*)&M, (void*)&K, (void*)&N,
-                  (void*)&eps, (void*)&S, (void*)&stages, (void*)&l2pf, (void*)&aptr, (void*)&row_scale};
+                  (void*)&eps, (void*)&S, (void*)&stages, (void*)&l2pf, (void*)&aptr, (void*)&row_scale,
+                  (void*)&rope};
   return cudaLaunchKernelExC(&cfg, fptr, args);
 }
 

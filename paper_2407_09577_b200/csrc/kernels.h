@@ -253,7 +253,8 @@ int gemv_wide_tokens(int M);
 bool gemv_wide_supported(int mode, int M, int K, int N, int num_sms);
 cudaError_t launch_gemv_wide(const CUtensorMap& tw, const CUtensorMap& ta, const float* cstar, __nv_bfloat16* z,
                              int M, int K, int N, float eps, int mode, int num_sms, cudaStream_t stream,
-                             const __nv_bfloat16* aptr, const float* row_scale = nullptr);
+                             const __nv_bfloat16* aptr, const float* row_scale = nullptr,
+                             RopeParams rope = RopeParams{nullptr, nullptr, nullptr, 0, 0, 1.f, nullptr, nullptr, 0, 0.f});
 int gemv_tc_split(int K, int N, int num_sms);      // K splits per tile
 int gemv_tc_tile_rows(int mode, int K, int N, int num_sms);  // W* rows per tile (128 or 256; the TMA box)
 // 64-wide k blocks per decode ring stage: 1 -> 2-D maps (box 64 x rows); 2 -> 3-D maps

@@ -79,6 +79,13 @@ def test_qkv_rope_decode_llama3_8b(M):
     assert O.rowwise_rel_err(z, ref) <= TOL_BF16
 
 
+@pytest.mark.parametrize("M", [17, 32, 64, 128])
+def test_qkv_rope_batched_decode_llama3_8b(M):
+    """config 2 shape at 17..128 tokens: the batched-decode kernel (K4w) rotates Q/K in its epilogue"""
+    z, ref = run_case(M, 4096, 128, 32, 8, 1.0 / math.sqrt(math.sqrt(128.0)))
+    assert O.rowwise_rel_err(z, ref) <= TOL_BF16
+
+
 @pytest.mark.parametrize("M,K,h,nq,nkv", [(300, 1024, 64, 8, 2), (64, 512, 128, 4, 4), (257, 2048, 128, 16, 4)])
 @pytest.mark.parametrize("qk_scale", [1.0, 0.5])
 def test_qkv_rope_prefill(M, K, h, nq, nkv, qk_scale):
