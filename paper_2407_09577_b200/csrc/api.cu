@@ -355,7 +355,8 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
   const int km_wide = wide_dyt ? fn::MODE_NONE : km;
   const bool wide_ok = (path == FN_PATH_AUTO || path == FN_PATH_GEMV) && !gemv_ok && ex.glu_act < 0 &&
                        ex.ln_u == nullptr && ex.ndst == 0 &&
-                       (ex.rope.pos == nullptr || (km_wide == fn::MODE_RMS && ex.rope.g_q == nullptr)) &&
+                       (ex.rope.pos == nullptr ||
+                        (km_wide == fn::MODE_RMS && (ex.rope.g_q == nullptr || 128 % ex.rope.h == 0))) &&
                        (ex.row_scale == nullptr || km_wide == fn::MODE_NONE) &&
                        (km_wide == fn::MODE_RMS || km_wide == fn::MODE_NONE) &&
                        fn::gemv_wide_supported(km_wide, (int)M, (int)K, (int)N, num_sms());

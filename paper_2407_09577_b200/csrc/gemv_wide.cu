@@ -18,8 +18,8 @@
 // + tokens T x 128 B per stage), warp 1 TMEM allocator + MMA issuer, warps 2-5 the per-token
 // partial ssq (RMS, from global after the dependency wait, off the ring) and then the epilogue, 16
 // tokens at a time.  Modes: rmsnorm / layernorm (pre-centered input) and none (optionally with a
-// per-row output scale), RoPE on the Q/K columns (rmsnorm, NEXT-2); DyT runs as the K8 tanh pre-pass
-// + none; QK-norm and GLU keep their kernels.  W* streams before the PDL dependency wait (a constant
+// per-row output scale), RoPE on the Q/K columns (rmsnorm, NEXT-2) with or without QK-norm (NEXT-4,
+// h | 128); DyT runs as the K8 tanh pre-pass + none; GLU keeps its kernels.  W* streams before the PDL dependency wait (a constant
 // operand, as in K4: include/flashnorm.h states the precondition); tokens are loaded after it.
 #include "common.cuh"
 #include "kernels.h"
@@ -256,6 +256,38 @@ __global__ void __launch_bounds__(dw::THREADS, 1)
 #pragma unroll
           for (int m = 0; m < 16; ++m) pv[m] = __shfl_xor_sync(0xffffffffu, acc[m], 1);
         }
+        // QK-norm (NEXT-4, Figs 6(b)/7(b), as K4): per Q/K head and token s_b = rsqrt(MS(head) +
+        // eps_qk MSe(a)) replaces r (s_a cancels); the head's rows (h | 128) are h / 32 warps of this
+        // tile: warp shuffles, then a [4 warps][16 tokens] exchange in the (free) ring
+        float sb[16];
+        float g_own = 1.0f, g_pair = 1.0f;
+        const bool qkn = MODE == MODE_RMS && rope_row && rope.g_q != nullptr;  // warp-uniform
+        if (qkn) {
+          float* red = reinterpret_cast<float*>(smem);
+#pragma unroll
+          for (int m = 0; m < 16; ++m) {
+            float q = acc[m] * acc[m];
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) q += __shfl_xor_sync(0xffffffffu, q, off);
+            if (lane == 0) red[q4 * 16 + m] = q;
+          }
+          named_bar_sync(3, 128);
+          const int wph = rope.h / 32;  // warps per head (h = 32, 64 or 128)
+          const int w0 = (int)(q4 / (uint32_t)wph) * wph;
+#pragma unroll
+          for (int m = 0; m < 16; ++m) {
+            float ss = 0.f;
+            for (int w = 0; w < wph; ++w) ss += red[(w0 + w) * 16 + m];
+            const float rr = rsqrtf(fmaf(ssq[m], invK, eps));
+            sb[m] = rsqrtf(fmaf(rope.eps_qk, 1.0f / (rr * rr), ss / (float)rope.h));
+          }
+          named_bar_sync(3, 128);  // red is rewritten by the next chunk
+          if (n < rope.n) {
+            const float* gsrc = n < rope.n_q ? rope.g_q : rope.g_k;
+            g_own = __ldg(gsrc + n % rope.h);
+            g_pair = __ldg(gsrc + (n ^ 1) % rope.h);
+          }
+        }
         if (n < N) {
           const bool rot = rope_row && n < rope.n;
           const int hh = rope.h >> 1;
@@ -271,9 +303,9 @@ __global__ void __launch_bounds__(dw::THREADS, 1)
                                                 : (row_scale != nullptr ? __ldg(row_scale + tok) : 1.0f);
               if (rot) {
                 const int pos = __ldg(rope.pos + tok);
-                const float rq = rr * rope.qk;
-                const float cc = __ldg(rope.cos_tab + (size_t)pos * hh + ri) * rq;
-                const float sn = __ldg(rope.sin_tab + (size_t)pos * hh + ri) * rq;
+                const float rq = (qkn ? sb[m] : rr) * rope.qk;
+                const float cc = __ldg(rope.cos_tab + (size_t)pos * hh + ri) * rq * g_own;
+                const float sn = __ldg(rope.sin_tab + (size_t)pos * hh + ri) * rq * g_pair;
                 z[(size_t)tok * N + n] = __float2bfloat16_rn(fmaf(acc[m], cc, sgn * pv[m] * sn));
               } else {
                 z[(size_t)tok * N + n] = __float2bfloat16_rn(fmaf(acc[m], rr, cb));

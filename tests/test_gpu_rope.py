@@ -139,9 +139,11 @@ def run_qkn(M, K, h, nq_heads, nk_heads, eps_qk, seed=5, max_pos=4096):
 
 
 @pytest.mark.parametrize("M,K,h,nq,nk", [(1, 2048, 64, 16, 4), (16, 1024, 128, 8, 2), (5, 512, 32, 8, 8),
-                                         (300, 1024, 64, 8, 2), (100, 768, 128, 4, 4), (40, 512, 256, 2, 2)])
+                                         (300, 1024, 64, 8, 2), (100, 768, 128, 4, 4), (40, 512, 256, 2, 2),
+                                         (17, 1024, 32, 8, 8), (64, 2048, 64, 16, 4), (128, 4096, 128, 32, 8)])
 @pytest.mark.parametrize("eps_qk", [0.0, 1e-6])
 def test_qk_norm_rope_parity(M, K, h, nq, nk, eps_qk):
-    """decode (tcgen05 split-K, h | 128) and GEMM paths vs the unfused Figs 6(a)+7(a)"""
+    """decode (tcgen05 split-K, h | 128), batched decode (17..128 tokens, h | 128) and GEMM paths vs
+    the unfused Figs 6(a)+7(a)"""
     z, ref = run_qkn(M, K, h, nq, nk, eps_qk)
     assert O.rowwise_rel_err(z, ref) <= TOL_BF16
