@@ -381,7 +381,7 @@ fn_status linear_impl(const void* a, const void* Wt_star, const float* c_star, i
     return FN_OK;
   }
   if ((path == FN_PATH_GEMV && !gemv_ok) || (path == FN_PATH_GEMV_MMA && !mma_ok))
-    return fail(FN_ERR_UNSUPPORTED, "decode path needs M <= 16 and M*K*2 <= ~192 KiB (M=%lld K=%lld)",
+    return fail(FN_ERR_UNSUPPORTED, "decode path needs M <= 16 (or 17..128 for the batched-decode kernel: rmsnorm / layernorm / none, N <= 128 x #SMs) (M=%lld K=%lld)",
                 (long long)M, (long long)K);
   const bool use_gemv = path == FN_PATH_GEMV || path == FN_PATH_GEMV_MMA || (path == FN_PATH_AUTO && gemv_ok);
   if (use_gemv && path != FN_PATH_GEMV_MMA && tc_ok) {
