@@ -185,7 +185,9 @@ __global__ void __launch_bounds__(dtc::THREADS, R == 4 ? 1 : 2)  // R < 4: <= 16
     }
   };
 
-  pdl_launch_dependents();  // the next call's CTAs may queue for free SMs right away
+  // the next call's CTAs may queue for free SMs right away (flags & 64: only once this CTA's W* loads are
+  // all issued — A/B knob FN_DECODE_PDL_LATE)
+  if (!(flags & 64)) pdl_launch_dependents();
 #ifdef FN_GEMV_TC_TRACE
   __shared__ int trace_par_s;
   if (threadIdx.x == 0) trace_par_s = (int)((atomicAdd(&g_tc_launch, 1u) / gridDim.x) & 1u);
@@ -271,6 +273,7 @@ __global__ void __launch_bounds__(dtc::THREADS, R == 4 ? 1 : 2)  // R < 4: <= 16
         if (!tokres) load_t(sT + stage * T_STAGE, &full[stage], kb0 + i);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
+      if (flags & 64) pdl_launch_dependents();
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
@@ -778,7 +781,8 @@ int dtc_flags() {
   // streams (N = 18432: 5.05 vs 6.78 TB/s) and no better on config 2 than a bounded TMA prefetch
   // (FN_DECODE_L2PF stages beyond the ring): off by default
   static const int f = (env_int("FN_DECODE_PUSH", 1) ? 1 : 0) | (env_int("FN_DECODE_PF2", 0) ? 2 : 0) |
-                       (env_int("FN_DECODE_LSUPF", 0) & 7) << 2;  // bit 2 of LSUPF: evict_normal hint
+                       (env_int("FN_DECODE_LSUPF", 0) & 7) << 2 |  // bit 2 of LSUPF: evict_normal hint
+                       (env_int("FN_DECODE_PDL_LATE", 0) ? 64 : 0);
   return f;
 }
 size_t dtc_recv_bytes(int R, int S) {

@@ -14,7 +14,7 @@ for r in range(NB):
     w, g, _, _ = SD.layer(100 + r, N, K, dev, torch.bfloat16)
     Wd.append(fn.fold_weights(w, g)[0])
 R = 200
-for M in (1, 4, 16):
+for M in tuple(int(x) for x in os.environ.get("DECODE_MS", "1,4,16").split(",")):
     a = SD.activations(7, M, K, dev, torch.bfloat16)
     z = torch.empty((M, N), dtype=torch.bfloat16, device=dev)
     for i in range(20):
